@@ -1,0 +1,668 @@
+"""CPU oracle for the HongTu partition-based full-graph GCN epoch.
+
+TEST INFRASTRUCTURE ONLY.  Nothing in ``paper_2311_14898_b200`` imports,
+links or calls this module; only ``tests/``, ``__graft_entry__.smoke()`` and
+the ``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` do, and only
+as the checker (or as the timed CPU baseline), never as the product path.
+
+It is a from-scratch numpy restatement of the reference's algorithm
+(``/root/reference/pkg/src/chunktrain``, abbreviated ``src/`` below); every
+function cites the reference lines it restates.  Parity pinning: the oracle
+is checked against golden vectors produced by running the reference itself
+(``tests/golden/make_golden.py`` -> ``tests/golden/*.npz`` / ``*.json``),
+see ``tests/test_oracle_golden.py``.
+
+Arithmetic conventions (they are what makes the GPU kernels checkable):
+
+* forward aggregation is a sequential multiply-then-add per destination in
+  canonical (destination, source) edge order - the exact semantics of
+  ``np.add.at`` at ``src/engine.py:139`` (no fused multiply-add);
+* backward transposed aggregation is a sequential multiply-then-add per
+  source in CSR order.  The reference uses ``np.add.reduceat``
+  (``src/engine.py:159``) whose association is numpy-internal, so this one
+  is compared at tolerance with the reference and bit-exact with the GPU
+  kernel's unsplit segments;
+* integer work (graph arrays, LDG partition, chunks, plan sets, slots,
+  volumes, reorganization, meters) is bit-exact with the reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+
+I64 = np.int64
+_NONE = np.zeros(0, dtype=I64)
+
+# ---------------------------------------------------------------------------
+# graph structure                                  (src/graph.py:91-150)
+# ---------------------------------------------------------------------------
+
+
+def build_graph(src, dst, num_vertices):
+    """Canonical CSC sorted by (dst, src), CSR sorted by (src, dst), the
+    CSR->canonical permutation and d_uv weights (src/graph.py:91-150).
+
+    Parallel edges and self loops are kept (src/graph.py:95-96)."""
+    src = np.asarray(src, dtype=I64).ravel()
+    dst = np.asarray(dst, dtype=I64).ravel()
+    V = int(num_vertices)
+    # a stable sort on the composite key reproduces lexsort((src, dst))
+    canon = np.argsort(dst * V + src, kind="stable")
+    csc_sources = src[canon]
+    indeg = np.bincount(dst, minlength=V).astype(I64)
+    csc_offsets = np.zeros(V + 1, dtype=I64)
+    np.cumsum(indeg, out=csc_offsets[1:])
+    by_src = np.argsort(src * V + dst, kind="stable")
+    csr_targets = dst[by_src]
+    outdeg = np.bincount(src, minlength=V).astype(I64)
+    csr_offsets = np.zeros(V + 1, dtype=I64)
+    np.cumsum(outdeg, out=csr_offsets[1:])
+    rank_of = np.empty_like(canon)
+    rank_of[canon] = np.arange(canon.size, dtype=I64)
+    csr_edge_perm = rank_of[by_src]
+    # d_uv = 1/sqrt((1+indeg u)(1+indeg v)) as a product of two inverse
+    # square roots, in float64 (src/graph.py:141-150)
+    r = 1.0 / np.sqrt(indeg.astype(np.float64) + 1.0)
+    dst_canon = np.repeat(np.arange(V, dtype=I64), indeg)
+    weights = r[csc_sources] * r[dst_canon]
+    return {
+        "num_vertices": V,
+        "csc_offsets": csc_offsets,
+        "csc_sources": csc_sources,
+        "csr_offsets": csr_offsets,
+        "csr_targets": csr_targets,
+        "csr_edge_perm": csr_edge_perm,
+        "edge_weights": weights,
+    }
+
+
+def graph_hash(g) -> str:
+    """Topology digest (src/graph.py:78-84)."""
+    h = hashlib.sha256()
+    h.update(int(g["num_vertices"]).to_bytes(8, "little"))
+    h.update(np.ascontiguousarray(g["csc_offsets"], dtype="<i8").tobytes())
+    h.update(np.ascontiguousarray(g["csc_sources"], dtype="<i8").tobytes())
+    return h.hexdigest()
+
+
+def _in_degrees(g):
+    return np.diff(g["csc_offsets"])
+
+
+def _dst_of_edges(g):
+    return np.repeat(np.arange(g["num_vertices"], dtype=I64), _in_degrees(g))
+
+
+# ---------------------------------------------------------------------------
+# level-1 partition: seeded LDG + one refinement sweep  (src/partition.py)
+# ---------------------------------------------------------------------------
+
+
+def vertex_cap(V, m, eps):
+    """src/partition.py:123-129."""
+    return max(math.ceil(V / m), math.floor((1.0 + eps) * V / m + 1e-12))
+
+
+def undirected_lists(g):
+    """Per-vertex neighbour multiset from in- and out-edges, self loops
+    dropped (src/partition.py:102-120).  Returned as (offsets, flat)."""
+    V = g["num_vertices"]
+    d_in = _dst_of_edges(g)
+    s_out = np.repeat(np.arange(V, dtype=I64), np.diff(g["csr_offsets"]))
+    ok_in = g["csc_sources"] != d_in
+    ok_out = g["csr_targets"] != s_out
+    owner_of_entry = np.concatenate([d_in[ok_in], s_out[ok_out]])
+    entry = np.concatenate([g["csc_sources"][ok_in], g["csr_targets"][ok_out]])
+    perm = np.argsort(owner_of_entry, kind="stable")
+    counts = np.bincount(owner_of_entry, minlength=V)
+    offs = np.zeros(V + 1, dtype=I64)
+    np.cumsum(counts, out=offs[1:])
+    return offs, entry[perm]
+
+
+def _fill_empty_parts(owner, sizes, adj_deg, m):
+    """Move the lowest-degree vertex of the largest partition into the first
+    empty one until none is empty (src/partition.py:199-209)."""
+    while (sizes == 0).any():
+        empty = int(np.flatnonzero(sizes == 0)[0])
+        donor = int(np.argmax(sizes))
+        cand = np.flatnonzero(owner == donor)
+        v = int(cand[np.argmin(adj_deg[cand])])
+        owner[v] = empty
+        sizes[donor] -= 1
+        sizes[empty] += 1
+
+
+def ldg_partition(g, m, eps=0.1, seed=0):
+    """Streaming linear-deterministic-greedy partition
+    (src/partition.py:132-196).  Returns the int64 owner map."""
+    V = g["num_vertices"]
+    if m < 1 or m > V or eps < 0:
+        raise ValueError("bad partition request")
+    cap = vertex_cap(V, m, eps)
+    offs, adj = undirected_lists(g)
+    adj_deg = np.diff(offs)
+    arrival = np.random.default_rng(seed).permutation(V)
+    owner = np.full(V, -1, dtype=I64)
+    sizes = np.zeros(m, dtype=I64)
+    for v in arrival:
+        near = owner[adj[offs[v]:offs[v + 1]]]
+        hits = np.bincount(near[near >= 0], minlength=m)
+        score = hits * (1.0 - sizes / cap)
+        best, best_key = -1, None
+        for p in range(m):                      # eligible: sizes < cap
+            if sizes[p] >= cap:
+                continue
+            key = (-score[p], sizes[p], p)      # lexsort priority order
+            if best_key is None or key < best_key:
+                best, best_key = p, key
+        owner[v] = best
+        sizes[best] += 1
+    _fill_empty_parts(owner, sizes, adj_deg, m)
+    for v in range(V):                          # refinement, ascending id
+        lo, hi = offs[v], offs[v + 1]
+        if lo == hi:
+            continue
+        cur = int(owner[v])
+        if sizes[cur] <= 1:
+            continue
+        hits = np.bincount(owner[adj[lo:hi]], minlength=m)
+        allowed = (np.arange(m) == cur) | (sizes < cap)
+        masked = np.where(allowed, hits, -1)
+        tgt = int(np.argmax(masked))
+        if tgt != cur and masked[tgt] > hits[cur]:
+            owner[v] = tgt
+            sizes[cur] -= 1
+            sizes[tgt] += 1
+    _fill_empty_parts(owner, sizes, adj_deg, m)
+    return owner
+
+
+def owner_hash(owner) -> str:
+    return hashlib.sha256(np.ascontiguousarray(owner, dtype="<i8").tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# level-2: in-edge balanced chunks                (src/partition.py:235-314)
+# ---------------------------------------------------------------------------
+
+
+def balanced_cuts(indeg, n):
+    """Greedy prefix-sum cut of a degree sequence (src/partition.py:270-293)."""
+    size = int(len(indeg))
+    pre = np.cumsum(indeg)
+    total = int(pre[-1]) if size else 0
+    out, lo = [], 0
+    for c in range(n):
+        if c == n - 1:
+            hi = size
+        else:
+            want = (c + 1) * total / n
+            hi = int(np.searchsorted(pre, want, side="left")) + 1
+            hi = min(max(hi, lo + 1), size - (n - c - 1))
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def chunk_of(g, verts, pid=0, cid=0):
+    """In-edge subgraph of a destination set (src/partition.py:235-267)."""
+    verts = np.asarray(verts, dtype=I64)
+    starts = g["csc_offsets"][verts]
+    deg = g["csc_offsets"][verts + 1] - starts
+    total = int(deg.sum())
+    base = np.repeat(starts - np.concatenate([[0], np.cumsum(deg)[:-1]]), deg)
+    epos = base + np.arange(total, dtype=I64)
+    src_glob = g["csc_sources"][epos]
+    w = g["edge_weights"][epos]
+    dl = np.repeat(np.arange(verts.size, dtype=I64), deg)
+    nbr = np.unique(src_glob)
+    sl = np.searchsorted(nbr, src_glob).astype(I64)
+    csc_offsets = np.zeros(verts.size + 1, dtype=I64)
+    np.cumsum(deg, out=csc_offsets[1:])
+    perm = np.argsort(sl * max(1, verts.size) + dl, kind="stable").astype(I64)
+    csr_offsets = np.zeros(nbr.size + 1, dtype=I64)
+    np.cumsum(np.bincount(sl, minlength=nbr.size), out=csr_offsets[1:])
+    return {
+        "partition_id": pid, "chunk_id": cid,
+        "vertices": verts, "sources": nbr,
+        "csc_offsets": csc_offsets, "csc_local_src": sl, "edge_weights": w,
+        "csr_offsets": csr_offsets, "csr_local_dst": dl[perm],
+        "csr_edge_perm": perm,
+    }
+
+
+def chunk_grid(g, owner, m, n):
+    """split_chunks (src/partition.py:296-314): grid[i][j]."""
+    indeg = _in_degrees(g)
+    grid = []
+    for i in range(m):
+        mine = np.flatnonzero(owner == i).astype(I64)
+        grid.append([chunk_of(g, mine[a:b], i, j)
+                     for j, (a, b) in enumerate(balanced_cuts(indeg[mine], n))])
+    return grid
+
+
+# ---------------------------------------------------------------------------
+# dedup communication plan                        (src/planner.py:132-371)
+# ---------------------------------------------------------------------------
+
+
+def _sorted_unique(a):
+    return np.unique(np.asarray(a, dtype=I64))
+
+
+def _isect(a, b):
+    return np.intersect1d(a, b, assume_unique=True) if a.size and b.size else _NONE.copy()
+
+
+def _minus(a, b):
+    return np.setdiff1d(a, b, assume_unique=True) if a.size and b.size else a.copy()
+
+
+def dedup_plan(neighbor_sets, owner, dest_sets=None):
+    """All plan sets and the slot layout (src/planner.py:132-315).
+
+    Returns a dict of nested lists: N[i][j], U[j], T[i][j], carry[i][j],
+    load[i][j], fetch[i][j][k] (k != i, ascending), nbr_carry[i][j],
+    live[i][j], slots[i][j] (aligned with live), caps[i], volumes."""
+    owner = np.asarray(owner, dtype=I64)
+    N = [[_sorted_unique(s) for s in row] for row in neighbor_sets]
+    m, n = len(N), len(N[0])
+    U = [_sorted_unique(np.concatenate([N[i][j] for i in range(m)] + [_NONE]))
+         for j in range(n)]
+    T = [[U[j][owner[U[j]] == i] for j in range(n)] for i in range(m)]
+    carry = [[_NONE.copy() if j == 0 else _isect(T[i][j], T[i][j - 1])
+              for j in range(n)] for i in range(m)]
+    load = [[T[i][j].copy() if j == 0 else _minus(T[i][j], T[i][j - 1])
+             for j in range(n)] for i in range(m)]
+    fetch = [[{k: N[i][j][owner[N[i][j]] == k] for k in range(m) if k != i}
+              for j in range(n)] for i in range(m)]
+    nbr_carry = [[_NONE.copy() if j == 0 else _isect(N[i][j], N[i][j - 1])
+                  for j in range(n)] for i in range(m)]
+    # stable slot layout, restated as rank/select: rows carried from the
+    # previous batch keep their slot; new rows (ascending id) take the free
+    # slots in ascending order, then fresh slots (src/planner.py:252-284)
+    live, slots, caps = [], [], []
+    for i in range(m):
+        live_i, slots_i = [], []
+        prev_live, prev_slot, top = _NONE, _NONE, 0
+        for j in range(n):
+            cur = _sorted_unique(np.concatenate([T[i][j], N[i][j]]))
+            s = np.full(cur.size, -1, dtype=I64)
+            kept = np.isin(cur, prev_live, assume_unique=True)
+            s[kept] = prev_slot[np.searchsorted(prev_live, cur[kept])]
+            held = np.zeros(top, dtype=bool)
+            held[s[kept]] = True
+            free = np.flatnonzero(~held)
+            fresh = int((~kept).sum())
+            take = np.concatenate([free[:fresh],
+                                   top + np.arange(max(0, fresh - free.size))])
+            s[~kept] = take.astype(I64)
+            top = max(top, int(s.max()) + 1 if s.size else 0)
+            live_i.append(cur)
+            slots_i.append(s)
+            prev_live, prev_slot = cur, s
+        live.append(live_i)
+        slots.append(slots_i)
+        caps.append(top)
+    v_ori = sum(int(N[i][j].size) for i in range(m) for j in range(n))
+    v_p2p = sum(int(u.size) for u in U)
+    v_ru = int(U[0].size) + sum(int(_minus(U[j], U[j - 1]).size) for j in range(1, n))
+    dests = None if dest_sets is None else [[_sorted_unique(s) for s in row] for row in dest_sets]
+    return {
+        "m": m, "n": n, "owner": owner, "N": N, "U": U, "T": T,
+        "carry": carry, "load": load, "fetch": fetch, "nbr_carry": nbr_carry,
+        "live": live, "slots": slots, "caps": caps,
+        "volumes": (v_ori, v_p2p, v_ru), "dest": dests,
+    }
+
+
+def plan_of_grid(grid, owner):
+    """plan_for_partition (src/planner.py:318-319)."""
+    return dedup_plan([[c["sources"] for c in row] for row in grid], owner,
+                      [[c["vertices"] for c in row] for row in grid])
+
+
+def transfer_cost(volumes, t_hd=25.0, t_dd=200.0, t_ru=1300.0):
+    """Eq. 4 (src/planner.py:230-244)."""
+    v_ori, v_p2p, v_ru = volumes
+    return v_ru / t_hd + (v_ori - v_p2p) / t_dd + (v_p2p - v_ru) / t_ru
+
+
+def expected_rows(plan, mode):
+    """Per-layer row counts per mode (src/planner.py:329-371)."""
+    m, n = plan["m"], plan["n"]
+    out = dict(fwd_h2d_rows=0, fwd_d2d_rows=0, fwd_reuse_rows=0,
+               bwd_d2h_rows=0, bwd_d2d_rows=0, peak_slots=[])
+    for i in range(m):
+        peak = 0
+        for j in range(n):
+            nn = int(plan["N"][i][j].size)
+            if mode == "baseline":
+                out["fwd_h2d_rows"] += nn
+                out["bwd_d2h_rows"] += nn
+                peak = max(peak, nn)
+                continue
+            peak = max(peak, int(plan["live"][i][j].size))
+            fsz = [int(f.size) for f in plan["fetch"][i][j].values()]
+            if mode == "p2p":
+                t = int(plan["T"][i][j].size)
+                out["fwd_h2d_rows"] += t
+                out["bwd_d2h_rows"] += t
+                out["fwd_d2d_rows"] += sum(fsz)
+            else:
+                ld = int(plan["load"][i][j].size)
+                out["fwd_h2d_rows"] += ld
+                out["bwd_d2h_rows"] += ld
+                out["fwd_reuse_rows"] += int(plan["carry"][i][j].size)
+                out["fwd_d2d_rows"] += sum(int(_minus(f, plan["nbr_carry"][i][j]).size)
+                                           for f in plan["fetch"][i][j].values())
+            out["bwd_d2d_rows"] += sum(fsz)
+        out["peak_slots"].append(peak)
+    return out
+
+
+def reorganize_grid(grid, move_all_rows=True):
+    """Alg. 4 two-phase greedy reordering (src/planner.py:386-450).
+    Returns (new_grid, chunk_orders, batch_order)."""
+    m, n = len(grid), len(grid[0])
+    N = [[_sorted_unique(c["sources"]) for c in row] for row in grid]
+    orders = [list(range(n))]
+    acc = [N[0][j].copy() for j in range(n)]
+    for i in range(1, m):
+        left = list(range(n))
+        order = []
+        for j in range(n):
+            scores = [int(_isect(N[i][k], acc[j]).size) for k in left]
+            k = left[int(np.argmax(scores))]     # first maximum
+            order.append(k)
+            left.remove(k)
+            acc[j] = _sorted_unique(np.concatenate([acc[j], N[i][k]]))
+        orders.append(order)
+    batch = [0]
+    left = list(range(1, n))
+    while left:
+        scores = [int(_isect(acc[k], acc[batch[-1]]).size) for k in left]
+        k = left[int(np.argmax(scores))]
+        batch.append(k)
+        left.remove(k)
+    new_grid, new_orders = [], []
+    for i in range(m):
+        if i == 0 and not move_all_rows:
+            new_orders.append(list(orders[0]))
+        else:
+            new_orders.append([orders[i][b] for b in batch])
+        new_grid.append([grid[i][c] for c in new_orders[i]])
+    return new_grid, new_orders, batch
+
+
+# ---------------------------------------------------------------------------
+# model init                                          (src/engine.py:72-99)
+# ---------------------------------------------------------------------------
+
+
+def glorot_weights(dims, seed, dtype=np.float64, gat=False):
+    gen = np.random.default_rng(seed)
+    ws, attn = [], []
+    for a, b in zip(dims[:-1], dims[1:]):
+        lim = math.sqrt(6.0 / (a + b))
+        ws.append(gen.uniform(-lim, lim, size=(a, b)).astype(dtype))
+        if gat:
+            la = math.sqrt(6.0 / (2 * b + 1))
+            attn.append(gen.uniform(-la, la, size=2 * b).astype(dtype))
+    return (ws, attn) if gat else ws
+
+
+# ---------------------------------------------------------------------------
+# GCN chunk kernels                                  (src/engine.py:128-171)
+# ---------------------------------------------------------------------------
+
+
+def seq_aggregate(offsets, idx, w, rows, out_rows):
+    """out[v] = sum over segment v of w_e * rows[idx_e], accumulated strictly
+    left to right with a separate rounding of each product (the np.add.at
+    semantics of src/engine.py:139).  Vectorised over segments by rank."""
+    dt = rows.dtype
+    out = np.zeros((out_rows, rows.shape[1]), dtype=dt)
+    deg = np.diff(offsets)
+    if deg.size == 0 or int(deg.max(initial=0)) == 0:
+        return out
+    w = w.astype(dt, copy=False)
+    for r in range(int(deg.max())):
+        seg = np.flatnonzero(deg > r)
+        e = offsets[seg] + r
+        prod = w[e][:, None] * rows[idx[e]]
+        out[seg] = out[seg] + prod
+    return out
+
+
+def gcn_chunk_forward(chunk, h_nbr, W):
+    """(h_out, agg, z) of one chunk (src/engine.py:128-142)."""
+    agg = seq_aggregate(chunk["csc_offsets"], chunk["csc_local_src"],
+                        chunk["edge_weights"], h_nbr, chunk["vertices"].size)
+    z = agg @ W
+    return np.maximum(z, 0), agg, z
+
+
+def gcn_chunk_backward(chunk, agg, grad_out, W):
+    """Hybrid backward from the agg checkpoint (src/engine.py:145-171).
+    The transposed aggregation sums each source's out-edges sequentially in
+    CSR order (the reference's reduceat association differs at rounding)."""
+    z = agg @ W
+    gz = grad_out * (z > 0)
+    gW = agg.T @ gz
+    gagg = gz @ W.T
+    perm = chunk["csr_edge_perm"]
+    gnbr = seq_aggregate(chunk["csr_offsets"], chunk["csr_local_dst"],
+                         chunk["edge_weights"][perm], gagg, chunk["sources"].size)
+    return gnbr, gW
+
+
+def softmax_xent(h_last, labels, mask):
+    """Masked mean softmax cross-entropy and its gradient
+    (src/engine.py:297-320)."""
+    mask = np.asarray(mask, dtype=bool)
+    g = np.zeros_like(h_last)
+    cnt = int(mask.sum())
+    if cnt == 0:
+        return 0.0, g
+    zz = h_last[mask]
+    yy = np.asarray(labels, dtype=I64)[mask]
+    zz = zz - zz.max(axis=1, keepdims=True)
+    ez = np.exp(zz)
+    p = ez / ez.sum(axis=1, keepdims=True)
+    rows = np.arange(cnt)
+    loss = float(-np.log(p[rows, yy]).mean())
+    p[rows, yy] -= 1
+    g[mask] = p / cnt
+    return loss, g
+
+
+# ---------------------------------------------------------------------------
+# partitioned epoch with the fleet's transfer semantics
+#            (src/engine.py:387-480, src/devices.py:44-488)
+# ---------------------------------------------------------------------------
+
+METER_KEYS = ("h2d_rows", "d2h_rows", "d2d_rows", "reuse_rows", "dest_h2d_rows",
+              "dest_d2h_rows", "chkpt_h2d_rows", "chkpt_d2h_rows", "h2d_bytes",
+              "d2h_bytes", "d2d_bytes", "dest_bytes", "chkpt_bytes")
+
+
+def partitioned_epoch(grid, plan, weights, X, labels, mask, *, lr=0.1,
+                      mode="full", flush_policy="on_eviction", dtype=np.float32):
+    """One GCN epoch over the chunk grid.  Values follow the reference's
+    accumulation order per mode; meters follow the fleet's counting rules.
+
+    Returns dict(loss, weights (updated copies), grads (summed over
+    devices), h, grad_h, agg, meters (per device), peaks)."""
+    dt = np.dtype(dtype)
+    m, n = plan["m"], plan["n"]
+    V = X.shape[0]
+    L = len(weights)
+    dims = [weights[0].shape[0]] + [w.shape[1] for w in weights]
+    W = [np.asarray(w, dtype=dt) for w in weights]
+    item = dt.itemsize
+    meters = [dict.fromkeys(METER_KEYS, 0) for _ in range(m)]
+    peaks = [0] * m
+    h = [np.zeros((V, d), dtype=dt) for d in dims]
+    gh = [np.zeros((V, d), dtype=dt) for d in dims]
+    h[0][:] = np.asarray(X, dtype=dt)
+    agg_store = {}
+
+    def nbr_live(i, j):
+        return int(plan["N"][i][j].size if mode == "baseline" else plan["live"][i][j].size)
+
+    # ---- forward: Alg. 1 lines 4-9 ----
+    for l in range(L):
+        rb = dims[l] * item
+        agg_store[l] = np.zeros((V, dims[l]), dtype=dt)
+        for j in range(n):
+            for i in range(m):
+                mt = meters[i]
+                if mode == "baseline":
+                    rows = int(plan["N"][i][j].size)
+                else:
+                    rows = int((plan["load"] if mode == "full" else plan["T"])[i][j].size)
+                    if mode == "full":
+                        mt["reuse_rows"] += int(plan["carry"][i][j].size)
+                    for k, f in plan["fetch"][i][j].items():
+                        ff = _minus(f, plan["nbr_carry"][i][j]) if mode == "full" else f
+                        mt["d2d_rows"] += int(ff.size)
+                        mt["d2d_bytes"] += int(ff.size) * rb
+                mt["h2d_rows"] += rows
+                mt["h2d_bytes"] += rows * rb
+                peaks[i] = max(peaks[i], nbr_live(i, j))
+            for i in range(m):
+                c = grid[i][j]
+                out, agg, _ = gcn_chunk_forward(c, h[l][c["sources"]], W[l])
+                h[l + 1][c["vertices"]] = out
+                agg_store[l][c["vertices"]] = agg
+                nv = int(c["vertices"].size)
+                meters[i]["dest_d2h_rows"] += nv
+                meters[i]["dest_bytes"] += nv * dims[l + 1] * item
+                meters[i]["chkpt_d2h_rows"] += nv
+                meters[i]["chkpt_bytes"] += nv * rb
+    loss, g_last = softmax_xent(h[L], labels, mask)
+    gh[L][:] = g_last
+
+    # ---- backward: Alg. 1 lines 12-20 ----
+    gW = [[np.zeros_like(w) for w in W] for _ in range(m)]
+    for l in reversed(range(L)):
+        rb = dims[l] * item
+        acc = [np.zeros((V, dims[l]), dtype=dt) for _ in range(m)]   # owner buffers
+        for j in range(n):
+            views = []
+            for i in range(m):
+                c = grid[i][j]
+                nv = int(c["vertices"].size)
+                meters[i]["chkpt_h2d_rows"] += nv
+                meters[i]["chkpt_bytes"] += nv * rb
+                meters[i]["dest_h2d_rows"] += nv
+                meters[i]["dest_bytes"] += nv * dims[l + 1] * item
+                gn, gw = gcn_chunk_backward(c, agg_store[l][c["vertices"]],
+                                            gh[l + 1][c["vertices"]], W[l])
+                gW[i][l] += gw
+                views.append(gn)
+            if mode == "baseline":
+                for i in range(m):
+                    nb = plan["N"][i][j]
+                    if nb.size:
+                        gh[l][nb] += views[i]
+                    meters[i]["d2h_rows"] += int(nb.size)
+                    meters[i]["d2h_bytes"] += int(nb.size) * rb
+                    peaks[i] = max(peaks[i], int(nb.size))
+                continue
+            for k in range(m):                       # owner k, sources ascending
+                for i in range(m):
+                    if i == k:
+                        rows = _isect(plan["N"][k][j], plan["T"][k][j])
+                    else:
+                        rows = plan["fetch"][i][j][k]
+                    if rows.size == 0:
+                        continue
+                    pos = np.searchsorted(plan["N"][i][j], rows)
+                    acc[k][rows] = acc[k][rows] + views[i][pos]
+                    if i != k:
+                        meters[i]["d2d_rows"] += int(rows.size)
+                        meters[i]["d2d_bytes"] += int(rows.size) * rb
+            for k in range(m):
+                peaks[k] = max(peaks[k], int(plan["live"][k][j].size))
+                mine = plan["T"][k][j]
+                if mode == "p2p" or flush_policy == "every_batch" or j + 1 == n:
+                    fl = mine
+                else:
+                    fl = _minus(mine, plan["T"][k][j + 1])
+                if fl.size:
+                    gh[l][fl] = gh[l][fl] + acc[k][fl]
+                    acc[k][fl] = 0
+                meters[k]["d2h_rows"] += int(fl.size)
+                meters[k]["d2h_bytes"] += int(fl.size) * rb
+
+    grads = []
+    newW = []
+    for l in range(L):
+        tot = np.zeros_like(W[l])
+        for i in range(m):          # ascending device id (src/engine.py:334-338)
+            tot += gW[i][l]
+        grads.append(tot)
+        newW.append(W[l] - np.asarray(lr, dtype=dt) * tot if dt == np.float32 else W[l] - lr * tot)
+    return {"loss": loss, "weights": newW, "grads": grads, "h": h, "grad_h": gh,
+            "agg": agg_store, "meters": meters, "peaks": peaks}
+
+
+# ---------------------------------------------------------------------------
+# monolithic fp64 store-all epoch                 (src/reference.py:126-159)
+# ---------------------------------------------------------------------------
+
+
+def monolithic_epoch(g, weights, X, labels, mask, lr=0.1):
+    """Whole-graph fp64 GCN epoch; returns (loss, new_weights, grads)."""
+    L = len(weights)
+    W = [np.asarray(w, dtype=np.float64) for w in weights]
+    dst = _dst_of_edges(g)
+    src = g["csc_sources"]
+    w = g["edge_weights"]
+    hs = [np.asarray(X, dtype=np.float64)]
+    saved = []
+    for l in range(L):
+        agg = np.zeros((g["num_vertices"], hs[l].shape[1]))
+        np.add.at(agg, dst, w[:, None] * hs[l][src])
+        z = agg @ W[l]
+        saved.append((agg, z))
+        hs.append(np.maximum(z, 0.0))
+    # logsumexp form of the loss (src/reference.py:27-42)
+    mask = np.asarray(mask, dtype=bool)
+    cnt = int(mask.sum())
+    grad = np.zeros_like(hs[L])
+    loss = 0.0
+    if cnt:
+        zz = hs[L][mask]
+        yy = np.asarray(labels, dtype=I64)[mask]
+        mx = zz.max(axis=1)
+        lse = mx + np.log(np.exp(zz - mx[:, None]).sum(axis=1))
+        loss = float((lse - zz[np.arange(cnt), yy]).mean())
+        p = np.exp(zz - lse[:, None])
+        p[np.arange(cnt), yy] -= 1.0
+        grad[mask] = p / cnt
+    grads = [None] * L
+    for l in reversed(range(L)):
+        agg, z = saved[l]
+        gz = grad * (z > 0.0)
+        grads[l] = agg.T @ gz
+        ga = gz @ W[l].T
+        grad = np.zeros((g["num_vertices"], W[l].shape[0]))
+        np.add.at(grad, src, w[:, None] * ga[dst])
+    return loss, [W[l] - lr * grads[l] for l in range(L)], grads
+
+
+def rel_err(a, b):
+    """Max-normalised relative error, the metric of the reference's tests
+    (tests/test_engine.py:122-124, src/cli.py:343-353)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    den = max(float(np.abs(b).max(initial=0.0)), 1e-300)
+    return float(np.abs(a - b).max(initial=0.0)) / den
