@@ -1,0 +1,195 @@
+/*
+ * hongtu_b200.h - C ABI of the B200-native HongTu GCN epoch path.
+ *
+ * The reference (`chunktrain`, /root/reference/pkg/src/chunktrain) is pure
+ * Python/numpy and has no FFI of its own; every entry point below replaces
+ * one Python-level operation of the reference and cites it (file:line,
+ * relative to /root/reference/pkg/src/chunktrain/).  The Python package
+ * `paper_2311_14898_b200` binds these with ctypes.
+ *
+ * Conventions
+ *   - every function returns 0 on success, a negative HT_E* code on error;
+ *     ht_last_error() returns the thread-local message of the last failure;
+ *   - all buffers are plain pointers + int64 sizes; the caller owns every
+ *     host array.  "Host" arrays passed to device operations must be pinned
+ *     (ht_host_alloc or ht_host_register) or device-resident;
+ *   - vertex ids, set members and index arrays are int64; edge weights are
+ *     float64 on input (as the reference stores them, graph.py:141-150) and
+ *     converted once to float32 for the device path;
+ *   - integer preprocessing (graph build, LDG, chunks, plan sets, slots,
+ *     reorganization) runs natively on the host CPU and is bit-exact with
+ *     the reference.
+ */
+#ifndef HONGTU_B200_H
+#define HONGTU_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HT_OK 0
+#define HT_EINVAL (-1)     /* bad argument (maps to SimulationError/PlanError) */
+#define HT_ECUDA (-2)      /* CUDA runtime failure                            */
+#define HT_ESTATE (-3)     /* call out of sequence (SimulationError)         */
+#define HT_ELIVE (-4)      /* row outside the live set (devices.py:177-187)   */
+#define HT_ENOMEM (-5)
+
+typedef struct ht_fleet ht_fleet; /* opaque: m virtual devices + uploaded plan */
+
+/* ---- library / runtime -------------------------------------------------- */
+const char* ht_last_error(void);
+int ht_version(void);
+int ht_device_count(int* count);
+
+/* Pinned, portable, mapped host memory (HostStore backing, devices.py:47-57). */
+int ht_host_alloc(int64_t bytes, void** out);
+int ht_host_free(void* p);
+int ht_host_register(void* p, int64_t bytes);
+int ht_host_unregister(void* p);
+/* Device-resident "host store" arrays for the HBM-resident (HongTu-IM) variant. */
+int ht_dev_alloc(int device, int64_t bytes, void** out);
+int ht_dev_free(int device, void* p);
+int ht_memcpy(void* dst, const void* src, int64_t bytes); /* any direction, synchronous */
+int ht_memset(void* dst, int value, int64_t bytes);
+
+/* ---- integer preprocessing (host CPU, bit-exact) ----------------------- */
+
+/* graph.py:91-150 from_edges + gcn_edge_weights: canonical CSC by
+ * (dst, src), CSR by (src, dst), csr_edge_perm, float64 weights. */
+int ht_build_graph(const int64_t* src, const int64_t* dst, int64_t E, int64_t V,
+                   int64_t* csc_offsets, int64_t* csc_sources, int64_t* csr_offsets,
+                   int64_t* csr_targets, int64_t* csr_edge_perm, double* weights);
+
+/* synth.py:154-157 parallel-edge removal: indices (into src/dst) of the
+ * first occurrence of each distinct (dst, src) pair, ascending by (dst, src),
+ * i.e. np.unique(dst*V + src, return_index=True)[1].  keep holds E entries. */
+int ht_dedup_edges(const int64_t* src, const int64_t* dst, int64_t E, int64_t V,
+                   int64_t* keep, int64_t* n_keep);
+
+/* partition.py:132-196 partition_vertices (LDG + one refinement sweep +
+ * _repair_empty).  `arrival` is numpy default_rng(seed).permutation(V). */
+int ht_ldg_partition(int64_t V, const int64_t* csc_offsets, const int64_t* csc_sources,
+                     const int64_t* csr_offsets, const int64_t* csr_targets,
+                     const int64_t* arrival, int64_t m, int64_t cap, int64_t* owner);
+
+/* partition.py:235-267 chunk_from_vertices.  The caller sizes the edge
+ * arrays with n_edges = sum of in-degrees of verts and `sources` with
+ * n_edges entries (upper bound); *n_sources returns |N_ij|, and csr_off
+ * must hold n_edges + 1 entries (only the first n_sources + 1 are used). */
+int ht_chunk_fill(const int64_t* csc_offsets, const int64_t* csc_sources,
+                  const double* weights, const int64_t* verts, int64_t nv,
+                  int64_t* sources, int64_t* n_sources, int64_t* csc_off,
+                  int64_t* csc_local_src, double* edge_w, int64_t* csr_off,
+                  int64_t* csr_local_dst, int64_t* csr_perm);
+
+/* Sorted-set algebra of planner.py:45-63 (inputs sorted unique int64).
+ * op: 0 = intersect, 1 = difference (a \ b), 2 = union.  Returns the
+ * output size through *n_out; out must hold |a|+|b| for union, |a| else. */
+int ht_set_op(int op, const int64_t* a, int64_t na, const int64_t* b, int64_t nb,
+              int64_t* out, int64_t* n_out);
+int64_t ht_intersect_count(const int64_t* a, int64_t na, const int64_t* b, int64_t nb);
+
+/* planner.py:252-284 build_buffer_layout for one device: given the n live
+ * sets (sorted, concatenated with offsets), produce the slot of every live
+ * row (aligned) and the capacity. */
+int ht_slot_layout(int64_t n, const int64_t* live_concat, const int64_t* live_offsets,
+                   int64_t* slots_concat, int64_t* capacity);
+
+/* planner.py:386-450 reorganize (Alg. 4); nbr_concat/nbr_offsets hold the
+ * m*n neighbour sets row-major [i][j].  Outputs chunk_orders (m*n, row-major
+ * [i][pos]) and batch_order (n). */
+int ht_reorganize(int64_t m, int64_t n, const int64_t* nbr_concat, const int64_t* nbr_offsets,
+                  int move_all_rows, int64_t* chunk_orders, int64_t* batch_order);
+
+/* ---- fleet: m virtual devices executing one DedupPlan (devices.py) ----- */
+
+#define HT_MODE_BASELINE 0
+#define HT_MODE_P2P 1
+#define HT_MODE_FULL 2
+#define HT_FLUSH_ON_EVICTION 0
+#define HT_FLUSH_EVERY_BATCH 1
+
+/* DeviceFleet.__init__ (devices.py:132-171).  ordinals[i] = CUDA device of
+ * virtual device i (several virtual devices may share one GPU). */
+int ht_fleet_create(int m, int n, const int* ordinals, int mode, int flush_policy,
+                    ht_fleet** out);
+int ht_fleet_destroy(ht_fleet* f);
+
+/* Plan sets of chunk (i, j) (planner.py:105-124).  live/slots aligned. */
+int ht_fleet_set_sets(ht_fleet* f, int i, int j,
+                      const int64_t* nbr, int64_t n_nbr,
+                      const int64_t* owned, int64_t n_owned,
+                      const int64_t* load, int64_t n_load,
+                      const int64_t* nbr_carry, int64_t n_nbr_carry,
+                      const int64_t* live, const int64_t* slots, int64_t n_live,
+                      const int64_t* dest, int64_t n_dest /* -1: none */);
+int ht_fleet_set_fetch(ht_fleet* f, int i, int j, int k, const int64_t* rows, int64_t n);
+/* Chunk structure (partition.py:44-78) for the layer kernels. */
+int ht_fleet_set_chunk(ht_fleet* f, int i, int j, int64_t nv, int64_t nn, int64_t ne,
+                       const int64_t* csc_off, const int64_t* csc_local_src,
+                       const double* edge_w, const int64_t* csr_off,
+                       const int64_t* csr_local_dst, const int64_t* csr_perm);
+/* Derive and upload every device index list (slot-translated CSC, copy
+ * lists, push/flush lists).  Fails with HT_ELIVE if a set row is outside
+ * its live set. */
+int ht_fleet_finalize(ht_fleet* f);
+int ht_fleet_capacity(ht_fleet* f, int i, int64_t* cap);
+
+/* begin_forward_layer / begin_backward_layer (devices.py:193-207). */
+int ht_begin_layer(ht_fleet* f, int dim, int elem_size, int backward);
+
+/* dedup_comm_fwd (devices.py:223-278): stage batch rows (host loads,
+ * barrier, staggered peer fetches, barrier) and copy each device's
+ * N_ij view into views_out (concatenated over i). */
+int ht_comm_fwd(ht_fleet* f, int batch, const void* host_rows, void* views_out);
+/* dedup_comm_bwd (devices.py:284-341): push views (concatenated over i) to
+ * owners in ascending source order, then flush per policy into host_grad. */
+int ht_comm_bwd(ht_fleet* f, int batch, const void* views_in, void* host_grad);
+/* load_dest_rows / store_dest_rows / add_dest_grads (devices.py:355-385):
+ * op 0 load (host -> rows), 1 store (rows -> host), 2 add (host += rows). */
+int ht_dest_rows(ht_fleet* f, int op, int batch, int dim, int elem_size,
+                 void* host_rows, void* rows_concat);
+
+/* ---- GCN epoch kernels (engine.py:387-480) ----------------------------- */
+
+#define HT_PREC_FP32 0   /* SIMT FP32 GEMMs: FP32 validation mode (1e-5)      */
+#define HT_PREC_TF32 1   /* tcgen05 TF32, 3xTF32 for z = agg.W (1e-3)         */
+
+/* Zero the per-device weight-gradient accumulators (engine.py:441-448). */
+int ht_epoch_begin(ht_fleet* f, int L, const int* dims);
+/* One forward layer over all batches (engine.py:409-434): dedup comm,
+ * CSC aggregation, z = agg.W, ReLU, dest-row + checkpoint stores. */
+int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
+                     const void* h_in, void* h_out, void* agg_out, int precision);
+/* downstream_loss (engine.py:297-320) on the last layer's device-resident
+ * output; writes grad rows to grad_out (host.grad_h[L]).  count = mask.sum(). */
+int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uint8_t* mask,
+            int64_t V, int64_t count, void* grad_out, double* loss);
+/* One backward layer over all batches (engine.py:449-477): checkpoint and
+ * dest-gradient reload, hybrid backward, transposed aggregation, owner push
+ * and flush into grad_in (host.grad_h[layer]). */
+int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
+                      const void* agg_in, const void* grad_out, void* grad_in,
+                      int precision);
+/* sync_and_update (engine.py:328-344): sum the device gradients in
+ * ascending device order, W -= lr * sum (in place on the host arrays);
+ * grads_out (may be NULL) receives the summed gradients. */
+int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, float lr,
+           float* const* grads_out);
+int ht_fleet_sync(ht_fleet* f);
+
+/* ---- timing of the dominant kernels (bench roofline) ------------------- */
+/* Enables CUDA-event timing of the aggregation kernels; ht_kernel_stats
+ * returns launches, summed milliseconds and summed algorithmic bytes of
+ * kernel class `which` (0 = forward CSC aggregation, 1 = backward CSR
+ * aggregation, 2 = GEMMs, 3 = host transfers) since the last reset. */
+int ht_set_timing(ht_fleet* f, int enabled);
+int ht_kernel_stats(ht_fleet* f, int which, int64_t* launches, double* ms, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1092 @@
+// Fleet runtime: m virtual devices executing one DedupPlan, and the GCN
+// epoch layer drivers (devices.py / engine.py of the reference, re-designed
+// for B200: slot buffers in HBM, zero-copy pinned host rows, peer-pointer
+// fetches, per-device streams with event barriers at the Alg. 2/3 sync
+// points).
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <vector>
+
+#include "ht_common.h"
+#include "ht_kernels.cuh"
+#include "ht_tc.cuh"
+
+using ht::fail;
+
+#define CU(expr)                                                                    \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return fail(HT_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), \
+                  __FILE__, __LINE__);                                              \
+  } while (0)
+
+namespace {
+
+constexpr int64_t kSplit = 4096;   // long-segment piece length (edges)
+constexpr int kThreads = 256;
+
+// Grow-only device allocation.
+struct DBuf {
+  void* p = nullptr;
+  int64_t bytes = 0;
+  int dev = 0;
+  int ensure(int64_t want) {
+    if (want <= bytes) return HT_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    if (want <= 0) return HT_OK;
+    CU(cudaMalloc(&p, want));
+    bytes = want;
+    return HT_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+template <class T>
+int upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
+  HT_TRY(b.ensure((int64_t)(v.size() * sizeof(T))));
+  if (!v.empty()) CU(cudaMemcpyAsync(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+  return HT_OK;
+}
+
+struct CopyList {
+  int64_t n = 0;
+  DBuf src, dst, flag;  // int64 src rows, int64 dst rows, uint8 flags
+};
+
+// Host-side plan sets of one chunk (i, j)
+struct HostSets {
+  std::vector<int64_t> nbr, owned, load, nbr_carry, live, slots, dest;
+  bool has_dest = false;
+  std::vector<std::vector<int64_t>> fetch;  // [k]
+  // chunk structure
+  bool has_chunk = false;
+  int64_t nv = 0, nn = 0, ne = 0;
+  std::vector<int64_t> csc_off, csc_src, csr_off, csr_dst, csr_perm;
+  std::vector<double> w;
+};
+
+struct DevChunk {
+  int64_t nv = 0, nn = 0, ne = 0, nlive = 0;
+  DBuf nbr_slot;   // int64 [nn]
+  DBuf dest_rows;  // int64 [nv]
+  CopyList h2d;    // host row -> slot
+  std::vector<CopyList> d2d;   // [step 1..m-1] peer slot -> own slot
+  std::vector<CopyList> push;  // [source device i] pos in N_ij(i) -> own slot (owner = this device)
+  CopyList flush;              // slot -> host row (+first flag)
+  CopyList base_bwd;           // baseline: pos -> host row
+  // graph
+  DBuf csc_off, csc_slot, csc_w;     // int64 [nv+1], int32 [ne], float [ne]
+  DBuf csr_off, csr_dst, csr_w;      // int64 [nn+1], int32 [ne], float [ne]
+  int64_t fw_np = 0, fw_nf = 0, bw_np = 0, bw_nf = 0;
+  DBuf fw_lo, fw_hi, fw_seg, fw_first, fw_cnt;  // long-segment pieces (forward)
+  DBuf bw_lo, bw_hi, bw_seg, bw_first, bw_cnt;  // (backward)
+};
+
+struct TimerRec {
+  cudaEvent_t a, b;
+  int which;
+  double bytes;
+};
+
+struct Device {
+  int ordinal = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev = nullptr;
+  int64_t cap = 0;
+  DBuf value, grad;                    // cap x dim slot buffers
+  DBuf sa, sb, sc, sd, se, partial;    // staging
+  DBuf gemm_ws;
+  DBuf W;                              // current layer weights
+  std::vector<DBuf> gW;                // per-layer weight-gradient accumulators
+  DBuf hL;                             // last-layer outputs (concat over batches)
+  std::vector<int64_t> hL_off;         // row offset of batch j inside hL
+  DBuf labels, mask, loss_part;
+  std::vector<DevChunk> chunks;
+};
+
+}  // namespace
+
+struct ht_fleet {
+  int m = 0, n = 0, mode = HT_MODE_FULL, flush = HT_FLUSH_ON_EVICTION;
+  std::vector<Device> dev;
+  std::vector<std::vector<HostSets>> sets;  // [i][j]
+  bool finalized = false;
+  int dim = 0, elem = 4;
+  int hL_dim = 0;
+  bool timing = false;
+  std::vector<TimerRec> timers;
+  int64_t t_launch[4] = {0, 0, 0, 0};
+  double t_ms[4] = {0, 0, 0, 0}, t_bytes[4] = {0, 0, 0, 0};
+  int L = 0;
+  std::vector<int> dims;
+};
+
+namespace {
+
+int set_dev(const Device& d) {
+  CU(cudaSetDevice(d.ordinal));
+  return HT_OK;
+}
+
+// all-to-all event barrier across the per-device streams
+int barrier(ht_fleet* f) {
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    CU(cudaEventRecord(d.ev, d.stream));
+  }
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    for (auto& o : f->dev)
+      if (&o != &d) CU(cudaStreamWaitEvent(d.stream, o.ev, 0));
+  }
+  return HT_OK;
+}
+
+int sync_all(ht_fleet* f) {
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    CU(cudaStreamSynchronize(d.stream));
+  }
+  return HT_OK;
+}
+
+int grid_for(int64_t warps_needed) {
+  int64_t blocks = (warps_needed * 32 + kThreads - 1) / kThreads;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
+  return (int)blocks;
+}
+
+// pinned host / device pointer -> device-usable pointer
+int dev_ptr(const void* p, void** out) {
+  if (!p) { *out = nullptr; return HT_OK; }
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HT_EINVAL, "array at %p is not pinned or device memory", p);
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) {
+    *out = const_cast<void*>(p);
+    return HT_OK;
+  }
+  if (a.type == cudaMemoryTypeHost) {
+    *out = a.devicePointer ? a.devicePointer : const_cast<void*>(p);
+    return HT_OK;
+  }
+  return fail(HT_EINVAL, "array at %p is pageable host memory; pin it first", p);
+}
+
+// Row copy with the widest vector the row size and alignment permit.
+int launch_copy(cudaStream_t s, void* dst, const void* src, const int64_t* didx,
+                const int64_t* sidx, int64_t rows, int64_t row_bytes, int64_t dstride,
+                int64_t sstride, int64_t dbase = 0) {
+  if (rows <= 0 || row_bytes <= 0) return HT_OK;
+  const uintptr_t al = (uintptr_t)dst | (uintptr_t)src | (uintptr_t)row_bytes |
+                       (uintptr_t)dstride | (uintptr_t)sstride;
+  const int g = grid_for(rows);
+  if ((al & 15) == 0)
+    ht::k_copy_rows<int4><<<g, kThreads, 0, s>>>((char*)dst, (const char*)src, didx, sidx, rows,
+                                                (int)(row_bytes / 16), dstride, sstride, dbase);
+  else if ((al & 7) == 0)
+    ht::k_copy_rows<int2><<<g, kThreads, 0, s>>>((char*)dst, (const char*)src, didx, sidx, rows,
+                                                (int)(row_bytes / 8), dstride, sstride, dbase);
+  else
+    ht::k_copy_rows<int><<<g, kThreads, 0, s>>>((char*)dst, (const char*)src, didx, sidx, rows,
+                                               (int)(row_bytes / 4), dstride, sstride, dbase);
+  CU(cudaGetLastError());
+  return HT_OK;
+}
+
+int launch_acc(cudaStream_t s, int elem, void* dst, void* src, const int64_t* didx,
+               const int64_t* sidx, const uint8_t* first, int64_t rows, int d, int zero_src,
+               int64_t sbase = 0) {
+  if (rows <= 0) return HT_OK;
+  const int g = grid_for(rows);
+  if (elem == 4)
+    ht::k_acc_rows<float><<<g, kThreads, 0, s>>>((float*)dst, (float*)src, didx, sidx, first, rows,
+                                                d, zero_src, sbase);
+  else
+    ht::k_acc_rows<double><<<g, kThreads, 0, s>>>((double*)dst, (double*)src, didx, sidx, first,
+                                                 rows, d, zero_src, sbase);
+  CU(cudaGetLastError());
+  return HT_OK;
+}
+
+void timer_begin(ht_fleet* f, Device& d, TimerRec& r) {
+  if (!f->timing) return;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, d.stream);
+}
+void timer_end(ht_fleet* f, Device& d, TimerRec& r, int which, double bytes) {
+  if (!f->timing) return;
+  cudaEventRecord(r.b, d.stream);
+  r.which = which;
+  r.bytes = bytes;
+  f->timers.push_back(r);
+}
+void timers_collect(ht_fleet* f) {
+  for (auto& r : f->timers) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    f->t_launch[r.which]++;
+    f->t_ms[r.which] += ms;
+    f->t_bytes[r.which] += r.bytes;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  f->timers.clear();
+}
+
+// Segment gather-sum over a chunk's CSC (forward) or CSR (backward) view.
+int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, const int64_t* off,
+               const int32_t* idx, const float* w, int64_t nseg, int64_t np, const DBuf& lo,
+               const DBuf& hi, int64_t nf, const DBuf& seg, const DBuf& first, const DBuf& cnt,
+               float* partial) {
+  if (nseg <= 0) return HT_OK;
+  const int g = grid_for(nseg);
+  if (d % 4 == 0 && d <= 512) {
+    const int nv = (d / 4 + 31) / 32;
+#define SEGV(NV)                                                                               \
+  ht::k_seg_gather_v4<NV><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); \
+  if (np) ht::k_seg_pieces_v4<NV><<<grid_for(np), kThreads, 0, s>>>(                           \
+      partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
+    switch (nv) {
+      case 1: SEGV(1); break;
+      case 2: SEGV(2); break;
+      case 3: SEGV(3); break;
+      default: SEGV(4); break;
+    }
+#undef SEGV
+  } else {
+    const int ns = (d + 31) / 32;
+    if (ns > 16) return fail(HT_EINVAL, "feature width %d too large", d);
+#define SEGS(NS)                                                                              \
+  ht::k_seg_gather_s<NS><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); \
+  if (np) ht::k_seg_pieces_s<NS><<<grid_for(np), kThreads, 0, s>>>(                           \
+      partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
+    if (ns <= 1) { SEGS(1); }
+    else if (ns <= 2) { SEGS(2); }
+    else if (ns <= 4) { SEGS(4); }
+    else if (ns <= 8) { SEGS(8); }
+    else { SEGS(16); }
+#undef SEGS
+  }
+  CU(cudaGetLastError());
+  if (nf) {
+    ht::k_seg_fixup<<<grid_for(nf), kThreads, 0, s>>>(out, partial, d, seg.as<int64_t>(),
+                                                       first.as<int64_t>(), cnt.as<int64_t>(), nf);
+    CU(cudaGetLastError());
+  }
+  return HT_OK;
+}
+
+template <bool TA, bool TB, int EPI>
+int gemm(cudaStream_t s, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+         int64_t ldc, const float* G, int64_t ldg, int64_t M, int64_t N, int64_t K, int splits,
+         int64_t kps) {
+  if (M <= 0 || N <= 0) return HT_OK;
+  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)splits);
+  ht::k_gemm<TA, TB, EPI><<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, G, ldg, M, N, K, kps);
+  CU(cudaGetLastError());
+  return HT_OK;
+}
+
+// long-segment pieces of an offsets array
+void make_pieces(const std::vector<int64_t>& off, std::vector<int64_t>& lo, std::vector<int64_t>& hi,
+                 std::vector<int64_t>& seg, std::vector<int64_t>& first, std::vector<int64_t>& cnt) {
+  for (size_t sg = 0; sg + 1 < off.size(); ++sg) {
+    const int64_t a = off[sg], b = off[sg + 1];
+    if (b - a <= kSplit) continue;
+    seg.push_back((int64_t)sg);
+    first.push_back((int64_t)lo.size());
+    int64_t c = 0;
+    for (int64_t x = a; x < b; x += kSplit, ++c) {
+      lo.push_back(x);
+      hi.push_back(std::min(b, x + kSplit));
+    }
+    cnt.push_back(c);
+  }
+}
+
+int lookup_slots(const HostSets& hs, const std::vector<int64_t>& rows, std::vector<int64_t>& out,
+                 int i, int j) {
+  out.resize(rows.size());
+  for (size_t q = 0; q < rows.size(); ++q) {
+    auto it = std::lower_bound(hs.live.begin(), hs.live.end(), rows[q]);
+    if (it == hs.live.end() || *it != rows[q])
+      return fail(HT_ELIVE, "device %d batch %d: rows requested outside the live set", i, j);
+    out[q] = hs.slots[it - hs.live.begin()];
+  }
+  return HT_OK;
+}
+
+std::vector<int64_t> vdiff(const std::vector<int64_t>& a, const std::vector<int64_t>& b) {
+  std::vector<int64_t> o;
+  std::set_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+  return o;
+}
+std::vector<int64_t> visect(const std::vector<int64_t>& a, const std::vector<int64_t>& b) {
+  std::vector<int64_t> o;
+  std::set_intersection(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+  return o;
+}
+
+int upload_list(CopyList& cl, const std::vector<int64_t>& src, const std::vector<int64_t>& dst,
+                cudaStream_t s, const std::vector<uint8_t>* flag = nullptr) {
+  cl.n = (int64_t)src.size();
+  HT_TRY(upload(cl.src, src, s));
+  HT_TRY(upload(cl.dst, dst, s));
+  if (flag) HT_TRY(upload(cl.flag, *flag, s));
+  return HT_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// runtime / memory
+// ===========================================================================
+
+extern "C" int ht_device_count(int* count) {
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *count = 0;
+  }
+  return HT_OK;
+}
+
+extern "C" int ht_host_alloc(int64_t bytes, void** out) {
+  CU(cudaHostAlloc(out, std::max<int64_t>(bytes, 16),
+                   cudaHostAllocPortable | cudaHostAllocMapped));
+  return HT_OK;
+}
+extern "C" int ht_host_free(void* p) {
+  CU(cudaFreeHost(p));
+  return HT_OK;
+}
+extern "C" int ht_host_register(void* p, int64_t bytes) {
+  CU(cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped));
+  return HT_OK;
+}
+extern "C" int ht_host_unregister(void* p) {
+  CU(cudaHostUnregister(p));
+  return HT_OK;
+}
+extern "C" int ht_dev_alloc(int device, int64_t bytes, void** out) {
+  CU(cudaSetDevice(device));
+  CU(cudaMalloc(out, std::max<int64_t>(bytes, 16)));
+  return HT_OK;
+}
+extern "C" int ht_dev_free(int device, void* p) {
+  CU(cudaSetDevice(device));
+  CU(cudaFree(p));
+  return HT_OK;
+}
+extern "C" int ht_memcpy(void* dst, const void* src, int64_t bytes) {
+  CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault));
+  return HT_OK;
+}
+extern "C" int ht_memset(void* dst, int value, int64_t bytes) {
+  CU(cudaMemset(dst, value, bytes));
+  CU(cudaDeviceSynchronize());
+  return HT_OK;
+}
+
+// ===========================================================================
+// fleet construction
+// ===========================================================================
+
+extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int flush_policy,
+                               ht_fleet** out) {
+  if (m < 1 || n < 1) return fail(HT_EINVAL, "fleet needs m >= 1 and n >= 1");
+  if (mode < 0 || mode > 2) return fail(HT_EINVAL, "unknown mode %d", mode);
+  if (flush_policy < 0 || flush_policy > 1) return fail(HT_EINVAL, "unknown flush policy");
+  int ndev = 0;
+  ht_device_count(&ndev);
+  if (ndev < 1) return fail(HT_ECUDA, "no CUDA device visible");
+  std::unique_ptr<ht_fleet> f(new ht_fleet);
+  f->m = m;
+  f->n = n;
+  f->mode = mode;
+  f->flush = flush_policy;
+  f->dev.resize(m);
+  f->sets.assign(m, std::vector<HostSets>(n));
+  for (int i = 0; i < m; ++i) {
+    Device& d = f->dev[i];
+    d.ordinal = ordinals ? ordinals[i] : 0;
+    if (d.ordinal < 0 || d.ordinal >= ndev) return fail(HT_EINVAL, "bad device ordinal %d", d.ordinal);
+    CU(cudaSetDevice(d.ordinal));
+    CU(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
+    d.chunks.resize(n);
+    for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
+                    &d.W, &d.hL, &d.labels, &d.mask, &d.loss_part})
+      b->dev = d.ordinal;
+    for (int k = 0; k < m; ++k) {
+      const int ok = ordinals ? ordinals[k] : 0;
+      if (ok == d.ordinal) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, d.ordinal, ok);
+      if (!can) return fail(HT_ECUDA, "device %d cannot access peer %d", d.ordinal, ok);
+      cudaError_t e = cudaDeviceEnablePeerAccess(ok, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(HT_ECUDA, "peer access %d->%d: %s", d.ordinal, ok, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+    for (int j = 0; j < n; ++j) f->sets[i][j].fetch.resize(m);
+  }
+  *out = f.release();
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_destroy(ht_fleet* f) {
+  if (!f) return HT_OK;
+  sync_all(f);
+  timers_collect(f);
+  for (auto& d : f->dev) {
+    cudaSetDevice(d.ordinal);
+    for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
+                    &d.W, &d.hL, &d.labels, &d.mask, &d.loss_part})
+      b->release();
+    for (auto& g : d.gW) g.release();
+    for (auto& c : d.chunks) {
+      for (auto* b : {&c.nbr_slot, &c.dest_rows, &c.csc_off, &c.csc_slot, &c.csc_w, &c.csr_off,
+                      &c.csr_dst, &c.csr_w, &c.fw_lo, &c.fw_hi, &c.fw_seg, &c.fw_first, &c.fw_cnt,
+                      &c.bw_lo, &c.bw_hi, &c.bw_seg, &c.bw_first, &c.bw_cnt})
+        b->release();
+      for (CopyList* cl : {&c.h2d, &c.flush, &c.base_bwd})
+        cl->src.release(), cl->dst.release(), cl->flag.release();
+      for (auto& cl : c.d2d) cl.src.release(), cl.dst.release();
+      for (auto& cl : c.push) cl.src.release(), cl.dst.release();
+    }
+    if (d.ev) cudaEventDestroy(d.ev);
+    if (d.stream) cudaStreamDestroy(d.stream);
+  }
+  delete f;
+  return HT_OK;
+}
+
+static std::vector<int64_t> vec(const int64_t* p, int64_t n) {
+  return n > 0 ? std::vector<int64_t>(p, p + n) : std::vector<int64_t>();
+}
+
+extern "C" int ht_fleet_set_sets(ht_fleet* f, int i, int j, const int64_t* nbr, int64_t n_nbr,
+                                 const int64_t* owned, int64_t n_owned, const int64_t* load,
+                                 int64_t n_load, const int64_t* nbr_carry, int64_t n_nbr_carry,
+                                 const int64_t* live, const int64_t* slots, int64_t n_live,
+                                 const int64_t* dest, int64_t n_dest) {
+  if (i < 0 || i >= f->m || j < 0 || j >= f->n) return fail(HT_EINVAL, "chunk index out of range");
+  HostSets& h = f->sets[i][j];
+  h.nbr = vec(nbr, n_nbr);
+  h.owned = vec(owned, n_owned);
+  h.load = vec(load, n_load);
+  h.nbr_carry = vec(nbr_carry, n_nbr_carry);
+  h.live = vec(live, n_live);
+  h.slots = vec(slots, n_live);
+  h.has_dest = n_dest >= 0;
+  h.dest = vec(dest, n_dest);
+  f->finalized = false;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_set_fetch(ht_fleet* f, int i, int j, int k, const int64_t* rows, int64_t n) {
+  if (i < 0 || i >= f->m || j < 0 || j >= f->n || k < 0 || k >= f->m)
+    return fail(HT_EINVAL, "fetch index out of range");
+  f->sets[i][j].fetch[k] = vec(rows, n);
+  f->finalized = false;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_set_chunk(ht_fleet* f, int i, int j, int64_t nv, int64_t nn, int64_t ne,
+                                  const int64_t* csc_off, const int64_t* csc_local_src,
+                                  const double* edge_w, const int64_t* csr_off,
+                                  const int64_t* csr_local_dst, const int64_t* csr_perm) {
+  if (i < 0 || i >= f->m || j < 0 || j >= f->n) return fail(HT_EINVAL, "chunk index out of range");
+  if (ne >= ((int64_t)1 << 31) || nn >= ((int64_t)1 << 31))
+    return fail(HT_EINVAL, "chunk too large for 32-bit local indices");
+  HostSets& h = f->sets[i][j];
+  h.has_chunk = true;
+  h.nv = nv;
+  h.nn = nn;
+  h.ne = ne;
+  h.csc_off = vec(csc_off, nv + 1);
+  h.csc_src = vec(csc_local_src, ne);
+  h.csr_off = vec(csr_off, nn + 1);
+  h.csr_dst = vec(csr_local_dst, ne);
+  h.csr_perm = vec(csr_perm, ne);
+  h.w.assign(edge_w, edge_w + ne);
+  f->finalized = false;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_finalize(ht_fleet* f) {
+  const int m = f->m, n = f->n;
+  const bool base = f->mode == HT_MODE_BASELINE;
+  for (int i = 0; i < m; ++i) {
+    Device& d = f->dev[i];
+    HT_TRY(set_dev(d));
+    cudaStream_t s = d.stream;
+    d.cap = 0;
+    for (int j = 0; j < n; ++j) {
+      HostSets& h = f->sets[i][j];
+      if (base) d.cap = std::max<int64_t>(d.cap, (int64_t)h.nbr.size());
+      else
+        for (int64_t sl : h.slots) d.cap = std::max<int64_t>(d.cap, sl + 1);
+    }
+    for (int j = 0; j < n; ++j) {
+      HostSets& h = f->sets[i][j];
+      DevChunk& c = d.chunks[j];
+      c.nn = (int64_t)h.nbr.size();
+      c.nlive = base ? c.nn : (int64_t)h.live.size();
+      c.nv = h.has_dest ? (int64_t)h.dest.size() : 0;
+      std::vector<int64_t> nbr_slot, a, b;
+      if (base) {
+        nbr_slot.resize(h.nbr.size());
+        std::iota(nbr_slot.begin(), nbr_slot.end(), 0);
+        HT_TRY(upload_list(c.h2d, h.nbr, nbr_slot, s));
+      } else {
+        HT_TRY(lookup_slots(h, h.nbr, nbr_slot, i, j));
+        const auto& rows = f->mode == HT_MODE_FULL ? h.load : h.owned;
+        HT_TRY(lookup_slots(h, rows, b, i, j));
+        HT_TRY(upload_list(c.h2d, rows, b, s));
+        c.d2d.assign(m, CopyList());
+        for (int st = 1; st < m; ++st) {
+          const int k = (i + st) % m;
+          std::vector<int64_t> rows_k = h.fetch[k];
+          if (f->mode == HT_MODE_FULL && !h.nbr_carry.empty()) rows_k = vdiff(rows_k, h.nbr_carry);
+          std::vector<int64_t> src_slot, dst_slot;
+          HT_TRY(lookup_slots(f->sets[k][j], rows_k, src_slot, k, j));
+          HT_TRY(lookup_slots(h, rows_k, dst_slot, i, j));
+          HT_TRY(upload_list(c.d2d[st], src_slot, dst_slot, s));
+        }
+      }
+      HT_TRY(upload(c.nbr_slot, nbr_slot, s));
+      if (h.has_dest) HT_TRY(upload(c.dest_rows, h.dest, s));
+      if (h.has_chunk) {
+        if (h.nn != c.nn || (h.has_dest && h.nv != c.nv))
+          return fail(HT_EINVAL, "chunk (%d,%d) structure does not match its plan sets", i, j);
+        std::vector<int32_t> slot32(h.ne), dst32(h.ne);
+        std::vector<float> w32(h.ne), wcsr(h.ne);
+        for (int64_t e = 0; e < h.ne; ++e) {
+          slot32[e] = (int32_t)nbr_slot[h.csc_src[e]];
+          w32[e] = (float)h.w[e];
+          dst32[e] = (int32_t)h.csr_dst[e];
+          wcsr[e] = (float)h.w[h.csr_perm[e]];
+        }
+        HT_TRY(upload(c.csc_off, h.csc_off, s));
+        HT_TRY(upload(c.csc_slot, slot32, s));
+        HT_TRY(upload(c.csc_w, w32, s));
+        HT_TRY(upload(c.csr_off, h.csr_off, s));
+        HT_TRY(upload(c.csr_dst, dst32, s));
+        HT_TRY(upload(c.csr_w, wcsr, s));
+        c.ne = h.ne;
+        std::vector<int64_t> lo, hi, sg, fi, cn;
+        make_pieces(h.csc_off, lo, hi, sg, fi, cn);
+        c.fw_np = (int64_t)lo.size();
+        c.fw_nf = (int64_t)sg.size();
+        HT_TRY(upload(c.fw_lo, lo, s)); HT_TRY(upload(c.fw_hi, hi, s));
+        HT_TRY(upload(c.fw_seg, sg, s)); HT_TRY(upload(c.fw_first, fi, s)); HT_TRY(upload(c.fw_cnt, cn, s));
+        lo.clear(); hi.clear(); sg.clear(); fi.clear(); cn.clear();
+        make_pieces(h.csr_off, lo, hi, sg, fi, cn);
+        c.bw_np = (int64_t)lo.size();
+        c.bw_nf = (int64_t)sg.size();
+        HT_TRY(upload(c.bw_lo, lo, s)); HT_TRY(upload(c.bw_hi, hi, s));
+        HT_TRY(upload(c.bw_seg, sg, s)); HT_TRY(upload(c.bw_first, fi, s)); HT_TRY(upload(c.bw_cnt, cn, s));
+      }
+      if (base) {
+        std::vector<int64_t> pos(h.nbr.size());
+        std::iota(pos.begin(), pos.end(), 0);
+        HT_TRY(upload_list(c.base_bwd, pos, h.nbr, s));
+      }
+    }
+  }
+  // owner-side push and flush lists
+  if (!base) {
+    std::vector<uint8_t> flushed;
+    for (int j = 0; j < n; ++j) {
+      for (int k = 0; k < m; ++k) {
+        Device& d = f->dev[k];
+        HT_TRY(set_dev(d));
+        cudaStream_t s = d.stream;
+        DevChunk& c = d.chunks[j];
+        HostSets& hk = f->sets[k][j];
+        c.push.assign(m, CopyList());
+        for (int i = 0; i < m; ++i) {
+          HostSets& hi = f->sets[i][j];
+          std::vector<int64_t> rows = (i == k) ? visect(hk.nbr, hk.owned) : hi.fetch[k];
+          std::vector<int64_t> pos(rows.size()), slot;
+          for (size_t q = 0; q < rows.size(); ++q) {
+            auto it = std::lower_bound(hi.nbr.begin(), hi.nbr.end(), rows[q]);
+            if (it == hi.nbr.end() || *it != rows[q])
+              return fail(HT_EINVAL, "fetch row %lld not in N_%d%d", (long long)rows[q], i, j);
+            pos[q] = it - hi.nbr.begin();
+          }
+          HT_TRY(lookup_slots(hk, rows, slot, k, j));
+          HT_TRY(upload_list(c.push[i], pos, slot, s));
+        }
+        std::vector<int64_t> fl;
+        if (f->mode == HT_MODE_P2P || f->flush == HT_FLUSH_EVERY_BATCH || j + 1 == n) fl = hk.owned;
+        else fl = vdiff(hk.owned, f->sets[k][j + 1].owned);
+        std::vector<int64_t> slot;
+        HT_TRY(lookup_slots(hk, fl, slot, k, j));
+        std::vector<uint8_t> first(fl.size());
+        for (size_t q = 0; q < fl.size(); ++q) {
+          const int64_t v = fl[q];
+          if ((int64_t)flushed.size() <= v) flushed.resize(v + 1, 0);
+          first[q] = flushed[v] ? 0 : 1;
+          flushed[v] = 1;
+        }
+        HT_TRY(upload_list(c.flush, slot, fl, s, &first));
+      }
+    }
+  }
+  HT_TRY(sync_all(f));
+  f->finalized = true;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_capacity(ht_fleet* f, int i, int64_t* cap) {
+  if (i < 0 || i >= f->m) return fail(HT_EINVAL, "device index out of range");
+  *cap = f->dev[i].cap;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_sync(ht_fleet* f) {
+  HT_TRY(sync_all(f));
+  timers_collect(f);
+  return HT_OK;
+}
+
+extern "C" int ht_begin_layer(ht_fleet* f, int dim, int elem_size, int backward) {
+  if (!f->finalized) return fail(HT_ESTATE, "fleet not finalized");
+  if (elem_size != 4 && elem_size != 8) return fail(HT_EINVAL, "element size must be 4 or 8");
+  f->dim = dim;
+  f->elem = elem_size;
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    const int64_t bytes = d.cap * (int64_t)dim * elem_size;
+    HT_TRY(d.value.ensure(bytes));
+    if (backward && f->mode != HT_MODE_BASELINE) {
+      HT_TRY(d.grad.ensure(bytes));
+      if (bytes) CU(cudaMemsetAsync(d.grad.p, 0, bytes, d.stream));
+    }
+  }
+  return HT_OK;
+}
+
+// ===========================================================================
+// communication steps (Alg. 2 / Alg. 3)
+// ===========================================================================
+namespace {
+
+// step 1 + barrier + step 2 + barrier of dedup_comm_fwd for batch j
+int stage_batch(ht_fleet* f, int j, const void* host_rows_dev) {
+  const int64_t rb = (int64_t)f->dim * f->elem;
+  for (int i = 0; i < f->m; ++i) {
+    Device& d = f->dev[i];
+    HT_TRY(set_dev(d));
+    DevChunk& c = d.chunks[j];
+    TimerRec tr;
+    timer_begin(f, d, tr);
+    HT_TRY(launch_copy(d.stream, d.value.p, host_rows_dev, c.h2d.dst.as<int64_t>(),
+                       c.h2d.src.as<int64_t>(), c.h2d.n, rb, rb, rb));
+    timer_end(f, d, tr, 3, (double)c.h2d.n * rb);
+  }
+  if (f->mode == HT_MODE_BASELINE || f->m == 1) return HT_OK;
+  HT_TRY(barrier(f));
+  for (int i = 0; i < f->m; ++i) {
+    Device& d = f->dev[i];
+    HT_TRY(set_dev(d));
+    DevChunk& c = d.chunks[j];
+    for (int st = 1; st < f->m; ++st) {
+      const int k = (i + st) % f->m;
+      const CopyList& cl = c.d2d[st];
+      HT_TRY(launch_copy(d.stream, d.value.p, f->dev[k].value.p, cl.dst.as<int64_t>(),
+                         cl.src.as<int64_t>(), cl.n, rb, rb, rb));
+    }
+  }
+  return barrier(f);
+}
+
+// push views (device-resident, per device in d.se at row stride dim) to the
+// owners, then flush.  assume_zero: first flush of a row stores.
+int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero) {
+  const int dim = f->dim;
+  if (f->mode == HT_MODE_BASELINE) {
+    // host_grad[N_ij] += view_i in ascending device order
+    for (int i = 0; i < f->m; ++i) {
+      Device& d = f->dev[i];
+      HT_TRY(set_dev(d));
+      if (i > 0) CU(cudaStreamWaitEvent(d.stream, f->dev[i - 1].ev, 0));
+      const CopyList& cl = d.chunks[j].base_bwd;
+      HT_TRY(launch_acc(d.stream, f->elem, host_grad_dev, d.se.p, cl.dst.as<int64_t>(),
+                        cl.src.as<int64_t>(), nullptr, cl.n, dim, 0));
+      CU(cudaEventRecord(d.ev, d.stream));
+    }
+    return barrier(f);
+  }
+  HT_TRY(barrier(f));
+  for (int k = 0; k < f->m; ++k) {
+    Device& d = f->dev[k];
+    HT_TRY(set_dev(d));
+    DevChunk& c = d.chunks[j];
+    for (int i = 0; i < f->m; ++i) {  // ascending source device
+      const CopyList& cl = c.push[i];
+      HT_TRY(launch_acc(d.stream, f->elem, d.grad.p, f->dev[i].se.p, cl.dst.as<int64_t>(),
+                        cl.src.as<int64_t>(), nullptr, cl.n, dim, 0));
+    }
+    const CopyList& fl = c.flush;
+    HT_TRY(launch_acc(d.stream, f->elem, host_grad_dev, d.grad.p, fl.dst.as<int64_t>(),
+                      fl.src.as<int64_t>(), assume_zero ? fl.flag.as<uint8_t>() : nullptr, fl.n,
+                      dim, 1));
+  }
+  return barrier(f);
+}
+
+}  // namespace
+
+extern "C" int ht_comm_fwd(ht_fleet* f, int batch, const void* host_rows, void* views_out) {
+  if (batch < 0 || batch >= f->n) return fail(HT_EINVAL, "batch out of range");
+  void *hsrc, *vout;
+  HT_TRY(dev_ptr(host_rows, &hsrc));
+  HT_TRY(dev_ptr(views_out, &vout));
+  HT_TRY(stage_batch(f, batch, hsrc));
+  const int64_t rb = (int64_t)f->dim * f->elem;
+  int64_t base = 0;
+  for (int i = 0; i < f->m; ++i) {
+    Device& d = f->dev[i];
+    HT_TRY(set_dev(d));
+    DevChunk& c = d.chunks[batch];
+    HT_TRY(launch_copy(d.stream, vout, d.value.p, nullptr, c.nbr_slot.as<int64_t>(), c.nn, rb, rb,
+                       rb, base));
+    base += c.nn;
+  }
+  return sync_all(f);
+}
+
+extern "C" int ht_comm_bwd(ht_fleet* f, int batch, const void* views_in, void* host_grad) {
+  if (batch < 0 || batch >= f->n) return fail(HT_EINVAL, "batch out of range");
+  void *vin, *hg;
+  HT_TRY(dev_ptr(views_in, &vin));
+  HT_TRY(dev_ptr(host_grad, &hg));
+  const int64_t rb = (int64_t)f->dim * f->elem;
+  int64_t base = 0;
+  for (int i = 0; i < f->m; ++i) {
+    Device& d = f->dev[i];
+    HT_TRY(set_dev(d));
+    DevChunk& c = d.chunks[batch];
+    HT_TRY(d.se.ensure(std::max<int64_t>(1, c.nn) * rb));
+    if (c.nn)
+      CU(cudaMemcpyAsync(d.se.p, (const char*)vin + base * rb, c.nn * rb, cudaMemcpyDefault,
+                         d.stream));
+    base += c.nn;
+  }
+  HT_TRY(push_flush(f, batch, hg, false));
+  return sync_all(f);
+}
+
+extern "C" int ht_dest_rows(ht_fleet* f, int op, int batch, int dim, int elem_size, void* host_rows,
+                            void* rows_concat) {
+  if (batch < 0 || batch >= f->n) return fail(HT_EINVAL, "batch out of range");
+  void *hp, *rp;
+  HT_TRY(dev_ptr(host_rows, &hp));
+  HT_TRY(dev_ptr(rows_concat, &rp));
+  const int64_t rb = (int64_t)dim * elem_size;
+  int64_t base = 0;
+  for (int i = 0; i < f->m; ++i) {
+    Device& d = f->dev[i];
+    HT_TRY(set_dev(d));
+    DevChunk& c = d.chunks[batch];
+    if (!f->sets[i][batch].has_dest)
+      return fail(HT_EINVAL, "plan carries no destination sets; build it from a partition");
+    const int64_t* rows = c.dest_rows.as<int64_t>();
+    if (op == 0)
+      HT_TRY(launch_copy(d.stream, rp, hp, nullptr, rows, c.nv, rb, rb, rb, base));
+    else if (op == 1)
+      HT_TRY(launch_copy(d.stream, (char*)hp, (char*)rp + base * rb, rows, nullptr, c.nv, rb, rb, rb));
+    else {
+      // ascending device order on one stream chain
+      if (i > 0) CU(cudaStreamWaitEvent(d.stream, f->dev[i - 1].ev, 0));
+      HT_TRY(launch_acc(d.stream, elem_size, hp, rp, rows, nullptr, nullptr, c.nv, dim, 0, base));
+      CU(cudaEventRecord(d.ev, d.stream));
+    }
+    base += c.nv;
+  }
+  return sync_all(f);
+}
+
+// ===========================================================================
+// GCN epoch
+// ===========================================================================
+
+extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
+  if (!f->finalized) return fail(HT_ESTATE, "fleet not finalized");
+  f->L = L;
+  f->dims.assign(dims, dims + L + 1);
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    if ((int)d.gW.size() < L) d.gW.resize(L);
+    for (int l = 0; l < L; ++l) {
+      d.gW[l].dev = d.ordinal;
+      const int64_t bytes = (int64_t)dims[l] * dims[l + 1] * 4;
+      HT_TRY(d.gW[l].ensure(bytes));
+      CU(cudaMemsetAsync(d.gW[l].p, 0, bytes, d.stream));
+    }
+  }
+  return HT_OK;
+}
+
+static int check_chunks(ht_fleet* f) {
+  for (int i = 0; i < f->m; ++i)
+    for (int j = 0; j < f->n; ++j)
+      if (!f->sets[i][j].has_chunk || !f->sets[i][j].has_dest)
+        return fail(HT_ESTATE, "chunk (%d,%d) has no graph structure uploaded", i, j);
+  return HT_OK;
+}
+
+extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
+                                const void* h_in, void* h_out, void* agg_out, int precision) {
+  HT_TRY(check_chunks(f));
+  void *hin, *hout, *aout;
+  HT_TRY(dev_ptr(h_in, &hin));
+  HT_TRY(dev_ptr(h_out, &hout));
+  HT_TRY(dev_ptr(agg_out, &aout));
+  HT_TRY(ht_begin_layer(f, d_in, 4, 0));
+  const bool last = layer == f->L - 1;
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    int64_t mv = 0, tot = 0;
+    d.hL_off.assign(f->n + 1, 0);
+    for (int j = 0; j < f->n; ++j) {
+      mv = std::max(mv, d.chunks[j].nv);
+      d.hL_off[j + 1] = d.hL_off[j] + d.chunks[j].nv;
+    }
+    tot = d.hL_off[f->n];
+    HT_TRY(d.sa.ensure(std::max<int64_t>(1, mv) * d_in * 4));
+    HT_TRY(d.sb.ensure(std::max<int64_t>(1, mv) * d_out * 4));
+    int64_t np = 0;
+    for (int j = 0; j < f->n; ++j) np = std::max(np, d.chunks[j].fw_np);
+    HT_TRY(d.partial.ensure(std::max<int64_t>(1, np) * d_in * 4));
+    HT_TRY(d.W.ensure((int64_t)d_in * d_out * 4));
+    CU(cudaMemcpyAsync(d.W.p, W, (int64_t)d_in * d_out * 4, cudaMemcpyHostToDevice, d.stream));
+    if (last) {
+      HT_TRY(d.hL.ensure(std::max<int64_t>(1, tot) * d_out * 4));
+      f->hL_dim = d_out;
+    }
+  }
+  for (int j = 0; j < f->n; ++j) {
+    HT_TRY(stage_batch(f, j, hin));
+    for (int i = 0; i < f->m; ++i) {
+      Device& d = f->dev[i];
+      HT_TRY(set_dev(d));
+      DevChunk& c = d.chunks[j];
+      float* agg = d.sa.as<float>();
+      TimerRec tr;
+      timer_begin(f, d, tr);
+      HT_TRY(launch_seg(d.stream, agg, d.value.as<float>(), d_in, d_in, c.csc_off.as<int64_t>(),
+                        c.csc_slot.as<int32_t>(), c.csc_w.as<float>(), c.nv, c.fw_np, c.fw_lo,
+                        c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt, d.partial.as<float>()));
+      timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nv * (4.0 * d_in + 4.0));
+      float* hdst = last ? d.hL.as<float>() + d.hL_off[j] * d_out : d.sb.as<float>();
+      TimerRec tg;
+      timer_begin(f, d, tg);
+      if (precision == HT_PREC_TF32) {
+        HT_TRY(ht::tc_gemm_fwd(d.stream, agg, d.W.as<float>(), hdst, c.nv, d_in, d_out));
+      } else {
+        HT_TRY((gemm<false, false, ht::EPI_RELU>(d.stream, agg, d_in, d.W.as<float>(), d_out, hdst,
+                                                 d_out, nullptr, 0, c.nv, d_out, d_in, 1, d_in)));
+      }
+      timer_end(f, d, tg, 2, 2.0 * c.nv * d_in * d_out);
+      // K5: dest rows + checkpoint rows to the host store
+      const int64_t* rows = c.dest_rows.as<int64_t>();
+      HT_TRY(launch_copy(d.stream, hout, hdst, rows, nullptr, c.nv, (int64_t)d_out * 4,
+                         (int64_t)d_out * 4, (int64_t)d_out * 4));
+      HT_TRY(launch_copy(d.stream, aout, agg, rows, nullptr, c.nv, (int64_t)d_in * 4,
+                         (int64_t)d_in * 4, (int64_t)d_in * 4));
+    }
+    // the next batch's host loads may overwrite slots peers still read
+    HT_TRY(barrier(f));
+  }
+  HT_TRY(sync_all(f));
+  timers_collect(f);
+  return HT_OK;
+}
+
+extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uint8_t* mask,
+                       int64_t V, int64_t count, void* grad_out, double* loss) {
+  if (f->hL_dim != d_last) return fail(HT_ESTATE, "loss before the last forward layer");
+  void* gout;
+  HT_TRY(dev_ptr(grad_out, &gout));
+  *loss = 0.0;
+  if (count == 0) return HT_OK;
+  const int blocks = 148 * 4;
+  std::vector<std::vector<double>> parts(f->m);
+  for (int i = 0; i < f->m; ++i) {
+    Device& d = f->dev[i];
+    HT_TRY(set_dev(d));
+    HT_TRY(d.labels.ensure(V * 8));
+    HT_TRY(d.mask.ensure(V));
+    HT_TRY(d.loss_part.ensure((int64_t)blocks * f->n * 8));
+    CU(cudaMemcpyAsync(d.labels.p, labels, V * 8, cudaMemcpyHostToDevice, d.stream));
+    CU(cudaMemcpyAsync(d.mask.p, mask, V, cudaMemcpyHostToDevice, d.stream));
+    for (int j = 0; j < f->n; ++j) {
+      DevChunk& c = d.chunks[j];
+      ht::k_loss<<<blocks, 256, 0, d.stream>>>(
+          d.hL.as<float>() + d.hL_off[j] * d_last, c.nv, d_last, d.labels.as<int64_t>(),
+          d.mask.as<uint8_t>(), c.dest_rows.as<int64_t>(), (float*)gout, (float)count,
+          d.loss_part.as<double>() + (int64_t)j * blocks);
+      CU(cudaGetLastError());
+    }
+    parts[i].resize((size_t)blocks * f->n);
+    CU(cudaMemcpyAsync(parts[i].data(), d.loss_part.p, parts[i].size() * 8, cudaMemcpyDeviceToHost,
+                       d.stream));
+  }
+  HT_TRY(sync_all(f));
+  double tot = 0.0;
+  for (int i = 0; i < f->m; ++i)
+    for (double p : parts[i]) tot += p;
+  *loss = tot / (double)count;
+  return HT_OK;
+}
+
+extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
+                                 const void* agg_in, const void* grad_out, void* grad_in,
+                                 int precision) {
+  HT_TRY(check_chunks(f));
+  if (layer < 0 || layer >= f->L) return fail(HT_EINVAL, "layer out of range");
+  void *ain, *gout, *gin;
+  HT_TRY(dev_ptr(agg_in, &ain));
+  HT_TRY(dev_ptr(grad_out, &gout));
+  HT_TRY(dev_ptr(grad_in, &gin));
+  HT_TRY(ht_begin_layer(f, d_in, 4, 1));
+  const int splits_max = 64;
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    int64_t mv = 1, mn = 1, np = 1;
+    for (int j = 0; j < f->n; ++j) {
+      mv = std::max(mv, d.chunks[j].nv);
+      mn = std::max(mn, d.chunks[j].nn);
+      np = std::max(np, d.chunks[j].bw_np);
+    }
+    HT_TRY(d.sa.ensure(mv * d_in * 4));   // agg checkpoint rows
+    HT_TRY(d.sb.ensure(mv * d_out * 4));  // dest gradient rows
+    HT_TRY(d.sc.ensure(mv * d_out * 4));  // gz
+    HT_TRY(d.sd.ensure(mv * d_in * 4));   // grad agg
+    HT_TRY(d.se.ensure(mn * d_in * 4));   // grad of neighbour rows (views)
+    HT_TRY(d.partial.ensure(np * d_in * 4));
+    HT_TRY(d.gemm_ws.ensure((int64_t)splits_max * d_in * d_out * 4));
+    HT_TRY(d.W.ensure((int64_t)d_in * d_out * 4));
+    CU(cudaMemcpyAsync(d.W.p, W, (int64_t)d_in * d_out * 4, cudaMemcpyHostToDevice, d.stream));
+  }
+  for (int j = 0; j < f->n; ++j) {
+    for (int i = 0; i < f->m; ++i) {
+      Device& d = f->dev[i];
+      HT_TRY(set_dev(d));
+      DevChunk& c = d.chunks[j];
+      const int64_t* rows = c.dest_rows.as<int64_t>();
+      float *A = d.sa.as<float>(), *G = d.sb.as<float>(), *GZ = d.sc.as<float>(),
+            *GA = d.sd.as<float>();
+      // K6: checkpoint + destination-gradient reload
+      HT_TRY(launch_copy(d.stream, A, ain, nullptr, rows, c.nv, (int64_t)d_in * 4,
+                         (int64_t)d_in * 4, (int64_t)d_in * 4));
+      HT_TRY(launch_copy(d.stream, G, gout, nullptr, rows, c.nv, (int64_t)d_out * 4,
+                         (int64_t)d_out * 4, (int64_t)d_out * 4));
+      // K7: z = agg W (recompute), gz = g * [z > 0], dW += agg^T gz, gagg = gz W^T
+      TimerRec tg;
+      timer_begin(f, d, tg);
+      const int64_t M = c.nv;
+      int splits = (int)std::min<int64_t>(splits_max, std::max<int64_t>(1, M / 2048));
+      int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
+      splits = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
+      if (precision == HT_PREC_TF32) {
+        HT_TRY(ht::tc_gemm_bwd(d.stream, A, G, d.W.as<float>(), GZ, GA, d.gemm_ws.as<float>(),
+                               d.gW[layer].as<float>(), M, d_in, d_out));
+      } else {
+        HT_TRY((gemm<false, false, ht::EPI_MASK>(d.stream, A, d_in, d.W.as<float>(), d_out, GZ,
+                                                 d_out, G, d_out, M, d_out, d_in, 1, d_in)));
+        if (M > 0) {
+          HT_TRY((gemm<true, false, ht::EPI_STORE>(d.stream, A, d_in, GZ, d_out,
+                                                   d.gemm_ws.as<float>(), d_out, nullptr, 0, d_in,
+                                                   d_out, M, splits, kps)));
+          const int64_t nw = (int64_t)d_in * d_out;
+          ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
+              d.gW[layer].as<float>(), d.gemm_ws.as<float>(), nw, splits);
+          CU(cudaGetLastError());
+        }
+        HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, d_out, d.W.as<float>(), d_out, GA,
+                                                 d_in, nullptr, 0, M, d_in, d_out, 1, d_out)));
+      }
+      timer_end(f, d, tg, 2, 6.0 * c.nv * d_in * d_out);
+      // K8: transposed aggregation over the CSR view -> neighbour-row grads
+      TimerRec tr;
+      timer_begin(f, d, tr);
+      HT_TRY(launch_seg(d.stream, d.se.as<float>(), GA, d_in, d_in, c.csr_off.as<int64_t>(),
+                        c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), c.nn, c.bw_np, c.bw_lo,
+                        c.bw_hi, c.bw_nf, c.bw_seg, c.bw_first, c.bw_cnt, d.partial.as<float>()));
+      timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nn * (4.0 * d_in + 4.0));
+    }
+    // K9/K10: owner push (ascending source device) + flush into host grads
+    HT_TRY(push_flush(f, j, gin, true));
+  }
+  HT_TRY(sync_all(f));
+  timers_collect(f);
+  return HT_OK;
+}
+
+extern "C" int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, float lr,
+                      float* const* grads_out) {
+  Device& d0 = f->dev[0];
+  HT_TRY(set_dev(d0));
+  HT_TRY(sync_all(f));
+  for (int l = 0; l < L; ++l) {
+    const int64_t nw = (int64_t)dims[l] * dims[l + 1];
+    std::vector<const float*> ptrs(f->m);
+    for (int i = 0; i < f->m; ++i) ptrs[i] = f->dev[i].gW[l].as<float>();
+    DBuf pbuf, wbuf, tbuf;
+    HT_TRY(upload(pbuf, ptrs, d0.stream));
+    HT_TRY(wbuf.ensure(nw * 4));
+    HT_TRY(tbuf.ensure(nw * 4));
+    CU(cudaMemcpyAsync(wbuf.p, W[l], nw * 4, cudaMemcpyHostToDevice, d0.stream));
+    ht::k_sgd<<<grid_for(nw / 32 + 1), 256, 0, d0.stream>>>(wbuf.as<float>(), tbuf.as<float>(),
+                                                           pbuf.as<const float*>(), f->m, nw, lr);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(W[l], wbuf.p, nw * 4, cudaMemcpyDeviceToHost, d0.stream));
+    if (grads_out && grads_out[l])
+      CU(cudaMemcpyAsync(grads_out[l], tbuf.p, nw * 4, cudaMemcpyDeviceToHost, d0.stream));
+    CU(cudaStreamSynchronize(d0.stream));
+    pbuf.release();
+    wbuf.release();
+    tbuf.release();
+  }
+  return HT_OK;
+}
+
+extern "C" int ht_set_timing(ht_fleet* f, int enabled) {
+  f->timing = enabled != 0;
+  for (int q = 0; q < 4; ++q) f->t_launch[q] = 0, f->t_ms[q] = 0, f->t_bytes[q] = 0;
+  return HT_OK;
+}
+
+extern "C" int ht_kernel_stats(ht_fleet* f, int which, int64_t* launches, double* ms,
+                               double* bytes) {
+  if (which < 0 || which > 3) return fail(HT_EINVAL, "bad kernel class");
+  timers_collect(f);
+  *launches = f->t_launch[which];
+  *ms = f->t_ms[which];
+  *bytes = f->t_bytes[which];
+  return HT_OK;
+}

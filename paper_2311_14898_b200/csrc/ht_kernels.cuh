@@ -1,0 +1,435 @@
+// Device kernels of the HongTu GCN epoch path (sm_100a).
+//
+//   k_copy_rows     K1/K2/K5/K6: row gathers/scatters between pinned host
+//                   memory (zero-copy over PCIe), peer HBM (NVLink/UVA) and
+//                   local slot buffers; 16-byte vectors when rows allow.
+//   k_acc_rows      K9/K10: owner-side gradient accumulation and the flush
+//                   into host gradients (read-modify-write or first store).
+//   k_seg_gather    K3/K8: warp-per-segment weighted gather-sum (CSC forward
+//                   aggregation, CSR transposed aggregation) with strictly
+//                   sequential multiply-then-add per segment (np.add.at order).
+//   k_seg_pieces / k_seg_fixup: long power-law segments split into pieces,
+//                   reduced deterministically in piece order.
+//   k_gemm          K4/K7 FP32 SIMT GEMM with fused epilogues (validation
+//                   precision; the tcgen05 TF32 path lives in ht_tc.cuh).
+//   k_loss          K11 masked softmax cross-entropy, gradient rows written
+//                   straight to the host gradient array.
+//   k_sgd           K12 ascending-device gradient sum + SGD step.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ht {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int64_t global_warp() {
+  return (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+}
+__device__ __forceinline__ int64_t num_warps() { return ((int64_t)gridDim.x * blockDim.x) >> 5; }
+
+// ---------------------------------------------------------------------------
+// row movement
+// ---------------------------------------------------------------------------
+
+// dst row didx[r] <- src row sidx[r]; a null index means identity.  `cpr` =
+// vector words per row.  Each warp owns one row at a time and issues up to
+// four 32-lane vector loads before its stores.
+template <typename Vec>
+__global__ void __launch_bounds__(256) k_copy_rows(char* __restrict__ dst, const char* __restrict__ src,
+                                                   const int64_t* __restrict__ didx,
+                                                   const int64_t* __restrict__ sidx, int64_t rows,
+                                                   int cpr, int64_t dstride, int64_t sstride,
+                                                   int64_t dbase) {
+  const int lane = lane_id();
+  for (int64_t r = global_warp(); r < rows; r += num_warps()) {
+    const int64_t sr = sidx ? sidx[r] : r;
+    const int64_t dr = (didx ? didx[r] : r) + dbase;
+    const Vec* s = reinterpret_cast<const Vec*>(src + sr * sstride);
+    Vec* d = reinterpret_cast<Vec*>(dst + dr * dstride);
+    for (int w = lane; w < cpr; w += 4 * kWarp) {
+      Vec t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (w + u * kWarp < cpr) t[u] = s[w + u * kWarp];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (w + u * kWarp < cpr) d[w + u * kWarp] = t[u];
+    }
+  }
+}
+
+// dst[didx[r]] += src[sidx[r]] (or = when store_first[r] != 0); optionally
+// zero the source row afterwards (the flush of devices.py:336-339).
+template <typename T>
+__global__ void __launch_bounds__(256) k_acc_rows(T* __restrict__ dst, T* __restrict__ src,
+                                                  const int64_t* __restrict__ didx,
+                                                  const int64_t* __restrict__ sidx,
+                                                  const uint8_t* __restrict__ store_first,
+                                                  int64_t rows, int d, int zero_src,
+                                                  int64_t sbase) {
+  const int lane = lane_id();
+  for (int64_t r = global_warp(); r < rows; r += num_warps()) {
+    const int64_t sr = (sidx ? sidx[r] : r) + sbase;
+    const int64_t dr = didx ? didx[r] : r;
+    T* s = src + sr * d;
+    T* o = dst + dr * d;
+    const bool st = store_first && store_first[r];
+    for (int c = lane; c < d; c += kWarp) {
+      const T v = s[c];
+      o[c] = st ? v : o[c] + v;
+      if (zero_src) s[c] = T(0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// segment gather-sum: out[seg] = sum_{e in [lo, hi)} w[e] * X[idx[e]]
+// sequential in e, product rounded before the add (no FMA contraction)
+// ---------------------------------------------------------------------------
+
+template <int NV>
+__device__ __forceinline__ void seg_sum_v4(float4 (&acc)[NV], const float* __restrict__ X,
+                                           int64_t ldx, int d4, const int32_t* __restrict__ idx,
+                                           const float* __restrict__ w, int64_t e0, int64_t e1,
+                                           int lane) {
+  for (int64_t base = e0; base < e1; base += kWarp) {
+    const int cnt = (int)((e1 - base) < (int64_t)kWarp ? (e1 - base) : (int64_t)kWarp);
+    const int my_i = lane < cnt ? idx[base + lane] : 0;
+    const float my_w = lane < cnt ? w[base + lane] : 0.f;
+    int k = 0;
+    for (; k + 4 <= cnt; k += 4) {
+      float4 x[4][NV];
+      float ww[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int s = __shfl_sync(0xffffffffu, my_i, k + u);
+        ww[u] = __shfl_sync(0xffffffffu, my_w, k + u);
+        const float4* row = reinterpret_cast<const float4*>(X + (int64_t)s * ldx);
+#pragma unroll
+        for (int t = 0; t < NV; ++t) {
+          const int c = lane + t * kWarp;
+          x[u][t] = c < d4 ? __ldg(row + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int t = 0; t < NV; ++t) {
+          acc[t].x = __fadd_rn(acc[t].x, __fmul_rn(ww[u], x[u][t].x));
+          acc[t].y = __fadd_rn(acc[t].y, __fmul_rn(ww[u], x[u][t].y));
+          acc[t].z = __fadd_rn(acc[t].z, __fmul_rn(ww[u], x[u][t].z));
+          acc[t].w = __fadd_rn(acc[t].w, __fmul_rn(ww[u], x[u][t].w));
+        }
+    }
+    for (; k < cnt; ++k) {
+      const int s = __shfl_sync(0xffffffffu, my_i, k);
+      const float wk = __shfl_sync(0xffffffffu, my_w, k);
+      const float4* row = reinterpret_cast<const float4*>(X + (int64_t)s * ldx);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const int c = lane + t * kWarp;
+        if (c < d4) {
+          const float4 x = __ldg(row + c);
+          acc[t].x = __fadd_rn(acc[t].x, __fmul_rn(wk, x.x));
+          acc[t].y = __fadd_rn(acc[t].y, __fmul_rn(wk, x.y));
+          acc[t].z = __fadd_rn(acc[t].z, __fmul_rn(wk, x.z));
+          acc[t].w = __fadd_rn(acc[t].w, __fmul_rn(wk, x.w));
+        }
+      }
+    }
+  }
+}
+
+template <int NS>
+__device__ __forceinline__ void seg_sum_s(float (&acc)[NS], const float* __restrict__ X, int64_t ldx,
+                                          int d, const int32_t* __restrict__ idx,
+                                          const float* __restrict__ w, int64_t e0, int64_t e1,
+                                          int lane) {
+  for (int64_t base = e0; base < e1; base += kWarp) {
+    const int cnt = (int)((e1 - base) < (int64_t)kWarp ? (e1 - base) : (int64_t)kWarp);
+    const int my_i = lane < cnt ? idx[base + lane] : 0;
+    const float my_w = lane < cnt ? w[base + lane] : 0.f;
+    for (int k = 0; k < cnt; ++k) {
+      const int s = __shfl_sync(0xffffffffu, my_i, k);
+      const float wk = __shfl_sync(0xffffffffu, my_w, k);
+      const float* row = X + (int64_t)s * ldx;
+#pragma unroll
+      for (int t = 0; t < NS; ++t) {
+        const int c = lane + t * kWarp;
+        if (c < d) acc[t] = __fadd_rn(acc[t], __fmul_rn(wk, __ldg(row + c)));
+      }
+    }
+  }
+}
+
+// One warp per segment; segments longer than `split` are skipped here and
+// handled by k_seg_pieces.  out row stride = d (dense), optional row map
+// `out_row` (null = identity).
+template <int NV>
+__global__ void __launch_bounds__(256) k_seg_gather_v4(float* __restrict__ out,
+                                                       const float* __restrict__ X, int64_t ldx,
+                                                       int d, const int64_t* __restrict__ off,
+                                                       const int32_t* __restrict__ idx,
+                                                       const float* __restrict__ w, int64_t nseg,
+                                                       int64_t split) {
+  const int lane = lane_id();
+  const int d4 = d >> 2;
+  for (int64_t sg = global_warp(); sg < nseg; sg += num_warps()) {
+    const int64_t e0 = off[sg], e1 = off[sg + 1];
+    if (e1 - e0 > split) continue;
+    float4 acc[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    seg_sum_v4<NV>(acc, X, ldx, d4, idx, w, e0, e1, lane);
+    float4* o = reinterpret_cast<float4*>(out + sg * (int64_t)d);
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      const int c = lane + t * kWarp;
+      if (c < d4) o[c] = acc[t];
+    }
+  }
+}
+
+template <int NS>
+__global__ void __launch_bounds__(256) k_seg_gather_s(float* __restrict__ out,
+                                                      const float* __restrict__ X, int64_t ldx,
+                                                      int d, const int64_t* __restrict__ off,
+                                                      const int32_t* __restrict__ idx,
+                                                      const float* __restrict__ w, int64_t nseg,
+                                                      int64_t split) {
+  const int lane = lane_id();
+  for (int64_t sg = global_warp(); sg < nseg; sg += num_warps()) {
+    const int64_t e0 = off[sg], e1 = off[sg + 1];
+    if (e1 - e0 > split) continue;
+    float acc[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) acc[t] = 0.f;
+    seg_sum_s<NS>(acc, X, ldx, d, idx, w, e0, e1, lane);
+    float* o = out + sg * (int64_t)d;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const int c = lane + t * kWarp;
+      if (c < d) o[c] = acc[t];
+    }
+  }
+}
+
+// Pieces of long segments: piece p sums edges [lo[p], hi[p]) into
+// partial row p.
+template <int NV>
+__global__ void __launch_bounds__(256) k_seg_pieces_v4(float* __restrict__ partial,
+                                                       const float* __restrict__ X, int64_t ldx,
+                                                       int d, const int64_t* __restrict__ lo,
+                                                       const int64_t* __restrict__ hi,
+                                                       const int32_t* __restrict__ idx,
+                                                       const float* __restrict__ w,
+                                                       int64_t npieces) {
+  const int lane = lane_id();
+  const int d4 = d >> 2;
+  for (int64_t p = global_warp(); p < npieces; p += num_warps()) {
+    float4 acc[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    seg_sum_v4<NV>(acc, X, ldx, d4, idx, w, lo[p], hi[p], lane);
+    float4* o = reinterpret_cast<float4*>(partial + p * (int64_t)d);
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      const int c = lane + t * kWarp;
+      if (c < d4) o[c] = acc[t];
+    }
+  }
+}
+
+template <int NS>
+__global__ void __launch_bounds__(256) k_seg_pieces_s(float* __restrict__ partial,
+                                                      const float* __restrict__ X, int64_t ldx,
+                                                      int d, const int64_t* __restrict__ lo,
+                                                      const int64_t* __restrict__ hi,
+                                                      const int32_t* __restrict__ idx,
+                                                      const float* __restrict__ w,
+                                                      int64_t npieces) {
+  const int lane = lane_id();
+  for (int64_t p = global_warp(); p < npieces; p += num_warps()) {
+    float acc[NS];
+#pragma unroll
+    for (int t = 0; t < NS; ++t) acc[t] = 0.f;
+    seg_sum_s<NS>(acc, X, ldx, d, idx, w, lo[p], hi[p], lane);
+    float* o = partial + p * (int64_t)d;
+#pragma unroll
+    for (int t = 0; t < NS; ++t) {
+      const int c = lane + t * kWarp;
+      if (c < d) o[c] = acc[t];
+    }
+  }
+}
+
+// out[seg[f]] = ((partial[first] + partial[first+1]) + ...) in piece order.
+__global__ void __launch_bounds__(256) k_seg_fixup(float* __restrict__ out,
+                                                   const float* __restrict__ partial, int d,
+                                                   const int64_t* __restrict__ seg,
+                                                   const int64_t* __restrict__ first,
+                                                   const int64_t* __restrict__ count, int64_t nfix) {
+  const int lane = lane_id();
+  for (int64_t f = global_warp(); f < nfix; f += num_warps()) {
+    const float* p = partial + first[f] * (int64_t)d;
+    float* o = out + seg[f] * (int64_t)d;
+    for (int c = lane; c < d; c += kWarp) {
+      float s = p[c];
+      for (int64_t q = 1; q < count[f]; ++q) s = __fadd_rn(s, p[q * (int64_t)d + c]);
+      o[c] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FP32 SIMT GEMM  C = A(MxK) * B(KxN), A(m,k) = TA ? A[k*lda+m] : A[m*lda+k],
+// B(k,n) = TB ? B[n*ldb+k] : B[k*ldb+n].  64x64x16 tiles, 4x4 per thread.
+// EPI: 0 store, 1 relu, 2 mask: C = (acc > 0) ? G[m*ldg+n] : 0.
+// Split-K over blockIdx.z writes slab z at C + z*M*ldc.
+// ---------------------------------------------------------------------------
+enum { EPI_STORE = 0, EPI_RELU = 1, EPI_MASK = 2 };
+
+template <bool TA, bool TB, int EPI>
+__global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ A, int64_t lda,
+                                              const float* __restrict__ B, int64_t ldb,
+                                              float* __restrict__ C, int64_t ldc,
+                                              const float* __restrict__ G, int64_t ldg, int64_t M,
+                                              int64_t N, int64_t K, int64_t k_per_split) {
+  constexpr int BM = 64, BN = 64, BK = 16;
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int t = threadIdx.x + q * 256;  // 0..1023 over a BK x BM tile
+      int kk, mm;
+      if (TA) { mm = t % BM; kk = t / BM; } else { kk = t % BK; mm = t / BK; }
+      const int64_t gm = m0 + mm, gk = k0 + kk;
+      float v = 0.f;
+      if (gm < M && gk < kend) v = TA ? A[gk * lda + gm] : A[gm * lda + gk];
+      As[kk][mm] = v;
+      int kb, nb;
+      if (TB) { kb = t % BK; nb = t / BK; } else { nb = t % BN; kb = t / BN; }
+      const int64_t gn = n0 + nb, gkb = k0 + kb;
+      float u = 0.f;
+      if (gn < N && gkb < kend) u = TB ? B[gn * ldb + gkb] : B[gkb * ldb + gn];
+      Bs[kb][nb] = u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* Cz = C + (int64_t)blockIdx.z * M * ldc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      float v = acc[i][j];
+      if (EPI == EPI_RELU) v = v > 0.f ? v : 0.f;
+      if (EPI == EPI_MASK) v = v > 0.f ? G[gm * ldg + gn] : 0.f;
+      Cz[gm * ldc + gn] = v;
+    }
+  }
+}
+
+// acc[e] = acc[e] + ((slab0[e] + slab1[e]) + ...) over `splits` slabs.
+__global__ void k_reduce_splits(float* __restrict__ acc, const float* __restrict__ slabs,
+                                int64_t n, int splits) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float s = slabs[e];
+    for (int z = 1; z < splits; ++z) s = __fadd_rn(s, slabs[(int64_t)z * n + e]);
+    acc[e] = __fadd_rn(acc[e], s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K11 loss: rows of H (ld = d); labels/mask aligned with rows; gradient rows
+// written to out (host or device) at out_rows[r] (stride d).  One warp per
+// row; per-block partial loss sums in double, fixed order.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64_t rows, int d,
+                                              const int64_t* __restrict__ labels,
+                                              const uint8_t* __restrict__ mask,
+                                              const int64_t* __restrict__ out_rows,
+                                              float* __restrict__ out, float count,
+                                              double* __restrict__ block_loss) {
+  __shared__ double wsum[8];
+  const int lane = lane_id(), wib = threadIdx.x >> 5;
+  double my = 0.0;
+  const int64_t warp = blockIdx.x * 8 + wib;
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t r = warp; r < rows; r += stride) {
+    const int64_t v = out_rows[r];
+    if (!mask[v]) {  // rows off the mask get a zero gradient (engine.py:305, 319)
+      for (int c = lane; c < d; c += kWarp) out[v * d + c] = 0.f;
+      continue;
+    }
+    const float* z = H + r * d;
+    float mx = -INFINITY;
+    for (int c = lane; c < d; c += kWarp) mx = fmaxf(mx, z[c]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float s = 0.f;
+    for (int c = lane; c < d; c += kWarp) s += expf(z[c] - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int64_t y = labels[v];
+    float* g = out + v * d;
+    for (int c = lane; c < d; c += kWarp) {
+      const float p = __fdiv_rn(expf(z[c] - mx), s);
+      if (c == y) my += -(double)logf(p);
+      g[c] = __fdiv_rn(c == y ? __fsub_rn(p, 1.f) : p, count);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
+  if (lane == 0) wsum[wib] = my;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < 8; ++q) t += wsum[q];
+    block_loss[blockIdx.x] = t;
+  }
+}
+
+// K12: total = ((0 + g_0) + g_1) + ...; W = W - lr * total (separate roundings)
+__global__ void k_sgd(float* __restrict__ W, float* __restrict__ total_out,
+                      const float* const* __restrict__ grads, int ndev, int64_t n, float lr) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float t = 0.f;
+    for (int i = 0; i < ndev; ++i) t = __fadd_rn(t, grads[i][e]);
+    if (total_out) total_out[e] = t;
+    W[e] = __fsub_rn(W[e], __fmul_rn(lr, t));
+  }
+}
+
+}  // namespace ht

@@ -1,0 +1,383 @@
+// Integer preprocessing of the HongTu path, native and bit-exact with the
+// reference (graph.py / partition.py / planner.py of chunktrain).
+//
+// Everything here is deterministic sequential or order-preserving code:
+// counting sorts instead of comparison sorts (stable, so duplicate edges
+// keep input order exactly like numpy's lexsort), merge-based set algebra,
+// and the LDG scores evaluated with the same IEEE double operations as the
+// numpy expression they restate.
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "ht_common.h"
+
+namespace ht {
+std::string& last_error() {
+  static thread_local std::string s;
+  return s;
+}
+}  // namespace ht
+
+using ht::fail;
+
+extern "C" const char* ht_last_error(void) { return ht::last_error().c_str(); }
+extern "C" int ht_version(void) { return 1; }
+
+namespace {
+
+// Stable counting sort of `idx` (positions into key[]) by key, keys in [0, K).
+void counting_pass(const int64_t* key, int64_t K, const std::vector<int64_t>& in,
+                   std::vector<int64_t>& out, std::vector<int64_t>& cnt) {
+  cnt.assign(K + 1, 0);
+  for (int64_t p : in) cnt[key[p] + 1]++;
+  for (int64_t k = 0; k < K; ++k) cnt[k + 1] += cnt[k];
+  out.resize(in.size());
+  for (int64_t p : in) out[cnt[key[p]]++] = p;
+}
+
+}  // namespace
+
+// graph.py:91-150 (from_edges + gcn_edge_weights)
+extern "C" int ht_build_graph(const int64_t* src, const int64_t* dst, int64_t E, int64_t V,
+                              int64_t* csc_offsets, int64_t* csc_sources, int64_t* csr_offsets,
+                              int64_t* csr_targets, int64_t* csr_edge_perm, double* weights) {
+  if (E < 0 || V < 0) return fail(HT_EINVAL, "negative graph size");
+  for (int64_t e = 0; e < E; ++e)
+    if (src[e] < 0 || dst[e] < 0 || src[e] >= V || dst[e] >= V)
+      return fail(HT_EINVAL, "edge %lld references a vertex outside [0, %lld)", (long long)e,
+                  (long long)V);
+  std::vector<int64_t> a(E), b, cnt;
+  std::iota(a.begin(), a.end(), 0);
+  // canonical order: by (dst, src), stable -> LSD: src pass then dst pass
+  counting_pass(src, V, a, b, cnt);
+  counting_pass(dst, V, b, a, cnt);
+  std::vector<int64_t> canon_rank(E);
+  for (int64_t p = 0; p < E; ++p) {
+    csc_sources[p] = src[a[p]];
+    canon_rank[a[p]] = p;
+  }
+  std::vector<int64_t> deg(V, 0);
+  for (int64_t e = 0; e < E; ++e) deg[dst[e]]++;
+  csc_offsets[0] = 0;
+  for (int64_t v = 0; v < V; ++v) csc_offsets[v + 1] = csc_offsets[v] + deg[v];
+  std::vector<double> inv(V);
+  for (int64_t v = 0; v < V; ++v) inv[v] = 1.0 / std::sqrt(1.0 + (double)deg[v]);
+  for (int64_t v = 0; v < V; ++v)
+    for (int64_t p = csc_offsets[v]; p < csc_offsets[v + 1]; ++p)
+      weights[p] = inv[csc_sources[p]] * inv[v];
+  // CSR order: by (src, dst), stable
+  std::iota(a.begin(), a.end(), 0);
+  counting_pass(dst, V, a, b, cnt);
+  counting_pass(src, V, b, a, cnt);
+  std::fill(deg.begin(), deg.end(), 0);
+  for (int64_t e = 0; e < E; ++e) deg[src[e]]++;
+  csr_offsets[0] = 0;
+  for (int64_t v = 0; v < V; ++v) csr_offsets[v + 1] = csr_offsets[v] + deg[v];
+  for (int64_t p = 0; p < E; ++p) {
+    csr_targets[p] = dst[a[p]];
+    csr_edge_perm[p] = canon_rank[a[p]];
+  }
+  return HT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// partition.py:102-209  LDG streaming partition + refinement + repair
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Adj {
+  const int64_t *co, *cs, *ro, *rt;
+  // visit every undirected neighbour of v (in-edges then out-edges, self
+  // loops dropped; duplicates kept, partition.py:102-120)
+  template <class F>
+  void each(int64_t v, F&& f) const {
+    for (int64_t p = co[v]; p < co[v + 1]; ++p)
+      if (cs[p] != v) f(cs[p]);
+    for (int64_t p = ro[v]; p < ro[v + 1]; ++p)
+      if (rt[p] != v) f(rt[p]);
+  }
+};
+
+void repair_empty(std::vector<int64_t>& sizes, int64_t* owner, int64_t V,
+                  const std::vector<int64_t>& adeg) {
+  const int64_t m = (int64_t)sizes.size();
+  for (;;) {
+    int64_t empty = -1;
+    for (int64_t p = 0; p < m; ++p)
+      if (sizes[p] == 0) { empty = p; break; }
+    if (empty < 0) return;
+    int64_t donor = 0;
+    for (int64_t p = 1; p < m; ++p)
+      if (sizes[p] > sizes[donor]) donor = p;
+    int64_t best = -1;
+    for (int64_t v = 0; v < V; ++v)
+      if (owner[v] == donor && (best < 0 || adeg[v] < adeg[best])) best = v;
+    owner[best] = empty;
+    sizes[donor]--;
+    sizes[empty]++;
+  }
+}
+
+}  // namespace
+
+extern "C" int ht_ldg_partition(int64_t V, const int64_t* csc_offsets, const int64_t* csc_sources,
+                                const int64_t* csr_offsets, const int64_t* csr_targets,
+                                const int64_t* arrival, int64_t m, int64_t cap, int64_t* owner) {
+  if (m < 1 || m > V) return fail(HT_EINVAL, "m=%lld outside [1, V]", (long long)m);
+  Adj adj{csc_offsets, csc_sources, csr_offsets, csr_targets};
+  std::vector<int64_t> adeg(V, 0);
+  for (int64_t v = 0; v < V; ++v) adj.each(v, [&](int64_t) { adeg[v]++; });
+  std::fill(owner, owner + V, (int64_t)-1);
+  std::vector<int64_t> sizes(m, 0), cnt(m);
+  const double dcap = (double)cap;
+  for (int64_t t = 0; t < V; ++t) {
+    const int64_t v = arrival[t];
+    std::fill(cnt.begin(), cnt.end(), 0);
+    adj.each(v, [&](int64_t u) {
+      if (owner[u] >= 0) cnt[owner[u]]++;
+    });
+    // pick the eligible partition minimising (-score, size, id)
+    int64_t pick = -1;
+    double best_neg = 0.0;
+    for (int64_t p = 0; p < m; ++p) {
+      if (sizes[p] >= cap) continue;
+      const double score = (double)cnt[p] * (1.0 - (double)sizes[p] / dcap);
+      const double neg = -score;
+      if (pick < 0 || neg < best_neg || (neg == best_neg && sizes[p] < sizes[pick])) {
+        pick = p;
+        best_neg = neg;
+      }
+    }
+    if (pick < 0) return fail(HT_EINVAL, "no partition below capacity");
+    owner[v] = pick;
+    sizes[pick]++;
+  }
+  repair_empty(sizes, owner, V, adeg);
+  // one refinement sweep, ascending vertex id
+  for (int64_t v = 0; v < V; ++v) {
+    if (adeg[v] == 0) continue;
+    const int64_t cur = owner[v];
+    if (sizes[cur] <= 1) continue;
+    std::fill(cnt.begin(), cnt.end(), 0);
+    adj.each(v, [&](int64_t u) { cnt[owner[u]]++; });
+    int64_t best = 0, best_val = 0;
+    for (int64_t p = 0; p < m; ++p) {
+      const int64_t val = (p == cur || sizes[p] < cap) ? cnt[p] : -1;
+      if (p == 0 || val > best_val) {
+        best = p;
+        best_val = val;
+      }
+    }
+    if (best != cur && best_val > cnt[cur]) {
+      owner[v] = best;
+      sizes[cur]--;
+      sizes[best]++;
+    }
+  }
+  repair_empty(sizes, owner, V, adeg);
+  return HT_OK;
+}
+
+// partition.py:235-267
+extern "C" int ht_chunk_fill(const int64_t* csc_offsets, const int64_t* csc_sources,
+                             const double* weights, const int64_t* verts, int64_t nv,
+                             int64_t* sources, int64_t* n_sources, int64_t* csc_off,
+                             int64_t* csc_local_src, double* edge_w, int64_t* csr_off,
+                             int64_t* csr_local_dst, int64_t* csr_perm) {
+  csc_off[0] = 0;
+  for (int64_t k = 0; k < nv; ++k) {
+    const int64_t v = verts[k];
+    csc_off[k + 1] = csc_off[k] + (csc_offsets[v + 1] - csc_offsets[v]);
+  }
+  const int64_t ne = csc_off[nv];
+  std::vector<int64_t> glob(ne), dl(ne);
+  for (int64_t k = 0; k < nv; ++k) {
+    const int64_t v = verts[k], base = csc_offsets[v];
+    for (int64_t q = csc_off[k]; q < csc_off[k + 1]; ++q) {
+      glob[q] = csc_sources[base + (q - csc_off[k])];
+      edge_w[q] = weights[base + (q - csc_off[k])];
+      dl[q] = k;
+    }
+  }
+  std::vector<int64_t> uniq(glob);
+  std::sort(uniq.begin(), uniq.end());
+  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+  const int64_t nn = (int64_t)uniq.size();
+  std::memcpy(sources, uniq.data(), nn * sizeof(int64_t));
+  *n_sources = nn;
+  std::vector<int64_t> cnt(nn + 1, 0);
+  for (int64_t q = 0; q < ne; ++q) {
+    csc_local_src[q] = std::lower_bound(uniq.begin(), uniq.end(), glob[q]) - uniq.begin();
+    cnt[csc_local_src[q] + 1]++;
+  }
+  for (int64_t s = 0; s < nn; ++s) cnt[s + 1] += cnt[s];
+  std::memcpy(csr_off, cnt.data(), (nn + 1) * sizeof(int64_t));
+  // stable by local source over canonical order == lexsort((dst, src))
+  for (int64_t q = 0; q < ne; ++q) {
+    const int64_t pos = cnt[csc_local_src[q]]++;
+    csr_perm[pos] = q;
+    csr_local_dst[pos] = dl[q];
+  }
+  return HT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// planner.py:45-63 sorted-set primitives, 252-284 layout, 386-450 reorganize
+// ---------------------------------------------------------------------------
+
+extern "C" int ht_set_op(int op, const int64_t* a, int64_t na, const int64_t* b, int64_t nb,
+                         int64_t* out, int64_t* n_out) {
+  int64_t* e;
+  switch (op) {
+    case 0: e = std::set_intersection(a, a + na, b, b + nb, out); break;
+    case 1: e = std::set_difference(a, a + na, b, b + nb, out); break;
+    case 2: e = std::set_union(a, a + na, b, b + nb, out); break;
+    default: return fail(HT_EINVAL, "unknown set op %d", op);
+  }
+  *n_out = e - out;
+  return HT_OK;
+}
+
+extern "C" int64_t ht_intersect_count(const int64_t* a, int64_t na, const int64_t* b,
+                                      int64_t nb) {
+  int64_t i = 0, j = 0, c = 0;
+  while (i < na && j < nb) {
+    if (a[i] < b[j]) ++i;
+    else if (b[j] < a[i]) ++j;
+    else { ++c; ++i; ++j; }
+  }
+  return c;
+}
+
+// Stable slots: rows live in consecutive batches keep their slot; new rows
+// (ascending id) take the free slots in ascending order, then fresh ones.
+// The reference's min-heap of evicted slots always holds exactly the slots
+// below the high-water mark not held by a carried row, so rank/select over
+// that complement reproduces it.
+extern "C" int ht_slot_layout(int64_t n, const int64_t* live, const int64_t* off,
+                              int64_t* slots, int64_t* capacity) {
+  int64_t top = 0;
+  std::vector<char> held;
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t lo = off[j], hi = off[j + 1];
+    held.assign(top, 0);
+    int64_t fresh = 0;
+    if (j > 0) {
+      const int64_t plo = off[j - 1], phi = off[j];
+      int64_t p = plo;
+      for (int64_t q = lo; q < hi; ++q) {
+        while (p < phi && live[p] < live[q]) ++p;
+        if (p < phi && live[p] == live[q]) {
+          slots[q] = slots[p];
+          held[slots[q]] = 1;
+        } else {
+          slots[q] = -1;
+          ++fresh;
+        }
+      }
+    } else {
+      for (int64_t q = lo; q < hi; ++q) slots[q] = -1;
+      fresh = hi - lo;
+    }
+    int64_t scan = 0;
+    for (int64_t q = lo; q < hi; ++q) {
+      if (slots[q] >= 0) continue;
+      while (scan < top && held[scan]) ++scan;
+      if (scan < top) {
+        slots[q] = scan++;
+      } else {
+        slots[q] = top++;
+        scan = top;
+      }
+    }
+    (void)fresh;
+  }
+  *capacity = top;
+  return HT_OK;
+}
+
+extern "C" int ht_reorganize(int64_t m, int64_t n, const int64_t* nbr, const int64_t* off,
+                             int move_all_rows, int64_t* chunk_orders, int64_t* batch_order) {
+  auto set = [&](int64_t i, int64_t j) {
+    const int64_t id = i * n + j;
+    return std::make_pair(nbr + off[id], off[id + 1] - off[id]);
+  };
+  std::vector<std::vector<int64_t>> acc(n);
+  for (int64_t j = 0; j < n; ++j) {
+    auto s = set(0, j);
+    acc[j].assign(s.first, s.first + s.second);
+    chunk_orders[j] = j;
+  }
+  std::vector<int64_t> tmp;
+  for (int64_t i = 1; i < m; ++i) {
+    std::vector<int64_t> left(n);
+    std::iota(left.begin(), left.end(), 0);
+    for (int64_t j = 0; j < n; ++j) {
+      int64_t best = 0, best_score = -1;
+      for (size_t t = 0; t < left.size(); ++t) {
+        auto s = set(i, left[t]);
+        const int64_t sc = ht_intersect_count(s.first, s.second, acc[j].data(), acc[j].size());
+        if (sc > best_score) { best_score = sc; best = (int64_t)t; }
+      }
+      const int64_t k = left[best];
+      left.erase(left.begin() + best);
+      chunk_orders[i * n + j] = k;
+      auto s = set(i, k);
+      tmp.resize(acc[j].size() + s.second);
+      tmp.resize(std::set_union(acc[j].begin(), acc[j].end(), s.first, s.first + s.second,
+                                tmp.begin()) - tmp.begin());
+      acc[j].swap(tmp);
+    }
+  }
+  std::vector<int64_t> left(n > 0 ? n - 1 : 0);
+  std::iota(left.begin(), left.end(), 1);
+  if (n > 0) batch_order[0] = 0;
+  for (int64_t pos = 1; pos < n; ++pos) {
+    const auto& prev = acc[batch_order[pos - 1]];
+    int64_t best = 0, best_score = -1;
+    for (size_t t = 0; t < left.size(); ++t) {
+      const auto& u = acc[left[t]];
+      const int64_t sc = ht_intersect_count(u.data(), u.size(), prev.data(), prev.size());
+      if (sc > best_score) { best_score = sc; best = (int64_t)t; }
+    }
+    batch_order[pos] = left[best];
+    left.erase(left.begin() + best);
+  }
+  // rows are emitted in batch order (row 0 optionally kept in place)
+  std::vector<int64_t> row(n);
+  for (int64_t i = 0; i < m; ++i) {
+    if (i == 0 && !move_all_rows) continue;
+    for (int64_t b = 0; b < n; ++b) row[b] = chunk_orders[i * n + batch_order[b]];
+    std::copy(row.begin(), row.end(), chunk_orders + i * n);
+  }
+  return HT_OK;
+}
+
+// synth.py:154-157: indices of the first occurrence of every distinct
+// (dst, src) pair, in ascending (dst, src) order - np.unique(dst*V+src,
+// return_index=True) without the 64-bit comparison sort.
+extern "C" int ht_dedup_edges(const int64_t* src, const int64_t* dst, int64_t E, int64_t V,
+                              int64_t* keep, int64_t* n_keep) {
+  for (int64_t e = 0; e < E; ++e)
+    if (src[e] < 0 || dst[e] < 0 || src[e] >= V || dst[e] >= V)
+      return fail(HT_EINVAL, "edge %lld outside [0, %lld)", (long long)e, (long long)V);
+  std::vector<int64_t> a(E), b, cnt;
+  std::iota(a.begin(), a.end(), 0);
+  counting_pass(src, V, a, b, cnt);
+  counting_pass(dst, V, b, a, cnt);
+  int64_t k = 0;
+  for (int64_t p = 0; p < E; ++p) {
+    const int64_t e = a[p];
+    if (p > 0) {
+      const int64_t q = a[p - 1];
+      if (src[q] == src[e] && dst[q] == dst[e]) continue;
+    }
+    keep[k++] = e;
+  }
+  *n_keep = k;
+  return HT_OK;
+}

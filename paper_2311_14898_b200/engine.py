@@ -1,0 +1,276 @@
+"""Model configuration and the partitioned full-graph GCN epoch on B200.
+
+Drop-in for the training entry points of ``chunktrain/engine.py``
+(``ModelConfig``, ``init_model``, ``train_epoch``, ``EpochResult``,
+``ActivationTracker``, ``sync_and_update``, ``comm_passes_per_epoch`` and
+the HTF1/HTL1 matrix files).  ``train_epoch`` drives the native layer
+kernels through the C ABI: per layer one call runs every batch of the
+chunk grid on the GPU(s), so Python only does bookkeeping (meters,
+sequencing, tracker) per batch.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .devices import PRECISIONS, DeviceArray, DeviceFleet, HostStore, _zero_rows
+from .errors import GraphFormatError, SimulationError
+from .partition import TwoLevelPartition
+
+KINDS = ("gcn", "gat")
+
+
+@dataclass(eq=False)
+class ModelConfig:
+    """Layer widths plus the replicated parameters (engine.py:37-69)."""
+
+    kind: str
+    dims: list
+    weights: list
+    attn: list | None
+    leaky_slope: float = 0.2
+    lr: float = 0.1
+    epochs: int = 1
+    seed: int = 0
+
+    @property
+    def num_layers(self) -> int:
+        return len(self.dims) - 1
+
+    def copy(self) -> "ModelConfig":
+        return ModelConfig(kind=self.kind, dims=list(self.dims),
+                           weights=[w.copy() for w in self.weights],
+                           attn=None if self.attn is None else [a.copy() for a in self.attn],
+                           leaky_slope=self.leaky_slope, lr=self.lr, epochs=self.epochs,
+                           seed=self.seed)
+
+
+def init_model(kind: str, dims: list, seed: int, *, lr: float = 0.1, epochs: int = 1,
+               leaky_slope: float = 0.2, dtype=np.float64) -> ModelConfig:
+    """Seeded Glorot-uniform weights, drawn in float64 in the order W (then
+    attention) layer by layer, then cast (engine.py:72-99)."""
+    if kind not in KINDS:
+        raise SimulationError(f"unknown model kind {kind!r}")
+    if len(dims) < 2:
+        raise SimulationError("dims needs at least an input and output width")
+    dtype = np.dtype(dtype)
+    gen = np.random.default_rng(seed)
+    weights, attn = [], ([] if kind == "gat" else None)
+    for a, b in zip(dims[:-1], dims[1:]):
+        lim = np.sqrt(6.0 / (a + b))
+        weights.append(gen.uniform(-lim, lim, size=(a, b)).astype(dtype))
+        if kind == "gat":
+            la = np.sqrt(6.0 / (2 * b + 1))
+            attn.append(gen.uniform(-la, la, size=2 * b).astype(dtype))
+    return ModelConfig(kind=kind, dims=list(dims), weights=weights, attn=attn,
+                       leaky_slope=leaky_slope, lr=lr, epochs=epochs, seed=seed)
+
+
+class ActivationTracker:
+    """Counts live chunk intermediates (engine.py:352-372)."""
+
+    def __init__(self):
+        self._live = set()
+        self.peak = 0
+
+    def acquire(self, tag) -> None:
+        if tag in self._live:
+            raise SimulationError(f"intermediate {tag} acquired twice")
+        self._live.add(tag)
+        self.peak = max(self.peak, len(self._live))
+
+    def release(self, tag) -> None:
+        self._live.discard(tag)
+
+    @property
+    def live_count(self) -> int:
+        return len(self._live)
+
+
+@dataclass(eq=False)
+class EpochResult:
+    loss: float
+    model: ModelConfig
+    tracker: ActivationTracker = field(default_factory=ActivationTracker)
+    grads: list | None = None   # summed weight gradients of this epoch (new)
+
+
+def sync_and_update(model: ModelConfig, device_grads: list, lr: float | None = None) -> ModelConfig:
+    """Replica-gradient sum in ascending device order + plain SGD
+    (engine.py:328-344), for callers holding per-device gradients."""
+    lr = model.lr if lr is None else lr
+    for l in range(model.num_layers):
+        tot = np.zeros_like(model.weights[l])
+        for dg in device_grads:
+            tot += dg["W"][l]
+        model.weights[l] -= lr * tot
+        if model.kind == "gat":
+            ta = np.zeros_like(model.attn[l])
+            for dg in device_grads:
+                ta += dg["a"][l]
+            model.attn[l] -= lr * ta
+    return model
+
+
+def comm_passes_per_epoch(model: ModelConfig) -> tuple:
+    L = model.num_layers
+    return (2 * L, L) if model.kind == "gat" else (L, L)
+
+
+def _epoch_reset(host: HostStore, fleet: DeviceFleet) -> None:
+    """reset_epoch with the same observable result but without rewriting
+    rows the epoch overwrites anyway: the loss writes every row of
+    grad_h[L], and in p2p/full mode the first flush of a row stores it, so
+    only rows no chunk ever reads need explicit zeros."""
+    L = len(host.dims) - 1
+    for l in range(1, len(host.h)):
+        host.h_valid[l] = False
+    host.agg_written.clear()
+    for l in range(L):
+        g = host.grad_h[l]
+        if isinstance(g, DeviceArray) or fleet.mode == "baseline":
+            _zero_rows(g, None)
+        else:
+            _zero_rows(g, fleet._untouched)
+
+
+def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, host: HostStore,
+                labels: np.ndarray, mask: np.ndarray,
+                tracker: ActivationTracker | None = None) -> EpochResult:
+    """One full-graph epoch over the chunk grid on the GPU (engine.py:387-480).
+
+    Forward: per layer, every batch stages its deduplicated neighbour rows
+    (host loads, barrier, peer fetches, barrier), aggregates them, applies
+    z = agg.W and ReLU, and writes h^{l+1} and the agg checkpoint rows to
+    the host store.  Loss on the last layer.  Backward: checkpoint and
+    dest-gradient reload, hybrid recompute, transposed aggregation, owner
+    push and flush into grad_h[l].  Then the ascending-device gradient sum
+    and the SGD step, in place on model.weights.
+    """
+    if tracker is None:
+        tracker = ActivationTracker()
+    if model.kind != "gcn":
+        raise SimulationError(f"model kind {model.kind!r} is not on the B200 path yet (gcn only)")
+    if not host.h_valid[0]:
+        raise SimulationError("host features not set; call set_features first")
+    if host.dtype != np.float32 or fleet.dtype != np.float32:
+        raise SimulationError("the B200 path computes in float32; build HostStore and "
+                              "DeviceFleet with dtype=np.float32")
+    m, n, L = p.m, p.n, model.num_layers
+    dims = [int(d) for d in model.dims]
+    if list(host.dims) != dims:
+        raise SimulationError("host store widths do not match the model")
+    W = []
+    for l, w in enumerate(model.weights):
+        if w.dtype != np.float32 or not w.flags.c_contiguous or w.shape != (dims[l], dims[l + 1]):
+            model.weights[l] = np.ascontiguousarray(w, dtype=np.float32).reshape(dims[l], dims[l + 1])
+        W.append(model.weights[l])
+    prec = PRECISIONS[fleet.precision]
+    fleet.attach_partition(p)
+    _epoch_reset(host, fleet)
+    h_ = fleet._handle
+    item = host.dtype.itemsize
+    dims_c = (C.c_int * (L + 1))(*dims)
+    N.call("ht_epoch_begin", h_, L, dims_c)
+
+    # ---- forward (Alg. 1 lines 4-9) ----
+    for l in range(L):
+        fleet._dim = dims[l]
+        fleet._fwd_next = None
+        agg = host.agg_array(l)
+        N.call("ht_forward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(host.h[l]),
+               N.ptr(host.h[l + 1]), N.ptr(agg), prec)
+        for j in range(n):
+            fleet._meter_fwd(j, dims[l] * item)
+            for i in range(m):
+                tag = ("fwd", l, i, j)
+                tracker.acquire(tag)
+                tracker.release(tag)
+                host.agg_written.add((l, i, j))
+            fleet._meter_dest(j, dims[l + 1] * item, "d2h")
+            fleet._meter_dest(j, dims[l] * item, "d2h", "chkpt")
+        host.h_valid[l + 1] = True
+
+    # ---- loss ----
+    mask_b = np.ascontiguousarray(np.asarray(mask, dtype=bool))
+    labels_i = np.ascontiguousarray(np.asarray(labels, dtype=np.int64))
+    count = int(mask_b.sum())
+    if count == 0:
+        warnings.warn("training mask is empty; loss is 0", stacklevel=2)
+    loss = C.c_double(0.0)
+    N.call("ht_loss", h_, dims[L], N.ptr(labels_i), N.ptr(mask_b.view(np.uint8)),
+           int(host.num_vertices), count, N.ptr(host.grad_h[L]), C.byref(loss))
+
+    # ---- backward (Alg. 1 lines 12-20) ----
+    for l in reversed(range(L)):
+        fleet._dim = dims[l]
+        N.call("ht_backward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(host.agg[l]),
+               N.ptr(host.grad_h[l + 1]), N.ptr(host.grad_h[l]), prec)
+        for j in range(n):
+            fleet._meter_dest(j, dims[l] * item, "h2d", "chkpt")
+            fleet._meter_dest(j, dims[l + 1] * item, "h2d")
+            for i in range(m):
+                tag = ("bwd", l, i, j)
+                tracker.acquire(tag)
+                tracker.release(tag)
+            fleet._meter_bwd(j, dims[l] * item)
+    fleet._fwd_next = fleet._bwd_next = None
+
+    # ---- replica gradient sum + SGD (engine.py:479) ----
+    grads = [np.empty_like(w) for w in W]
+    wp = (C.c_void_p * L)(*[N.ptr(w) for w in W])
+    gp = (C.c_void_p * L)(*[N.ptr(g) for g in grads])
+    N.call("ht_sgd", h_, L, dims_c, wp, C.c_float(model.lr), gp)
+    return EpochResult(loss=float(loss.value), model=model, tracker=tracker, grads=grads)
+
+
+_MATRIX_MAGIC = b"HTF1"
+_LABELS_MAGIC = b"HTL1"
+
+
+def save_matrix(X: np.ndarray, path: str) -> None:
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim != 2:
+        raise GraphFormatError("matrix files hold 2-D arrays")
+    with open(path, "wb") as fh:
+        fh.write(_MATRIX_MAGIC)
+        fh.write(struct.pack("<QQ", X.shape[0], X.shape[1]))
+        fh.write(X.astype("<f8").tobytes())
+
+
+def load_matrix(path: str) -> np.ndarray:
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != _MATRIX_MAGIC:
+            raise GraphFormatError(f"{path}: bad magic {magic!r}, expected {_MATRIX_MAGIC!r}")
+        rows, cols = struct.unpack("<QQ", fh.read(16))
+        raw = fh.read(rows * cols * 8)
+        if len(raw) != rows * cols * 8:
+            raise GraphFormatError(f"{path}: truncated payload")
+        return np.frombuffer(raw, dtype="<f8").reshape(rows, cols).copy()
+
+
+def save_labels(y: np.ndarray, path: str) -> None:
+    y = np.asarray(y, dtype=np.int64)
+    with open(path, "wb") as fh:
+        fh.write(_LABELS_MAGIC)
+        fh.write(struct.pack("<Q", y.shape[0]))
+        fh.write(y.astype("<i8").tobytes())
+
+
+def load_labels(path: str) -> np.ndarray:
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != _LABELS_MAGIC:
+            raise GraphFormatError(f"{path}: bad magic {magic!r}, expected {_LABELS_MAGIC!r}")
+        (count,) = struct.unpack("<Q", fh.read(8))
+        raw = fh.read(count * 8)
+        if len(raw) != count * 8:
+            raise GraphFormatError(f"{path}: truncated payload")
+        return np.frombuffer(raw, dtype="<i8").copy()

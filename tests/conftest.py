@@ -21,6 +21,7 @@ for p in (ROOT, GOLDEN):
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path)")
+    config.addinivalue_line("markers", "slow: config-1 sized checks (seconds to a minute)")
 
 
 def _has_gpu():
@@ -90,3 +91,19 @@ def random_set_instances(count=200, seed=123):
             nbrs.append(row)
         out.append((nbrs, owner))
     return out
+
+
+def random_graph(rng, num_vertices=None, num_edges=None):
+    """Random directed multigraph (reference tests/conftest.py:85-91 recipe)."""
+    import paper_2311_14898_b200 as H
+    V = int(rng.integers(4, 40)) if num_vertices is None else num_vertices
+    E = int(rng.integers(V, 6 * V)) if num_edges is None else num_edges
+    src = rng.integers(0, V, size=E)
+    dst = rng.integers(0, V, size=E)
+    return H.from_edges(src, dst, num_vertices=V)
+
+
+def random_two_level(g, rng, m, n):
+    import paper_2311_14898_b200 as H
+    owner = rng.permutation(np.arange(g.num_vertices, dtype=np.int64) % m)
+    return H.split_chunks(g, H.PartitionAssignment(owner=owner, m=m), n)
