@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native HongTu GCN epoch (one step = one full-graph
+training epoch: forward over every layer and batch, loss, backward, SGD).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+    python bench.py --impl reference ...     # CPU reference arm (oracle port)
+
+Workload (N=1): BASELINE config 2 - 3-layer GCN 100-256-256-47 on an
+ogbn-products-shape synthetic graph (2.4M vertices, ~62M edges), m = N
+partitions, n = 1 chunk per partition, mode "full", reorganized when the
+Eq. 4 cost is lower (the reference CLI's rule).
+
+Two measurements of the same metric (GTEPS = L*|E| / epoch seconds):
+  value  HBM-resident vertex store (HongTu-IM: inputs already in HBM),
+  e2e    the reference-facing path: HostStore in pinned host memory, every
+         row crossing PCIe inside the timed region (the HongTu setting).
+Both are timed with CUDA events recorded on the fleet's own streams
+(max over devices), after W warm-up epochs, around exactly K epochs.
+Inputs exceed L2 (62M edges, 2.4M x 1 KB rows), so no explicit flush.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(V=100_000, avg_degree=20.0, dims=[64, 128, 16], n=4, seed=0,
+                 name="2-layer GCN 64-128-16, synthetic power-law 100K V / ~1.87M E"),
+    "cfg2": dict(V=2_400_000, avg_degree=26.8, dims=[100, 256, 256, 47], n=1, seed=0,
+                 name="3-layer GCN 100-256-256-47, ogbn-products-shape synthetic 2.4M V / ~62M E"),
+}
+METRIC = "full-graph GCN epoch GTEPS (L*|E|/epoch_s)"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu=0):
+        self.rows, self.gpu, self.proc = [], gpu, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for nm, v in zip(names, r[4:8]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+def build_inputs(cfg, m):
+    import paper_2311_14898_b200 as H
+    t0 = time.time()
+    spec = H.SynthSpec(num_vertices=cfg["V"], avg_degree=cfg["avg_degree"], seed=cfg["seed"])
+    ds = H.synth_dataset(spec, cfg["dims"][0], cfg["dims"][-1])
+    t1 = time.time()
+    a = H.partition_vertices(ds.graph, m, seed=cfg["seed"])
+    p = H.split_chunks(ds.graph, a, cfg["n"])
+    plan = H.plan_for_partition(p)
+    chosen = "identity"
+    if cfg["n"] > 1:
+        r = H.reorganize(p)
+        plan_r = H.plan_for_partition(r.partition)
+        if H.comm_cost(plan_r.volumes) <= H.comm_cost(plan.volumes):
+            p, plan, chosen = r.partition, plan_r, "reorganized"
+    t2 = time.time()
+    log(f"[bench] synth {t1 - t0:.1f}s  partition+plan {t2 - t1:.1f}s  |E|={ds.graph.num_edges}")
+    return ds, p, plan, chosen
+
+
+def host_bytes_per_epoch(plan, dims, mode="full"):
+    """Host<->GPU bytes of one epoch from the plan (SURVEY 8(d) formulas,
+    fp32): neighbour loads/flushes + destination + checkpoint rows, plus the
+    loss gradient rows this path writes to host.grad_h[L]."""
+    import paper_2311_14898_b200 as H
+    L = len(dims) - 1
+    pred = H.predicted_transfers(plan, mode)
+    V = int(plan.owner.shape[0])
+    h2d = d2h = 0
+    for l in range(L):
+        h2d += 4 * (pred["fwd_h2d_rows"] * dims[l] + V * (dims[l] + dims[l + 1]))
+        d2h += 4 * (V * (dims[l + 1] + dims[l]) + pred["bwd_d2h_rows"] * dims[l])
+    d2h += 4 * V * dims[L]
+    h2d += V * 9  # labels (int64) + mask (uint8) upload for the loss
+    return h2d, d2h
+
+
+def reference_cpu_sample(ds, dims, budget_edges=1_500_000, threads=None):
+    """Time the oracle port (numpy restatement of the reference's chunk
+    kernels, the CPU implementation of this path) on a bounded sample:
+    layer-0 forward + hybrid backward over the first destination vertices
+    holding ~budget_edges in-edges; extrapolate to a full epoch by
+    sum_l |E| * d_l."""
+    from oracle import hongtu_oracle as O
+    g = ds.graph
+    gd = {k: getattr(g, k) for k in ("csc_offsets", "csc_sources", "edge_weights")}
+    gd["num_vertices"] = g.num_vertices
+    k = int(np.searchsorted(g.csc_offsets, budget_edges))
+    verts = np.arange(max(k, 1), dtype=np.int64)
+    ch = O.chunk_of(gd, verts)
+    X = np.asarray(ds.features[ch["sources"]], dtype=np.float32)
+    W = O.glorot_weights(dims[:2], 0, dtype=np.float32)[0]
+    gout = np.random.default_rng(0).standard_normal((verts.size, dims[1])).astype(np.float32)
+    t0 = time.perf_counter()
+    _, agg, _ = O.gcn_chunk_forward(ch, X, W)
+    O.gcn_chunk_backward(ch, agg, gout, W)
+    dt = time.perf_counter() - t0
+    es = int(ch["csc_local_src"].size)
+    L = len(dims) - 1
+    scale = sum(g.num_edges * dims[l] for l in range(L)) / (es * dims[0])
+    epoch_s = dt * scale
+    return {"epoch_s_extrapolated": epoch_s, "gteps": L * g.num_edges / epoch_s / 1e9,
+            "sample_s": dt, "sample_edges": es,
+            "sample": (f"layer-0 forward+backward (oracle port, numpy fp32) over the first "
+                       f"{verts.size} destinations ({es} edges, d={dims[0]}->{dims[1]}), "
+                       f"extrapolated x{scale:.1f} by sum_l |E|*d_l"),
+            "cores": threads or os.cpu_count()}
+
+
+# ---------------------------------------------------------------------------
+# timed epochs
+# ---------------------------------------------------------------------------
+def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed):
+    import paper_2311_14898_b200 as H
+    from paper_2311_14898_b200 import _native as N
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement)
+    host.set_features(ds.features)
+    fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision)
+    model = H.init_model("gcn", dims, seed=seed, lr=0.1, dtype=np.float32)
+    losses = []
+    for _ in range(warmup):
+        losses.append(H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss)
+    fleet.set_timing(timing)
+    for d in fleet.devices:  # meters of the timed region only
+        for k, v in d.counter_dict().items():
+            setattr(d, k, 0)
+    l0 = N.lib().ht_launches()
+    N.call("ht_fleet_mark", fleet._handle, 0)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        losses.append(H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss)
+    N.call("ht_fleet_mark", fleet._handle, 1)
+    ms = C.c_double(0)
+    N.call("ht_fleet_elapsed", fleet._handle, C.byref(ms))
+    wall = time.perf_counter() - t0
+    launches = N.lib().ht_launches() - l0
+    stats = {w: fleet.kernel_stats(w) for w in range(4)} if timing else {}
+    rep = fleet.transfer_report()
+    del host
+    return {"ms_total": ms.value, "wall_s": wall, "losses": losses, "launches": launches,
+            "stats": stats, "report": rep, "fleet": fleet}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fp32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    N_gpus = args.gpus if world == 1 else world
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    cfg = CONFIGS[args.config]
+    dims = cfg["dims"]
+    L = len(dims) - 1
+    if rank != 0:
+        # the fleet drives every GPU from rank 0 (single-process multi-GPU
+        # until the per-rank path lands); other ranks only join barriers
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    m = N_gpus
+    ds, p, plan, chosen = build_inputs(cfg, m)
+    E = ds.graph.num_edges
+    config = {"workload": cfg["name"], "config_id": args.config, "vertices": cfg["V"],
+              "edges": E, "dims": dims, "m": m, "n": cfg["n"], "mode": "full",
+              "ordering": chosen, "l2": "inputs larger than L2 (no flush)"}
+
+    if args.impl == "reference":
+        threads = os.cpu_count()
+        times = []
+        for s in range(args.warmup + args.steps):
+            r = reference_cpu_sample(ds, dims, threads=threads)
+            if s >= args.warmup:
+                times.append(r["epoch_s_extrapolated"])
+        epoch_s = statistics.mean(times)
+        v = L * E / epoch_s / 1e9
+        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GTEPS",
+               "n_gpus": N_gpus, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": epoch_s * 1e3, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+               "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": threads, "kind": "port",
+                                "sample": r["sample"]},
+               "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+
+    # ---- value: HBM-resident vertex store ----
+    with Clocks() as clk_v:
+        val = run_epochs(p, plan, ds, dims, "device", args.steps, args.warmup, args.precision,
+                         True, cfg["seed"])
+    ms_v = val["ms_total"] / args.steps
+    # ---- e2e: pinned host-resident vertex store through train_epoch ----
+    with Clocks() as clk_e:
+        e2e = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,
+                         True, cfg["seed"])
+    ms_e = e2e["ms_total"] / args.steps
+    h2d, d2h = host_bytes_per_epoch(plan, dims)
+    base_h2d, base_d2h = host_bytes_per_epoch(plan, dims, "baseline")
+
+    # dominant kernel of the value run: the aggregation kernels (fwd CSC + bwd CSR)
+    lf, msf, bf = val["stats"][0]
+    lb, msb, bb = val["stats"][1]
+    agg_ms = msf + msb
+    achieved = (bf + bb) / (agg_ms / 1e3) / 1e9 if agg_ms > 0 else 0.0
+    lg, msg, flops = val["stats"][2]
+    lt, mst, tb = e2e["stats"][3]
+    roofline = {"bound": "hbm", "kernel": "k_seg_gather (CSC forward + CSR backward aggregation)",
+                "achieved": achieved, "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
+                "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                "launches_per_step": (lf + lb) / args.steps,
+                "share_of_step": agg_ms / val["ms_total"] if val["ms_total"] else None}
+    cpu = None
+    if not args.no_cpu_baseline:
+        r = reference_cpu_sample(ds, dims)
+        cpu = {"value": r["gteps"], "unit": "GTEPS", "cores": r["cores"], "kind": "port",
+               "sample": r["sample"], "epoch_s_extrapolated": r["epoch_s_extrapolated"],
+               "note": "numpy np.add.at-style aggregation is single-threaded; BLAS uses all cores"}
+    value = L * E / (ms_v / 1e3) / 1e9
+    e2e_v = L * E / (ms_e / 1e3) / 1e9
+    out = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": N_gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_v,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded clustered power-law graph, random-init Glorot weights)",
+        "config": config,
+        "e2e": {"value": e2e_v, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e,
+                "pcie_gbs": (h2d + d2h) / (ms_e / 1e3) / 1e9,
+                "transfer_kernel_ms_per_step": mst / args.steps},
+        "epoch_s": {"hbm_resident": ms_v / 1e3, "host_resident": ms_e / 1e3},
+        "host_gb_per_epoch": {"dedup_full": (h2d + d2h) / 1e9,
+                              "non_dedup_baseline_plan": (base_h2d + base_d2h) / 1e9},
+        "gpu_launches": int(val["launches"]),
+        "gpu_launches_e2e": int(e2e["launches"]),
+        "roofline": roofline,
+        "gemm": {"ms_per_step": msg / args.steps, "tflops": flops / (msg / 1e3) / 1e12 if msg else None,
+                 "precision": args.precision},
+        "cpu_baseline": cpu,
+        "clocks": clk_e.summary(),
+        "clocks_value_run": clk_v.summary(),
+        "losses": {"value": val["losses"][-1], "e2e": e2e["losses"][-1]},
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

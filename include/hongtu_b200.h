@@ -189,6 +189,14 @@ int ht_fleet_sync(ht_fleet* f);
 int ht_set_timing(ht_fleet* f, int enabled);
 int ht_kernel_stats(ht_fleet* f, int which, int64_t* launches, double* ms, double* bytes);
 
+/* Device-timeline marks: record event `which` (0 = start, 1 = stop) on
+ * every device stream; ht_fleet_elapsed returns the max over devices of
+ * stop - start in milliseconds (bench.py's CUDA-event timing). */
+int ht_fleet_mark(ht_fleet* f, int which);
+int ht_fleet_elapsed(ht_fleet* f, double* ms);
+/* Number of kernels this library has launched (process-wide). */
+int64_t ht_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

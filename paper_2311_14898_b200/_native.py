@@ -71,6 +71,9 @@ _SIGS = {
     "ht_fleet_sync": (i32, [vp]),
     "ht_set_timing": (i32, [vp, i32]),
     "ht_kernel_stats": (i32, [vp, i32, P_I64, P_F64, P_F64]),
+    "ht_fleet_mark": (i32, [vp, i32]),
+    "ht_fleet_elapsed": (i32, [vp, P_F64]),
+    "ht_launches": (i64, []),
 }
 
 _lib = None

@@ -5,6 +5,7 @@
 // points).
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -28,6 +29,8 @@ namespace {
 
 constexpr int64_t kSplit = 4096;   // long-segment piece length (edges)
 constexpr int kThreads = 256;
+std::atomic<int64_t> g_launches{0};  // kernels launched by this library
+inline void count_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 // Grow-only device allocation.
 struct DBuf {
@@ -114,6 +117,7 @@ struct Device {
   std::vector<int64_t> hL_off;         // row offset of batch j inside hL
   DBuf labels, mask, loss_part;
   std::vector<DevChunk> chunks;
+  cudaEvent_t mark[2] = {nullptr, nullptr};
 };
 
 }  // namespace
@@ -196,6 +200,7 @@ int launch_copy(cudaStream_t s, void* dst, const void* src, const int64_t* didx,
   const uintptr_t al = (uintptr_t)dst | (uintptr_t)src | (uintptr_t)row_bytes |
                        (uintptr_t)dstride | (uintptr_t)sstride;
   const int g = grid_for(rows);
+  count_launch();
   if ((al & 15) == 0)
     ht::k_copy_rows<int4><<<g, kThreads, 0, s>>>((char*)dst, (const char*)src, didx, sidx, rows,
                                                 (int)(row_bytes / 16), dstride, sstride, dbase);
@@ -214,6 +219,7 @@ int launch_acc(cudaStream_t s, int elem, void* dst, void* src, const int64_t* di
                int64_t sbase = 0) {
   if (rows <= 0) return HT_OK;
   const int g = grid_for(rows);
+  count_launch();
   if (elem == 4)
     ht::k_acc_rows<float><<<g, kThreads, 0, s>>>((float*)dst, (float*)src, didx, sidx, first, rows,
                                                 d, zero_src, sbase);
@@ -258,6 +264,7 @@ int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, c
                float* partial) {
   if (nseg <= 0) return HT_OK;
   const int g = grid_for(nseg);
+  count_launch(1 + (np ? 1 : 0) + (nf ? 1 : 0));
   if (d % 4 == 0 && d <= 512) {
     const int nv = (d / 4 + 31) / 32;
 #define SEGV(NV)                                                                               \
@@ -300,6 +307,7 @@ int gemm(cudaStream_t s, const float* A, int64_t lda, const float* B, int64_t ld
          int64_t kps) {
   if (M <= 0 || N <= 0) return HT_OK;
   dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)splits);
+  count_launch();
   ht::k_gemm<TA, TB, EPI><<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, G, ldg, M, N, K, kps);
   CU(cudaGetLastError());
   return HT_OK;
@@ -474,6 +482,8 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
       for (auto& cl : c.push) cl.src.release(), cl.dst.release();
     }
     if (d.ev) cudaEventDestroy(d.ev);
+    for (auto& e : d.mark)
+      if (e) cudaEventDestroy(e);
     if (d.stream) cudaStreamDestroy(d.stream);
   }
   delete f;
@@ -945,6 +955,7 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
     CU(cudaMemcpyAsync(d.mask.p, mask, V, cudaMemcpyHostToDevice, d.stream));
     for (int j = 0; j < f->n; ++j) {
       DevChunk& c = d.chunks[j];
+      count_launch();
       ht::k_loss<<<blocks, 256, 0, d.stream>>>(
           d.hL.as<float>() + d.hL_off[j] * d_last, c.nv, d_last, d.labels.as<int64_t>(),
           d.mask.as<uint8_t>(), c.dest_rows.as<int64_t>(), (float*)gout, (float)count,
@@ -1023,6 +1034,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
                                                    d.gemm_ws.as<float>(), d_out, nullptr, 0, d_in,
                                                    d_out, M, splits, kps)));
           const int64_t nw = (int64_t)d_in * d_out;
+          count_launch();
           ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
               d.gW[layer].as<float>(), d.gemm_ws.as<float>(), nw, splits);
           CU(cudaGetLastError());
@@ -1061,6 +1073,7 @@ extern "C" int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, floa
     HT_TRY(wbuf.ensure(nw * 4));
     HT_TRY(tbuf.ensure(nw * 4));
     CU(cudaMemcpyAsync(wbuf.p, W[l], nw * 4, cudaMemcpyHostToDevice, d0.stream));
+    count_launch();
     ht::k_sgd<<<grid_for(nw / 32 + 1), 256, 0, d0.stream>>>(wbuf.as<float>(), tbuf.as<float>(),
                                                            pbuf.as<const float*>(), f->m, nw, lr);
     CU(cudaGetLastError());
@@ -1090,3 +1103,32 @@ extern "C" int ht_kernel_stats(ht_fleet* f, int which, int64_t* launches, double
   *bytes = f->t_bytes[which];
   return HT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// device-timeline marks for the benchmark: events on every device stream
+// ---------------------------------------------------------------------------
+extern "C" int ht_fleet_mark(ht_fleet* f, int which) {
+  if (which < 0 || which > 1) return fail(HT_EINVAL, "mark index must be 0 or 1");
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    if (!d.mark[which]) CU(cudaEventCreate(&d.mark[which]));
+    CU(cudaEventRecord(d.mark[which], d.stream));
+  }
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_elapsed(ht_fleet* f, double* ms) {
+  double mx = 0.0;
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    if (!d.mark[0] || !d.mark[1]) return fail(HT_ESTATE, "marks not recorded");
+    CU(cudaEventSynchronize(d.mark[1]));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, d.mark[0], d.mark[1]));
+    mx = std::max(mx, (double)t);
+  }
+  *ms = mx;
+  return HT_OK;
+}
+
+extern "C" int64_t ht_launches(void) { return g_launches.load(); }
