@@ -14,7 +14,8 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libhongtu_b200.so")
 SOURCES = ["ht_fleet.cu", "ht_prep.cpp"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
-              "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC,-O3,-fopenmp", "-shared", "-cudart", "static", "-lgomp",
+              "-Xptxas", "-v"]
 
 
 def _stale() -> bool:

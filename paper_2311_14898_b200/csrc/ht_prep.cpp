@@ -13,6 +13,8 @@
 #include <numeric>
 #include <vector>
 
+#include <omp.h>
+
 #include "ht_common.h"
 
 namespace ht {
@@ -29,14 +31,33 @@ extern "C" int ht_version(void) { return 1; }
 
 namespace {
 
-// Stable counting sort of `idx` (positions into key[]) by key, keys in [0, K).
-void counting_pass(const int64_t* key, int64_t K, const std::vector<int64_t>& in,
-                   std::vector<int64_t>& out, std::vector<int64_t>& cnt) {
-  cnt.assign(K + 1, 0);
-  for (int64_t p : in) cnt[key[p] + 1]++;
-  for (int64_t k = 0; k < K; ++k) cnt[k + 1] += cnt[k];
-  out.resize(in.size());
-  for (int64_t p : in) out[cnt[key[p]]++] = p;
+// Edge positions grouped by key (stable, original order inside a group):
+// one counting scatter.  Returns the group offsets.
+void group_by(const int64_t* key, int64_t E, int64_t K, std::vector<int64_t>& out,
+              std::vector<int64_t>& off) {
+  off.assign(K + 1, 0);
+  for (int64_t e = 0; e < E; ++e) off[key[e] + 1]++;
+  for (int64_t k = 0; k < K; ++k) off[k + 1] += off[k];
+  std::vector<int64_t> cur(off.begin(), off.end() - 1);
+  out.resize(E);
+  for (int64_t e = 0; e < E; ++e) out[cur[key[e]]++] = e;
+}
+
+// Inside every group, order positions by (key2, position): a stable sort
+// on key2.  Groups are small (degrees), so this is cache friendly and runs
+// group-parallel.
+void sort_groups(std::vector<int64_t>& pos, const std::vector<int64_t>& off, const int64_t* key2) {
+  const int64_t G = (int64_t)off.size() - 1;
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t g = 0; g < G; ++g) {
+    int64_t* b = pos.data() + off[g];
+    int64_t* e = pos.data() + off[g + 1];
+    if (e - b < 2) continue;
+    bool sorted = true;
+    for (int64_t* q = b + 1; q < e; ++q)
+      if (key2[*(q - 1)] > key2[*q]) { sorted = false; break; }
+    if (!sorted) std::stable_sort(b, e, [&](int64_t x, int64_t y) { return key2[x] < key2[y]; });
+  }
 }
 
 }  // namespace
@@ -46,41 +67,50 @@ extern "C" int ht_build_graph(const int64_t* src, const int64_t* dst, int64_t E,
                               int64_t* csc_offsets, int64_t* csc_sources, int64_t* csr_offsets,
                               int64_t* csr_targets, int64_t* csr_edge_perm, double* weights) {
   if (E < 0 || V < 0) return fail(HT_EINVAL, "negative graph size");
+  int bad = 0;
+#pragma omp parallel for reduction(| : bad)
   for (int64_t e = 0; e < E; ++e)
-    if (src[e] < 0 || dst[e] < 0 || src[e] >= V || dst[e] >= V)
-      return fail(HT_EINVAL, "edge %lld references a vertex outside [0, %lld)", (long long)e,
-                  (long long)V);
-  std::vector<int64_t> a(E), b, cnt;
-  std::iota(a.begin(), a.end(), 0);
-  // canonical order: by (dst, src), stable -> LSD: src pass then dst pass
-  counting_pass(src, V, a, b, cnt);
-  counting_pass(dst, V, b, a, cnt);
+    bad |= (src[e] < 0 || dst[e] < 0 || src[e] >= V || dst[e] >= V);
+  if (bad) return fail(HT_EINVAL, "an edge references a vertex outside [0, %lld)", (long long)V);
+  // canonical order: by (dst, src), ties by input position
+  bool canonical = true;
+  for (int64_t e = 1; e < E && canonical; ++e)
+    canonical = dst[e - 1] < dst[e] || (dst[e - 1] == dst[e] && src[e - 1] <= src[e]);
+  std::vector<int64_t> a, off;
+  if (canonical) {
+    a.resize(E);
+    std::iota(a.begin(), a.end(), 0);
+    off.assign(V + 1, 0);
+    for (int64_t e = 0; e < E; ++e) off[dst[e] + 1]++;
+    for (int64_t v = 0; v < V; ++v) off[v + 1] += off[v];
+  } else {
+    group_by(dst, E, V, a, off);
+    sort_groups(a, off, src);
+  }
+  std::memcpy(csc_offsets, off.data(), (V + 1) * sizeof(int64_t));
   std::vector<int64_t> canon_rank(E);
+#pragma omp parallel for
   for (int64_t p = 0; p < E; ++p) {
     csc_sources[p] = src[a[p]];
     canon_rank[a[p]] = p;
   }
-  std::vector<int64_t> deg(V, 0);
-  for (int64_t e = 0; e < E; ++e) deg[dst[e]]++;
-  csc_offsets[0] = 0;
-  for (int64_t v = 0; v < V; ++v) csc_offsets[v + 1] = csc_offsets[v] + deg[v];
   std::vector<double> inv(V);
-  for (int64_t v = 0; v < V; ++v) inv[v] = 1.0 / std::sqrt(1.0 + (double)deg[v]);
+#pragma omp parallel for
+  for (int64_t v = 0; v < V; ++v) inv[v] = 1.0 / std::sqrt(1.0 + (double)(off[v + 1] - off[v]));
+#pragma omp parallel for schedule(dynamic, 4096)
   for (int64_t v = 0; v < V; ++v)
-    for (int64_t p = csc_offsets[v]; p < csc_offsets[v + 1]; ++p)
-      weights[p] = inv[csc_sources[p]] * inv[v];
-  // CSR order: by (src, dst), stable
-  std::iota(a.begin(), a.end(), 0);
-  counting_pass(dst, V, a, b, cnt);
-  counting_pass(src, V, b, a, cnt);
-  std::fill(deg.begin(), deg.end(), 0);
-  for (int64_t e = 0; e < E; ++e) deg[src[e]]++;
-  csr_offsets[0] = 0;
-  for (int64_t v = 0; v < V; ++v) csr_offsets[v + 1] = csr_offsets[v] + deg[v];
-  for (int64_t p = 0; p < E; ++p) {
-    csr_targets[p] = dst[a[p]];
-    csr_edge_perm[p] = canon_rank[a[p]];
-  }
+    for (int64_t p = off[v]; p < off[v + 1]; ++p) weights[p] = inv[csc_sources[p]] * inv[v];
+  // CSR: canonical positions grouped by source keep (dst, position) order
+  std::vector<int64_t> cnt(V + 1, 0);
+  for (int64_t p = 0; p < E; ++p) cnt[csc_sources[p] + 1]++;
+  for (int64_t v = 0; v < V; ++v) cnt[v + 1] += cnt[v];
+  std::memcpy(csr_offsets, cnt.data(), (V + 1) * sizeof(int64_t));
+  for (int64_t v = 0; v < V; ++v)
+    for (int64_t p = off[v]; p < off[v + 1]; ++p) {
+      const int64_t q = cnt[csc_sources[p]]++;
+      csr_targets[q] = v;
+      csr_edge_perm[q] = p;
+    }
   return HT_OK;
 }
 
@@ -128,6 +158,10 @@ extern "C" int ht_ldg_partition(int64_t V, const int64_t* csc_offsets, const int
                                 const int64_t* csr_offsets, const int64_t* csr_targets,
                                 const int64_t* arrival, int64_t m, int64_t cap, int64_t* owner) {
   if (m < 1 || m > V) return fail(HT_EINVAL, "m=%lld outside [1, V]", (long long)m);
+  if (m == 1) {  // every choice is partition 0; refinement and repair are no-ops
+    std::fill(owner, owner + V, (int64_t)0);
+    return HT_OK;
+  }
   Adj adj{csc_offsets, csc_sources, csr_offsets, csr_targets};
   std::vector<int64_t> adeg(V, 0);
   for (int64_t v = 0; v < V; ++v) adj.each(v, [&](int64_t) { adeg[v]++; });
@@ -194,34 +228,49 @@ extern "C" int ht_chunk_fill(const int64_t* csc_offsets, const int64_t* csc_sour
     csc_off[k + 1] = csc_off[k] + (csc_offsets[v + 1] - csc_offsets[v]);
   }
   const int64_t ne = csc_off[nv];
-  std::vector<int64_t> glob(ne), dl(ne);
+  int64_t vmax = -1;
+#pragma omp parallel for reduction(max : vmax) schedule(dynamic, 1024)
   for (int64_t k = 0; k < nv; ++k) {
     const int64_t v = verts[k], base = csc_offsets[v];
     for (int64_t q = csc_off[k]; q < csc_off[k + 1]; ++q) {
-      glob[q] = csc_sources[base + (q - csc_off[k])];
+      const int64_t u = csc_sources[base + (q - csc_off[k])];
+      csc_local_src[q] = u;  // global id for now
       edge_w[q] = weights[base + (q - csc_off[k])];
-      dl[q] = k;
+      vmax = std::max(vmax, u);
     }
   }
-  std::vector<int64_t> uniq(glob);
-  std::sort(uniq.begin(), uniq.end());
-  uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
-  const int64_t nn = (int64_t)uniq.size();
-  std::memcpy(sources, uniq.data(), nn * sizeof(int64_t));
+  int64_t nn = 0;
+  if (ne > 0 && vmax + 1 <= 8 * ne) {
+    // dense id map: mark, prefix-sum, translate
+    std::vector<int32_t> map(vmax + 1, 0);
+#pragma omp parallel for
+    for (int64_t q = 0; q < ne; ++q) map[csc_local_src[q]] = 1;
+    for (int64_t u = 0; u <= vmax; ++u)
+      if (map[u]) { sources[nn] = u; map[u] = (int32_t)nn++; }
+#pragma omp parallel for
+    for (int64_t q = 0; q < ne; ++q) csc_local_src[q] = map[csc_local_src[q]];
+  } else if (ne > 0) {
+    std::vector<int64_t> uniq(csc_local_src, csc_local_src + ne);
+    std::sort(uniq.begin(), uniq.end());
+    uniq.erase(std::unique(uniq.begin(), uniq.end()), uniq.end());
+    nn = (int64_t)uniq.size();
+    std::memcpy(sources, uniq.data(), nn * sizeof(int64_t));
+#pragma omp parallel for
+    for (int64_t q = 0; q < ne; ++q)
+      csc_local_src[q] = std::lower_bound(uniq.begin(), uniq.end(), csc_local_src[q]) - uniq.begin();
+  }
   *n_sources = nn;
   std::vector<int64_t> cnt(nn + 1, 0);
-  for (int64_t q = 0; q < ne; ++q) {
-    csc_local_src[q] = std::lower_bound(uniq.begin(), uniq.end(), glob[q]) - uniq.begin();
-    cnt[csc_local_src[q] + 1]++;
-  }
-  for (int64_t s = 0; s < nn; ++s) cnt[s + 1] += cnt[s];
+  for (int64_t q = 0; q < ne; ++q) cnt[csc_local_src[q] + 1]++;
+  for (int64_t u = 0; u < nn; ++u) cnt[u + 1] += cnt[u];
   std::memcpy(csr_off, cnt.data(), (nn + 1) * sizeof(int64_t));
   // stable by local source over canonical order == lexsort((dst, src))
-  for (int64_t q = 0; q < ne; ++q) {
-    const int64_t pos = cnt[csc_local_src[q]]++;
-    csr_perm[pos] = q;
-    csr_local_dst[pos] = dl[q];
-  }
+  for (int64_t k = 0; k < nv; ++k)
+    for (int64_t q = csc_off[k]; q < csc_off[k + 1]; ++q) {
+      const int64_t pos = cnt[csc_local_src[q]]++;
+      csr_perm[pos] = q;
+      csr_local_dst[pos] = k;
+    }
   return HT_OK;
 }
 
@@ -362,13 +411,14 @@ extern "C" int ht_reorganize(int64_t m, int64_t n, const int64_t* nbr, const int
 // return_index=True) without the 64-bit comparison sort.
 extern "C" int ht_dedup_edges(const int64_t* src, const int64_t* dst, int64_t E, int64_t V,
                               int64_t* keep, int64_t* n_keep) {
+  int bad = 0;
+#pragma omp parallel for reduction(| : bad)
   for (int64_t e = 0; e < E; ++e)
-    if (src[e] < 0 || dst[e] < 0 || src[e] >= V || dst[e] >= V)
-      return fail(HT_EINVAL, "edge %lld outside [0, %lld)", (long long)e, (long long)V);
-  std::vector<int64_t> a(E), b, cnt;
-  std::iota(a.begin(), a.end(), 0);
-  counting_pass(src, V, a, b, cnt);
-  counting_pass(dst, V, b, a, cnt);
+    bad |= (src[e] < 0 || dst[e] < 0 || src[e] >= V || dst[e] >= V);
+  if (bad) return fail(HT_EINVAL, "an edge lies outside [0, %lld)", (long long)V);
+  std::vector<int64_t> a, off;
+  group_by(dst, E, V, a, off);
+  sort_groups(a, off, src);
   int64_t k = 0;
   for (int64_t p = 0; p < E; ++p) {
     const int64_t e = a[p];
