@@ -197,6 +197,13 @@ int ht_fleet_elapsed(ht_fleet* f, double* ms);
 /* Number of kernels this library has launched (process-wide). */
 int64_t ht_launches(void);
 
+/* GEMM unit entry for tests: runs the launchers the layer drivers use on
+ * host arrays (device 0).  op 0: C = relu(A W); 1: C = [A W > 0] * G;
+ * 2: C = A W^T (A: M x N, W: K x N); 3: C = A^T G (A: M x K, G: M x N).
+ * precision HT_PREC_FP32 (SIMT) or HT_PREC_TF32 (tcgen05). */
+int ht_gemm_test(int op, int precision, const float* A, const float* W, const float* G,
+                 float* C, int64_t M, int K, int N);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,7 @@ _SIGS = {
     "ht_fleet_mark": (i32, [vp, i32]),
     "ht_fleet_elapsed": (i32, [vp, P_F64]),
     "ht_launches": (i64, []),
+    "ht_gemm_test": (i32, [i32, i32, vp, vp, vp, vp, i64, i32, i32]),
 }
 
 _lib = None

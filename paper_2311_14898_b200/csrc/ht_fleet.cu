@@ -111,7 +111,7 @@ struct Device {
   DBuf value, grad;                    // cap x dim slot buffers
   DBuf sa, sb, sc, sd, se, partial;    // staging
   DBuf gemm_ws;
-  DBuf W;                              // current layer weights
+  DBuf W, Wt;                          // current layer weights and transpose
   std::vector<DBuf> gW;                // per-layer weight-gradient accumulators
   DBuf hL;                             // last-layer outputs (concat over batches)
   std::vector<int64_t> hL_off;         // row offset of batch j inside hL
@@ -313,6 +313,20 @@ int gemm(cudaStream_t s, const float* A, int64_t lda, const float* B, int64_t ld
   return HT_OK;
 }
 
+// W (d_in x d_out) and its transpose, for the current layer
+int upload_weights(Device& d, const float* W, int d_in, int d_out) {
+  const int64_t nw = (int64_t)d_in * d_out;
+  HT_TRY(d.W.ensure(nw * 4));
+  HT_TRY(d.Wt.ensure(nw * 4));
+  std::vector<float> wt(nw);
+  for (int a = 0; a < d_in; ++a)
+    for (int b = 0; b < d_out; ++b) wt[(int64_t)b * d_in + a] = W[(int64_t)a * d_out + b];
+  CU(cudaMemcpyAsync(d.W.p, W, nw * 4, cudaMemcpyHostToDevice, d.stream));
+  CU(cudaMemcpyAsync(d.Wt.p, wt.data(), nw * 4, cudaMemcpyHostToDevice, d.stream));
+  CU(cudaStreamSynchronize(d.stream));
+  return HT_OK;
+}
+
 // long-segment pieces of an offsets array
 void make_pieces(const std::vector<int64_t>& off, std::vector<int64_t>& lo, std::vector<int64_t>& hi,
                  std::vector<int64_t>& seg, std::vector<int64_t>& first, std::vector<int64_t>& cnt) {
@@ -442,7 +456,7 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
     CU(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
     d.chunks.resize(n);
     for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
-                    &d.W, &d.hL, &d.labels, &d.mask, &d.loss_part})
+                    &d.W, &d.Wt, &d.hL, &d.labels, &d.mask, &d.loss_part})
       b->dev = d.ordinal;
     for (int k = 0; k < m; ++k) {
       const int ok = ordinals ? ordinals[k] : 0;
@@ -468,7 +482,7 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
   for (auto& d : f->dev) {
     cudaSetDevice(d.ordinal);
     for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
-                    &d.W, &d.hL, &d.labels, &d.mask, &d.loss_part})
+                    &d.W, &d.Wt, &d.hL, &d.labels, &d.mask, &d.loss_part})
       b->release();
     for (auto& g : d.gW) g.release();
     for (auto& c : d.chunks) {
@@ -891,8 +905,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
     int64_t np = 0;
     for (int j = 0; j < f->n; ++j) np = std::max(np, d.chunks[j].fw_np);
     HT_TRY(d.partial.ensure(std::max<int64_t>(1, np) * d_in * 4));
-    HT_TRY(d.W.ensure((int64_t)d_in * d_out * 4));
-    CU(cudaMemcpyAsync(d.W.p, W, (int64_t)d_in * d_out * 4, cudaMemcpyHostToDevice, d.stream));
+    HT_TRY(upload_weights(d, W, d_in, d_out));
     if (last) {
       HT_TRY(d.hL.ensure(std::max<int64_t>(1, tot) * d_out * 4));
       f->hL_dim = d_out;
@@ -915,7 +928,8 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       TimerRec tg;
       timer_begin(f, d, tg);
       if (precision == HT_PREC_TF32) {
-        HT_TRY(ht::tc_gemm_fwd(d.stream, agg, d.W.as<float>(), hdst, c.nv, d_in, d_out));
+        HT_TRY(ht::tc::rows<ht::tc::TC_RELU>(d.stream, true, agg, d_in, c.nv, d_in, d.Wt.as<float>(),
+                                             d_in, d_out, hdst, d_out, nullptr, 0));
       } else {
         HT_TRY((gemm<false, false, ht::EPI_RELU>(d.stream, agg, d_in, d.W.as<float>(), d_out, hdst,
                                                  d_out, nullptr, 0, c.nv, d_out, d_in, 1, d_in)));
@@ -1000,8 +1014,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
     HT_TRY(d.se.ensure(mn * d_in * 4));   // grad of neighbour rows (views)
     HT_TRY(d.partial.ensure(np * d_in * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)splits_max * d_in * d_out * 4));
-    HT_TRY(d.W.ensure((int64_t)d_in * d_out * 4));
-    CU(cudaMemcpyAsync(d.W.p, W, (int64_t)d_in * d_out * 4, cudaMemcpyHostToDevice, d.stream));
+    HT_TRY(upload_weights(d, W, d_in, d_out));
   }
   for (int j = 0; j < f->n; ++j) {
     for (int i = 0; i < f->m; ++i) {
@@ -1024,8 +1037,20 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
       splits = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
       if (precision == HT_PREC_TF32) {
-        HT_TRY(ht::tc_gemm_bwd(d.stream, A, G, d.W.as<float>(), GZ, GA, d.gemm_ws.as<float>(),
-                               d.gW[layer].as<float>(), M, d_in, d_out));
+        HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, d.Wt.as<float>(),
+                                             d_in, d_out, GZ, d_out, G, d_out));
+        HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, d_out, M, d_out,
+                                              d.W.as<float>(), d_out, d_in, GA, d_in, nullptr, 0));
+        if (M > 0) {
+          int used = 1;
+          HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, d_out, d_out, M, splits_max,
+                               d.gemm_ws.as<float>(), &used));
+          const int64_t nw = (int64_t)d_in * d_out;
+          count_launch(4);
+          ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
+              d.gW[layer].as<float>(), d.gemm_ws.as<float>(), nw, used);
+          CU(cudaGetLastError());
+        }
       } else {
         HT_TRY((gemm<false, false, ht::EPI_MASK>(d.stream, A, d_in, d.W.as<float>(), d_out, GZ,
                                                  d_out, G, d_out, M, d_out, d_in, 1, d_in)));
@@ -1132,3 +1157,78 @@ extern "C" int ht_fleet_elapsed(ht_fleet* f, double* ms) {
 }
 
 extern "C" int64_t ht_launches(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// GEMM unit entry (tests): the exact launchers the layer drivers use, on
+// host arrays.  op 0: C = relu(A W); 1: C = [A W > 0] * G; 2: C = A W^T
+// (A is M x N, W is K x N); 3: C = A^T G (A is M x K, G is M x N).
+// precision: HT_PREC_FP32 (SIMT) or HT_PREC_TF32 (tcgen05; 3xTF32 for ops
+// 0/1, 1xTF32 for ops 2/3).
+// ---------------------------------------------------------------------------
+extern "C" int ht_gemm_test(int op, int precision, const float* A, const float* W, const float* G,
+                            float* C, int64_t M, int K, int N) {
+  CU(cudaSetDevice(0));
+  cudaStream_t s = nullptr;
+  CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const int64_t a_cols = op == 2 ? N : K;
+  const int64_t c_rows = op == 3 ? K : M, c_cols = op == 2 ? K : N;
+  DBuf dA, dW, dWt, dG, dC, ws;
+  HT_TRY(dA.ensure(std::max<int64_t>(1, M * a_cols) * 4));
+  HT_TRY(dW.ensure((int64_t)K * N * 4 + 4));
+  HT_TRY(dWt.ensure((int64_t)K * N * 4 + 4));
+  HT_TRY(dG.ensure(std::max<int64_t>(1, M * N) * 4));
+  HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * c_cols) * 4));
+  HT_TRY(ws.ensure((int64_t)148 * K * N * 4 + 4));
+  CU(cudaMemcpy(dA.p, A, M * a_cols * 4, cudaMemcpyHostToDevice));
+  if (W) {
+    std::vector<float> wt((size_t)K * N);
+    for (int a = 0; a < K; ++a)
+      for (int b = 0; b < N; ++b) wt[(size_t)b * K + a] = W[(size_t)a * N + b];
+    CU(cudaMemcpy(dW.p, W, (int64_t)K * N * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(dWt.p, wt.data(), (int64_t)K * N * 4, cudaMemcpyHostToDevice));
+  }
+  if (G) CU(cudaMemcpy(dG.p, G, M * N * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemset(dC.p, 0, c_rows * c_cols * 4));
+  const bool tc = precision == HT_PREC_TF32;
+  int rc = HT_OK;
+  if (op == 0) {
+    rc = tc ? ht::tc::rows<ht::tc::TC_RELU>(s, true, dA.as<float>(), K, M, K, dWt.as<float>(), K, N,
+                                            dC.as<float>(), N, nullptr, 0)
+            : gemm<false, false, ht::EPI_RELU>(s, dA.as<float>(), K, dW.as<float>(), N,
+                                               dC.as<float>(), N, nullptr, 0, M, N, K, 1, K);
+  } else if (op == 1) {
+    rc = tc ? ht::tc::rows<ht::tc::TC_MASK>(s, true, dA.as<float>(), K, M, K, dWt.as<float>(), K, N,
+                                            dC.as<float>(), N, dG.as<float>(), N)
+            : gemm<false, false, ht::EPI_MASK>(s, dA.as<float>(), K, dW.as<float>(), N,
+                                               dC.as<float>(), N, dG.as<float>(), N, M, N, K, 1, K);
+  } else if (op == 2) {
+    rc = tc ? ht::tc::rows<ht::tc::TC_STORE>(s, false, dA.as<float>(), N, M, N, dW.as<float>(), N, K,
+                                             dC.as<float>(), K, nullptr, 0)
+            : gemm<false, true, ht::EPI_STORE>(s, dA.as<float>(), N, dW.as<float>(), N,
+                                               dC.as<float>(), K, nullptr, 0, M, K, N, 1, N);
+  } else if (op == 3) {
+    int used = 1;
+    if (tc) {
+      rc = ht::tc::wgrad(s, dA.as<float>(), K, K, dG.as<float>(), N, N, M, 148, ws.as<float>(), &used);
+    } else {
+      int splits = (int)std::min<int64_t>(64, std::max<int64_t>(1, M / 2048));
+      int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
+      used = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
+      rc = gemm<true, false, ht::EPI_STORE>(s, dA.as<float>(), K, dG.as<float>(), N, ws.as<float>(), N,
+                                            nullptr, 0, K, N, M, used, kps);
+    }
+    if (rc == HT_OK) {
+      ht::k_reduce_splits<<<64, 256, 0, s>>>(dC.as<float>(), ws.as<float>(), (int64_t)K * N, used);
+      CU(cudaGetLastError());
+    }
+  } else {
+    rc = fail(HT_EINVAL, "unknown gemm op %d", op);
+  }
+  if (rc == HT_OK) {
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(C, dC.p, c_rows * c_cols * 4, cudaMemcpyDeviceToHost));
+  }
+  for (DBuf* b : {&dA, &dW, &dWt, &dG, &dC, &ws}) b->release();
+  cudaStreamDestroy(s);
+  return rc;
+}
