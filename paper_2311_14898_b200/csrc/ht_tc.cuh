@@ -317,7 +317,9 @@ __global__ void __launch_bounds__(128, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t idesc = idesc_tf32(BN, true, true);
+  // K-major operands: MN-major TF32 operands read back as zeros on sm_100a
+  // (measured), so tiles are transposed while staging instead
+  const uint32_t idesc = idesc_tf32(BN, false, false);
   const bool avec = (lda & 3) == 0, gvec = (ldg & 3) == 0;
   uint32_t phase[NST] = {0, 0, 0};
   bool pend[NST] = {false, false, false};
@@ -328,22 +330,30 @@ __global__ void __launch_bounds__(128, 1)
     if (pend[s]) { mbar_wait(&bar[s], phase[s]); phase[s] ^= 1; pend[s] = false; }
     uint8_t* sa = smem + s * STAGE;
     uint8_t* sb = sa + A_BYTES;
-    // A: ROWS rows x 128 features (4 atoms of 32)
+    // Transposing loads into K-major tiles (feature rows, 32 reduction
+    // values per 128-byte row): lane = reduction row, so each warp store
+    // fills one swizzled 128-byte smem row without bank conflicts.
     for (int idx = tid; idx < ROWS * 32; idx += 128) {
-      const int c = idx & 7, atom = (idx >> 3) & 3, r = idx >> 5;
+      const int r = idx & 31, fc = idx >> 5;
       const int64_t m = rb + r;
-      const int k = k0 + atom * 32 + c * 4;
+      const int k = k0 + fc * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (m < r1 && k < K) v = ld4(A + m * lda + k, K - k, avec);
-      put4<false>(sa, nullptr, (uint32_t)atom * ROWS * 128 + sw128(r, c), v);
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float*>(sa + sw128(fc * 4 + q, r >> 2) + (r & 3) * 4) = tf32_rna(e[q]);
     }
     for (int idx = tid; idx < ROWS * (BN / 4); idx += 128) {
-      const int c = idx & 7, atom = (idx >> 3) % (BN / 32), r = idx / (BN / 4);
+      const int r = idx & 31, fc = idx >> 5;
       const int64_t m = rb + r;
-      const int n = n0 + atom * 32 + c * 4;
+      const int n = n0 + fc * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (m < r1 && n < N) v = ld4(Gm + m * ldg + n, N - n, gvec);
-      put4<false>(sb, nullptr, (uint32_t)atom * ROWS * 128 + sw128(r, c), v);
+      const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float*>(sb + sw128(fc * 4 + q, r >> 2) + (r & 3) * 4) = tf32_rna(e[q]);
     }
     fence_proxy_async();
     __syncthreads();
@@ -352,8 +362,8 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
 #pragma unroll
       for (int ks = 0; ks < ROWS / 8; ++ks) {
-        mma_tf32(tmem, sdesc(a0 + ks * 1024, ROWS * 128, 1024),
-                 sdesc(b0 + ks * 1024, ROWS * 128, 1024), idesc, (any || ks) ? 1u : 0u);
+        mma_tf32(tmem, sdesc(a0 + ks * 32, 16, 1024), sdesc(b0 + ks * 32, 16, 1024), idesc,
+                 (any || ks) ? 1u : 0u);
       }
       mma_commit(&bar[s]);
     }

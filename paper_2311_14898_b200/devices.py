@@ -214,7 +214,7 @@ class DeviceFleet:
     ordinal (default: round-robin over the visible GPUs)."""
 
     def __init__(self, plan: DedupPlan, mode: str = "full", flush_policy: str = "on_eviction",
-                 dtype=np.float64, devices=None, precision: str = "fp32"):
+                 dtype=np.float64, devices=None, precision: str = "tf32"):
         if mode not in _MODES:
             raise SimulationError(f"unknown mode {mode!r}")
         if flush_policy not in _FLUSH_POLICIES:
