@@ -197,6 +197,12 @@ int ht_fleet_elapsed(ht_fleet* f, double* ms);
 /* Number of kernels this library has launched (process-wide). */
 int64_t ht_launches(void);
 
+/* PCIe peaks of the box in GB/s (roofline denominators of the transfer
+ * kernels): out[0] copy-engine H2D, out[1] D2H, out[2] both directions at
+ * once (sum), out[3] zero-copy row kernel reading pinned memory, out[4]
+ * zero-copy row kernel writing pinned memory.  `bytes` per transfer. */
+int ht_pcie_probe(int device, int64_t bytes, double* out);
+
 /* GEMM unit entry for tests: runs the launchers the layer drivers use on
  * host arrays (device 0).  op 0: C = relu(A W); 1: C = [A W > 0] * G;
  * 2: C = A W^T (A: M x N, W: K x N); 3: C = A^T G (A: M x K, G: M x N).

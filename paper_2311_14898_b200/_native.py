@@ -75,6 +75,7 @@ _SIGS = {
     "ht_fleet_elapsed": (i32, [vp, P_F64]),
     "ht_launches": (i64, []),
     "ht_gemm_test": (i32, [i32, i32, vp, vp, vp, vp, i64, i32, i32]),
+    "ht_pcie_probe": (i32, [i32, i64, vp]),
 }
 
 _lib = None

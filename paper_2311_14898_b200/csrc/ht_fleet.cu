@@ -1159,6 +1159,67 @@ extern "C" int ht_fleet_elapsed(ht_fleet* f, double* ms) {
 extern "C" int64_t ht_launches(void) { return g_launches.load(); }
 
 // ---------------------------------------------------------------------------
+// PCIe peaks of this box (roofline denominators of the host-transfer
+// kernels): copy-engine H2D, D2H, both directions at once, and the
+// zero-copy row kernels reading / writing pinned memory (1 KB rows).
+// ---------------------------------------------------------------------------
+extern "C" int ht_pcie_probe(int device, int64_t bytes, double* out /* [5] GB/s */) {
+  CU(cudaSetDevice(device));
+  void *h0 = nullptr, *h1 = nullptr, *d0 = nullptr, *d1 = nullptr;
+  CU(cudaHostAlloc(&h0, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  CU(cudaHostAlloc(&h1, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  CU(cudaMalloc(&d0, bytes));
+  CU(cudaMalloc(&d1, bytes));
+  memset(h0, 1, bytes);
+  memset(h1, 2, bytes);
+  cudaStream_t s0, s1;
+  CU(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+  cudaEvent_t a, b, c;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  CU(cudaEventCreate(&c));
+  void *hd0 = nullptr, *hd1 = nullptr;
+  CU(cudaHostGetDevicePointer(&hd0, h0, 0));
+  CU(cudaHostGetDevicePointer(&hd1, h1, 0));
+  const int64_t rb = 1024, rows = bytes / rb;
+  for (int t = 0; t < 5; ++t) {
+    double best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+      CU(cudaEventRecord(a, s0));
+      if (t == 0) CU(cudaMemcpyAsync(d0, h0, bytes, cudaMemcpyHostToDevice, s0));
+      if (t == 1) CU(cudaMemcpyAsync(h0, d0, bytes, cudaMemcpyDeviceToHost, s0));
+      if (t == 2) {
+        CU(cudaStreamWaitEvent(s1, a, 0));
+        CU(cudaMemcpyAsync(d0, h0, bytes, cudaMemcpyHostToDevice, s0));
+        CU(cudaMemcpyAsync(h1, d1, bytes, cudaMemcpyDeviceToHost, s1));
+        CU(cudaEventRecord(c, s1));
+        CU(cudaStreamWaitEvent(s0, c, 0));
+      }
+      if (t == 3) HT_TRY(launch_copy(s0, d0, hd0, nullptr, nullptr, rows, rb, rb, rb));
+      if (t == 4) HT_TRY(launch_copy(s0, hd1, d1, nullptr, nullptr, rows, rb, rb, rb));
+      CU(cudaEventRecord(b, s0));
+      CU(cudaEventSynchronize(b));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, a, b));
+      const double moved = (t == 2 ? 2.0 : 1.0) * (double)bytes;
+      best = std::max(best, moved / (ms * 1e-3) / 1e9);
+    }
+    out[t] = best;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaEventDestroy(c);
+  cudaStreamDestroy(s0);
+  cudaStreamDestroy(s1);
+  cudaFree(d0);
+  cudaFree(d1);
+  cudaFreeHost(h0);
+  cudaFreeHost(h1);
+  return HT_OK;
+}
+
+// ---------------------------------------------------------------------------
 // GEMM unit entry (tests): the exact launchers the layer drivers use, on
 // host arrays.  op 0: C = relu(A W); 1: C = [A W > 0] * G; 2: C = A W^T
 // (A is M x N, W is K x N); 3: C = A^T G (A is M x K, G is M x N).
