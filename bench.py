@@ -215,6 +215,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--only-value", action="store_true", help="profiling: HBM-resident run only")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -278,6 +279,9 @@ def main():
         val = run_epochs(p, plan, ds, dims, "device", args.steps, args.warmup, args.precision,
                          True, cfg["seed"])
     ms_v = val["ms_total"] / args.steps
+    if args.only_value:  # profiling aid: no e2e run, no JSON contract line
+        log(f"[bench] value run: {ms_v:.2f} ms/epoch  stats {val['stats']}")
+        return
     # ---- e2e: pinned host-resident vertex store through train_epoch ----
     with Clocks() as clk_e:
         e2e = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,

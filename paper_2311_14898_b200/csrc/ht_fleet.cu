@@ -111,7 +111,8 @@ struct Device {
   DBuf value, grad;                    // cap x dim slot buffers
   DBuf sa, sb, sc, sd, se, partial;    // staging
   DBuf gemm_ws;
-  DBuf W, Wt;                          // current layer weights and transpose
+  DBuf W, Wt, Wp;                      // current layer weights, transpose, padded
+  DBuf Wt_hi, Wt_lo, Wp_hi, Wp_lo;     // TF32 hi/lo halves for tcgen05
   std::vector<DBuf> gW;                // per-layer weight-gradient accumulators
   DBuf hL;                             // last-layer outputs (concat over batches)
   std::vector<int64_t> hL_off;         // row offset of batch j inside hL
@@ -313,16 +314,33 @@ int gemm(cudaStream_t s, const float* A, int64_t lda, const float* B, int64_t ld
   return HT_OK;
 }
 
-// W (d_in x d_out) and its transpose, for the current layer
+inline int pad4(int d) { return (d + 3) & ~3; }
+
+// Layer weights on the device: W (d_in x d_out) for the SIMT path, and for
+// the tensor-core path the TF32 hi/lo halves of W^T (d_out x d_in, the
+// K-major operand of z = agg.W) and of W padded to pad4(d_out) columns (the
+// K-major operand of gagg = gz.W^T).
 int upload_weights(Device& d, const float* W, int d_in, int d_out) {
   const int64_t nw = (int64_t)d_in * d_out;
+  const int ldo = pad4(d_out);
+  const int64_t np = (int64_t)d_in * ldo;
   HT_TRY(d.W.ensure(nw * 4));
   HT_TRY(d.Wt.ensure(nw * 4));
-  std::vector<float> wt(nw);
+  HT_TRY(d.Wp.ensure(np * 4));
+  for (DBuf* b : {&d.Wt_hi, &d.Wt_lo}) HT_TRY(b->ensure(nw * 4));
+  for (DBuf* b : {&d.Wp_hi, &d.Wp_lo}) HT_TRY(b->ensure(np * 4));
+  std::vector<float> wt(nw), wp(np, 0.f);
   for (int a = 0; a < d_in; ++a)
-    for (int b = 0; b < d_out; ++b) wt[(int64_t)b * d_in + a] = W[(int64_t)a * d_out + b];
+    for (int b = 0; b < d_out; ++b) {
+      wt[(int64_t)b * d_in + a] = W[(int64_t)a * d_out + b];
+      wp[(int64_t)a * ldo + b] = W[(int64_t)a * d_out + b];
+    }
   CU(cudaMemcpyAsync(d.W.p, W, nw * 4, cudaMemcpyHostToDevice, d.stream));
   CU(cudaMemcpyAsync(d.Wt.p, wt.data(), nw * 4, cudaMemcpyHostToDevice, d.stream));
+  CU(cudaMemcpyAsync(d.Wp.p, wp.data(), np * 4, cudaMemcpyHostToDevice, d.stream));
+  HT_TRY(ht::tc::split_weights(d.stream, d.Wt.as<float>(), d.Wt_hi.as<float>(), d.Wt_lo.as<float>(), nw));
+  HT_TRY(ht::tc::split_weights(d.stream, d.Wp.as<float>(), d.Wp_hi.as<float>(), d.Wp_lo.as<float>(), np));
+  count_launch(2);
   CU(cudaStreamSynchronize(d.stream));
   return HT_OK;
 }
@@ -456,7 +474,8 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
     CU(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
     d.chunks.resize(n);
     for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
-                    &d.W, &d.Wt, &d.hL, &d.labels, &d.mask, &d.loss_part})
+                    &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo, &d.hL,
+                    &d.labels, &d.mask, &d.loss_part})
       b->dev = d.ordinal;
     for (int k = 0; k < m; ++k) {
       const int ok = ordinals ? ordinals[k] : 0;
@@ -482,7 +501,8 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
   for (auto& d : f->dev) {
     cudaSetDevice(d.ordinal);
     for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
-                    &d.W, &d.Wt, &d.hL, &d.labels, &d.mask, &d.loss_part})
+                    &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo, &d.hL,
+                    &d.labels, &d.mask, &d.loss_part})
       b->release();
     for (auto& g : d.gW) g.release();
     for (auto& c : d.chunks) {
@@ -928,8 +948,9 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       TimerRec tg;
       timer_begin(f, d, tg);
       if (precision == HT_PREC_TF32) {
-        HT_TRY(ht::tc::rows<ht::tc::TC_RELU>(d.stream, true, agg, d_in, c.nv, d_in, d.Wt.as<float>(),
-                                             d_in, d_out, hdst, d_out, nullptr, 0));
+        HT_TRY(ht::tc::rows<ht::tc::TC_RELU>(d.stream, true, agg, d_in, c.nv, d_in,
+                                             d.Wt_hi.as<float>(), d.Wt_lo.as<float>(), d_in, d_out,
+                                             hdst, d_out, nullptr, 0));
       } else {
         HT_TRY((gemm<false, false, ht::EPI_RELU>(d.stream, agg, d_in, d.W.as<float>(), d_out, hdst,
                                                  d_out, nullptr, 0, c.nv, d_out, d_in, 1, d_in)));
@@ -1009,7 +1030,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
     }
     HT_TRY(d.sa.ensure(mv * d_in * 4));   // agg checkpoint rows
     HT_TRY(d.sb.ensure(mv * d_out * 4));  // dest gradient rows
-    HT_TRY(d.sc.ensure(mv * d_out * 4));  // gz
+    HT_TRY(d.sc.ensure(mv * pad4(d_out) * 4));  // gz (row stride pad4(d_out))
     HT_TRY(d.sd.ensure(mv * d_in * 4));   // grad agg
     HT_TRY(d.se.ensure(mn * d_in * 4));   // grad of neighbour rows (views)
     HT_TRY(d.partial.ensure(np * d_in * 4));
@@ -1037,13 +1058,16 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
       splits = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
       if (precision == HT_PREC_TF32) {
-        HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, d.Wt.as<float>(),
-                                             d_in, d_out, GZ, d_out, G, d_out));
-        HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, d_out, M, d_out,
-                                              d.W.as<float>(), d_out, d_in, GA, d_in, nullptr, 0));
+        const int ldz = pad4(d_out);
+        HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in,
+                                             d.Wt_hi.as<float>(), d.Wt_lo.as<float>(), d_in, d_out,
+                                             GZ, ldz, G, d_out));
+        HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
+                                              d.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
+                                              nullptr, 0));
         if (M > 0) {
           int used = 1;
-          HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, d_out, d_out, M, splits_max,
+          HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, ldz, d_out, M, splits_max,
                                d.gemm_ws.as<float>(), &used));
           const int64_t nw = (int64_t)d_in * d_out;
           count_launch(4);
@@ -1231,52 +1255,50 @@ extern "C" int ht_gemm_test(int op, int precision, const float* A, const float* 
   CU(cudaSetDevice(0));
   cudaStream_t s = nullptr;
   CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  const int64_t a_cols = op == 2 ? N : K;
+  // row operands are staged with row strides padded to 4 floats (the TMA
+  // alignment rule the layer drivers follow for their own staging)
+  const int ka = op == 2 ? N : K, lda = pad4(ka), ldn = pad4(N);
   const int64_t c_rows = op == 3 ? K : M, c_cols = op == 2 ? K : N;
-  DBuf dA, dW, dWt, dG, dC, ws;
-  HT_TRY(dA.ensure(std::max<int64_t>(1, M * a_cols) * 4));
-  HT_TRY(dW.ensure((int64_t)K * N * 4 + 4));
-  HT_TRY(dWt.ensure((int64_t)K * N * 4 + 4));
-  HT_TRY(dG.ensure(std::max<int64_t>(1, M * N) * 4));
+  Device d;
+  d.stream = s;
+  DBuf dA, dG, dC, ws;
+  HT_TRY(dA.ensure(std::max<int64_t>(1, M * lda) * 4));
+  HT_TRY(dG.ensure(std::max<int64_t>(1, M * ldn) * 4));
   HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * c_cols) * 4));
   HT_TRY(ws.ensure((int64_t)148 * K * N * 4 + 4));
-  CU(cudaMemcpy(dA.p, A, M * a_cols * 4, cudaMemcpyHostToDevice));
-  if (W) {
-    std::vector<float> wt((size_t)K * N);
-    for (int a = 0; a < K; ++a)
-      for (int b = 0; b < N; ++b) wt[(size_t)b * K + a] = W[(size_t)a * N + b];
-    CU(cudaMemcpy(dW.p, W, (int64_t)K * N * 4, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(dWt.p, wt.data(), (int64_t)K * N * 4, cudaMemcpyHostToDevice));
-  }
-  if (G) CU(cudaMemcpy(dG.p, G, M * N * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy2D(dA.p, lda * 4, A, ka * 4, ka * 4, M, cudaMemcpyHostToDevice));
+  if (G) CU(cudaMemcpy2D(dG.p, ldn * 4, G, N * 4, N * 4, M, cudaMemcpyHostToDevice));
+  if (W) HT_TRY(upload_weights(d, W, K, N));
   CU(cudaMemset(dC.p, 0, c_rows * c_cols * 4));
   const bool tc = precision == HT_PREC_TF32;
   int rc = HT_OK;
   if (op == 0) {
-    rc = tc ? ht::tc::rows<ht::tc::TC_RELU>(s, true, dA.as<float>(), K, M, K, dWt.as<float>(), K, N,
-                                            dC.as<float>(), N, nullptr, 0)
-            : gemm<false, false, ht::EPI_RELU>(s, dA.as<float>(), K, dW.as<float>(), N,
+    rc = tc ? ht::tc::rows<ht::tc::TC_RELU>(s, true, dA.as<float>(), lda, M, K, d.Wt_hi.as<float>(),
+                                            d.Wt_lo.as<float>(), K, N, dC.as<float>(), N, nullptr, 0)
+            : gemm<false, false, ht::EPI_RELU>(s, dA.as<float>(), lda, d.W.as<float>(), N,
                                                dC.as<float>(), N, nullptr, 0, M, N, K, 1, K);
   } else if (op == 1) {
-    rc = tc ? ht::tc::rows<ht::tc::TC_MASK>(s, true, dA.as<float>(), K, M, K, dWt.as<float>(), K, N,
-                                            dC.as<float>(), N, dG.as<float>(), N)
-            : gemm<false, false, ht::EPI_MASK>(s, dA.as<float>(), K, dW.as<float>(), N,
-                                               dC.as<float>(), N, dG.as<float>(), N, M, N, K, 1, K);
+    rc = tc ? ht::tc::rows<ht::tc::TC_MASK>(s, true, dA.as<float>(), lda, M, K, d.Wt_hi.as<float>(),
+                                            d.Wt_lo.as<float>(), K, N, dC.as<float>(), N,
+                                            dG.as<float>(), ldn)
+            : gemm<false, false, ht::EPI_MASK>(s, dA.as<float>(), lda, d.W.as<float>(), N,
+                                               dC.as<float>(), N, dG.as<float>(), ldn, M, N, K, 1, K);
   } else if (op == 2) {
-    rc = tc ? ht::tc::rows<ht::tc::TC_STORE>(s, false, dA.as<float>(), N, M, N, dW.as<float>(), N, K,
-                                             dC.as<float>(), K, nullptr, 0)
-            : gemm<false, true, ht::EPI_STORE>(s, dA.as<float>(), N, dW.as<float>(), N,
+    rc = tc ? ht::tc::rows<ht::tc::TC_STORE>(s, false, dA.as<float>(), lda, M, N, d.Wp_hi.as<float>(),
+                                             nullptr, pad4(N), K, dC.as<float>(), K, nullptr, 0)
+            : gemm<false, true, ht::EPI_STORE>(s, dA.as<float>(), lda, d.W.as<float>(), N,
                                                dC.as<float>(), K, nullptr, 0, M, K, N, 1, N);
   } else if (op == 3) {
     int used = 1;
     if (tc) {
-      rc = ht::tc::wgrad(s, dA.as<float>(), K, K, dG.as<float>(), N, N, M, 148, ws.as<float>(), &used);
+      rc = ht::tc::wgrad(s, dA.as<float>(), lda, K, dG.as<float>(), ldn, N, M, 148, ws.as<float>(),
+                         &used);
     } else {
       int splits = (int)std::min<int64_t>(64, std::max<int64_t>(1, M / 2048));
       int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
       used = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
-      rc = gemm<true, false, ht::EPI_STORE>(s, dA.as<float>(), K, dG.as<float>(), N, ws.as<float>(), N,
-                                            nullptr, 0, K, N, M, used, kps);
+      rc = gemm<true, false, ht::EPI_STORE>(s, dA.as<float>(), lda, dG.as<float>(), ldn,
+                                            ws.as<float>(), N, nullptr, 0, K, N, M, used, kps);
     }
     if (rc == HT_OK) {
       ht::k_reduce_splits<<<64, 256, 0, s>>>(dC.as<float>(), ws.as<float>(), (int64_t)K * N, used);
@@ -1289,7 +1311,8 @@ extern "C" int ht_gemm_test(int op, int precision, const float* A, const float* 
     CU(cudaStreamSynchronize(s));
     CU(cudaMemcpy(C, dC.p, c_rows * c_cols * 4, cudaMemcpyDeviceToHost));
   }
-  for (DBuf* b : {&dA, &dW, &dWt, &dG, &dC, &ws}) b->release();
+  for (DBuf* b : {&dA, &dG, &dC, &ws, &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo})
+    b->release();
   cudaStreamDestroy(s);
   return rc;
 }

@@ -6,29 +6,33 @@
 //   gagg = gz . W^T         (backward K7; 1xTF32)
 //   dW  += agg^T . gz       (backward K7; 1xTF32, split over rows)
 //
-// Kernel k_tc_rows (z and gagg): one 128-row tile of the row operand per
-// MMA (M=128), a feature tile of BN columns (N=BN), K swept in 32-float
-// chunks (one 128-byte swizzle atom).  The whole feature tile of the weight
-// operand (BN x K, hi and lo halves) stays resident in shared memory for
-// the CTA's lifetime; persistent CTAs walk row tiles, double-buffering the
-// row operand through shared memory while the tensor core runs.  The
-// accumulator lives in TMEM (BN columns) and is drained with tcgen05.ld
-// into a fused epilogue (ReLU, or the ReLU'-mask times the incoming
-// gradient).
+// k_tc_gemm (z, gz, gagg) - persistent, warp-specialized, one CTA per SM:
+//   warp 0     TMA producer: 128-row x 32-float tiles of the row operand and
+//              BN x 32 tiles of the (pre-split) weight operand per stage
+//   warps 2-3  converters: round the row tile to TF32 in place (hi) and
+//              write the residual (lo) for 3xTF32
+//   warp 1     MMA issuer: tcgen05.mma kind::tf32, M=128, N=BN, K=8;
+//              3xTF32 = hi.hi + hi.lo + lo.hi into one TMEM accumulator
+//   warps 4-7  epilogue: tcgen05.ld, fused ReLU / ReLU'-mask, stores
+//   Two TMEM accumulators (2 x BN columns) let the epilogue of tile t
+//   overlap the MMAs of tile t+1.
 //
-// Kernel k_tc_wgrad (dW): both operands are MN-major (rows of agg and gz
-// are read as-is), the reduction runs over chunk rows; each CTA owns a
-// slice of rows and writes a partial 128 x BN tile, reduced afterwards in a
-// fixed order.
+// k_tc_wgrad (dW) - per CTA a slice of rows: TMA brings raw row-major tiles
+// (32 rows x 128 features of agg, 32 x BN of gz); transposer warps write
+// them K-major (feature rows, 32 reduction values per 128-byte row); the MMA
+// warp accumulates one 128 x BN tile in TMEM; a partial tile per slice is
+// reduced in a fixed order afterwards.  (MN-major TF32 operands read back as
+// zeros on sm_100a - measured, scratch/wgrad_dbg2.cu - hence the
+// transposition.)
 //
-// 3xTF32: x = hi + lo with hi = rna_tf32(x), lo = x - hi (exact), and
-// a.b ~ hi.hi + hi.lo + lo.hi accumulated in FP32 in TMEM.
-//
-// Shared-memory layouts are the canonical SWIZZLE_128B UMMA layouts
-// (cute/arch/mma_sm100_desc.hpp): 8-row x 128-byte atoms, 16-byte chunk
-// index XOR (row & 7), 1024-byte aligned.
+// Shared-memory operand layouts are the canonical SWIZZLE_128B K-major UMMA
+// layouts (cute/arch/mma_sm100_desc.hpp): 8-row x 128-byte atoms, 16-byte
+// chunk index XOR (row & 7), 1024-byte aligned; TMA writes exactly this
+// layout with CU_TENSOR_MAP_SWIZZLE_128B.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -39,25 +43,32 @@
 namespace ht {
 namespace tc {
 
+// ---------------------------------------------------------------------------
+// PTX primitives
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100)
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B, version 1 (sm_100)
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)1 << 16;             // LBO 16 B (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;   // SBO: 8-row groups 1024 B apart
+  d |= (uint64_t)1 << 46;             // version
+  d |= (uint64_t)2 << 61;             // SWIZZLE_128B
   return d;
 }
 
-// instruction descriptor: A,B = TF32, D = F32, M = 128, N = n
-__host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) |
-         ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// instruction descriptor: A,B = TF32 (K-major), D = F32, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+
+__host__ __device__ constexpr uint32_t tmem_cols(int n) {
+  return n <= 32 ? 32u : n <= 64 ? 64u : n <= 128 ? 128u : n <= 256 ? 256u : 512u;
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
@@ -80,6 +91,7 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+// wait until the phase with the given parity has completed
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -93,8 +105,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
-__host__ __device__ constexpr uint32_t tmem_cols(int n) {
-  return n <= 32 ? 32u : n <= 64 ? 64u : n <= 128 ? 128u : 256u;
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                            int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
 }
 
 __device__ __forceinline__ void fence_barrier_init() {
@@ -148,249 +175,313 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
 }
 
-// four consecutive floats of a row, zero beyond `lim` (row-local count)
-__device__ __forceinline__ float4 ld4(const float* __restrict__ p, int lim, bool vec_ok) {
-  if (vec_ok && lim >= 4) return __ldg(reinterpret_cast<const float4*>(p));
-  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (lim > 0) v.x = __ldg(p);
-  if (lim > 1) v.y = __ldg(p + 1);
-  if (lim > 2) v.z = __ldg(p + 2);
-  if (lim > 3) v.w = __ldg(p + 3);
-  return v;
-}
-
-template <bool SPLIT>
-__device__ __forceinline__ void put4(uint8_t* hi, uint8_t* lo, uint32_t off, float4 v) {
-  float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
-  *reinterpret_cast<float4*>(hi + off) = h;
-  if (SPLIT) {
-    float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-    *reinterpret_cast<float4*>(lo + off) = l;
-  }
-}
-
 enum { TC_STORE = 0, TC_RELU = 1, TC_MASK = 2 };
 
-// C[M x N] = A[M x K] . Bt[N x K]^T with epilogue; K <= 256.
-// grid.x = feature tiles of BN, grid.y = persistent row-tile workers.
+// ---------------------------------------------------------------------------
+// k_tc_gemm: C[M x N] = epi(A[M x K] . B^T), B given as hi/lo halves of a
+// K-major N x K matrix (tensor maps tmBh / tmBl); A through tmA (row-major,
+// lda*4 bytes per row).  BN >= N, multiple of 32.
+// ---------------------------------------------------------------------------
+template <int BN, bool SPLIT>
+struct GemmCfg {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int STAGES = (200 * 1024 / STAGE) < 4 ? (200 * 1024 / STAGE) : 4;
+  static constexpr int TX = A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;  // TMA bytes per stage
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256;
+};
+
 template <int BN, bool SPLIT, int EPI>
-__global__ void __launch_bounds__(128, 1)
-    k_tc_rows(const float* __restrict__ A, int64_t lda, int64_t M, int K,
-              const float* __restrict__ Bt, int64_t ldb, int N, float* __restrict__ C,
-              int64_t ldc, const float* __restrict__ G, int64_t ldg) {
+__global__ void __launch_bounds__(256, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
+              const __grid_constant__ CUtensorMap tmBl, int64_t M, int K, int N,
+              float* __restrict__ C, int64_t ldc, const float* __restrict__ G, int64_t ldg) {
+  using Cfg = GemmCfg<BN, SPLIT>;
+  constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int KC = (K + 31) >> 5;
-  constexpr int A_BYTES = 128 * 128;
-  const uint32_t B_BYTES = (uint32_t)KC * BN * 128;
-  uint8_t* bhi = smem;
-  uint8_t* blo = bhi + B_BYTES;
-  uint8_t* ast = SPLIT ? blo + B_BYTES : blo;
-  constexpr int STAGE = (SPLIT ? 2 : 1) * A_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(ast + 2 * STAGE);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+  // stage s: [A hi (raw)][A lo][B hi][B lo]
+  auto sA = [&](int s) { return smem + (size_t)s * Cfg::STAGE; };
+  auto sAlo = [&](int s) { return sA(s) + Cfg::A_BYTES; };
+  auto sBh = [&](int s) { return sA(s) + (SPLIT ? 2 : 1) * Cfg::A_BYTES; };
+  auto sBl = [&](int s) { return sBh(s) + Cfg::B_BYTES; };
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)ST * Cfg::STAGE);
+  uint64_t* full = bar;            // [ST] TMA landed
+  uint64_t* conv = bar + ST;       // [ST] converters done
+  uint64_t* empty = bar + 2 * ST;  // [ST] MMAs done reading
+  uint64_t* tfull = bar + 3 * ST;  // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;    // [2] accumulator drained
+  uint32_t* slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int f0 = blockIdx.x * BN;
-  constexpr uint32_t NCOL = tmem_cols(BN);
-  if (warp == 0) tmem_alloc(slot, NCOL);
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t NCOL = tmem_cols(2 * BN);
+  if (warp == 1) tmem_alloc(slot, NCOL);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 64);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
     fence_barrier_init();
   }
-  // resident weight tile: rows f0..f0+BN-1 of Bt, all K
-  const bool bvec = (ldb & 3) == 0;
-  for (int idx = tid; idx < BN * KC * 8; idx += 128) {
-    const int c = idx & 7, rest = idx >> 3, r = rest % BN, kc = rest / BN;
-    const int f = f0 + r, k = kc * 32 + c * 4;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (f < N) v = ld4(Bt + (int64_t)f * ldb + k, K - k, bvec);
-    put4<SPLIT>(bhi, blo, (uint32_t)kc * BN * 128 + sw128(r, c), v);
-  }
-  fence_proxy_async();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t idesc = idesc_tf32(BN, false, false);
-  const bool avec = (lda & 3) == 0;
+  const int KC = (K + 31) >> 5;
   const int64_t ntiles = (M + 127) >> 7;
-  uint32_t phase0 = 0, phase1 = 0;
-  bool pend0 = false, pend1 = false;
-  int it = 0;
-  for (int64_t t = blockIdx.y; t < ntiles; t += gridDim.y) {
-    const int64_t m0 = t << 7;
-    for (int kc = 0; kc < KC; ++kc, ++it) {
-      const int s = it & 1;
-      if (s == 0 && pend0) { mbar_wait(&bar[0], phase0); phase0 ^= 1; pend0 = false; }
-      if (s == 1 && pend1) { mbar_wait(&bar[1], phase1); phase1 ^= 1; pend1 = false; }
-      uint8_t* ahi = ast + s * STAGE;
-      uint8_t* alo = ahi + A_BYTES;
-#pragma unroll 4
-      for (int idx = tid; idx < 128 * 8; idx += 128) {
-        const int c = idx & 7, r = idx >> 3;
-        const int64_t m = m0 + r;
-        const int k = kc * 32 + c * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (m < M) v = ld4(A + m * lda + k, K - k, avec);
-        put4<SPLIT>(ahi, alo, sw128(r, c), v);
-      }
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer ----------------
+      int it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int kc = 0; kc < KC; ++kc, ++it) {
+          const int s = it % ST;
+          mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+          mbar_expect_tx(&full[s], Cfg::TX);
+          tma_load_2d(sA(s), &tmA, &full[s], kc * 32, (int)(t * 128));
+          tma_load_2d(sBh(s), &tmBh, &full[s], kc * 32, 0);
+          if (SPLIT) tma_load_2d(sBl(s), &tmBl, &full[s], kc * 32, 0);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer ----------------
+      const uint32_t idesc = idesc_tf32(BN);
+      int it = 0, acc = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
+        const int a = acc & 1;
+        mbar_wait(&tempty[a], ((acc >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t a0 = smem_u32(ahi), b0 = smem_u32(bhi + (uint32_t)kc * BN * 128);
-        const uint32_t al0 = smem_u32(alo), bl0 = smem_u32(blo + (uint32_t)kc * BN * 128);
+        const uint32_t d = tmem + (uint32_t)(a * BN);
+        for (int kc = 0; kc < KC; ++kc, ++it) {
+          const int s = it % ST;
+          mbar_wait(&conv[s], (it / ST) & 1);
+          tc_fence_after();
+          const uint32_t ah = smem_u32(sA(s)), al = smem_u32(sAlo(s));
+          const uint32_t bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint64_t da = sdesc(a0 + ks * 32, 16, 1024);
-          const uint64_t db = sdesc(b0 + ks * 32, 16, 1024);
-          mma_tf32(tmem, da, db, idesc, (kc | ks) != 0);
-          if (SPLIT) {
-            mma_tf32(tmem, da, sdesc(bl0 + ks * 32, 16, 1024), idesc, 1);
-            mma_tf32(tmem, sdesc(al0 + ks * 32, 16, 1024), db, idesc, 1);
+          for (int ks = 0; ks < 4; ++ks) {
+            const uint64_t dah = sdesc(ah + ks * 32), dbh = sdesc(bh + ks * 32);
+            mma_tf32(d, dah, dbh, idesc, (kc | ks) != 0);
+            if (SPLIT) {
+              mma_tf32(d, dah, sdesc(bl + ks * 32), idesc, 1);
+              mma_tf32(d, sdesc(al + ks * 32), dbh, idesc, 1);
+            }
           }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&bar[s]);
+        mma_commit(&tfull[a]);
       }
-      __syncwarp();
-      if (s == 0) pend0 = true; else pend1 = true;
     }
-    // drain: every MMA of this tile has completed once both stages are idle
-    if (pend0) { mbar_wait(&bar[0], phase0); phase0 ^= 1; pend0 = false; }
-    if (pend1) { mbar_wait(&bar[1], phase1); phase1 ^= 1; pend1 = false; }
-    tc_fence_after();
-    const int64_t m = m0 + warp * 32 + lane;
+  } else if (warp < 4) {  // ---------------- converters (64 threads) ----------------
+    const int ct = threadIdx.x - 64;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      for (int kc = 0; kc < KC; ++kc, ++it) {
+        const int s = it % ST;
+        mbar_wait(&full[s], (it / ST) & 1);
+        float4* hi = reinterpret_cast<float4*>(sA(s));
+        float4* lo = reinterpret_cast<float4*>(sAlo(s));
+#pragma unroll 4
+        for (int q = ct; q < Cfg::A_BYTES / 16; q += 64) {
+          const float4 v = hi[q];
+          const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
+          hi[q] = h;
+          if (SPLIT) lo[q] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        fence_proxy_async();
+        mbar_arrive(&conv[s]);
+      }
+  } else {  // ---------------- epilogue (warps 4-7) ----------------
+    const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
+      const int a = acc & 1;
+      mbar_wait(&tfull[a], (acc >> 1) & 1);
+      tc_fence_after();
+      const int64_t m = t * 128 + q4 * 32 + lane;
+      const uint32_t base = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(a * BN);
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-      if (m < M) {
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(base + (uint32_t)c0, v);
+        if (m < M && c0 < N) {
+          float* crow = C + m * ldc + c0;
+          const float* grow = EPI == TC_MASK ? G + m * ldg + c0 : nullptr;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int f = f0 + c0 + q;
-          if (f < N) {
-            float x = v[q];
-            if (EPI == TC_RELU) x = x > 0.f ? x : 0.f;
-            if (EPI == TC_MASK) x = x > 0.f ? G[m * ldg + f] : 0.f;
-            C[m * ldc + f] = x;
+          for (int j = 0; j < 16; ++j) {
+            if (c0 + j < N) {
+              float x = v[j];
+              if (EPI == TC_RELU) x = x > 0.f ? x : 0.f;
+              if (EPI == TC_MASK) x = x > 0.f ? grow[j] : 0.f;
+              crow[j] = x;
+            }
           }
         }
       }
+      tc_fence_before();
+      mbar_arrive(&tempty[a]);
     }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, NCOL);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, NCOL);
+  }
 }
 
-// Partial dW tiles: P[z][k][n] = sum over rows m of slice z of A[m][k] G[m][n].
-// grid.x = k tiles of 128, grid.y = n tiles of BN, grid.z = row slices.
-// Both operands MN-major: each staged row is 128 bytes of 32 features.
+// ---------------------------------------------------------------------------
+// k_tc_wgrad: P[z][k][n] = sum_{m in slice z} A[m][k] G[m][n], tile 128 x BN
+// grid (ceil(K/128), ceil(N/BN), slices); rows_per_slice multiple of 32.
+// ---------------------------------------------------------------------------
 template <int BN>
-__global__ void __launch_bounds__(128, 1)
-    k_tc_wgrad(const float* __restrict__ A, int64_t lda, int K, const float* __restrict__ Gm,
-               int64_t ldg, int N, int64_t M, int64_t rows_per_slice, float* __restrict__ P) {
+struct WgradCfg {
+  static constexpr int RA = 32 * 128 * 4;     // raw A: 32 rows x 128 floats
+  static constexpr int RG = 32 * BN * 4;      // raw G: 32 rows x BN floats
+  static constexpr int KA = 128 * 128;        // K-major A: 128 rows x 128 B
+  static constexpr int KG = BN * 128;         // K-major G: BN rows x 128 B
+  static constexpr int RAW = RA + RG;
+  static constexpr int KM = KA + KG;
+  static constexpr size_t SMEM = 1024 + 2 * (size_t)RAW + 2 * (size_t)KM + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(256, 1)
+    k_tc_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmG,
+               int K, int N, int64_t M, int64_t rows_per_slice, float* __restrict__ P) {
+  using Cfg = WgradCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  constexpr int ROWS = 32;                       // reduction rows per stage
-  constexpr int A_BYTES = 4 * ROWS * 128;        // 128 features = 4 atoms
-  constexpr int B_BYTES = (BN / 32) * ROWS * 128;
-  constexpr int STAGE = A_BYTES + B_BYTES;
-  constexpr int NST = 3;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + NST);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* km = smem;                  // [2][KA + KG]  (1024-aligned stages)
+  uint8_t* raw = smem + 2 * Cfg::KM;   // [2][RA + RG]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + 2 * Cfg::RAW);
+  uint64_t* rfull = bar;       // [2] TMA landed
+  uint64_t* rempty = bar + 2;  // [2] transposers done reading raw
+  uint64_t* kfull = bar + 4;   // [2] K-major tiles written
+  uint64_t* kempty = bar + 6;  // [2] MMAs done
+  uint64_t* accf = bar + 8;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 9);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
   const int64_t r0 = (int64_t)blockIdx.z * rows_per_slice;
   const int64_t r1 = min(M, r0 + rows_per_slice);
+  const int nst = r1 > r0 ? (int)((r1 - r0 + 31) / 32) : 0;
   constexpr uint32_t NCOL = tmem_cols(BN);
-  if (warp == 0) tmem_alloc(slot, NCOL);
-  if (tid == 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(&bar[s], 1);
+  if (warp == 1) tmem_alloc(slot, NCOL);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], 128);
+      mbar_init(&kfull[s], 128);
+      mbar_init(&kempty[s], 1);
+    }
+    mbar_init(accf, 1);
     fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  // K-major operands: MN-major TF32 operands read back as zeros on sm_100a
-  // (measured), so tiles are transposed while staging instead
-  const uint32_t idesc = idesc_tf32(BN, false, false);
-  const bool avec = (lda & 3) == 0, gvec = (ldg & 3) == 0;
-  uint32_t phase[NST] = {0, 0, 0};
-  bool pend[NST] = {false, false, false};
-  int it = 0;
-  bool any = false;
-  for (int64_t rb = r0; rb < r1; rb += ROWS, ++it) {
-    const int s = it % NST;
-    if (pend[s]) { mbar_wait(&bar[s], phase[s]); phase[s] ^= 1; pend[s] = false; }
-    uint8_t* sa = smem + s * STAGE;
-    uint8_t* sb = sa + A_BYTES;
-    // Transposing loads into K-major tiles (feature rows, 32 reduction
-    // values per 128-byte row): lane = reduction row, so each warp store
-    // fills one swizzled 128-byte smem row without bank conflicts.
-    for (int idx = tid; idx < ROWS * 32; idx += 128) {
-      const int r = idx & 31, fc = idx >> 5;
-      const int64_t m = rb + r;
-      const int k = k0 + fc * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < r1 && k < K) v = ld4(A + m * lda + k, K - k, avec);
-      const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float*>(sa + sw128(fc * 4 + q, r >> 2) + (r & 3) * 4) = tf32_rna(e[q]);
-    }
-    for (int idx = tid; idx < ROWS * (BN / 4); idx += 128) {
-      const int r = idx & 31, fc = idx >> 5;
-      const int64_t m = rb + r;
-      const int n = n0 + fc * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < r1 && n < N) v = ld4(Gm + m * ldg + n, N - n, gvec);
-      const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        *reinterpret_cast<float*>(sb + sw128(fc * 4 + q, r >> 2) + (r & 3) * 4) = tf32_rna(e[q]);
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
-#pragma unroll
-      for (int ks = 0; ks < ROWS / 8; ++ks) {
-        mma_tf32(tmem, sdesc(a0 + ks * 32, 16, 1024), sdesc(b0 + ks * 32, 16, 1024), idesc,
-                 (any || ks) ? 1u : 0u);
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int it = 0; it < nst; ++it) {
+        const int s = it & 1;
+        mbar_wait(&rempty[s], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&rfull[s], Cfg::RAW);
+        uint8_t* ra = raw + s * Cfg::RAW;
+        const int row = (int)(r0 + it * 32);
+        tma_load_2d(ra, &tmA, &rfull[s], k0, row);
+        tma_load_2d(ra + Cfg::RA, &tmG, &rfull[s], n0, row);
       }
-      mma_commit(&bar[s]);
     }
-    __syncwarp();
-    pend[s] = true;
-    any = true;
-  }
-  for (int s = 0; s < NST; ++s)
-    if (pend[s]) { mbar_wait(&bar[s], phase[s]); phase[s] ^= 1; pend[s] = false; }
-  tc_fence_after();
-  const int k = k0 + warp * 32 + lane;
-  float* out = P + (int64_t)blockIdx.z * K * N;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    float v[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-    if (k < K) {
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t idesc = idesc_tf32(BN);
+      for (int it = 0; it < nst; ++it) {
+        const int s = it & 1;
+        mbar_wait(&kfull[s], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t a = smem_u32(km + s * Cfg::KM), b = a + Cfg::KA;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int n = n0 + c0 + q;
-        if (n < N) out[(int64_t)k * N + n] = any ? v[q] : 0.f;
+        for (int ks = 0; ks < 4; ++ks)
+          mma_tf32(tmem, sdesc(a + ks * 32), sdesc(b + ks * 32), idesc, (it | ks) != 0);
+        mma_commit(&kempty[s]);
+      }
+      mma_commit(accf);
+    }
+  } else if (warp < 6) {  // transposers + epilogue (warps 2-5, 128 threads)
+    const int tt = threadIdx.x - 64;
+    for (int it = 0; it < nst; ++it) {
+      const int s = it & 1;
+      mbar_wait(&rfull[s], (it >> 1) & 1);
+      mbar_wait(&kempty[s], ((it >> 1) & 1) ^ 1);
+      const float* ra = reinterpret_cast<const float*>(raw + s * Cfg::RAW);
+      const float* rg = ra + 32 * 128;
+      uint8_t* ka = km + s * Cfg::KM;
+      uint8_t* kg = ka + Cfg::KA;
+      // each thread: one feature row x 4 reduction rows (float4 store)
+      for (int w = tt; w < (128 + BN) * 8; w += 128) {
+        const int f = w % (128 + BN), rq = w / (128 + BN);  // rq: which 4-row group
+        float4 v;
+        if (f < 128) {
+          const float* p = ra + (rq * 4) * 128 + f;
+          v = make_float4(tf32_rna(p[0]), tf32_rna(p[128]), tf32_rna(p[256]), tf32_rna(p[384]));
+          *reinterpret_cast<float4*>(ka + sw128(f, rq)) = v;
+        } else {
+          const int g = f - 128;
+          const float* p = rg + (rq * 4) * BN + g;
+          v = make_float4(tf32_rna(p[0]), tf32_rna(p[BN]), tf32_rna(p[2 * BN]), tf32_rna(p[3 * BN]));
+          *reinterpret_cast<float4*>(kg + sw128(g, rq)) = v;
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(&rempty[s]);
+      mbar_arrive(&kfull[s]);
+    }
+    // epilogue: drain the 128 x BN accumulator into the slice's partial tile
+    const int q4 = warp & 3;
+    const int k = k0 + q4 * 32 + lane;
+    float* out = P + (int64_t)blockIdx.z * K * N;
+    if (nst > 0) {
+      mbar_wait(accf, 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      float v[16];
+      if (nst > 0) tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0, v);
+      if (k < K) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int n = n0 + c0 + j;
+          if (n < N) out[(int64_t)k * N + n] = nst > 0 ? v[j] : 0.f;
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, NCOL);
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, NCOL);
+  }
+}
+
+// W (rows x cols, ld) -> hi = rna_tf32(W), lo = W - hi (same layout)
+__global__ void k_split_tf32(const float* __restrict__ W, float* __restrict__ hi,
+                             float* __restrict__ lo, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float h = tf32_rna(W[e]);
+    hi[e] = h;
+    lo[e] = W[e] - h;
+  }
 }
 
 }  // namespace tc
@@ -402,70 +493,117 @@ __global__ void __launch_bounds__(128, 1)
 namespace ht {
 namespace tc {
 
-inline size_t rows_smem(int bn, bool split, int K) {
-  const size_t kc = (size_t)(K + 31) / 32;
-  return 1024 + kc * bn * 128 * (split ? 2 : 1) + 2 * 128 * 128 * (split ? 2 : 1) + 64;
+inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
 }
 
-template <int BN, bool SPLIT, int EPI>
-int launch_rows_t(cudaStream_t s, const float* A, int64_t lda, int64_t M, int K, const float* Bt,
-                  int64_t ldb, int N, float* C, int64_t ldc, const float* G, int64_t ldg) {
-  const size_t smem = rows_smem(BN, SPLIT, K);
-  auto kern = k_tc_rows<BN, SPLIT, EPI>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return fail(HT_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
-  const int gx = (N + BN - 1) / BN;
-  const int64_t ntiles = (M + 127) / 128;
-  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
-  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)148 * per_sm / gx));
-  kern<<<dim3(gx, (unsigned)gy), 128, smem, s>>>(A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return fail(HT_ECUDA, "k_tc_rows launch: %s", cudaGetErrorString(e));
+// 2-D fp32 tensor map: inner dim `cols` (contiguous), outer `rows`, row
+// stride `ld` floats; box = box_cols x box_rows.
+inline int tmap(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
+                int box_cols, int box_rows, bool swizzle) {
+  auto fn = encode_fn();
+  if (!fn) return fail(HT_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  if (((uintptr_t)base & 15) || (ld * 4) % 16)
+    return fail(HT_EINVAL, "TMA operand needs 16-byte aligned base and row stride (ld=%lld)",
+                (long long)ld);
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)std::max<int64_t>(rows, 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HT_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return HT_OK;
 }
 
-// C = epi(A[M x K] . Bt[N x K]^T); split = 3xTF32
-template <int EPI>
-int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t M, int K,
-         const float* Bt, int64_t ldb, int N, float* C, int64_t ldc, const float* G, int64_t ldg) {
-  if (M <= 0 || N <= 0) return HT_OK;
-  if (K > 256 || K < 1) return fail(HT_EINVAL, "tcgen05 GEMM supports 1 <= K <= 256 (got %d)", K);
-  if (split) {
-    if (N <= 16) return launch_rows_t<16, true, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-    if (N <= 32) return launch_rows_t<32, true, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-    if (N <= 48) return launch_rows_t<48, true, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-    return launch_rows_t<64, true, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
+inline int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
   }
-  if (N <= 16) return launch_rows_t<16, false, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-  if (N <= 32) return launch_rows_t<32, false, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-  if (N <= 48) return launch_rows_t<48, false, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-  if (N <= 64) return launch_rows_t<64, false, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
-  return launch_rows_t<128, false, EPI>(s, A, lda, M, K, Bt, ldb, N, C, ldc, G, ldg);
+  return n;
 }
 
-inline size_t wgrad_smem(int bn) { return 1024 + 3 * (size_t)(4 * 32 * 128 + (bn / 32) * 32 * 128) + 64; }
+template <int BN, bool SPLIT, int EPI>
+int launch_gemm_t(cudaStream_t s, const float* A, int64_t lda, int64_t M, int K, const float* Bh,
+                  const float* Bl, int64_t ldb, int N, float* C, int64_t ldc, const float* G,
+                  int64_t ldg) {
+  using Cfg = GemmCfg<BN, SPLIT>;
+  CUtensorMap ta, tbh, tbl;
+  HT_TRY(tmap(&ta, A, M, K, lda, 32, 128, true));
+  HT_TRY(tmap(&tbh, Bh, N, K, ldb, 32, BN, true));
+  HT_TRY(tmap(&tbl, SPLIT ? Bl : Bh, N, K, ldb, 32, BN, true));
+  auto kern = k_tc_gemm<BN, SPLIT, EPI>;
+  cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+  if (e != cudaSuccess) return fail(HT_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
+  const int64_t ntiles = (M + 127) / 128;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count()));
+  kern<<<grid, 256, Cfg::SMEM, s>>>(ta, tbh, tbl, M, K, N, C, ldc, G, ldg);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HT_ECUDA, "k_tc_gemm launch: %s", cudaGetErrorString(e));
+  return HT_OK;
+}
+
+// C = epi(A[M x K] . B^T) with B = Bh (+ Bl) given K-major (N rows x K,
+// row stride ldb); split = 3xTF32 (Bl required).
+template <int EPI>
+int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t M, int K,
+         const float* Bh, const float* Bl, int64_t ldb, int N, float* C, int64_t ldc,
+         const float* G, int64_t ldg) {
+  if (M <= 0 || N <= 0) return HT_OK;
+  if (K < 1 || N > 256) return fail(HT_EINVAL, "tcgen05 GEMM supports N <= 256 (got %d)", N);
+  if (split) {
+    if (N <= 32) return launch_gemm_t<32, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+    if (N <= 64) return launch_gemm_t<64, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+    if (N <= 128) return launch_gemm_t<128, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+    return launch_gemm_t<256, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+  }
+  if (N <= 32) return launch_gemm_t<32, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+  if (N <= 64) return launch_gemm_t<64, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+  if (N <= 128) return launch_gemm_t<128, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+  return launch_gemm_t<256, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+}
 
 template <int BN>
 int launch_wgrad_t(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
                    int N, int64_t M, int splits, int64_t rps, float* P) {
-  const size_t smem = wgrad_smem(BN);
+  using Cfg = WgradCfg<BN>;
+  CUtensorMap ta, tg;
+  HT_TRY(tmap(&ta, A, M, K, lda, 128, 32, false));
+  HT_TRY(tmap(&tg, G, M, N, ldg, BN, 32, false));
   auto kern = k_tc_wgrad<BN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
   if (e != cudaSuccess) return fail(HT_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
   dim3 grid((unsigned)((K + 127) / 128), (unsigned)((N + BN - 1) / BN), (unsigned)splits);
-  kern<<<grid, 128, smem, s>>>(A, lda, K, G, ldg, N, M, rps, P);
+  kern<<<grid, 256, Cfg::SMEM, s>>>(ta, tg, K, N, M, rps, P);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HT_ECUDA, "k_tc_wgrad launch: %s", cudaGetErrorString(e));
   return HT_OK;
 }
 
-// P[z] = partial A^T G over row slice z; returns the number of slices used.
+// P[z] = partial A^T G over row slice z; *splits_out = number of slices.
 inline int wgrad(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
                  int N, int64_t M, int max_splits, float* P, int* splits_out) {
   if (K > 256 || N > 256) return fail(HT_EINVAL, "tcgen05 wgrad supports K, N <= 256");
   const int gx = (K + 127) / 128;
-  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((M + 31) / 32, 148 / gx));
-  splits = std::min(splits, max_splits);
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((M + 31) / 32, sm_count() / gx));
+  splits = std::max(1, std::min(splits, max_splits));
   int64_t rps = ((M + splits - 1) / splits + 31) / 32 * 32;
   if (rps < 32) rps = 32;
   splits = (int)std::max<int64_t>(1, (M + rps - 1) / rps);
@@ -473,8 +611,14 @@ inline int wgrad(cudaStream_t s, const float* A, int64_t lda, int K, const float
   if (N <= 32) return launch_wgrad_t<32>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
   if (N <= 64) return launch_wgrad_t<64>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
   if (N <= 128) return launch_wgrad_t<128>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
-  if (N <= 192) return launch_wgrad_t<192>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
   return launch_wgrad_t<256>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
+}
+
+inline int split_weights(cudaStream_t s, const float* W, float* hi, float* lo, int64_t n) {
+  k_split_tf32<<<(int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, s>>>(W, hi, lo, n);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(HT_ECUDA, "k_split_tf32: %s", cudaGetErrorString(e));
+  return HT_OK;
 }
 
 }  // namespace tc
