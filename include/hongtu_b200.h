@@ -168,6 +168,10 @@ int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W
  * output; writes grad rows to grad_out (host.grad_h[L]).  count = mask.sum(). */
 int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uint8_t* mask,
             int64_t V, int64_t count, void* grad_out, double* loss);
+/* Layer calls and ht_loss only enqueue work (no host synchronization);
+ * with loss == NULL the value is read later with ht_loss_value, which
+ * waits for the loss kernels. */
+int ht_loss_value(ht_fleet* f, double* loss);
 /* One backward layer over all batches (engine.py:449-477): checkpoint and
  * dest-gradient reload, hybrid backward, transposed aggregation, owner push
  * and flush into grad_in (host.grad_h[layer]). */

@@ -66,6 +66,7 @@ _SIGS = {
     "ht_epoch_begin": (i32, [vp, i32, vp]),
     "ht_forward_layer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, i32]),
     "ht_loss": (i32, [vp, i32, vp, vp, i64, i64, vp, P_F64]),
+    "ht_loss_value": (i32, [vp, P_F64]),
     "ht_backward_layer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, i32]),
     "ht_sgd": (i32, [vp, i32, vp, vp, f32, vp]),
     "ht_fleet_sync": (i32, [vp]),

@@ -97,6 +97,14 @@ struct DevChunk {
   DBuf bw_lo, bw_hi, bw_seg, bw_first, bw_cnt;  // (backward)
 };
 
+struct LayerW {
+  DBuf W, Wt, Wp, Wt_hi, Wt_lo, Wp_hi, Wp_lo;
+  bool valid = false;
+};
+
+constexpr int kHostGrid = 128;    // CTAs of a zero-copy host transfer kernel
+constexpr int kSplitsMax = 64;    // row slices of the weight-gradient GEMM
+
 struct TimerRec {
   cudaEvent_t a, b;
   int which;
@@ -119,6 +127,20 @@ struct Device {
   DBuf labels, mask, loss_part;
   std::vector<DevChunk> chunks;
   cudaEvent_t mark[2] = {nullptr, nullptr};
+  // epoch pipeline: transfer streams, double-buffered staging, events
+  cudaStream_t tin = nullptr, tout = nullptr;
+  DBuf fa[2], fb[2], ba[2], bb[2];
+  cudaEvent_t e_in = nullptr, e_fetch = nullptr, e_agg = nullptr, e_comp = nullptr;
+  cudaEvent_t e_out[2] = {nullptr, nullptr}, e_hst = nullptr, e_loss = nullptr;
+  cudaEvent_t e_bin = nullptr, e_bcomp[2] = {nullptr, nullptr}, e_flush = nullptr;
+  std::vector<cudaEvent_t> e_aggst;  // per layer: checkpoint rows stored
+  int64_t fwd_count = 0, bwd_count = 0;
+  std::vector<LayerW> lw;            // per-layer weights (valid until the SGD step)
+  float* wpin = nullptr;             // pinned scratch for weight uploads
+  std::vector<int64_t> wpin_off;
+  int64_t wpin_cap = 0;
+  uint8_t* lpin = nullptr;           // pinned labels + mask
+  int64_t lpin_cap = 0;
 };
 
 }  // namespace
@@ -136,6 +158,7 @@ struct ht_fleet {
   double t_ms[4] = {0, 0, 0, 0}, t_bytes[4] = {0, 0, 0, 0};
   int L = 0;
   std::vector<int> dims;
+  int64_t loss_count = 0;
 };
 
 namespace {
@@ -163,6 +186,8 @@ int sync_all(ht_fleet* f) {
   for (auto& d : f->dev) {
     HT_TRY(set_dev(d));
     CU(cudaStreamSynchronize(d.stream));
+    if (d.tin) CU(cudaStreamSynchronize(d.tin));
+    if (d.tout) CU(cudaStreamSynchronize(d.tout));
   }
   return HT_OK;
 }
@@ -196,11 +221,12 @@ int dev_ptr(const void* p, void** out) {
 // Row copy with the widest vector the row size and alignment permit.
 int launch_copy(cudaStream_t s, void* dst, const void* src, const int64_t* didx,
                 const int64_t* sidx, int64_t rows, int64_t row_bytes, int64_t dstride,
-                int64_t sstride, int64_t dbase = 0) {
+                int64_t sstride, int64_t dbase = 0, int max_grid = 0) {
   if (rows <= 0 || row_bytes <= 0) return HT_OK;
   const uintptr_t al = (uintptr_t)dst | (uintptr_t)src | (uintptr_t)row_bytes |
                        (uintptr_t)dstride | (uintptr_t)sstride;
-  const int g = grid_for(rows);
+  int g = grid_for(rows);
+  if (max_grid > 0) g = std::min(g, max_grid);
   count_launch();
   if ((al & 15) == 0)
     ht::k_copy_rows<int4><<<g, kThreads, 0, s>>>((char*)dst, (const char*)src, didx, sidx, rows,
@@ -231,15 +257,16 @@ int launch_acc(cudaStream_t s, int elem, void* dst, void* src, const int64_t* di
   return HT_OK;
 }
 
-void timer_begin(ht_fleet* f, Device& d, TimerRec& r) {
+void timer_begin(ht_fleet* f, Device& d, TimerRec& r, cudaStream_t s = nullptr) {
   if (!f->timing) return;
   cudaEventCreate(&r.a);
   cudaEventCreate(&r.b);
-  cudaEventRecord(r.a, d.stream);
+  cudaEventRecord(r.a, s ? s : d.stream);
 }
-void timer_end(ht_fleet* f, Device& d, TimerRec& r, int which, double bytes) {
+void timer_end(ht_fleet* f, Device& d, TimerRec& r, int which, double bytes,
+               cudaStream_t s = nullptr) {
   if (!f->timing) return;
-  cudaEventRecord(r.b, d.stream);
+  cudaEventRecord(r.b, s ? s : d.stream);
   r.which = which;
   r.bytes = bytes;
   f->timers.push_back(r);
@@ -471,6 +498,8 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
     if (d.ordinal < 0 || d.ordinal >= ndev) return fail(HT_EINVAL, "bad device ordinal %d", d.ordinal);
     CU(cudaSetDevice(d.ordinal));
     CU(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&d.tin, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&d.tout, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
     d.chunks.resize(n);
     for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
@@ -518,7 +547,20 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     if (d.ev) cudaEventDestroy(d.ev);
     for (auto& e : d.mark)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : {d.e_in, d.e_fetch, d.e_agg, d.e_comp, d.e_out[0], d.e_out[1], d.e_hst,
+                          d.e_loss, d.e_bin, d.e_bcomp[0], d.e_bcomp[1], d.e_flush})
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : d.e_aggst)
+      if (e) cudaEventDestroy(e);
+    for (int s = 0; s < 2; ++s)
+      for (DBuf* b : {&d.fa[s], &d.fb[s], &d.ba[s], &d.bb[s]}) b->release();
+    for (auto& w : d.lw)
+      for (DBuf* b : {&w.W, &w.Wt, &w.Wp, &w.Wt_hi, &w.Wt_lo, &w.Wp_hi, &w.Wp_lo}) b->release();
+    if (d.wpin) cudaFreeHost(d.wpin);
+    if (d.lpin) cudaFreeHost(d.lpin);
     if (d.stream) cudaStreamDestroy(d.stream);
+    if (d.tin) cudaStreamDestroy(d.tin);
+    if (d.tout) cudaStreamDestroy(d.tout);
   }
   delete f;
   return HT_OK;
@@ -875,12 +917,73 @@ extern "C" int ht_dest_rows(ht_fleet* f, int op, int batch, int dim, int elem_si
 
 // ===========================================================================
 // GCN epoch
+//
+// Three streams per device: `stream` (compute + peer traffic), `tin`
+// (host -> device rows) and `tout` (device -> host rows).  Events order
+// them; nothing in a layer call synchronizes the host, so host loads of the
+// next batch / layer, device compute and host stores of the previous batch
+// overlap (PCIe is full duplex).  Staging buffers alternate between two sets
+// by an epoch-wide batch counter.
 // ===========================================================================
+namespace {
+
+int ev_rec(cudaEvent_t& e, cudaStream_t s) {
+  if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CU(cudaEventRecord(e, s));
+  return HT_OK;
+}
+
+int ev_wait(cudaStream_t s, cudaEvent_t e) {
+  if (e) CU(cudaStreamWaitEvent(s, e, 0));
+  return HT_OK;
+}
+
+// weights of layer l into the per-layer device buffers (async, from a
+// pinned host scratch): W, W^T and W padded, plus the TF32 hi/lo halves
+int upload_layer_weights(Device& d, int l, const float* W, int d_in, int d_out) {
+  LayerW& w = d.lw[l];
+  const int64_t nw = (int64_t)d_in * d_out;
+  const int ldo = pad4(d_out);
+  const int64_t np = (int64_t)d_in * ldo;
+  float* wt = d.wpin + d.wpin_off[l];
+  float* wn = wt + nw;
+  float* wp = wn + nw;
+  std::memcpy(wn, W, nw * 4);
+  for (int a = 0; a < d_in; ++a)
+    for (int b = 0; b < ldo; ++b) {
+      if (b < d_out) wt[(int64_t)b * d_in + a] = W[(int64_t)a * d_out + b];
+      wp[(int64_t)a * ldo + b] = b < d_out ? W[(int64_t)a * d_out + b] : 0.f;
+    }
+  for (DBuf* b : {&w.W, &w.Wt, &w.Wt_hi, &w.Wt_lo}) HT_TRY(b->ensure(nw * 4));
+  for (DBuf* b : {&w.Wp, &w.Wp_hi, &w.Wp_lo}) HT_TRY(b->ensure(np * 4));
+  CU(cudaMemcpyAsync(w.W.p, wn, nw * 4, cudaMemcpyHostToDevice, d.stream));
+  CU(cudaMemcpyAsync(w.Wt.p, wt, nw * 4, cudaMemcpyHostToDevice, d.stream));
+  CU(cudaMemcpyAsync(w.Wp.p, wp, np * 4, cudaMemcpyHostToDevice, d.stream));
+  HT_TRY(ht::tc::split_weights(d.stream, w.Wt.as<float>(), w.Wt_hi.as<float>(), w.Wt_lo.as<float>(), nw));
+  HT_TRY(ht::tc::split_weights(d.stream, w.Wp.as<float>(), w.Wp_hi.as<float>(), w.Wp_lo.as<float>(), np));
+  count_launch(2);
+  w.valid = true;
+  return HT_OK;
+}
+
+int check_chunks(ht_fleet* f) {
+  for (int i = 0; i < f->m; ++i)
+    for (int j = 0; j < f->n; ++j)
+      if (!f->sets[i][j].has_chunk || !f->sets[i][j].has_dest)
+        return fail(HT_ESTATE, "chunk (%d,%d) has no graph structure uploaded", i, j);
+  return HT_OK;
+}
+
+}  // namespace
 
 extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
   if (!f->finalized) return fail(HT_ESTATE, "fleet not finalized");
+  HT_TRY(check_chunks(f));
+  HT_TRY(sync_all(f));
   f->L = L;
   f->dims.assign(dims, dims + L + 1);
+  int dmax = 0;
+  for (int l = 0; l <= L; ++l) dmax = std::max(dmax, pad4(dims[l]));
   for (auto& d : f->dev) {
     HT_TRY(set_dev(d));
     if ((int)d.gW.size() < L) d.gW.resize(L);
@@ -890,84 +993,142 @@ extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
       HT_TRY(d.gW[l].ensure(bytes));
       CU(cudaMemsetAsync(d.gW[l].p, 0, bytes, d.stream));
     }
+    // every buffer of the epoch is sized here, once: no allocation (and no
+    // implicit device synchronization) inside the layer calls
+    int64_t mv = 1, mn = 1, np = 1;
+    d.hL_off.assign(f->n + 1, 0);
+    for (int j = 0; j < f->n; ++j) {
+      mv = std::max(mv, d.chunks[j].nv);
+      mn = std::max(mn, d.chunks[j].nn);
+      np = std::max({np, d.chunks[j].fw_np, d.chunks[j].bw_np});
+      d.hL_off[j + 1] = d.hL_off[j] + d.chunks[j].nv;
+    }
+    HT_TRY(d.value.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
+    HT_TRY(d.grad.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
+    for (int s = 0; s < 2; ++s) {
+      HT_TRY(d.fa[s].ensure(mv * dmax * 4));
+      HT_TRY(d.fb[s].ensure(mv * dmax * 4));
+      HT_TRY(d.ba[s].ensure(mv * dmax * 4));
+      HT_TRY(d.bb[s].ensure(mv * dmax * 4));
+    }
+    HT_TRY(d.sc.ensure(mv * dmax * 4));
+    HT_TRY(d.sd.ensure(mv * dmax * 4));
+    HT_TRY(d.se.ensure(mn * dmax * 4));
+    HT_TRY(d.partial.ensure(np * dmax * 4));
+    HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
+    HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
+    // pinned scratch for weight uploads, one slot per layer
+    d.wpin_off.assign(L + 1, 0);
+    for (int l = 0; l < L; ++l)
+      d.wpin_off[l + 1] = d.wpin_off[l] + 2 * (int64_t)dims[l] * dims[l + 1] +
+                          (int64_t)dims[l] * pad4(dims[l + 1]);
+    if (d.wpin_cap < d.wpin_off[L]) {
+      if (d.wpin) cudaFreeHost(d.wpin);
+      CU(cudaHostAlloc(reinterpret_cast<void**>(&d.wpin), d.wpin_off[L] * 4, cudaHostAllocPortable));
+      d.wpin_cap = d.wpin_off[L];
+    }
+    d.lw.resize(L);
+    for (auto& w : d.lw) w.valid = false;
+    d.fwd_count = d.bwd_count = 0;
+    if ((int)d.e_aggst.size() < L) d.e_aggst.resize(L, nullptr);
   }
-  return HT_OK;
-}
-
-static int check_chunks(ht_fleet* f) {
-  for (int i = 0; i < f->m; ++i)
-    for (int j = 0; j < f->n; ++j)
-      if (!f->sets[i][j].has_chunk || !f->sets[i][j].has_dest)
-        return fail(HT_ESTATE, "chunk (%d,%d) has no graph structure uploaded", i, j);
   return HT_OK;
 }
 
 extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
                                 const void* h_in, void* h_out, void* agg_out, int precision) {
-  HT_TRY(check_chunks(f));
+  if (layer < 0 || layer >= f->L || f->dims[layer] != d_in || f->dims[layer + 1] != d_out)
+    return fail(HT_EINVAL, "layer %d shape does not match ht_epoch_begin", layer);
   void *hin, *hout, *aout;
   HT_TRY(dev_ptr(h_in, &hin));
   HT_TRY(dev_ptr(h_out, &hout));
   HT_TRY(dev_ptr(agg_out, &aout));
-  HT_TRY(ht_begin_layer(f, d_in, 4, 0));
+  if (precision == HT_PREC_TF32 && (d_in & 3))
+    return fail(HT_EINVAL, "tf32 path needs layer input widths divisible by 4 (got %d)", d_in);
+  f->dim = d_in;
+  f->elem = 4;
   const bool last = layer == f->L - 1;
+  const int64_t rbi = (int64_t)d_in * 4, rbo = (int64_t)d_out * 4;
   for (auto& d : f->dev) {
     HT_TRY(set_dev(d));
-    int64_t mv = 0, tot = 0;
-    d.hL_off.assign(f->n + 1, 0);
-    for (int j = 0; j < f->n; ++j) {
-      mv = std::max(mv, d.chunks[j].nv);
-      d.hL_off[j + 1] = d.hL_off[j] + d.chunks[j].nv;
-    }
-    tot = d.hL_off[f->n];
-    HT_TRY(d.sa.ensure(std::max<int64_t>(1, mv) * d_in * 4));
-    HT_TRY(d.sb.ensure(std::max<int64_t>(1, mv) * d_out * 4));
-    int64_t np = 0;
-    for (int j = 0; j < f->n; ++j) np = std::max(np, d.chunks[j].fw_np);
-    HT_TRY(d.partial.ensure(std::max<int64_t>(1, np) * d_in * 4));
-    HT_TRY(upload_weights(d, W, d_in, d_out));
-    if (last) {
-      HT_TRY(d.hL.ensure(std::max<int64_t>(1, tot) * d_out * 4));
-      f->hL_dim = d_out;
-    }
+    HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
   }
+  if (last) f->hL_dim = d_out;
   for (int j = 0; j < f->n; ++j) {
-    HT_TRY(stage_batch(f, j, hin));
+    // ---- step 1: host loads into slots (tin) ----
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
-      float* agg = d.sa.as<float>();
+      if (d.fwd_count > 0) {  // slots of the previous batch no longer read
+        HT_TRY(ev_wait(d.tin, d.e_agg));
+        for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_fetch));
+      }
+      if (j == 0 && layer > 0)  // h^l rows stored (baseline loads rows of every owner)
+        for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_hst));
       TimerRec tr;
-      timer_begin(f, d, tr);
+      timer_begin(f, d, tr, d.tin);
+      HT_TRY(launch_copy(d.tin, d.value.p, hin, c.h2d.dst.as<int64_t>(), c.h2d.src.as<int64_t>(),
+                         c.h2d.n, rbi, rbi, rbi, 0, kHostGrid));
+      timer_end(f, d, tr, 3, (double)c.h2d.n * rbi, d.tin);
+      HT_TRY(ev_rec(d.e_in, d.tin));
+    }
+    // ---- barrier + step 2: staggered peer fetches (compute stream) ----
+    for (int i = 0; i < f->m; ++i) {
+      Device& d = f->dev[i];
+      HT_TRY(set_dev(d));
+      DevChunk& c = d.chunks[j];
+      for (auto& o : f->dev) HT_TRY(ev_wait(d.stream, o.e_in));
+      if (f->mode != HT_MODE_BASELINE)
+        for (int st = 1; st < f->m; ++st) {
+          const int k = (i + st) % f->m;
+          const CopyList& cl = c.d2d[st];
+          HT_TRY(launch_copy(d.stream, d.value.p, f->dev[k].value.p, cl.dst.as<int64_t>(),
+                             cl.src.as<int64_t>(), cl.n, rbi, rbi, rbi));
+        }
+      HT_TRY(ev_rec(d.e_fetch, d.stream));
+    }
+    // ---- aggregation, dense transform, stores (tout) ----
+    for (int i = 0; i < f->m; ++i) {
+      Device& d = f->dev[i];
+      HT_TRY(set_dev(d));
+      DevChunk& c = d.chunks[j];
+      const int s = (int)(d.fwd_count & 1);
+      if (d.fwd_count >= 2) HT_TRY(ev_wait(d.stream, d.e_out[s]));  // staging set s drained
+      float* agg = d.fa[s].as<float>();
+      TimerRec tr;
+      timer_begin(f, d, tr, d.stream);
       HT_TRY(launch_seg(d.stream, agg, d.value.as<float>(), d_in, d_in, c.csc_off.as<int64_t>(),
                         c.csc_slot.as<int32_t>(), c.csc_w.as<float>(), c.nv, c.fw_np, c.fw_lo,
                         c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt, d.partial.as<float>()));
-      timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nv * (4.0 * d_in + 4.0));
-      float* hdst = last ? d.hL.as<float>() + d.hL_off[j] * d_out : d.sb.as<float>();
+      timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nv * (4.0 * d_in + 4.0),
+                d.stream);
+      HT_TRY(ev_rec(d.e_agg, d.stream));
+      float* hdst = last ? d.hL.as<float>() + d.hL_off[j] * d_out : d.fb[s].as<float>();
+      LayerW& w = d.lw[layer];
       TimerRec tg;
-      timer_begin(f, d, tg);
+      timer_begin(f, d, tg, d.stream);
       if (precision == HT_PREC_TF32) {
         HT_TRY(ht::tc::rows<ht::tc::TC_RELU>(d.stream, true, agg, d_in, c.nv, d_in,
-                                             d.Wt_hi.as<float>(), d.Wt_lo.as<float>(), d_in, d_out,
-                                             hdst, d_out, nullptr, 0));
+                                             w.Wt_hi.as<float>(), w.Wt_lo.as<float>(), d_in,
+                                             d_out, hdst, d_out, nullptr, 0));
       } else {
-        HT_TRY((gemm<false, false, ht::EPI_RELU>(d.stream, agg, d_in, d.W.as<float>(), d_out, hdst,
+        HT_TRY((gemm<false, false, ht::EPI_RELU>(d.stream, agg, d_in, w.W.as<float>(), d_out, hdst,
                                                  d_out, nullptr, 0, c.nv, d_out, d_in, 1, d_in)));
       }
-      timer_end(f, d, tg, 2, 2.0 * c.nv * d_in * d_out);
-      // K5: dest rows + checkpoint rows to the host store
+      timer_end(f, d, tg, 2, 2.0 * c.nv * d_in * d_out, d.stream);
+      HT_TRY(ev_rec(d.e_comp, d.stream));
+      // K5: destination rows, then checkpoint rows, to the host store
+      HT_TRY(ev_wait(d.tout, d.e_comp));
       const int64_t* rows = c.dest_rows.as<int64_t>();
-      HT_TRY(launch_copy(d.stream, hout, hdst, rows, nullptr, c.nv, (int64_t)d_out * 4,
-                         (int64_t)d_out * 4, (int64_t)d_out * 4));
-      HT_TRY(launch_copy(d.stream, aout, agg, rows, nullptr, c.nv, (int64_t)d_in * 4,
-                         (int64_t)d_in * 4, (int64_t)d_in * 4));
+      HT_TRY(launch_copy(d.tout, hout, hdst, rows, nullptr, c.nv, rbo, rbo, rbo, 0, kHostGrid));
+      if (j == f->n - 1) HT_TRY(ev_rec(d.e_hst, d.tout));
+      HT_TRY(launch_copy(d.tout, aout, agg, rows, nullptr, c.nv, rbi, rbi, rbi, 0, kHostGrid));
+      HT_TRY(ev_rec(d.e_out[s], d.tout));
+      if (j == f->n - 1) HT_TRY(ev_rec(d.e_aggst[layer], d.tout));
+      d.fwd_count++;
     }
-    // the next batch's host loads may overwrite slots peers still read
-    HT_TRY(barrier(f));
   }
-  HT_TRY(sync_all(f));
-  timers_collect(f);
   return HT_OK;
 }
 
@@ -976,143 +1137,168 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
   if (f->hL_dim != d_last) return fail(HT_ESTATE, "loss before the last forward layer");
   void* gout;
   HT_TRY(dev_ptr(grad_out, &gout));
-  *loss = 0.0;
-  if (count == 0) return HT_OK;
+  f->loss_count = count;
   const int blocks = 148 * 4;
-  std::vector<std::vector<double>> parts(f->m);
   for (int i = 0; i < f->m; ++i) {
     Device& d = f->dev[i];
     HT_TRY(set_dev(d));
+    // labels/mask through a pinned copy so the upload does not block the host
+    if (d.lpin_cap < V * 9) {
+      if (d.lpin) cudaFreeHost(d.lpin);
+      CU(cudaHostAlloc(reinterpret_cast<void**>(&d.lpin), V * 9, cudaHostAllocPortable));
+      d.lpin_cap = V * 9;
+    }
+    std::memcpy(d.lpin, labels, V * 8);
+    std::memcpy(d.lpin + V * 8, mask, V);
     HT_TRY(d.labels.ensure(V * 8));
     HT_TRY(d.mask.ensure(V));
     HT_TRY(d.loss_part.ensure((int64_t)blocks * f->n * 8));
-    CU(cudaMemcpyAsync(d.labels.p, labels, V * 8, cudaMemcpyHostToDevice, d.stream));
-    CU(cudaMemcpyAsync(d.mask.p, mask, V, cudaMemcpyHostToDevice, d.stream));
-    for (int j = 0; j < f->n; ++j) {
-      DevChunk& c = d.chunks[j];
-      count_launch();
-      ht::k_loss<<<blocks, 256, 0, d.stream>>>(
-          d.hL.as<float>() + d.hL_off[j] * d_last, c.nv, d_last, d.labels.as<int64_t>(),
-          d.mask.as<uint8_t>(), c.dest_rows.as<int64_t>(), (float*)gout, (float)count,
-          d.loss_part.as<double>() + (int64_t)j * blocks);
-      CU(cudaGetLastError());
-    }
-    parts[i].resize((size_t)blocks * f->n);
-    CU(cudaMemcpyAsync(parts[i].data(), d.loss_part.p, parts[i].size() * 8, cudaMemcpyDeviceToHost,
-                       d.stream));
+    CU(cudaMemcpyAsync(d.labels.p, d.lpin, V * 8, cudaMemcpyHostToDevice, d.stream));
+    CU(cudaMemcpyAsync(d.mask.p, d.lpin + V * 8, V, cudaMemcpyHostToDevice, d.stream));
+    CU(cudaMemsetAsync(d.loss_part.p, 0, (int64_t)blocks * f->n * 8, d.stream));
+    if (count > 0)
+      for (int j = 0; j < f->n; ++j) {
+        DevChunk& c = d.chunks[j];
+        count_launch();
+        ht::k_loss<<<blocks, 256, 0, d.stream>>>(
+            d.hL.as<float>() + d.hL_off[j] * d_last, c.nv, d_last, d.labels.as<int64_t>(),
+            d.mask.as<uint8_t>(), c.dest_rows.as<int64_t>(), (float*)gout, (float)count,
+            d.loss_part.as<double>() + (int64_t)j * blocks);
+        CU(cudaGetLastError());
+      }
+    HT_TRY(ev_rec(d.e_loss, d.stream));
   }
-  HT_TRY(sync_all(f));
+  if (loss) return ht_loss_value(f, loss);
+  return HT_OK;
+}
+
+extern "C" int ht_loss_value(ht_fleet* f, double* loss) {
+  *loss = 0.0;
+  if (f->loss_count <= 0) return HT_OK;
   double tot = 0.0;
-  for (int i = 0; i < f->m; ++i)
-    for (double p : parts[i]) tot += p;
-  *loss = tot / (double)count;
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    std::vector<double> parts(d.loss_part.bytes / 8);
+    CU(cudaMemcpyAsync(parts.data(), d.loss_part.p, parts.size() * 8, cudaMemcpyDeviceToHost,
+                       d.stream));
+    CU(cudaStreamSynchronize(d.stream));
+    for (double p : parts) tot += p;
+  }
+  *loss = tot / (double)f->loss_count;
   return HT_OK;
 }
 
 extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
                                  const void* agg_in, const void* grad_out, void* grad_in,
                                  int precision) {
-  HT_TRY(check_chunks(f));
-  if (layer < 0 || layer >= f->L) return fail(HT_EINVAL, "layer out of range");
+  if (layer < 0 || layer >= f->L || f->dims[layer] != d_in || f->dims[layer + 1] != d_out)
+    return fail(HT_EINVAL, "layer %d shape does not match ht_epoch_begin", layer);
   void *ain, *gout, *gin;
   HT_TRY(dev_ptr(agg_in, &ain));
   HT_TRY(dev_ptr(grad_out, &gout));
   HT_TRY(dev_ptr(grad_in, &gin));
-  HT_TRY(ht_begin_layer(f, d_in, 4, 1));
-  const int splits_max = 64;
+  f->dim = d_in;
+  f->elem = 4;
+  const int64_t rbi = (int64_t)d_in * 4, rbo = (int64_t)d_out * 4;
+  const int ldz = precision == HT_PREC_TF32 ? pad4(d_out) : d_out;
   for (auto& d : f->dev) {
     HT_TRY(set_dev(d));
-    int64_t mv = 1, mn = 1, np = 1;
-    for (int j = 0; j < f->n; ++j) {
-      mv = std::max(mv, d.chunks[j].nv);
-      mn = std::max(mn, d.chunks[j].nn);
-      np = std::max(np, d.chunks[j].bw_np);
-    }
-    HT_TRY(d.sa.ensure(mv * d_in * 4));   // agg checkpoint rows
-    HT_TRY(d.sb.ensure(mv * d_out * 4));  // dest gradient rows
-    HT_TRY(d.sc.ensure(mv * pad4(d_out) * 4));  // gz (row stride pad4(d_out))
-    HT_TRY(d.sd.ensure(mv * d_in * 4));   // grad agg
-    HT_TRY(d.se.ensure(mn * d_in * 4));   // grad of neighbour rows (views)
-    HT_TRY(d.partial.ensure(np * d_in * 4));
-    HT_TRY(d.gemm_ws.ensure((int64_t)splits_max * d_in * d_out * 4));
-    HT_TRY(upload_weights(d, W, d_in, d_out));
+    if (!d.lw[layer].valid) HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
+    if (f->mode != HT_MODE_BASELINE)  // begin_backward_layer: zeroed gradient slots
+      CU(cudaMemsetAsync(d.grad.p, 0, d.cap * rbi, d.stream));
   }
   for (int j = 0; j < f->n; ++j) {
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
+      const int s = (int)(d.bwd_count & 1);
       const int64_t* rows = c.dest_rows.as<int64_t>();
-      float *A = d.sa.as<float>(), *G = d.sb.as<float>(), *GZ = d.sc.as<float>(),
-            *GA = d.sd.as<float>();
-      // K6: checkpoint + destination-gradient reload
-      HT_TRY(launch_copy(d.stream, A, ain, nullptr, rows, c.nv, (int64_t)d_in * 4,
-                         (int64_t)d_in * 4, (int64_t)d_in * 4));
-      HT_TRY(launch_copy(d.stream, G, gout, nullptr, rows, c.nv, (int64_t)d_out * 4,
-                         (int64_t)d_out * 4, (int64_t)d_out * 4));
-      // K7: z = agg W (recompute), gz = g * [z > 0], dW += agg^T gz, gagg = gz W^T
+      float *A = d.ba[s].as<float>(), *G = d.bb[s].as<float>();
+      // K6 on tin: checkpoint rows (ready since the forward), then the
+      // destination gradients (ready once the layer above has flushed)
+      if (d.bwd_count >= 2) HT_TRY(ev_wait(d.tin, d.e_bcomp[s]));
+      HT_TRY(ev_wait(d.tin, d.e_aggst[layer]));
+      HT_TRY(launch_copy(d.tin, A, ain, nullptr, rows, c.nv, rbi, rbi, rbi, 0, kHostGrid));
+      if (j == 0) {
+        if (layer == f->L - 1) {
+          HT_TRY(ev_wait(d.tin, d.e_loss));
+        } else if (f->mode == HT_MODE_BASELINE) {
+          for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_flush));
+        } else {
+          HT_TRY(ev_wait(d.tin, d.e_flush));
+        }
+      }
+      HT_TRY(launch_copy(d.tin, G, gout, nullptr, rows, c.nv, rbo, rbo, rbo, 0, kHostGrid));
+      HT_TRY(ev_rec(d.e_bin, d.tin));
+      // K7 on the compute stream
+      HT_TRY(ev_wait(d.stream, d.e_bin));
+      float *GZ = d.sc.as<float>(), *GA = d.sd.as<float>();
+      LayerW& w = d.lw[layer];
       TimerRec tg;
-      timer_begin(f, d, tg);
+      timer_begin(f, d, tg, d.stream);
       const int64_t M = c.nv;
-      int splits = (int)std::min<int64_t>(splits_max, std::max<int64_t>(1, M / 2048));
-      int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
-      splits = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
+      const int64_t nw = (int64_t)d_in * d_out;
       if (precision == HT_PREC_TF32) {
-        const int ldz = pad4(d_out);
-        HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in,
-                                             d.Wt_hi.as<float>(), d.Wt_lo.as<float>(), d_in, d_out,
-                                             GZ, ldz, G, d_out));
+        HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, w.Wt_hi.as<float>(),
+                                             w.Wt_lo.as<float>(), d_in, d_out, GZ, ldz, G, d_out));
         HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
-                                              d.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
+                                              w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
                                               nullptr, 0));
         if (M > 0) {
           int used = 1;
-          HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, ldz, d_out, M, splits_max,
+          HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, ldz, d_out, M, kSplitsMax,
                                d.gemm_ws.as<float>(), &used));
-          const int64_t nw = (int64_t)d_in * d_out;
           count_launch(4);
           ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
               d.gW[layer].as<float>(), d.gemm_ws.as<float>(), nw, used);
           CU(cudaGetLastError());
         }
       } else {
-        HT_TRY((gemm<false, false, ht::EPI_MASK>(d.stream, A, d_in, d.W.as<float>(), d_out, GZ,
-                                                 d_out, G, d_out, M, d_out, d_in, 1, d_in)));
+        int splits = (int)std::min<int64_t>(kSplitsMax, std::max<int64_t>(1, M / 2048));
+        int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
+        splits = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
+        HT_TRY((gemm<false, false, ht::EPI_MASK>(d.stream, A, d_in, w.W.as<float>(), d_out, GZ,
+                                                 ldz, G, d_out, M, d_out, d_in, 1, d_in)));
         if (M > 0) {
-          HT_TRY((gemm<true, false, ht::EPI_STORE>(d.stream, A, d_in, GZ, d_out,
+          HT_TRY((gemm<true, false, ht::EPI_STORE>(d.stream, A, d_in, GZ, ldz,
                                                    d.gemm_ws.as<float>(), d_out, nullptr, 0, d_in,
                                                    d_out, M, splits, kps)));
-          const int64_t nw = (int64_t)d_in * d_out;
           count_launch();
           ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
               d.gW[layer].as<float>(), d.gemm_ws.as<float>(), nw, splits);
           CU(cudaGetLastError());
         }
-        HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, d_out, d.W.as<float>(), d_out, GA,
+        HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, ldz, w.W.as<float>(), d_out, GA,
                                                  d_in, nullptr, 0, M, d_in, d_out, 1, d_out)));
       }
-      timer_end(f, d, tg, 2, 6.0 * c.nv * d_in * d_out);
+      timer_end(f, d, tg, 2, 6.0 * c.nv * d_in * d_out, d.stream);
+      HT_TRY(ev_rec(d.e_bcomp[s], d.stream));
       // K8: transposed aggregation over the CSR view -> neighbour-row grads
       TimerRec tr;
-      timer_begin(f, d, tr);
+      timer_begin(f, d, tr, d.stream);
       HT_TRY(launch_seg(d.stream, d.se.as<float>(), GA, d_in, d_in, c.csr_off.as<int64_t>(),
                         c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), c.nn, c.bw_np, c.bw_lo,
                         c.bw_hi, c.bw_nf, c.bw_seg, c.bw_first, c.bw_cnt, d.partial.as<float>()));
-      timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nn * (4.0 * d_in + 4.0));
+      timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nn * (4.0 * d_in + 4.0),
+                d.stream);
+      d.bwd_count++;
     }
     // K9/K10: owner push (ascending source device) + flush into host grads
     HT_TRY(push_flush(f, j, gin, true));
   }
-  HT_TRY(sync_all(f));
-  timers_collect(f);
+  for (auto& d : f->dev) {
+    HT_TRY(set_dev(d));
+    HT_TRY(ev_rec(d.e_flush, d.stream));
+  }
   return HT_OK;
 }
 
 extern "C" int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, float lr,
                       float* const* grads_out) {
   Device& d0 = f->dev[0];
-  HT_TRY(set_dev(d0));
   HT_TRY(sync_all(f));
+  HT_TRY(set_dev(d0));
   for (int l = 0; l < L; ++l) {
     const int64_t nw = (int64_t)dims[l] * dims[l + 1];
     std::vector<const float*> ptrs(f->m);
@@ -1134,6 +1320,8 @@ extern "C" int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, floa
     wbuf.release();
     tbuf.release();
   }
+  for (auto& d : f->dev)
+    for (auto& w : d.lw) w.valid = false;
   return HT_OK;
 }
 

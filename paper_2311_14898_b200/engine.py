@@ -205,7 +205,7 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
         warnings.warn("training mask is empty; loss is 0", stacklevel=2)
     loss = C.c_double(0.0)
     N.call("ht_loss", h_, dims[L], N.ptr(labels_i), N.ptr(mask_b.view(np.uint8)),
-           int(host.num_vertices), count, N.ptr(host.grad_h[L]), C.byref(loss))
+           int(host.num_vertices), count, N.ptr(host.grad_h[L]), None)  # value read after SGD
 
     # ---- backward (Alg. 1 lines 12-20) ----
     for l in reversed(range(L)):
@@ -227,6 +227,7 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     wp = (C.c_void_p * L)(*[N.ptr(w) for w in W])
     gp = (C.c_void_p * L)(*[N.ptr(g) for g in grads])
     N.call("ht_sgd", h_, L, dims_c, wp, C.c_float(model.lr), gp)
+    N.call("ht_loss_value", h_, C.byref(loss))
     return EpochResult(loss=float(loss.value), model=model, tracker=tracker, grads=grads)
 
 
