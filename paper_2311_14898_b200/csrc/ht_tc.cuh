@@ -164,6 +164,24 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -189,7 +207,8 @@ struct GemmCfg {
   static constexpr int STAGE = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024 / STAGE) < 4 ? (200 * 1024 / STAGE) : 4;
   static constexpr int TX = A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;  // TMA bytes per stage
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256;
+  static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // per-warp 32x32 transpose tiles
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256 + EPI_BYTES;
 };
 
 template <int BN, bool SPLIT, int EPI>
@@ -298,31 +317,39 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(&conv[s]);
       }
   } else {  // ---------------- epilogue (warps 4-7) ----------------
+    // TMEM gives a thread one row; a padded 32x32 smem transpose turns that
+    // into row-contiguous 128-byte stores (and G loads) per warp instruction
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+    float* tile = reinterpret_cast<float*>(smem + (size_t)ST * Cfg::STAGE + 256) + q4 * 32 * 33;
     int acc = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
       const int a = acc & 1;
       mbar_wait(&tfull[a], (acc >> 1) & 1);
       tc_fence_after();
-      const int64_t m = t * 128 + q4 * 32 + lane;
+      const int64_t r0 = t * 128 + q4 * 32;
       const uint32_t base = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(a * BN);
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(base + (uint32_t)c0, v);
-        if (m < M && c0 < N) {
-          float* crow = C + m * ldc + c0;
-          const float* grow = EPI == TC_MASK ? G + m * ldg + c0 : nullptr;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(base + (uint32_t)c0, v);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (c0 + j < N) {
-              float x = v[j];
+        for (int q = 0; q < 32; ++q) tile[lane * 33 + q] = v[q];
+        __syncwarp();
+        const int col = c0 + lane;
+        if (c0 < N) {
+#pragma unroll 4
+          for (int r = 0; r < 32; ++r) {
+            const int64_t m = r0 + r;
+            if (m >= M) break;
+            float x = tile[r * 33 + lane];
+            if (col < N) {
               if (EPI == TC_RELU) x = x > 0.f ? x : 0.f;
-              if (EPI == TC_MASK) x = x > 0.f ? grow[j] : 0.f;
-              crow[j] = x;
+              if (EPI == TC_MASK) x = x > 0.f ? __ldg(G + m * ldg + col) : 0.f;
+              C[m * ldc + col] = x;
             }
           }
         }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[a]);
