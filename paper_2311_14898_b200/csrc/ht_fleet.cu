@@ -66,7 +66,41 @@ int upload(DBuf& b, const std::vector<T>& v, cudaStream_t s) {
 struct CopyList {
   int64_t n = 0;
   DBuf src, dst, flag;  // int64 src rows, int64 dst rows, uint8 flags
+  // maximal runs of consecutive (host row, device row) pairs, sorted by
+  // host row; when there are few of them the copy engines move the list
+  // (no SMs, full PCIe duplex) instead of the zero-copy kernel
+  std::vector<int64_t> run_host, run_dev, run_len;
+  bool dma = false;
 };
+
+constexpr int64_t kMaxDmaRuns = 512;
+constexpr int kChunks = 8;  // host-row chunks for store -> load streaming
+
+// runs of a list whose host-side rows are `host` and device-side rows `dev`
+void make_runs(CopyList& cl, const std::vector<int64_t>& host, const std::vector<int64_t>& dev,
+               const std::vector<uint8_t>* flag) {
+  cl.run_host.clear();
+  cl.run_dev.clear();
+  cl.run_len.clear();
+  bool sorted = true;
+  for (size_t q = 0; q < host.size(); ++q) {
+    if (q > 0 && host[q] < host[q - 1]) sorted = false;
+    if (q > 0 && host[q] == host[q - 1] + 1 && dev[q] == dev[q - 1] + 1 &&
+        (!flag || (*flag)[q] == (*flag)[q - 1])) {
+      cl.run_len.back()++;
+    } else {
+      cl.run_host.push_back(host[q]);
+      cl.run_dev.push_back(dev[q]);
+      cl.run_len.push_back(1);
+    }
+    if ((int64_t)cl.run_len.size() > kMaxDmaRuns) break;
+  }
+  bool first_only = true;
+  if (flag)
+    for (uint8_t v : *flag) first_only &= v != 0;
+  cl.dma = sorted && (int64_t)cl.run_len.size() <= kMaxDmaRuns && first_only;
+  if (!cl.dma) cl.run_host.clear(), cl.run_dev.clear(), cl.run_len.clear();
+}
 
 // Host-side plan sets of one chunk (i, j)
 struct HostSets {
@@ -84,6 +118,7 @@ struct DevChunk {
   int64_t nv = 0, nn = 0, ne = 0, nlive = 0;
   DBuf nbr_slot;   // int64 [nn]
   DBuf dest_rows;  // int64 [nv]
+  CopyList dest;   // runs of (host row = dest_rows[r], staging row r)
   CopyList h2d;    // host row -> slot
   std::vector<CopyList> d2d;   // [step 1..m-1] peer slot -> own slot
   std::vector<CopyList> push;  // [source device i] pos in N_ij(i) -> own slot (owner = this device)
@@ -133,6 +168,7 @@ struct Device {
   cudaEvent_t e_in = nullptr, e_fetch = nullptr, e_agg = nullptr, e_comp = nullptr;
   cudaEvent_t e_out[2] = {nullptr, nullptr}, e_hst = nullptr, e_loss = nullptr;
   cudaEvent_t e_bin = nullptr, e_bcomp[2] = {nullptr, nullptr}, e_flush = nullptr;
+  cudaEvent_t e_hchunk[kChunks] = {}, e_fchunk[kChunks] = {};  // stores / flushes per host-row chunk
   std::vector<cudaEvent_t> e_aggst;  // per layer: checkpoint rows stored
   int64_t fwd_count = 0, bwd_count = 0;
   std::vector<LayerW> lw;            // per-layer weights (valid until the SGD step)
@@ -159,6 +195,7 @@ struct ht_fleet {
   int L = 0;
   std::vector<int> dims;
   int64_t loss_count = 0;
+  int64_t nrows = 0;  // host rows addressed by the plan (max vertex id + 1)
 };
 
 namespace {
@@ -189,6 +226,17 @@ int sync_all(ht_fleet* f) {
     if (d.tin) CU(cudaStreamSynchronize(d.tin));
     if (d.tout) CU(cudaStreamSynchronize(d.tout));
   }
+  return HT_OK;
+}
+
+int ev_rec(cudaEvent_t& e, cudaStream_t s) {
+  if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CU(cudaEventRecord(e, s));
+  return HT_OK;
+}
+
+int ev_wait(cudaStream_t s, cudaEvent_t e) {
+  if (e) CU(cudaStreamWaitEvent(s, e, 0));
   return HT_OK;
 }
 
@@ -240,6 +288,32 @@ int launch_copy(cudaStream_t s, void* dst, const void* src, const int64_t* didx,
   CU(cudaGetLastError());
   return HT_OK;
 }
+
+// Copy-engine transfer of the rows of a DMA-eligible list whose host row
+// lies in [lo, hi): to_host moves device rows -> host rows, else host ->
+// device.  Row strides may differ from the row size (2-D copies).
+int xfer(cudaStream_t s, const CopyList& cl, bool to_host, void* host_v, int64_t hld, void* dev_v,
+         int64_t dld, int64_t rb, int64_t lo, int64_t hi) {
+  char* host = static_cast<char*>(host_v);
+  char* dev = static_cast<char*>(dev_v);
+  for (size_t r = 0; r < cl.run_len.size(); ++r) {
+    const int64_t a = cl.run_host[r], len = cl.run_len[r];
+    const int64_t a0 = std::max(a, lo), a1 = std::min(a + len, hi);
+    if (a0 >= a1) continue;
+    char* hp = host + a0 * hld;
+    char* dp = dev + (cl.run_dev[r] + (a0 - a)) * dld;
+    const int64_t rows = a1 - a0;
+    if (hld == rb && dld == rb) {
+      CU(cudaMemcpyAsync(to_host ? hp : dp, to_host ? dp : hp, rows * rb, cudaMemcpyDefault, s));
+    } else {
+      CU(cudaMemcpy2DAsync(to_host ? hp : dp, to_host ? hld : dld, to_host ? dp : hp,
+                           to_host ? dld : hld, rb, rows, cudaMemcpyDefault, s));
+    }
+  }
+  return HT_OK;
+}
+
+inline int64_t chunk_bound(int64_t V, int g) { return V * g / kChunks; }
 
 int launch_acc(cudaStream_t s, int elem, void* dst, void* src, const int64_t* didx,
                const int64_t* sidx, const uint8_t* first, int64_t rows, int d, int zero_src,
@@ -550,6 +624,10 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (cudaEvent_t e : {d.e_in, d.e_fetch, d.e_agg, d.e_comp, d.e_out[0], d.e_out[1], d.e_hst,
                           d.e_loss, d.e_bin, d.e_bcomp[0], d.e_bcomp[1], d.e_flush})
       if (e) cudaEventDestroy(e);
+    for (int g = 0; g < kChunks; ++g) {
+      if (d.e_hchunk[g]) cudaEventDestroy(d.e_hchunk[g]);
+      if (d.e_fchunk[g]) cudaEventDestroy(d.e_fchunk[g]);
+    }
     for (cudaEvent_t e : d.e_aggst)
       if (e) cudaEventDestroy(e);
     for (int s = 0; s < 2; ++s)
@@ -622,6 +700,12 @@ extern "C" int ht_fleet_set_chunk(ht_fleet* f, int i, int j, int64_t nv, int64_t
 extern "C" int ht_fleet_finalize(ht_fleet* f) {
   const int m = f->m, n = f->n;
   const bool base = f->mode == HT_MODE_BASELINE;
+  f->nrows = 0;
+  for (auto& row : f->sets)
+    for (auto& h : row) {
+      if (!h.nbr.empty()) f->nrows = std::max(f->nrows, h.nbr.back() + 1);
+      if (!h.dest.empty()) f->nrows = std::max(f->nrows, h.dest.back() + 1);
+    }
   for (int i = 0; i < m; ++i) {
     Device& d = f->dev[i];
     HT_TRY(set_dev(d));
@@ -644,11 +728,13 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         nbr_slot.resize(h.nbr.size());
         std::iota(nbr_slot.begin(), nbr_slot.end(), 0);
         HT_TRY(upload_list(c.h2d, h.nbr, nbr_slot, s));
+        make_runs(c.h2d, h.nbr, nbr_slot, nullptr);
       } else {
         HT_TRY(lookup_slots(h, h.nbr, nbr_slot, i, j));
         const auto& rows = f->mode == HT_MODE_FULL ? h.load : h.owned;
         HT_TRY(lookup_slots(h, rows, b, i, j));
         HT_TRY(upload_list(c.h2d, rows, b, s));
+        make_runs(c.h2d, rows, b, nullptr);
         c.d2d.assign(m, CopyList());
         for (int st = 1; st < m; ++st) {
           const int k = (i + st) % m;
@@ -661,7 +747,12 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         }
       }
       HT_TRY(upload(c.nbr_slot, nbr_slot, s));
-      if (h.has_dest) HT_TRY(upload(c.dest_rows, h.dest, s));
+      if (h.has_dest) {
+        HT_TRY(upload(c.dest_rows, h.dest, s));
+        std::vector<int64_t> pos(h.dest.size());
+        std::iota(pos.begin(), pos.end(), 0);
+        make_runs(c.dest, h.dest, pos, nullptr);
+      }
       if (h.has_chunk) {
         if (h.nn != c.nn || (h.has_dest && h.nv != c.nv))
           return fail(HT_EINVAL, "chunk (%d,%d) structure does not match its plan sets", i, j);
@@ -737,6 +828,7 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
           flushed[v] = 1;
         }
         HT_TRY(upload_list(c.flush, slot, fl, s, &first));
+        make_runs(c.flush, fl, slot, &first);
       }
     }
   }
@@ -823,7 +915,13 @@ int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero) {
                         cl.src.as<int64_t>(), nullptr, cl.n, dim, 0));
       CU(cudaEventRecord(d.ev, d.stream));
     }
-    return barrier(f);
+    HT_TRY(barrier(f));
+    if (j == f->n - 1)
+      for (auto& d : f->dev) {
+        HT_TRY(set_dev(d));
+        for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_fchunk[g], d.stream));
+      }
+    return HT_OK;
   }
   HT_TRY(barrier(f));
   for (int k = 0; k < f->m; ++k) {
@@ -836,9 +934,27 @@ int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero) {
                         cl.src.as<int64_t>(), nullptr, cl.n, dim, 0));
     }
     const CopyList& fl = c.flush;
-    HT_TRY(launch_acc(d.stream, f->elem, host_grad_dev, d.grad.p, fl.dst.as<int64_t>(),
-                      fl.src.as<int64_t>(), assume_zero ? fl.flag.as<uint8_t>() : nullptr, fl.n,
-                      dim, 1));
+    const int64_t rb = (int64_t)dim * f->elem;
+    const bool lastb = j == f->n - 1;
+    if (assume_zero && fl.dma) {
+      // every row is a first flush (a store): copy engines, chunked so the
+      // next layer can start loading finished chunks
+      for (int g = 0; g < kChunks; ++g) {
+        HT_TRY(xfer(d.stream, fl, true, host_grad_dev, rb, d.grad.p, rb, rb,
+                    chunk_bound(f->nrows, g), chunk_bound(f->nrows, g + 1)));
+        if (lastb) HT_TRY(ev_rec(d.e_fchunk[g], d.stream));
+      }
+      if (!lastb)  // flushed slots restart from zero (devices.py:339)
+        for (size_t r = 0; r < fl.run_len.size(); ++r)
+          CU(cudaMemsetAsync(static_cast<char*>(d.grad.p) + fl.run_dev[r] * rb, 0,
+                             fl.run_len[r] * rb, d.stream));
+    } else {
+      HT_TRY(launch_acc(d.stream, f->elem, host_grad_dev, d.grad.p, fl.dst.as<int64_t>(),
+                        fl.src.as<int64_t>(), assume_zero ? fl.flag.as<uint8_t>() : nullptr, fl.n,
+                        dim, 1));
+      if (lastb)
+        for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_fchunk[g], d.stream));
+    }
   }
   return barrier(f);
 }
@@ -926,17 +1042,6 @@ extern "C" int ht_dest_rows(ht_fleet* f, int op, int batch, int dim, int elem_si
 // by an epoch-wide batch counter.
 // ===========================================================================
 namespace {
-
-int ev_rec(cudaEvent_t& e, cudaStream_t s) {
-  if (!e) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CU(cudaEventRecord(e, s));
-  return HT_OK;
-}
-
-int ev_wait(cudaStream_t s, cudaEvent_t e) {
-  if (e) CU(cudaStreamWaitEvent(s, e, 0));
-  return HT_OK;
-}
 
 // weights of layer l into the per-layer device buffers (async, from a
 // pinned host scratch): W, W^T and W padded, plus the TF32 hi/lo halves
@@ -1064,12 +1169,25 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
         HT_TRY(ev_wait(d.tin, d.e_agg));
         for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_fetch));
       }
-      if (j == 0 && layer > 0)  // h^l rows stored (baseline loads rows of every owner)
-        for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_hst));
+      // h^l rows come from the previous layer's stores (every owner's in
+      // baseline mode); with copy-engine lists each host-row chunk is
+      // loaded as soon as it has been stored (D2H and H2D overlap)
+      const bool after = j == 0 && layer > 0;
       TimerRec tr;
       timer_begin(f, d, tr, d.tin);
-      HT_TRY(launch_copy(d.tin, d.value.p, hin, c.h2d.dst.as<int64_t>(), c.h2d.src.as<int64_t>(),
-                         c.h2d.n, rbi, rbi, rbi, 0, kHostGrid));
+      if (c.h2d.dma) {
+        for (int g = 0; g < kChunks; ++g) {
+          if (after)
+            for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_hchunk[g]));
+          HT_TRY(xfer(d.tin, c.h2d, false, hin, rbi, d.value.p, rbi, rbi,
+                      chunk_bound(f->nrows, g), chunk_bound(f->nrows, g + 1)));
+        }
+      } else {
+        if (after)
+          for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_hchunk[kChunks - 1]));
+        HT_TRY(launch_copy(d.tin, d.value.p, hin, c.h2d.dst.as<int64_t>(), c.h2d.src.as<int64_t>(),
+                           c.h2d.n, rbi, rbi, rbi, 0, kHostGrid));
+      }
       timer_end(f, d, tr, 3, (double)c.h2d.n * rbi, d.tin);
       HT_TRY(ev_rec(d.e_in, d.tin));
     }
@@ -1121,9 +1239,20 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       // K5: destination rows, then checkpoint rows, to the host store
       HT_TRY(ev_wait(d.tout, d.e_comp));
       const int64_t* rows = c.dest_rows.as<int64_t>();
-      HT_TRY(launch_copy(d.tout, hout, hdst, rows, nullptr, c.nv, rbo, rbo, rbo, 0, kHostGrid));
-      if (j == f->n - 1) HT_TRY(ev_rec(d.e_hst, d.tout));
-      HT_TRY(launch_copy(d.tout, aout, agg, rows, nullptr, c.nv, rbi, rbi, rbi, 0, kHostGrid));
+      const bool lastb = j == f->n - 1;
+      if (c.dest.dma) {
+        for (int g = 0; g < kChunks; ++g) {
+          HT_TRY(xfer(d.tout, c.dest, true, hout, rbo, hdst, rbo, rbo, chunk_bound(f->nrows, g),
+                      chunk_bound(f->nrows, g + 1)));
+          if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
+        }
+        HT_TRY(xfer(d.tout, c.dest, true, aout, rbi, agg, rbi, rbi, 0, f->nrows));
+      } else {
+        HT_TRY(launch_copy(d.tout, hout, hdst, rows, nullptr, c.nv, rbo, rbo, rbo, 0, kHostGrid));
+        if (lastb)
+          for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
+        HT_TRY(launch_copy(d.tout, aout, agg, rows, nullptr, c.nv, rbi, rbi, rbi, 0, kHostGrid));
+      }
       HT_TRY(ev_rec(d.e_out[s], d.tout));
       if (j == f->n - 1) HT_TRY(ev_rec(d.e_aggst[layer], d.tout));
       d.fwd_count++;
@@ -1219,17 +1348,35 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // destination gradients (ready once the layer above has flushed)
       if (d.bwd_count >= 2) HT_TRY(ev_wait(d.tin, d.e_bcomp[s]));
       HT_TRY(ev_wait(d.tin, d.e_aggst[layer]));
-      HT_TRY(launch_copy(d.tin, A, ain, nullptr, rows, c.nv, rbi, rbi, rbi, 0, kHostGrid));
-      if (j == 0) {
-        if (layer == f->L - 1) {
-          HT_TRY(ev_wait(d.tin, d.e_loss));
-        } else if (f->mode == HT_MODE_BASELINE) {
-          for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_flush));
-        } else {
-          HT_TRY(ev_wait(d.tin, d.e_flush));
+      if (c.dest.dma)
+        HT_TRY(xfer(d.tin, c.dest, false, ain, rbi, A, rbi, rbi, 0, f->nrows));
+      else
+        HT_TRY(launch_copy(d.tin, A, ain, nullptr, rows, c.nv, rbi, rbi, rbi, 0, kHostGrid));
+      // gradient rows of the layer above: written by the loss, or by the
+      // flushes of the previous backward layer (of every device in baseline
+      // mode); streamed per host-row chunk when both sides use copy engines
+      const bool top = layer == f->L - 1;
+      if (j == 0 && top) HT_TRY(ev_wait(d.tin, d.e_loss));
+      if (c.dest.dma) {
+        for (int g = 0; g < kChunks; ++g) {
+          if (j == 0 && !top) {
+            if (f->mode == HT_MODE_BASELINE)
+              for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_fchunk[g]));
+            else
+              HT_TRY(ev_wait(d.tin, d.e_fchunk[g]));
+          }
+          HT_TRY(xfer(d.tin, c.dest, false, gout, rbo, G, rbo, rbo, chunk_bound(f->nrows, g),
+                      chunk_bound(f->nrows, g + 1)));
         }
+      } else {
+        if (j == 0 && !top) {
+          if (f->mode == HT_MODE_BASELINE)
+            for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_fchunk[kChunks - 1]));
+          else
+            HT_TRY(ev_wait(d.tin, d.e_fchunk[kChunks - 1]));
+        }
+        HT_TRY(launch_copy(d.tin, G, gout, nullptr, rows, c.nv, rbo, rbo, rbo, 0, kHostGrid));
       }
-      HT_TRY(launch_copy(d.tin, G, gout, nullptr, rows, c.nv, rbo, rbo, rbo, 0, kHostGrid));
       HT_TRY(ev_rec(d.e_bin, d.tin));
       // K7 on the compute stream
       HT_TRY(ev_wait(d.stream, d.e_bin));
