@@ -123,6 +123,37 @@ def build_inputs(cfg, m):
     return ds, p, plan, chosen
 
 
+def pcie_peaks():
+    """Measured PCIe peaks of this box (GB/s): [h2d, d2h, bidir, zc_read, zc_write]."""
+    from paper_2311_14898_b200 import _native as N
+    out = np.zeros(5)
+    try:
+        N.call("ht_pcie_probe", 0, 1 << 30, N.ptr(out))
+    except Exception as exc:  # noqa: BLE001 - report, do not fail the bench
+        log(f"[bench] pcie probe failed: {exc}")
+        return None
+    return [float(x) for x in out]
+
+
+def dedup_report():
+    """Host<->GPU bytes per epoch of the deduplicated ('full') plan vs the
+    non-deduplicated ('baseline') plan on BASELINE config 1 (m=4, n=4,
+    reorganized) - the configuration where chunks share neighbours.  At the
+    bench workload's m=1, n=1 the two plans coincide."""
+    import paper_2311_14898_b200 as H
+    c = CONFIGS["cfg1"]
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=c["V"], avg_degree=c["avg_degree"], seed=0),
+                         c["dims"][0], c["dims"][-1])
+    p = H.reorganize(H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 4, seed=0), 4)).partition
+    plan = H.plan_for_partition(p)
+    f = sum(host_bytes_per_epoch(plan, c["dims"], "full"))
+    b = sum(host_bytes_per_epoch(plan, c["dims"], "baseline"))
+    v = plan.volumes
+    return {"config": "cfg1 m=4 n=4 reorganized", "host_gb_full": f / 1e9,
+            "host_gb_baseline": b / 1e9, "reduction": 1.0 - f / b,
+            "volumes": {"v_ori": v.v_ori, "v_p2p": v.v_p2p, "v_ru": v.v_ru}}
+
+
 def host_bytes_per_epoch(plan, dims, mode="full"):
     """Host<->GPU bytes of one epoch from the plan (SURVEY 8(d) formulas,
     fp32): neighbour loads/flushes + destination + checkpoint rows, plus the
@@ -289,6 +320,9 @@ def main():
     ms_e = e2e["ms_total"] / args.steps
     h2d, d2h = host_bytes_per_epoch(plan, dims)
     base_h2d, base_d2h = host_bytes_per_epoch(plan, dims, "baseline")
+    dedup = dedup_report()
+    pcie = pcie_peaks()
+    pcie_bidir = pcie[2] if pcie else None
 
     # dominant kernel of the value run: the aggregation kernels (fwd CSC + bwd CSR)
     lf, msf, bf = val["stats"][0]
@@ -329,6 +363,14 @@ def main():
         "gemm": {"ms_per_step": msg / args.steps, "tflops": flops / (msg / 1e3) / 1e12 if msg else None,
                  "precision": args.precision},
         "cpu_baseline": cpu,
+        "roofline_pcie": {
+            "bound": "pcie", "what": "all host<->GPU bytes of the e2e epoch / epoch time",
+            "achieved": (h2d + d2h) / (ms_e / 1e3) / 1e9, "unit": "GB/s",
+            "peak": pcie_bidir, "peak_source": "measured (copy engines, both directions at once)",
+            "frac": ((h2d + d2h) / (ms_e / 1e3) / 1e9) / pcie_bidir if pcie_bidir else None,
+            "peaks_gbs": {"h2d": pcie[0], "d2h": pcie[1], "bidir": pcie[2],
+                          "zero_copy_read": pcie[3], "zero_copy_write": pcie[4]} if pcie else None},
+        "dedup": dedup,
         "clocks": clk_e.summary(),
         "clocks_value_run": clk_v.summary(),
         "losses": {"value": val["losses"][-1], "e2e": e2e["losses"][-1]},

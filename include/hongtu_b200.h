@@ -118,6 +118,18 @@ int ht_fleet_create(int m, int n, const int* ordinals, int mode, int flush_polic
                     ht_fleet** out);
 int ht_fleet_destroy(ht_fleet* f);
 
+/* Rank mode (one process per GPU, torchrun): this process drives virtual
+ * device `rank` on CUDA device `ordinal`; peers' slot buffers, gradient
+ * views, weight-gradient accumulators and barrier counters are reached
+ * through CUDA IPC, and the Alg. 2/3 barriers become device-side counter
+ * waits (no host round trip).  Modes p2p/full only.  After the first
+ * ht_epoch_begin, exchange HT_IPC_BYTES of handles with every peer. */
+#define HT_IPC_BYTES 256
+int ht_fleet_create_rank(int m, int n, int rank, int ordinal, int mode, int flush_policy,
+                         ht_fleet** out);
+int ht_fleet_ipc_export(ht_fleet* f, void* handles);
+int ht_fleet_ipc_import(ht_fleet* f, int peer, const void* handles);
+
 /* Plan sets of chunk (i, j) (planner.py:105-124).  live/slots aligned. */
 int ht_fleet_set_sets(ht_fleet* f, int i, int j,
                       const int64_t* nbr, int64_t n_nbr,

@@ -53,6 +53,9 @@ _SIGS = {
     "ht_reorganize": (i32, [i64, i64, vp, vp, i32, vp, vp]),
     "ht_fleet_create": (i32, [i32, i32, vp, i32, i32, C.POINTER(vp)]),
     "ht_fleet_destroy": (i32, [vp]),
+    "ht_fleet_create_rank": (i32, [i32, i32, i32, i32, i32, i32, C.POINTER(vp)]),
+    "ht_fleet_ipc_export": (i32, [vp, vp]),
+    "ht_fleet_ipc_import": (i32, [vp, i32, vp]),
     "ht_fleet_set_sets": (i32, [vp, i32, i32, vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, i64,
                                 vp, i64]),
     "ht_fleet_set_fetch": (i32, [vp, i32, i32, i32, vp, i64]),

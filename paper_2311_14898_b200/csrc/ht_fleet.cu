@@ -37,8 +37,10 @@ struct DBuf {
   void* p = nullptr;
   int64_t bytes = 0;
   int dev = 0;
+  bool owned = true;  // false: a peer process's buffer mapped through CUDA IPC
   int ensure(int64_t want) {
     if (want <= bytes) return HT_OK;
+    if (!owned) return fail(HT_ESTATE, "cannot grow a buffer shared with peer processes");
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -48,9 +50,13 @@ struct DBuf {
     return HT_OK;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (owned) cudaFree(p);
+      else cudaIpcCloseMemHandle(p);
+    }
     p = nullptr;
     bytes = 0;
+    owned = true;
   }
   template <class T>
   T* as() const { return static_cast<T*>(p); }
@@ -156,7 +162,10 @@ struct Device {
   DBuf gemm_ws;
   DBuf W, Wt, Wp;                      // current layer weights, transpose, padded
   DBuf Wt_hi, Wt_lo, Wp_hi, Wp_lo;     // TF32 hi/lo halves for tcgen05
-  std::vector<DBuf> gW;                // per-layer weight-gradient accumulators
+  DBuf gWall;                          // weight-gradient accumulators, all layers
+  std::vector<int64_t> gW_off;         // float offset of layer l inside gWall
+  DBuf flags;                          // cross-process barrier counter (rank mode)
+  bool local = true;                   // false: a peer rank's device (IPC views only)
   DBuf hL;                             // last-layer outputs (concat over batches)
   std::vector<int64_t> hL_off;         // row offset of batch j inside hL
   DBuf labels, mask, loss_part;
@@ -196,6 +205,12 @@ struct ht_fleet {
   std::vector<int> dims;
   int64_t loss_count = 0;
   int64_t nrows = 0;  // host rows addressed by the plan (max vertex id + 1)
+  // rank mode (one process per GPU): index of the local device, barrier
+  // sequence, device array of every rank's barrier counter
+  int rank = -1;
+  int64_t seq = 0;
+  DBuf flag_ptrs;
+  int imported = 0;
 };
 
 namespace {
@@ -206,7 +221,29 @@ int set_dev(const Device& d) {
 }
 
 // all-to-all event barrier across the per-device streams
+// Cross-process barrier of rank mode, on the local compute stream: publish
+// the next sequence number in the local counter, wait (device-side) until
+// every rank's counter reached it.  Every rank issues the same barriers.
+int xbarrier(ht_fleet* f) {
+  Device& d = f->dev[f->rank];
+  HT_TRY(set_dev(d));
+  if (f->imported != f->m - 1) return fail(HT_ESTATE, "rank mode: peer buffers not imported");
+  if (!f->flag_ptrs.p) {
+    std::vector<uint32_t*> ptrs(f->m);
+    for (int k = 0; k < f->m; ++k) ptrs[k] = f->dev[k].flags.as<uint32_t>();
+    HT_TRY(f->flag_ptrs.ensure(f->m * sizeof(uint32_t*)));
+    CU(cudaMemcpy(f->flag_ptrs.p, ptrs.data(), f->m * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  }
+  f->seq++;
+  count_launch();
+  ht::k_xbarrier<<<1, 32, 0, d.stream>>>(d.flags.as<uint32_t>(), f->flag_ptrs.as<uint32_t*>(), f->m,
+                                         (uint32_t)f->seq);
+  CU(cudaGetLastError());
+  return HT_OK;
+}
+
 int barrier(ht_fleet* f) {
+  if (f->rank >= 0) return xbarrier(f);
   for (auto& d : f->dev) {
     HT_TRY(set_dev(d));
     CU(cudaEventRecord(d.ev, d.stream));
@@ -221,6 +258,7 @@ int barrier(ht_fleet* f) {
 
 int sync_all(ht_fleet* f) {
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     CU(cudaStreamSynchronize(d.stream));
     if (d.tin) CU(cudaStreamSynchronize(d.tin));
@@ -597,6 +635,75 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
   return HT_OK;
 }
 
+// Rank mode: this process drives virtual device `rank` on CUDA device
+// `ordinal`; the other m-1 devices belong to peer processes and are reached
+// through CUDA IPC (ht_fleet_ipc_export / _import).  p2p/full modes only:
+// in those every host row a device touches is owned by it, so each process
+// needs only its own host store rows.
+extern "C" int ht_fleet_create_rank(int m, int n, int rank, int ordinal, int mode,
+                                    int flush_policy, ht_fleet** out) {
+  if (m < 1 || n < 1 || rank < 0 || rank >= m) return fail(HT_EINVAL, "bad rank fleet shape");
+  if (mode == HT_MODE_BASELINE)
+    return fail(HT_EINVAL, "rank mode needs mode p2p or full (baseline touches peers' host rows)");
+  std::vector<int> ords(m, ordinal);
+  HT_TRY(ht_fleet_create(1, n, &ordinal, mode, flush_policy, out));
+  ht_fleet* f = *out;
+  // re-shape: m devices, only `rank` local (it takes the device created above)
+  Device local = std::move(f->dev[0]);
+  f->dev.clear();
+  f->dev.resize(m);
+  for (int k = 0; k < m; ++k) {
+    f->dev[k].ordinal = ordinal;
+    f->dev[k].local = false;
+    f->dev[k].chunks.resize(n);
+  }
+  f->dev[rank] = std::move(local);
+  f->dev[rank].local = true;
+  f->m = m;
+  f->rank = rank;
+  f->sets.assign(m, std::vector<HostSets>(n));
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < n; ++j) f->sets[i][j].fetch.resize(m);
+  return HT_OK;
+}
+
+// IPC handles of the local buffers peers read: slot values, neighbour
+// gradient views, weight-gradient accumulators, barrier counter.  Call after
+// ht_epoch_begin (which sizes them once for the run).
+extern "C" int ht_fleet_ipc_export(ht_fleet* f, void* out) {
+  if (f->rank < 0) return fail(HT_ESTATE, "not a rank-mode fleet");
+  Device& d = f->dev[f->rank];
+  HT_TRY(set_dev(d));
+  cudaIpcMemHandle_t* h = static_cast<cudaIpcMemHandle_t*>(out);
+  DBuf* bufs[4] = {&d.value, &d.se, &d.gWall, &d.flags};
+  for (int q = 0; q < 4; ++q) {
+    if (!bufs[q]->p) return fail(HT_ESTATE, "export before ht_epoch_begin");
+    CU(cudaIpcGetMemHandle(&h[q], bufs[q]->p));
+  }
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_ipc_import(ht_fleet* f, int peer, const void* in) {
+  if (f->rank < 0 || peer < 0 || peer >= f->m || peer == f->rank)
+    return fail(HT_EINVAL, "bad peer %d", peer);
+  Device& me = f->dev[f->rank];
+  HT_TRY(set_dev(me));
+  Device& d = f->dev[peer];
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(in);
+  DBuf* bufs[4] = {&d.value, &d.se, &d.gWall, &d.flags};
+  for (int q = 0; q < 4; ++q) {
+    if (bufs[q]->p) continue;  // already imported
+    void* p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, h[q], cudaIpcMemLazyEnablePeerAccess));
+    bufs[q]->p = p;
+    bufs[q]->owned = false;
+  }
+  d.gW_off = me.gW_off;
+  f->imported++;
+  f->flag_ptrs.release();
+  return HT_OK;
+}
+
 extern "C" int ht_fleet_destroy(ht_fleet* f) {
   if (!f) return HT_OK;
   sync_all(f);
@@ -605,9 +712,8 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     cudaSetDevice(d.ordinal);
     for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
                     &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo, &d.hL,
-                    &d.labels, &d.mask, &d.loss_part})
+                    &d.labels, &d.mask, &d.loss_part, &d.gWall, &d.flags})
       b->release();
-    for (auto& g : d.gW) g.release();
     for (auto& c : d.chunks) {
       for (auto* b : {&c.nbr_slot, &c.dest_rows, &c.csc_off, &c.csc_slot, &c.csc_w, &c.csr_off,
                       &c.csr_dst, &c.csr_w, &c.fw_lo, &c.fw_hi, &c.fw_seg, &c.fw_first, &c.fw_cnt,
@@ -708,6 +814,7 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
     }
   for (int i = 0; i < m; ++i) {
     Device& d = f->dev[i];
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     cudaStream_t s = d.stream;
     d.cap = 0;
@@ -797,6 +904,7 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
     for (int j = 0; j < n; ++j) {
       for (int k = 0; k < m; ++k) {
         Device& d = f->dev[k];
+        if (!d.local) continue;  // rank mode: a peer process drives it
         HT_TRY(set_dev(d));
         cudaStream_t s = d.stream;
         DevChunk& c = d.chunks[j];
@@ -855,6 +963,7 @@ extern "C" int ht_begin_layer(ht_fleet* f, int dim, int elem_size, int backward)
   f->dim = dim;
   f->elem = elem_size;
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     const int64_t bytes = d.cap * (int64_t)dim * elem_size;
     HT_TRY(d.value.ensure(bytes));
@@ -926,6 +1035,7 @@ int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero) {
   HT_TRY(barrier(f));
   for (int k = 0; k < f->m; ++k) {
     Device& d = f->dev[k];
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     DevChunk& c = d.chunks[j];
     for (int i = 0; i < f->m; ++i) {  // ascending source device
@@ -963,6 +1073,7 @@ int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero) {
 
 extern "C" int ht_comm_fwd(ht_fleet* f, int batch, const void* host_rows, void* views_out) {
   if (batch < 0 || batch >= f->n) return fail(HT_EINVAL, "batch out of range");
+  if (f->rank >= 0) return fail(HT_ESTATE, "per-batch fleet calls need a single-process fleet");
   void *hsrc, *vout;
   HT_TRY(dev_ptr(host_rows, &hsrc));
   HT_TRY(dev_ptr(views_out, &vout));
@@ -982,6 +1093,7 @@ extern "C" int ht_comm_fwd(ht_fleet* f, int batch, const void* host_rows, void* 
 
 extern "C" int ht_comm_bwd(ht_fleet* f, int batch, const void* views_in, void* host_grad) {
   if (batch < 0 || batch >= f->n) return fail(HT_EINVAL, "batch out of range");
+  if (f->rank >= 0) return fail(HT_ESTATE, "per-batch fleet calls need a single-process fleet");
   void *vin, *hg;
   HT_TRY(dev_ptr(views_in, &vin));
   HT_TRY(dev_ptr(host_grad, &hg));
@@ -1004,6 +1116,7 @@ extern "C" int ht_comm_bwd(ht_fleet* f, int batch, const void* views_in, void* h
 extern "C" int ht_dest_rows(ht_fleet* f, int op, int batch, int dim, int elem_size, void* host_rows,
                             void* rows_concat) {
   if (batch < 0 || batch >= f->n) return fail(HT_EINVAL, "batch out of range");
+  if (f->rank >= 0) return fail(HT_ESTATE, "per-batch fleet calls need a single-process fleet");
   void *hp, *rp;
   HT_TRY(dev_ptr(host_rows, &hp));
   HT_TRY(dev_ptr(rows_concat, &rp));
@@ -1090,13 +1203,15 @@ extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
   int dmax = 0;
   for (int l = 0; l <= L; ++l) dmax = std::max(dmax, pad4(dims[l]));
   for (auto& d : f->dev) {
+    d.gW_off.assign(L + 1, 0);
+    for (int l = 0; l < L; ++l) d.gW_off[l + 1] = d.gW_off[l] + (int64_t)dims[l] * dims[l + 1];
+    if (!d.local) continue;  // a peer rank sizes and zeroes its own buffers
     HT_TRY(set_dev(d));
-    if ((int)d.gW.size() < L) d.gW.resize(L);
-    for (int l = 0; l < L; ++l) {
-      d.gW[l].dev = d.ordinal;
-      const int64_t bytes = (int64_t)dims[l] * dims[l + 1] * 4;
-      HT_TRY(d.gW[l].ensure(bytes));
-      CU(cudaMemsetAsync(d.gW[l].p, 0, bytes, d.stream));
+    HT_TRY(d.gWall.ensure(d.gW_off[L] * 4));
+    CU(cudaMemsetAsync(d.gWall.p, 0, d.gW_off[L] * 4, d.stream));
+    if (f->rank >= 0 && !d.flags.p) {  // barrier counter: zeroed once, monotonic afterwards
+      HT_TRY(d.flags.ensure(64));
+      CU(cudaMemset(d.flags.p, 0, 64));
     }
     // every buffer of the epoch is sized here, once: no allocation (and no
     // implicit device synchronization) inside the layer calls
@@ -1155,6 +1270,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
   const bool last = layer == f->L - 1;
   const int64_t rbi = (int64_t)d_in * 4, rbo = (int64_t)d_out * 4;
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
   }
@@ -1163,6 +1279,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
     // ---- step 1: host loads into slots (tin) ----
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
+      if (!d.local) continue;  // rank mode: a peer process drives it
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
       if (d.fwd_count > 0) {  // slots of the previous batch no longer read
@@ -1194,9 +1311,11 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
     // ---- barrier + step 2: staggered peer fetches (compute stream) ----
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
+      if (!d.local) continue;  // rank mode: a peer process drives it
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
       for (auto& o : f->dev) HT_TRY(ev_wait(d.stream, o.e_in));
+      if (f->rank >= 0 && f->m > 1) HT_TRY(xbarrier(f));  // every rank's hosted rows staged
       if (f->mode != HT_MODE_BASELINE)
         for (int st = 1; st < f->m; ++st) {
           const int k = (i + st) % f->m;
@@ -1204,11 +1323,13 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
           HT_TRY(launch_copy(d.stream, d.value.p, f->dev[k].value.p, cl.dst.as<int64_t>(),
                              cl.src.as<int64_t>(), cl.n, rbi, rbi, rbi));
         }
+      if (f->rank >= 0 && f->m > 1) HT_TRY(xbarrier(f));  // peers done reading our slots
       HT_TRY(ev_rec(d.e_fetch, d.stream));
     }
     // ---- aggregation, dense transform, stores (tout) ----
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
+      if (!d.local) continue;  // rank mode: a peer process drives it
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
       const int s = (int)(d.fwd_count & 1);
@@ -1270,6 +1391,7 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
   const int blocks = 148 * 4;
   for (int i = 0; i < f->m; ++i) {
     Device& d = f->dev[i];
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     // labels/mask through a pinned copy so the upload does not block the host
     if (d.lpin_cap < V * 9) {
@@ -1306,6 +1428,7 @@ extern "C" int ht_loss_value(ht_fleet* f, double* loss) {
   if (f->loss_count <= 0) return HT_OK;
   double tot = 0.0;
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     std::vector<double> parts(d.loss_part.bytes / 8);
     CU(cudaMemcpyAsync(parts.data(), d.loss_part.p, parts.size() * 8, cudaMemcpyDeviceToHost,
@@ -1331,6 +1454,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
   const int64_t rbi = (int64_t)d_in * 4, rbo = (int64_t)d_out * 4;
   const int ldz = precision == HT_PREC_TF32 ? pad4(d_out) : d_out;
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     if (!d.lw[layer].valid) HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
     if (f->mode != HT_MODE_BASELINE)  // begin_backward_layer: zeroed gradient slots
@@ -1339,6 +1463,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
   for (int j = 0; j < f->n; ++j) {
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
+      if (!d.local) continue;  // rank mode: a peer process drives it
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
       const int s = (int)(d.bwd_count & 1);
@@ -1398,7 +1523,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
                                d.gemm_ws.as<float>(), &used));
           count_launch(4);
           ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
-              d.gW[layer].as<float>(), d.gemm_ws.as<float>(), nw, used);
+              d.gWall.as<float>() + d.gW_off[layer], d.gemm_ws.as<float>(), nw, used);
           CU(cudaGetLastError());
         }
       } else {
@@ -1413,7 +1538,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
                                                    d_out, M, splits, kps)));
           count_launch();
           ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
-              d.gW[layer].as<float>(), d.gemm_ws.as<float>(), nw, splits);
+              d.gWall.as<float>() + d.gW_off[layer], d.gemm_ws.as<float>(), nw, splits);
           CU(cudaGetLastError());
         }
         HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, ldz, w.W.as<float>(), d_out, GA,
@@ -1435,6 +1560,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
     HT_TRY(push_flush(f, j, gin, true));
   }
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     HT_TRY(ev_rec(d.e_flush, d.stream));
   }
@@ -1443,13 +1569,16 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
 
 extern "C" int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, float lr,
                       float* const* grads_out) {
-  Device& d0 = f->dev[0];
+  // rank mode: every rank sums all ranks' accumulators (IPC views) in
+  // ascending device order and applies the identical update
+  Device& d0 = f->dev[f->rank >= 0 ? f->rank : 0];
+  if (f->rank >= 0 && f->m > 1) HT_TRY(xbarrier(f));  // every rank's dW complete
   HT_TRY(sync_all(f));
   HT_TRY(set_dev(d0));
   for (int l = 0; l < L; ++l) {
     const int64_t nw = (int64_t)dims[l] * dims[l + 1];
     std::vector<const float*> ptrs(f->m);
-    for (int i = 0; i < f->m; ++i) ptrs[i] = f->dev[i].gW[l].as<float>();
+    for (int i = 0; i < f->m; ++i) ptrs[i] = f->dev[i].gWall.as<float>() + f->dev[i].gW_off[l];
     DBuf pbuf, wbuf, tbuf;
     HT_TRY(upload(pbuf, ptrs, d0.stream));
     HT_TRY(wbuf.ensure(nw * 4));
@@ -1466,6 +1595,10 @@ extern "C" int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, floa
     pbuf.release();
     wbuf.release();
     tbuf.release();
+  }
+  if (f->rank >= 0 && f->m > 1) {  // nobody zeroes its dW while a peer still reads it
+    HT_TRY(xbarrier(f));
+    CU(cudaStreamSynchronize(d0.stream));
   }
   for (auto& d : f->dev)
     for (auto& w : d.lw) w.valid = false;
@@ -1494,6 +1627,7 @@ extern "C" int ht_kernel_stats(ht_fleet* f, int which, int64_t* launches, double
 extern "C" int ht_fleet_mark(ht_fleet* f, int which) {
   if (which < 0 || which > 1) return fail(HT_EINVAL, "mark index must be 0 or 1");
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     if (!d.mark[which]) CU(cudaEventCreate(&d.mark[which]));
     CU(cudaEventRecord(d.mark[which], d.stream));
@@ -1504,6 +1638,7 @@ extern "C" int ht_fleet_mark(ht_fleet* f, int which) {
 extern "C" int ht_fleet_elapsed(ht_fleet* f, double* ms) {
   double mx = 0.0;
   for (auto& d : f->dev) {
+    if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     if (!d.mark[0] || !d.mark[1]) return fail(HT_ESTATE, "marks not recorded");
     CU(cudaEventSynchronize(d.mark[1]));

@@ -90,21 +90,28 @@ __global__ void __launch_bounds__(256) k_acc_rows(T* __restrict__ dst, T* __rest
 // sequential in e, product rounded before the add (no FMA contraction)
 // ---------------------------------------------------------------------------
 
-template <int NV>
+// U edges' rows are requested before any is accumulated; the next 32
+// edge indices/weights are prefetched while the current ones are summed.
+template <int NV, int U = 8>
 __device__ __forceinline__ void seg_sum_v4(float4 (&acc)[NV], const float* __restrict__ X,
                                            int64_t ldx, int d4, const int32_t* __restrict__ idx,
                                            const float* __restrict__ w, int64_t e0, int64_t e1,
                                            int lane) {
-  for (int64_t base = e0; base < e1; base += kWarp) {
-    const int cnt = (int)((e1 - base) < (int64_t)kWarp ? (e1 - base) : (int64_t)kWarp);
-    const int my_i = lane < cnt ? idx[base + lane] : 0;
-    const float my_w = lane < cnt ? w[base + lane] : 0.f;
+  int64_t base = e0;
+  int cnt = (int)((e1 - base) < (int64_t)kWarp ? (e1 - base) : (int64_t)kWarp);
+  int my_i = lane < cnt ? __ldg(idx + base + lane) : 0;
+  float my_w = lane < cnt ? __ldg(w + base + lane) : 0.f;
+  while (cnt > 0) {
+    const int64_t nb = base + kWarp;
+    const int ncnt = nb < e1 ? (int)((e1 - nb) < (int64_t)kWarp ? (e1 - nb) : (int64_t)kWarp) : 0;
+    const int nx_i = lane < ncnt ? __ldg(idx + nb + lane) : 0;
+    const float nx_w = lane < ncnt ? __ldg(w + nb + lane) : 0.f;
     int k = 0;
-    for (; k + 4 <= cnt; k += 4) {
-      float4 x[4][NV];
-      float ww[4];
+    for (; k + U <= cnt; k += U) {
+      float4 x[U][NV];
+      float ww[U];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int s = __shfl_sync(0xffffffffu, my_i, k + u);
         ww[u] = __shfl_sync(0xffffffffu, my_w, k + u);
         const float4* row = reinterpret_cast<const float4*>(X + (int64_t)s * ldx);
@@ -115,7 +122,7 @@ __device__ __forceinline__ void seg_sum_v4(float4 (&acc)[NV], const float* __res
         }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int t = 0; t < NV; ++t) {
           acc[t].x = __fadd_rn(acc[t].x, __fmul_rn(ww[u], x[u][t].x));
@@ -140,6 +147,10 @@ __device__ __forceinline__ void seg_sum_v4(float4 (&acc)[NV], const float* __res
         }
       }
     }
+    base = nb;
+    cnt = ncnt;
+    my_i = nx_i;
+    my_w = nx_w;
   }
 }
 
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(256) k_seg_gather_v4(float* __restrict__ out,
     float4 acc[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    seg_sum_v4<NV>(acc, X, ldx, d4, idx, w, e0, e1, lane);
+    seg_sum_v4<NV, (NV <= 2 ? 8 : 4)>(acc, X, ldx, d4, idx, w, e0, e1, lane);
     float4* o = reinterpret_cast<float4*>(out + sg * (int64_t)d);
 #pragma unroll
     for (int t = 0; t < NV; ++t) {
@@ -233,7 +244,7 @@ __global__ void __launch_bounds__(256) k_seg_pieces_v4(float* __restrict__ parti
     float4 acc[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    seg_sum_v4<NV>(acc, X, ldx, d4, idx, w, lo[p], hi[p], lane);
+    seg_sum_v4<NV, (NV <= 2 ? 8 : 4)>(acc, X, ldx, d4, idx, w, lo[p], hi[p], lane);
     float4* o = reinterpret_cast<float4*>(partial + p * (int64_t)d);
 #pragma unroll
     for (int t = 0; t < NV; ++t) {
@@ -418,6 +429,32 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64
     for (int q = 0; q < 8; ++q) t += wsum[q];
     block_loss[blockIdx.x] = t;
   }
+}
+
+// Cross-process barrier (rank mode): make this rank's prior writes visible
+// system-wide, publish `seq`, then spin (acquire) until every rank's
+// counter reached it.  Traps after 60 s so a dead peer fails loudly
+// instead of hanging the GPU.
+__global__ void k_xbarrier(uint32_t* self, uint32_t* const* peers, int m, uint32_t seq) {
+  __threadfence_system();
+  __syncwarp();
+  if (threadIdx.x == 0)
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(self), "r"(seq) : "memory");
+  if ((int)threadIdx.x < m) {
+    const uint32_t* p = peers[threadIdx.x];
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      if ((int32_t)(v - seq) >= 0) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60000000000ull) __trap();
+      __nanosleep(256);
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
 }
 
 // K12: total = ((0 + g_0) + g_1) + ...; W = W - lr * total (separate roundings)

@@ -330,6 +330,16 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t base = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(a * BN);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        // the mask epilogue's incoming-gradient block is fetched before the
+        // accumulator so its 32 independent row loads overlap (one
+        // 128-byte coalesced load per row per warp)
+        float g[32];
+        if (EPI == TC_MASK) {
+          const int colg = c0 + lane;
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            g[r] = (r0 + r < M && colg < N) ? __ldg(G + (r0 + r) * ldg + colg) : 0.f;
+        }
         float v[32];
         tmem_ld32(base + (uint32_t)c0, v);
 #pragma unroll
@@ -337,14 +347,13 @@ __global__ void __launch_bounds__(256, 1)
         __syncwarp();
         const int col = c0 + lane;
         if (c0 < N) {
-#pragma unroll 4
+#pragma unroll
           for (int r = 0; r < 32; ++r) {
             const int64_t m = r0 + r;
-            if (m >= M) break;
             float x = tile[r * 33 + lane];
-            if (col < N) {
+            if (m < M && col < N) {
               if (EPI == TC_RELU) x = x > 0.f ? x : 0.f;
-              if (EPI == TC_MASK) x = x > 0.f ? __ldg(G + m * ldg + col) : 0.f;
+              if (EPI == TC_MASK) x = x > 0.f ? g[r] : 0.f;
               C[m * ldc + col] = x;
             }
           }
