@@ -214,7 +214,7 @@ class DeviceFleet:
     ordinal (default: round-robin over the visible GPUs)."""
 
     def __init__(self, plan: DedupPlan, mode: str = "full", flush_policy: str = "on_eviction",
-                 dtype=np.float64, devices=None, precision: str = "tf32"):
+                 dtype=np.float64, devices=None, precision: str = "tf32", rank: int | None = None):
         if mode not in _MODES:
             raise SimulationError(f"unknown mode {mode!r}")
         if flush_policy not in _FLUSH_POLICIES:
@@ -231,7 +231,20 @@ class DeviceFleet:
         ngpu = N.device_count()
         if ngpu < 1:
             raise DeviceError("no CUDA device visible; the fleet runs on B200 GPUs only")
-        self.ordinals = list(devices) if devices is not None else [i % ngpu for i in range(self.m)]
+        # rank mode: this process drives virtual device `rank` only (one
+        # process per GPU); peers are other processes (see dist.py)
+        self.rank = rank
+        if rank is not None:
+            if not 0 <= rank < self.m:
+                raise SimulationError(f"rank {rank} outside the plan's {self.m} devices")
+            if mode == "baseline":
+                raise SimulationError("rank mode needs mode 'p2p' or 'full'")
+            import os
+            local = int(os.environ.get("LOCAL_RANK", rank))
+            self.ordinals = [list(devices)[0] if devices is not None else local % ngpu]
+        else:
+            self.ordinals = list(devices) if devices is not None else [i % ngpu for i in range(self.m)]
+        self._ipc_ready = rank is None or self.m == 1
         self._handle = None
         self._create_native()
         self._precompute_meters()
@@ -244,9 +257,13 @@ class DeviceFleet:
     def _create_native(self):
         plan = self.plan
         h = C.c_void_p()
-        ords = (C.c_int * self.m)(*self.ordinals)
-        N.call("ht_fleet_create", self.m, self.n, ords, _MODE_ID[self.mode],
-               0 if self.flush_policy == "on_eviction" else 1, C.byref(h))
+        flush = 0 if self.flush_policy == "on_eviction" else 1
+        if self.rank is not None:
+            N.call("ht_fleet_create_rank", self.m, self.n, self.rank, self.ordinals[0],
+                   _MODE_ID[self.mode], flush, C.byref(h))
+        else:
+            ords = (C.c_int * self.m)(*self.ordinals)
+            N.call("ht_fleet_create", self.m, self.n, ords, _MODE_ID[self.mode], flush, C.byref(h))
         self._handle = h.value
         weakref.finalize(self, N.lib().ht_fleet_destroy, self._handle)
         keep = []
@@ -512,6 +529,22 @@ class DeviceFleet:
         for u in self.plan.union_sets:
             touched[u] = True
         self._untouched = np.flatnonzero(~touched)
+
+    def connect_peers(self) -> None:
+        """Rank mode: exchange CUDA IPC handles of the shared device buffers
+        with every peer rank (once; buffers are sized by the first
+        ht_epoch_begin and never move afterwards)."""
+        if self._ipc_ready:
+            return
+        from . import dist
+        mine = (C.c_byte * dist.HT_IPC_BYTES)()
+        N.call("ht_fleet_ipc_export", self._handle, mine)
+        blobs = dist.exchange(bytes(mine))
+        for k, blob in enumerate(blobs):
+            if k != self.rank:
+                buf = (C.c_byte * dist.HT_IPC_BYTES).from_buffer_copy(blob)
+                N.call("ht_fleet_ipc_import", self._handle, k, buf)
+        self._ipc_ready = True
 
     def set_timing(self, enabled: bool) -> None:
         N.call("ht_set_timing", self._handle, int(bool(enabled)))

@@ -178,6 +178,7 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     item = host.dtype.itemsize
     dims_c = (C.c_int * (L + 1))(*dims)
     N.call("ht_epoch_begin", h_, L, dims_c)
+    fleet.connect_peers()  # rank mode: IPC handles, once
 
     # ---- forward (Alg. 1 lines 4-9) ----
     for l in range(L):
@@ -228,7 +229,11 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     gp = (C.c_void_p * L)(*[N.ptr(g) for g in grads])
     N.call("ht_sgd", h_, L, dims_c, wp, C.c_float(model.lr), gp)
     N.call("ht_loss_value", h_, C.byref(loss))
-    return EpochResult(loss=float(loss.value), model=model, tracker=tracker, grads=grads)
+    value = float(loss.value)
+    if fleet.rank is not None and fleet.m > 1:  # per-rank partials of the mean
+        from . import dist
+        value = dist.allreduce_sum(value)
+    return EpochResult(loss=value, model=model, tracker=tracker, grads=grads)
 
 
 _MATRIX_MAGIC = b"HTF1"
