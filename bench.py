@@ -206,12 +206,15 @@ def reference_cpu_sample(ds, dims, budget_edges=1_500_000, threads=None):
 # ---------------------------------------------------------------------------
 # timed epochs
 # ---------------------------------------------------------------------------
-def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed):
+def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed, rank=None):
     import paper_2311_14898_b200 as H
     from paper_2311_14898_b200 import _native as N
-    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement)
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count()) if rank is not None else 0
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement,
+                       device=dev)
     host.set_features(ds.features)
-    fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision)
+    fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision, rank=rank,
+                          devices=[dev] if rank is not None else None)
     model = H.init_model("gcn", dims, seed=seed, lr=0.1, dtype=np.float32)
     losses = []
     for _ in range(warmup):
@@ -252,18 +255,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     N_gpus = args.gpus if world == 1 else world
     if world > 1:
+        # host plumbing only (IPC handles, loss partials, max-over-ranks
+        # timing); the data path is CUDA IPC + device-side barriers
         import torch.distributed as dist
         dist.init_process_group("gloo")
     cfg = CONFIGS[args.config]
     dims = cfg["dims"]
     L = len(dims) - 1
-    if rank != 0:
-        # the fleet drives every GPU from rank 0 (single-process multi-GPU
-        # until the per-rank path lands); other ranks only join barriers
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-            dist.destroy_process_group()
+    if args.impl == "reference" and rank != 0:
+        dist.destroy_process_group()  # the CPU reference arm runs on rank 0 only
         return
     m = N_gpus
     ds, p, plan, chosen = build_inputs(cfg, m)
@@ -305,19 +305,31 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
 
+    rk = rank if world > 1 else None  # torchrun: one process per GPU (rank mode)
+
+    def slowest(ms):  # device time, max over ranks
+        if world > 1:
+            from paper_2311_14898_b200 import dist as hd
+            return hd.allreduce_max(ms)
+        return ms
+
     # ---- value: HBM-resident vertex store ----
-    with Clocks() as clk_v:
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk_v:
         val = run_epochs(p, plan, ds, dims, "device", args.steps, args.warmup, args.precision,
-                         True, cfg["seed"])
-    ms_v = val["ms_total"] / args.steps
+                         True, cfg["seed"], rank=rk)
+    ms_v = slowest(val["ms_total"]) / args.steps
     if args.only_value:  # profiling aid: no e2e run, no JSON contract line
         log(f"[bench] value run: {ms_v:.2f} ms/epoch  stats {val['stats']}")
         return
     # ---- e2e: pinned host-resident vertex store through train_epoch ----
-    with Clocks() as clk_e:
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk_e:
         e2e = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,
-                         True, cfg["seed"])
-    ms_e = e2e["ms_total"] / args.steps
+                         True, cfg["seed"], rank=rk)
+    ms_e = slowest(e2e["ms_total"]) / args.steps
+    if rank != 0:
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     h2d, d2h = host_bytes_per_epoch(plan, dims)
     base_h2d, base_d2h = host_bytes_per_epoch(plan, dims, "baseline")
     dedup = dedup_report()
