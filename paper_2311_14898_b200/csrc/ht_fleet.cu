@@ -397,6 +397,25 @@ void timers_collect(ht_fleet* f) {
   f->timers.clear();
 }
 
+// Aggregation kernel variant: edges in flight per warp (U) and the
+// register cap (MINB resident CTAs per SM); HT_SEG_VARIANT selects one for
+// tuning runs, the default is the measured best.
+template <int NV>
+void seg_variant(int g, cudaStream_t s, float* out, const float* X, int64_t ldx, int d,
+                 const int64_t* off, const int32_t* idx, const float* w, int64_t nseg) {
+  static int v = [] {
+    const char* e = getenv("HT_SEG_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  switch (v) {
+    case 1: ht::k_seg_gather_v4<NV, 4, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    case 2: ht::k_seg_gather_v4<NV, 8, 2><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    case 3: ht::k_seg_gather_v4<NV, 8, 3><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    case 4: ht::k_seg_gather_v4<NV, 2, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    default: ht::k_seg_gather_v4<NV, 4, 1><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+  }
+}
+
 // Segment gather-sum over a chunk's CSC (forward) or CSR (backward) view.
 int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, const int64_t* off,
                const int32_t* idx, const float* w, int64_t nseg, int64_t np, const DBuf& lo,
@@ -408,7 +427,7 @@ int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, c
   if (d % 4 == 0 && d <= 512) {
     const int nv = (d / 4 + 31) / 32;
 #define SEGV(NV)                                                                               \
-  ht::k_seg_gather_v4<NV><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); \
+  seg_variant<NV>(g, s, out, X, ldx, d, off, idx, w, nseg);                                \
   if (np) ht::k_seg_pieces_v4<NV><<<grid_for(np), kThreads, 0, s>>>(                           \
       partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
     switch (nv) {

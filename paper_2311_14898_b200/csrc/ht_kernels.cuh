@@ -179,8 +179,8 @@ __device__ __forceinline__ void seg_sum_s(float (&acc)[NS], const float* __restr
 // One warp per segment; segments longer than `split` are skipped here and
 // handled by k_seg_pieces.  out row stride = d (dense), optional row map
 // `out_row` (null = identity).
-template <int NV>
-__global__ void __launch_bounds__(256) k_seg_gather_v4(float* __restrict__ out,
+template <int NV, int U = 4, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_seg_gather_v4(float* __restrict__ out,
                                                        const float* __restrict__ X, int64_t ldx,
                                                        int d, const int64_t* __restrict__ off,
                                                        const int32_t* __restrict__ idx,
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) k_seg_gather_v4(float* __restrict__ out,
     float4 acc[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    seg_sum_v4<NV, (NV <= 2 ? 8 : 4)>(acc, X, ldx, d4, idx, w, e0, e1, lane);
+    seg_sum_v4<NV, U>(acc, X, ldx, d4, idx, w, e0, e1, lane);
     float4* o = reinterpret_cast<float4*>(out + sg * (int64_t)d);
 #pragma unroll
     for (int t = 0; t < NV; ++t) {
