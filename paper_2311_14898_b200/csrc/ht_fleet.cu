@@ -411,8 +411,11 @@ void seg_variant(int g, cudaStream_t s, float* out, const float* X, int64_t ldx,
     case 1: ht::k_seg_gather_v4<NV, 4, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
     case 2: ht::k_seg_gather_v4<NV, 8, 2><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
     case 3: ht::k_seg_gather_v4<NV, 8, 3><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    case 4: ht::k_seg_gather_v4<NV, 2, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    default: ht::k_seg_gather_v4<NV, 4, 1><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    case 4: ht::k_seg_gather_v4<NV, 4, 1><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    case 5: ht::k_seg_gather_v4<NV, 2, 6><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    case 6: ht::k_seg_gather_v4<NV, 1, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    case 7: ht::k_seg_gather_v4<NV, 4, 5><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
+    default: ht::k_seg_gather_v4<NV, 2, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
   }
 }
 
