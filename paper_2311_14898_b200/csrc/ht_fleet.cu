@@ -178,7 +178,7 @@ struct Device {
   cudaEvent_t e_out[2] = {nullptr, nullptr}, e_hst = nullptr, e_loss = nullptr;
   cudaEvent_t e_bin = nullptr, e_bcomp[2] = {nullptr, nullptr}, e_flush = nullptr;
   cudaEvent_t e_hchunk[kChunks] = {}, e_fchunk[kChunks] = {};  // stores / flushes per host-row chunk
-  std::vector<cudaEvent_t> e_aggst;  // per layer: checkpoint rows stored
+  std::vector<cudaEvent_t> e_aggst;  // [layer * kChunks + chunk]: checkpoint rows stored
   int64_t fwd_count = 0, bwd_count = 0;
   std::vector<LayerW> lw;            // per-layer weights (valid until the SGD step)
   float* wpin = nullptr;             // pinned scratch for weight uploads
@@ -1272,7 +1272,7 @@ extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
     d.lw.resize(L);
     for (auto& w : d.lw) w.valid = false;
     d.fwd_count = d.bwd_count = 0;
-    if ((int)d.e_aggst.size() < L) d.e_aggst.resize(L, nullptr);
+    if ((int)d.e_aggst.size() < L * kChunks) d.e_aggst.resize(L * kChunks, nullptr);
   }
   return HT_OK;
 }
@@ -1389,15 +1389,22 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
                       chunk_bound(f->nrows, g + 1)));
           if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
         }
-        HT_TRY(xfer(d.tout, c.dest, true, aout, rbi, agg, rbi, rbi, 0, f->nrows));
+        // checkpoint rows, chunked: the first backward layer reloads the last
+        // forward layer's checkpoints chunk by chunk as they land
+        for (int g = 0; g < kChunks; ++g) {
+          HT_TRY(xfer(d.tout, c.dest, true, aout, rbi, agg, rbi, rbi, chunk_bound(f->nrows, g),
+                      chunk_bound(f->nrows, g + 1)));
+          if (lastb) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
+        }
       } else {
         HT_TRY(launch_copy(d.tout, hout, hdst, rows, nullptr, c.nv, rbo, rbo, rbo, 0, kHostGrid));
         if (lastb)
           for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
         HT_TRY(launch_copy(d.tout, aout, agg, rows, nullptr, c.nv, rbi, rbi, rbi, 0, kHostGrid));
+        if (lastb)
+          for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
       }
       HT_TRY(ev_rec(d.e_out[s], d.tout));
-      if (j == f->n - 1) HT_TRY(ev_rec(d.e_aggst[layer], d.tout));
       d.fwd_count++;
     }
   }
@@ -1494,11 +1501,16 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // K6 on tin: checkpoint rows (ready since the forward), then the
       // destination gradients (ready once the layer above has flushed)
       if (d.bwd_count >= 2) HT_TRY(ev_wait(d.tin, d.e_bcomp[s]));
-      HT_TRY(ev_wait(d.tin, d.e_aggst[layer]));
-      if (c.dest.dma)
-        HT_TRY(xfer(d.tin, c.dest, false, ain, rbi, A, rbi, rbi, 0, f->nrows));
-      else
+      if (c.dest.dma) {
+        for (int g = 0; g < kChunks; ++g) {
+          if (j == 0) HT_TRY(ev_wait(d.tin, d.e_aggst[layer * kChunks + g]));
+          HT_TRY(xfer(d.tin, c.dest, false, ain, rbi, A, rbi, rbi, chunk_bound(f->nrows, g),
+                      chunk_bound(f->nrows, g + 1)));
+        }
+      } else {
+        if (j == 0) HT_TRY(ev_wait(d.tin, d.e_aggst[layer * kChunks + kChunks - 1]));
         HT_TRY(launch_copy(d.tin, A, ain, nullptr, rows, c.nv, rbi, rbi, rbi, 0, kHostGrid));
+      }
       // gradient rows of the layer above: written by the loss, or by the
       // flushes of the previous backward layer (of every device in baseline
       // mode); streamed per host-row chunk when both sides use copy engines
