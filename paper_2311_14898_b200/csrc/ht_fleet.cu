@@ -173,6 +173,11 @@ struct Device {
   cudaEvent_t mark[2] = {nullptr, nullptr};
   // epoch pipeline: transfer streams, double-buffered staging, events
   cudaStream_t tin = nullptr, tout = nullptr;
+  // checkpoint prefetch: agg rows of layer l come back from the host as
+  // soon as they are stored (same bytes, moved while the link is idle)
+  cudaStream_t tpre = nullptr;
+  std::vector<DBuf> ck;
+  std::vector<cudaEvent_t> e_ck;
   DBuf fa[2], fb[2], ba[2], bb[2];
   cudaEvent_t e_in = nullptr, e_fetch = nullptr, e_agg = nullptr, e_comp = nullptr;
   cudaEvent_t e_out[2] = {nullptr, nullptr}, e_hst = nullptr, e_loss = nullptr;
@@ -204,6 +209,7 @@ struct ht_fleet {
   int L = 0;
   std::vector<int> dims;
   int64_t loss_count = 0;
+  bool prefetch = true;  // checkpoint prefetch (HT_CKPT_PREFETCH=0 disables)
   int64_t nrows = 0;  // host rows addressed by the plan (max vertex id + 1)
   // rank mode (one process per GPU): index of the local device, barrier
   // sequence, device array of every rank's barrier counter
@@ -263,6 +269,7 @@ int sync_all(ht_fleet* f) {
     CU(cudaStreamSynchronize(d.stream));
     if (d.tin) CU(cudaStreamSynchronize(d.tin));
     if (d.tout) CU(cudaStreamSynchronize(d.tout));
+    if (d.tpre) CU(cudaStreamSynchronize(d.tpre));
   }
   return HT_OK;
 }
@@ -624,6 +631,10 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
   f->n = n;
   f->mode = mode;
   f->flush = flush_policy;
+  {
+    const char* e = getenv("HT_CKPT_PREFETCH");
+    f->prefetch = !(e && e[0] == '0');
+  }
   f->dev.resize(m);
   f->sets.assign(m, std::vector<HostSets>(n));
   for (int i = 0; i < m; ++i) {
@@ -634,6 +645,11 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
     CU(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&d.tin, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&d.tout, cudaStreamNonBlocking));
+    {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      CU(cudaStreamCreateWithPriority(&d.tpre, cudaStreamNonBlocking, lo));
+    }
     CU(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
     d.chunks.resize(n);
     for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
@@ -767,6 +783,10 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     if (d.stream) cudaStreamDestroy(d.stream);
     if (d.tin) cudaStreamDestroy(d.tin);
     if (d.tout) cudaStreamDestroy(d.tout);
+    if (d.tpre) cudaStreamDestroy(d.tpre);
+    for (auto& b : d.ck) b.release();
+    for (cudaEvent_t e : d.e_ck)
+      if (e) cudaEventDestroy(e);
   }
   delete f;
   return HT_OK;
@@ -1214,6 +1234,30 @@ int check_chunks(ht_fleet* f) {
   return HT_OK;
 }
 
+// K6, early: reload the checkpoint rows of `layer` into their per-layer
+// device buffer on the low-priority prefetch stream, chunk by chunk as the
+// stores land.  The backward then reads them from HBM.
+int prefetch_checkpoints(ht_fleet* f, Device& d, int layer, void* aout, int64_t rbi) {
+  float* ck = d.ck[layer].as<float>();
+  const int dl = f->dims[layer];
+  for (int j = 0; j < f->n; ++j) {
+    DevChunk& c = d.chunks[j];
+    float* dst = ck + d.hL_off[j] * dl;
+    if (c.dest.dma) {
+      for (int g = 0; g < kChunks; ++g) {
+        if (j == 0) HT_TRY(ev_wait(d.tpre, d.e_aggst[layer * kChunks + g]));
+        HT_TRY(xfer(d.tpre, c.dest, false, aout, rbi, dst, rbi, rbi, chunk_bound(f->nrows, g),
+                    chunk_bound(f->nrows, g + 1)));
+      }
+    } else {
+      if (j == 0) HT_TRY(ev_wait(d.tpre, d.e_aggst[layer * kChunks + kChunks - 1]));
+      HT_TRY(launch_copy(d.tpre, dst, aout, nullptr, c.dest_rows.as<int64_t>(), c.nv, rbi, rbi,
+                         rbi, 0, kHostGrid));
+    }
+  }
+  return ev_rec(d.e_ck[layer], d.tpre);
+}
+
 }  // namespace
 
 extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
@@ -1259,6 +1303,12 @@ extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
     HT_TRY(d.partial.ensure(np * dmax * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
+    if (f->prefetch) {
+      if ((int)d.ck.size() < L) d.ck.resize(L);
+      if ((int)d.e_ck.size() < L) d.e_ck.resize(L, nullptr);
+      for (int l = 0; l < L; ++l)
+        HT_TRY(d.ck[l].ensure(std::max<int64_t>(1, d.hL_off[f->n]) * dims[l] * 4));
+    }
     // pinned scratch for weight uploads, one slot per layer
     d.wpin_off.assign(L + 1, 0);
     for (int l = 0; l < L; ++l)
@@ -1405,6 +1455,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
           for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
       }
       HT_TRY(ev_rec(d.e_out[s], d.tout));
+      if (lastb && f->prefetch) HT_TRY(prefetch_checkpoints(f, d, layer, aout, rbi));
       d.fwd_count++;
     }
   }
@@ -1501,7 +1552,9 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // K6 on tin: checkpoint rows (ready since the forward), then the
       // destination gradients (ready once the layer above has flushed)
       if (d.bwd_count >= 2) HT_TRY(ev_wait(d.tin, d.e_bcomp[s]));
-      if (c.dest.dma) {
+      if (f->prefetch) {
+        A = d.ck[layer].as<float>() + d.hL_off[j] * d_in;  // reloaded during the forward
+      } else if (c.dest.dma) {
         for (int g = 0; g < kChunks; ++g) {
           if (j == 0) HT_TRY(ev_wait(d.tin, d.e_aggst[layer * kChunks + g]));
           HT_TRY(xfer(d.tin, c.dest, false, ain, rbi, A, rbi, rbi, chunk_bound(f->nrows, g),
@@ -1539,6 +1592,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       HT_TRY(ev_rec(d.e_bin, d.tin));
       // K7 on the compute stream
       HT_TRY(ev_wait(d.stream, d.e_bin));
+      if (f->prefetch && j == 0) HT_TRY(ev_wait(d.stream, d.e_ck[layer]));
       float *GZ = d.sc.as<float>(), *GA = d.sd.as<float>();
       LayerW& w = d.lw[layer];
       TimerRec tg;
