@@ -125,6 +125,7 @@ struct DevChunk {
   DBuf nbr_slot;   // int64 [nn]
   DBuf dest_rows;  // int64 [nv]
   CopyList dest;   // runs of (host row = dest_rows[r], staging row r)
+  std::vector<int64_t> dest_pos;  // [kChunks+1]: first staging row of each host-row chunk
   CopyList h2d;    // host row -> slot
   std::vector<CopyList> d2d;   // [step 1..m-1] peer slot -> own slot
   std::vector<CopyList> push;  // [source device i] pos in N_ij(i) -> own slot (owner = this device)
@@ -183,6 +184,7 @@ struct Device {
   cudaEvent_t e_out[2] = {nullptr, nullptr}, e_hst = nullptr, e_loss = nullptr;
   cudaEvent_t e_bin = nullptr, e_bcomp[2] = {nullptr, nullptr}, e_flush = nullptr;
   cudaEvent_t e_hchunk[kChunks] = {}, e_fchunk[kChunks] = {};  // stores / flushes per host-row chunk
+  cudaEvent_t e_gchunk[kChunks] = {}, e_gin[kChunks] = {};     // GEMM / gradient-load chunks
   std::vector<cudaEvent_t> e_aggst;  // [layer * kChunks + chunk]: checkpoint rows stored
   int64_t fwd_count = 0, bwd_count = 0;
   std::vector<LayerW> lw;            // per-layer weights (valid until the SGD step)
@@ -768,10 +770,9 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (cudaEvent_t e : {d.e_in, d.e_fetch, d.e_agg, d.e_comp, d.e_out[0], d.e_out[1], d.e_hst,
                           d.e_loss, d.e_bin, d.e_bcomp[0], d.e_bcomp[1], d.e_flush})
       if (e) cudaEventDestroy(e);
-    for (int g = 0; g < kChunks; ++g) {
-      if (d.e_hchunk[g]) cudaEventDestroy(d.e_hchunk[g]);
-      if (d.e_fchunk[g]) cudaEventDestroy(d.e_fchunk[g]);
-    }
+    for (int g = 0; g < kChunks; ++g)
+      for (cudaEvent_t e : {d.e_hchunk[g], d.e_fchunk[g], d.e_gchunk[g], d.e_gin[g]})
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : d.e_aggst)
       if (e) cudaEventDestroy(e);
     for (int s = 0; s < 2; ++s)
@@ -901,6 +902,12 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         std::vector<int64_t> pos(h.dest.size());
         std::iota(pos.begin(), pos.end(), 0);
         make_runs(c.dest, h.dest, pos, nullptr);
+        c.dest_pos.clear();
+        if (c.dest.dma && std::is_sorted(h.dest.begin(), h.dest.end())) {
+          for (int g = 0; g <= kChunks; ++g)
+            c.dest_pos.push_back(std::lower_bound(h.dest.begin(), h.dest.end(),
+                                                  chunk_bound(f->nrows, g)) - h.dest.begin());
+        }
       }
       if (h.has_chunk) {
         if (h.nn != c.nn || (h.has_dest && h.nv != c.nv))
@@ -1417,28 +1424,46 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       HT_TRY(ev_rec(d.e_agg, d.stream));
       float* hdst = last ? d.hL.as<float>() + d.hL_off[j] * d_out : d.fb[s].as<float>();
       LayerW& w = d.lw[layer];
-      TimerRec tg;
-      timer_begin(f, d, tg, d.stream);
-      if (precision == HT_PREC_TF32) {
-        HT_TRY(ht::tc::rows<ht::tc::TC_RELU>(d.stream, true, agg, d_in, c.nv, d_in,
-                                             w.Wt_hi.as<float>(), w.Wt_lo.as<float>(), d_in,
-                                             d_out, hdst, d_out, nullptr, 0));
-      } else {
-        HT_TRY((gemm<false, false, ht::EPI_RELU>(d.stream, agg, d_in, w.W.as<float>(), d_out, hdst,
-                                                 d_out, nullptr, 0, c.nv, d_out, d_in, 1, d_in)));
-      }
-      timer_end(f, d, tg, 2, 2.0 * c.nv * d_in * d_out, d.stream);
-      HT_TRY(ev_rec(d.e_comp, d.stream));
-      // K5: destination rows, then checkpoint rows, to the host store
-      HT_TRY(ev_wait(d.tout, d.e_comp));
       const int64_t* rows = c.dest_rows.as<int64_t>();
       const bool lastb = j == f->n - 1;
-      if (c.dest.dma) {
-        for (int g = 0; g < kChunks; ++g) {
+      // K4 in host-row chunks when the destination rows are copy-engine
+      // runs: chunk g's h rows go to the host (K5) while chunk g+1 computes
+      const int nck = c.dest_pos.empty() ? 1 : kChunks;
+      for (int g = 0; g < nck; ++g) {
+        const int64_t r0 = nck > 1 ? c.dest_pos[g] : 0, r1 = nck > 1 ? c.dest_pos[g + 1] : c.nv;
+        if (r1 > r0) {
+          TimerRec tg;
+          timer_begin(f, d, tg, d.stream);
+          if (precision == HT_PREC_TF32) {
+            HT_TRY(ht::tc::rows<ht::tc::TC_RELU>(d.stream, true, agg + r0 * d_in, d_in, r1 - r0,
+                                                 d_in, w.Wt_hi.as<float>(), w.Wt_lo.as<float>(),
+                                                 d_in, d_out, hdst + r0 * d_out, d_out, nullptr, 0));
+          } else {
+            HT_TRY((gemm<false, false, ht::EPI_RELU>(d.stream, agg + r0 * d_in, d_in,
+                                                     w.W.as<float>(), d_out, hdst + r0 * d_out,
+                                                     d_out, nullptr, 0, r1 - r0, d_out, d_in, 1,
+                                                     d_in)));
+          }
+          timer_end(f, d, tg, 2, 2.0 * (r1 - r0) * d_in * d_out, d.stream);
+        }
+        if (nck > 1) {
+          HT_TRY(ev_rec(d.e_gchunk[g], d.stream));
+          HT_TRY(ev_wait(d.tout, d.e_gchunk[g]));
           HT_TRY(xfer(d.tout, c.dest, true, hout, rbo, hdst, rbo, rbo, chunk_bound(f->nrows, g),
                       chunk_bound(f->nrows, g + 1)));
           if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
         }
+      }
+      HT_TRY(ev_rec(d.e_comp, d.stream));
+      // K5: (remaining) destination rows, then checkpoint rows, to the host store
+      HT_TRY(ev_wait(d.tout, d.e_comp));
+      if (c.dest.dma) {
+        if (nck == 1)
+          for (int g = 0; g < kChunks; ++g) {
+            HT_TRY(xfer(d.tout, c.dest, true, hout, rbo, hdst, rbo, rbo, chunk_bound(f->nrows, g),
+                        chunk_bound(f->nrows, g + 1)));
+            if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
+          }
         // checkpoint rows, chunked: the first backward layer reloads the last
         // forward layer's checkpoints chunk by chunk as they land
         for (int g = 0; g < kChunks; ++g) {

@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(256, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], 128);
-      mbar_init(&kfull[s], 128);
+      mbar_init(&rempty[s], 192);
+      mbar_init(&kfull[s], 192);
       mbar_init(&kempty[s], 1);
     }
     mbar_init(accf, 1);
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       mma_commit(accf);
     }
-  } else if (warp < 6) {  // transposers + epilogue (warps 2-5, 128 threads)
+  } else {  // transposers (warps 2-7, 192 threads); epilogue on warps 4-7
     const int tt = threadIdx.x - 64;
     for (int it = 0; it < nst; ++it) {
       const int s = it & 1;
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(256, 1)
       uint8_t* ka = km + s * Cfg::KM;
       uint8_t* kg = ka + Cfg::KA;
       // each thread: one feature row x 4 reduction rows (float4 store)
-      for (int w = tt; w < (128 + BN) * 8; w += 128) {
+      for (int w = tt; w < (128 + BN) * 8; w += 192) {
         const int f = w % (128 + BN), rq = w / (128 + BN);  // rq: which 4-row group
         float4 v;
         if (f < 128) {
@@ -481,6 +481,8 @@ __global__ void __launch_bounds__(256, 1)
       mbar_arrive(&kfull[s]);
     }
     // epilogue: drain the 128 x BN accumulator into the slice's partial tile
+    if (warp < 4) goto done;
+    {
     const int q4 = warp & 3;
     const int k = k0 + q4 * 32 + lane;
     float* out = P + (int64_t)blockIdx.z * K * N;
@@ -500,7 +502,9 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
+    }
   }
+done:
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

@@ -161,3 +161,26 @@ def test_tf32_epoch_within_north_star_tolerance(m, n):
     assert O.rel_err(snaps[0]["hL"], ref["h"][-1]) < 1e-3
     for l in range(2):
         assert O.rel_err(snaps[0]["grads"][l], ref["grads"][l]) < 1e-3
+
+
+def test_hbm_resident_store_matches_host_store(golden_small):
+    """The HongTu-IM variant (vertex store in HBM, bench.py's `value`) runs
+    the same kernels on device memory: identical results to the pinned
+    host store, bitwise."""
+    meta, arr, ds, p = _small(golden_small)
+    dims = meta["dims"]
+    plan = H.plan_for_partition(p)
+    out = {}
+    for placement in ("host", "device"):
+        model = H.init_model("gcn", dims, seed=5, lr=0.1, dtype=np.float32)
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32)
+        losses = [H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss for _ in range(2)]
+        out[placement] = (losses, [w.copy() for w in model.weights], np.asarray(host.grad_h[0]),
+                          np.asarray(host.agg[1]))
+    assert out["host"][0] == out["device"][0]
+    for a, b in zip(out["host"][1], out["device"][1]):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(out["host"][2], out["device"][2])
+    np.testing.assert_array_equal(out["host"][3], out["device"][3])
