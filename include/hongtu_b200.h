@@ -104,6 +104,24 @@ int ht_slot_layout(int64_t n, const int64_t* live_concat, const int64_t* live_of
 int ht_reorganize(int64_t m, int64_t n, const int64_t* nbr_concat, const int64_t* nbr_offsets,
                   int move_all_rows, int64_t* chunk_orders, int64_t* batch_order);
 
+/* ---- GPU dedup planner (K13): planner.py:292-315 build_plan on the device -
+ * Input: the owner map (V) and, per chunk (i,j) row-major, the raw source
+ * ids of its edges (duplicates allowed; src_offsets has m*n+1 entries).
+ * Every set is computed on the GPU by radix sort / unique / membership and
+ * is bit-identical with the host planner.  Sets come back concatenated in
+ * this order (row-major over the indices named):
+ *   N[i][j], U[j], T[i][j], carry[i][j], load[i][j], nbr_carry[i][j],
+ *   fetch[i][j][k] (k != i, ascending; only when m > 1), live[i][j],
+ *   slots[i][j] (aligned with live[i][j]);
+ * caps has m entries (buffer capacities), volumes = (v_ori, v_p2p, v_ru). */
+typedef struct ht_gplan ht_gplan;
+int ht_gplan_build(int device, int m, int n, int64_t V, const int64_t* owner,
+                   const int64_t* src_concat, const int64_t* src_offsets, ht_gplan** out);
+int ht_gplan_count(ht_gplan* g, int64_t* nsets);
+int ht_gplan_sizes(ht_gplan* g, int64_t* sizes, int64_t* caps, int64_t* volumes);
+int ht_gplan_fetch(ht_gplan* g, int64_t* concat);
+int ht_gplan_free(ht_gplan* g);
+
 /* ---- fleet: m virtual devices executing one DedupPlan (devices.py) ----- */
 
 #define HT_MODE_BASELINE 0

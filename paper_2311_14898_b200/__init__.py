@@ -16,7 +16,7 @@ from .partition import (ChunkSubgraph, PartitionAssignment, TwoLevelPartition, b
                         replication_factor, save_partition, split_chunks, split_ranges,
                         two_level_from_ranges)
 from .planner import (MODES, BufferLayout, CostParams, DedupPlan, ReorgResult, Volumes,
-                      build_buffer_layout, build_plan, comm_cost, comm_volumes, intra_split,
+                      build_buffer_layout, build_plan, build_plan_gpu, chunk_edge_sources, comm_cost, comm_volumes, intra_split,
                       plan_for_partition, plan_summary, predicted_transfers, remote_fetch_sets,
                       reorganize, save_plan, transition_sets)
 from .devices import DeviceArray, DeviceFleet, DeviceState, HostStore

@@ -51,6 +51,11 @@ _SIGS = {
     "ht_intersect_count": (i64, [vp, i64, vp, i64]),
     "ht_slot_layout": (i32, [i64, vp, vp, vp, P_I64]),
     "ht_reorganize": (i32, [i64, i64, vp, vp, i32, vp, vp]),
+    "ht_gplan_build": (i32, [i32, i32, i32, i64, vp, vp, vp, C.POINTER(vp)]),
+    "ht_gplan_count": (i32, [vp, P_I64]),
+    "ht_gplan_sizes": (i32, [vp, vp, vp, vp]),
+    "ht_gplan_fetch": (i32, [vp, vp]),
+    "ht_gplan_free": (i32, [vp]),
     "ht_fleet_create": (i32, [i32, i32, vp, i32, i32, C.POINTER(vp)]),
     "ht_fleet_destroy": (i32, [vp]),
     "ht_fleet_create_rank": (i32, [i32, i32, i32, i32, i32, i32, C.POINTER(vp)]),

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libhongtu_b200.so")
-SOURCES = ["ht_fleet.cu", "ht_prep.cpp"]
+SOURCES = ["ht_fleet.cu", "ht_gplan.cu", "ht_prep.cpp"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
               "-Xcompiler", "-fPIC,-O3,-fopenmp", "-shared", "-cudart", "static", "-lgomp",
               "-Xptxas", "-v"]
