@@ -462,6 +462,82 @@ def gcn_chunk_backward(chunk, agg, grad_out, W):
     return gnbr, gW
 
 
+# ---------------------------------------------------------------------------
+# GAT chunk kernels                                  (src/engine.py:196-289)
+# ---------------------------------------------------------------------------
+
+
+def _seg_ids(offsets):
+    """Destination (segment) index of every edge of a CSC/CSR offsets array."""
+    return np.repeat(np.arange(offsets.size - 1, dtype=I64), np.diff(offsets))
+
+
+def gat_chunk_forward(chunk, h_nbr, h_dst, W, a, slope=0.2):
+    """One GAT chunk (src/engine.py:196-237): p = h_dst W, q = h_nbr W,
+    t_e = a_dst.p_v + a_src.q_u, LeakyReLU, max-subtracted softmax over the
+    in-edges of v, s_v = sum_e alpha_e q_u accumulated in CSC edge order
+    (the np.add.at of src/engine.py:236), h = ReLU(s).  Returns (h, state)
+    with state = dict(p, q, t, alpha, s)."""
+    dt = np.result_type(h_nbr.dtype, W.dtype)
+    d_out = W.shape[1]
+    p = h_dst @ W
+    q = h_nbr @ W
+    off = chunk["csc_offsets"]
+    src = chunk["csc_local_src"]
+    nv = off.size - 1
+    ne = src.size
+    s = np.zeros((nv, d_out), dtype=dt)
+    if ne == 0:
+        e0 = np.zeros(0, dtype=dt)
+        return np.maximum(s, 0), {"p": p, "q": q, "t": e0, "alpha": e0, "s": s}
+    dst = _seg_ids(off)
+    t = (p @ a[:d_out])[dst] + (q @ a[d_out:])[src]
+    logit = np.where(t > 0, t, np.asarray(slope, dtype=t.dtype) * t)
+    deg = np.diff(off)
+    has = deg > 0
+    mx = np.full(nv, -np.inf, dtype=logit.dtype)
+    np.maximum.at(mx, dst, logit)
+    ex = np.exp(logit - mx[dst])
+    den = np.zeros(nv, dtype=ex.dtype)
+    np.add.at(den, dst, ex)
+    alpha = ex / den[dst]
+    # sequential multiply-then-add per destination in CSC order
+    s = seq_aggregate(off, src, alpha, q, nv)
+    s[~has] = 0
+    return np.maximum(s, 0), {"p": p, "q": q, "t": t, "alpha": alpha, "s": s}
+
+
+def gat_chunk_backward(chunk, h_nbr, h_dst, grad_out, W, a, slope=0.2):
+    """Recompute backward of one GAT chunk (src/engine.py:240-289): re-runs
+    the forward, then differentiates the ReLU, the alpha-weighted sum, the
+    segment softmax, the LeakyReLU and both projections.  Returns
+    (grad_h_nbr, grad_h_dst, grad_W, grad_a)."""
+    d_out = W.shape[1]
+    _, st = gat_chunk_forward(chunk, h_nbr, h_dst, W, a, slope)
+    p, q, t, alpha, s = st["p"], st["q"], st["t"], st["alpha"], st["s"]
+    gs = grad_out * (s > 0)
+    gq = np.zeros_like(q)
+    gp = np.zeros_like(p)
+    ga = np.zeros_like(a)
+    off = chunk["csc_offsets"]
+    src = chunk["csc_local_src"]
+    if src.size:
+        dst = _seg_ids(off)
+        nv = off.size - 1
+        g_alpha = np.einsum("ij,ij->i", gs[dst], q[src])
+        sdot = np.zeros(nv, dtype=alpha.dtype)
+        np.add.at(sdot, dst, alpha * g_alpha)
+        g_t = alpha * (g_alpha - sdot[dst]) * np.where(t > 0, 1.0, slope).astype(t.dtype)
+        ga[:d_out] = g_t @ p[dst]
+        ga[d_out:] = g_t @ q[src]
+        seg_gt = np.zeros(nv, dtype=g_t.dtype)
+        np.add.at(seg_gt, dst, g_t)
+        gp += seg_gt[:, None] * a[:d_out][None, :]
+        np.add.at(gq, src, alpha[:, None] * gs[dst] + g_t[:, None] * a[d_out:][None, :])
+    gW = h_dst.T @ gp + h_nbr.T @ gq
+    return gq @ W.T, gp @ W.T, gW, ga
+
+
 def softmax_xent(h_last, labels, mask):
     """Masked mean softmax cross-entropy and its gradient
     (src/engine.py:297-320)."""
@@ -493,12 +569,20 @@ METER_KEYS = ("h2d_rows", "d2h_rows", "d2d_rows", "reuse_rows", "dest_h2d_rows",
 
 
 def partitioned_epoch(grid, plan, weights, X, labels, mask, *, lr=0.1,
-                      mode="full", flush_policy="on_eviction", dtype=np.float32):
-    """One GCN epoch over the chunk grid.  Values follow the reference's
-    accumulation order per mode; meters follow the fleet's counting rules.
+                      mode="full", flush_policy="on_eviction", dtype=np.float32,
+                      kind="gcn", attn=None, slope=0.2):
+    """One GCN (or GAT, ``kind="gat"`` with ``attn``) epoch over the chunk
+    grid.  Values follow the reference's accumulation order per mode; meters
+    follow the fleet's counting rules.  GAT (src/engine.py:411-476): the
+    forward also loads destination input rows; no checkpoints; the backward
+    re-stages the layer inputs through the forward machinery
+    (src/devices.py:427-432), loads destination inputs and gradients, adds
+    the destination-input gradients to the host (src/devices.py:376-385)
+    before the deduplicated neighbour-gradient accumulation.
 
     Returns dict(loss, weights (updated copies), grads (summed over
-    devices), h, grad_h, agg, meters (per device), peaks)."""
+    devices), h, grad_h, agg, meters (per device), peaks; GAT adds attn and
+    attn_grads)."""
     dt = np.dtype(dtype)
     m, n = plan["m"], plan["n"]
     V = X.shape[0]
@@ -516,57 +600,98 @@ def partitioned_epoch(grid, plan, weights, X, labels, mask, *, lr=0.1,
     def nbr_live(i, j):
         return int(plan["N"][i][j].size if mode == "baseline" else plan["live"][i][j].size)
 
+    gat = kind == "gat"
+    A = [np.asarray(x, dtype=dt) for x in attn] if gat else None
+    slope_dt = dt.type(slope)
+
+    def meter_comm_fwd(j, rb):  # dedup_comm_fwd (src/devices.py:223-278)
+        for i in range(m):
+            mt = meters[i]
+            if mode == "baseline":
+                rows = int(plan["N"][i][j].size)
+            else:
+                rows = int((plan["load"] if mode == "full" else plan["T"])[i][j].size)
+                if mode == "full":
+                    mt["reuse_rows"] += int(plan["carry"][i][j].size)
+                for k, f in plan["fetch"][i][j].items():
+                    ff = _minus(f, plan["nbr_carry"][i][j]) if mode == "full" else f
+                    mt["d2d_rows"] += int(ff.size)
+                    mt["d2d_bytes"] += int(ff.size) * rb
+            mt["h2d_rows"] += rows
+            mt["h2d_bytes"] += rows * rb
+            peaks[i] = max(peaks[i], nbr_live(i, j))
+
+    def meter_dest(i, nv, width, key):
+        meters[i][key] += nv
+        meters[i]["dest_bytes"] += nv * width * item
+
     # ---- forward: Alg. 1 lines 4-9 ----
     for l in range(L):
         rb = dims[l] * item
-        agg_store[l] = np.zeros((V, dims[l]), dtype=dt)
+        if not gat:
+            agg_store[l] = np.zeros((V, dims[l]), dtype=dt)
         for j in range(n):
-            for i in range(m):
-                mt = meters[i]
-                if mode == "baseline":
-                    rows = int(plan["N"][i][j].size)
-                else:
-                    rows = int((plan["load"] if mode == "full" else plan["T"])[i][j].size)
-                    if mode == "full":
-                        mt["reuse_rows"] += int(plan["carry"][i][j].size)
-                    for k, f in plan["fetch"][i][j].items():
-                        ff = _minus(f, plan["nbr_carry"][i][j]) if mode == "full" else f
-                        mt["d2d_rows"] += int(ff.size)
-                        mt["d2d_bytes"] += int(ff.size) * rb
-                mt["h2d_rows"] += rows
-                mt["h2d_bytes"] += rows * rb
-                peaks[i] = max(peaks[i], nbr_live(i, j))
+            meter_comm_fwd(j, rb)
+            if gat:
+                for i in range(m):
+                    meter_dest(i, int(grid[i][j]["vertices"].size), dims[l], "dest_h2d_rows")
             for i in range(m):
                 c = grid[i][j]
-                out, agg, _ = gcn_chunk_forward(c, h[l][c["sources"]], W[l])
-                h[l + 1][c["vertices"]] = out
-                agg_store[l][c["vertices"]] = agg
                 nv = int(c["vertices"].size)
-                meters[i]["dest_d2h_rows"] += nv
-                meters[i]["dest_bytes"] += nv * dims[l + 1] * item
-                meters[i]["chkpt_d2h_rows"] += nv
-                meters[i]["chkpt_bytes"] += nv * rb
+                if gat:
+                    out, _ = gat_chunk_forward(c, h[l][c["sources"]], h[l][c["vertices"]], W[l],
+                                               A[l], slope_dt)
+                else:
+                    out, agg, _ = gcn_chunk_forward(c, h[l][c["sources"]], W[l])
+                    agg_store[l][c["vertices"]] = agg
+                h[l + 1][c["vertices"]] = out
+                meter_dest(i, nv, dims[l + 1], "dest_d2h_rows")
+                if not gat:
+                    meters[i]["chkpt_d2h_rows"] += nv
+                    meters[i]["chkpt_bytes"] += nv * rb
     loss, g_last = softmax_xent(h[L], labels, mask)
     gh[L][:] = g_last
 
     # ---- backward: Alg. 1 lines 12-20 ----
     gW = [[np.zeros_like(w) for w in W] for _ in range(m)]
+    gA = [[np.zeros_like(a) for a in A] for _ in range(m)] if gat else None
     for l in reversed(range(L)):
         rb = dims[l] * item
         acc = [np.zeros((V, dims[l]), dtype=dt) for _ in range(m)]   # owner buffers
         for j in range(n):
-            views = []
+            if gat:
+                meter_comm_fwd(j, rb)  # inputs re-staged (src/devices.py:427-432)
+            views, dgrads = [], []
             for i in range(m):
                 c = grid[i][j]
                 nv = int(c["vertices"].size)
-                meters[i]["chkpt_h2d_rows"] += nv
-                meters[i]["chkpt_bytes"] += nv * rb
-                meters[i]["dest_h2d_rows"] += nv
-                meters[i]["dest_bytes"] += nv * dims[l + 1] * item
-                gn, gw = gcn_chunk_backward(c, agg_store[l][c["vertices"]],
-                                            gh[l + 1][c["vertices"]], W[l])
+                if gat:
+                    meter_dest(i, nv, dims[l], "dest_h2d_rows")
+                else:
+                    meters[i]["chkpt_h2d_rows"] += nv
+                    meters[i]["chkpt_bytes"] += nv * rb
+            for i in range(m):
+                c = grid[i][j]
+                meter_dest(i, int(c["vertices"].size), dims[l + 1], "dest_h2d_rows")
+            for i in range(m):
+                c = grid[i][j]
+                if gat:
+                    gn, gd, gw, ga = gat_chunk_backward(
+                        c, h[l][c["sources"]], h[l][c["vertices"]], gh[l + 1][c["vertices"]],
+                        W[l], A[l], slope_dt)
+                    gA[i][l] += ga
+                    dgrads.append(gd)
+                else:
+                    gn, gw = gcn_chunk_backward(c, agg_store[l][c["vertices"]],
+                                                gh[l + 1][c["vertices"]], W[l])
                 gW[i][l] += gw
                 views.append(gn)
+            if gat:  # add_dest_grads, ascending device (src/devices.py:376-385)
+                for i in range(m):
+                    vv = grid[i][j]["vertices"]
+                    if vv.size:
+                        gh[l][vv] += dgrads[i]
+                    meter_dest(i, int(vv.size), dims[l], "dest_d2h_rows")
             if mode == "baseline":
                 for i in range(m):
                     nb = plan["N"][i][j]
@@ -602,16 +727,26 @@ def partitioned_epoch(grid, plan, weights, X, labels, mask, *, lr=0.1,
                 meters[k]["d2h_rows"] += int(fl.size)
                 meters[k]["d2h_bytes"] += int(fl.size) * rb
 
-    grads = []
-    newW = []
-    for l in range(L):
-        tot = np.zeros_like(W[l])
+    def sgd(P, G):
+        tot = np.zeros_like(P)
         for i in range(m):          # ascending device id (src/engine.py:334-338)
-            tot += gW[i][l]
+            tot += G[i]
+        return tot, (P - np.asarray(lr, dtype=dt) * tot if dt == np.float32 else P - lr * tot)
+
+    grads, newW = [], []
+    for l in range(L):
+        tot, nw = sgd(W[l], [gW[i][l] for i in range(m)])
         grads.append(tot)
-        newW.append(W[l] - np.asarray(lr, dtype=dt) * tot if dt == np.float32 else W[l] - lr * tot)
-    return {"loss": loss, "weights": newW, "grads": grads, "h": h, "grad_h": gh,
-            "agg": agg_store, "meters": meters, "peaks": peaks}
+        newW.append(nw)
+    out = {"loss": loss, "weights": newW, "grads": grads, "h": h, "grad_h": gh,
+           "agg": agg_store, "meters": meters, "peaks": peaks}
+    if gat:
+        out["attn_grads"], out["attn"] = [], []
+        for l in range(L):
+            tot, na = sgd(A[l], [gA[i][l] for i in range(m)])
+            out["attn_grads"].append(tot)
+            out["attn"].append(na)
+    return out
 
 
 # ---------------------------------------------------------------------------

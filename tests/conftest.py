@@ -69,6 +69,13 @@ def golden_small():
 
 
 @pytest.fixture(scope="session")
+def golden_gat():
+    meta = load_json("gat.json")
+    arr = dict(np.load(os.path.join(GOLDEN, "gat.npz")))
+    return meta, arr
+
+
+@pytest.fixture(scope="session")
 def golden_sets():
     return load_json("sets.json")
 

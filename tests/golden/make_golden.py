@@ -18,6 +18,9 @@ writes small fixtures next to this file:
 * ``sets.json``      - plan digests + predicted transfers for 200 random
                         set instances (the reference's random_set_instance
                         recipe, tests/conftest.py:101-111).
+* ``gat.json`` / ``gat.npz`` - GAT (config 5's model) on the small graph:
+                        2-epoch runs (fp64 + fp32, three modes), the
+                        monolithic fp64 trainer, single-chunk kernel vectors.
 * ``cfg1.json`` / ``cfg1.npz`` - BASELINE config 1 (100K V, 64-128-16,
                         m=4, n=4, reorganized): hashes, volumes, caps,
                         predicted transfers, fp32 losses and weights.
@@ -123,8 +126,8 @@ def toy():
     return out
 
 
-def _epochs(g, p, plan, ds, dims, mode, dtype, epochs=2, seed=5):
-    model = engine.init_model("gcn", dims, seed=seed, lr=0.1, dtype=dtype)
+def _epochs(g, p, plan, ds, dims, mode, dtype, epochs=2, seed=5, kind="gcn"):
+    model = engine.init_model(kind, dims, seed=seed, lr=0.1, dtype=dtype)
     host = devices.HostStore(g.num_vertices, dims, dtype=dtype)
     host.set_features(ds.features)
     fleet = devices.DeviceFleet(plan, mode=mode, dtype=dtype)
@@ -138,9 +141,14 @@ def _epochs(g, p, plan, ds, dims, mode, dtype, epochs=2, seed=5):
             snaps["hL"] = host.h[len(dims) - 1].copy()
             snaps["gh0"] = host.grad_h[0].copy()
             snaps["gh1"] = host.grad_h[1].copy()
-            snaps["agg0"] = host.agg[0].copy()
+            if kind == "gcn":
+                snaps["agg0"] = host.agg[0].copy()
             snaps["w_e0"] = [w.copy() for w in model.weights]
+            if kind == "gat":
+                snaps["a_e0"] = [a.copy() for a in model.attn]
     rep = fleet.transfer_report(*engine.comm_passes_per_epoch(model))
+    if kind == "gat":
+        snaps["a_after"] = [a.copy() for a in model.attn]
     return losses, [w.copy() for w in model.weights], snaps, rep
 
 
@@ -210,6 +218,65 @@ def small(arrays, meta):
         arrays[f"mono_W{l}_after2"] = w
 
 
+def gat(arrays, meta):
+    """GAT on the 2,000-vertex graph of small(): m=3,
+    n=4 reorganized, dims 8-12-4, two epochs per dtype and mode through the
+    reference's train_epoch; the fp64 monolithic trainer; and single-chunk
+    kernel vectors (gat_layer_forward / gat_layer_backward_recompute)."""
+    spec = synth.SynthSpec(num_vertices=2000, avg_degree=8.0, seed=7)
+    ds = synth.synth_dataset(spec, 8, 4)
+    g = ds.graph
+    meta["hash"] = g.content_hash()
+    a3 = partition.partition_vertices(g, 3, epsilon=0.1, seed=7)
+    pr = planner.reorganize(partition.split_chunks(g, a3, 4)).partition
+    plan = planner.plan_for_partition(pr)
+    meta["plan_digest_reorg"] = ref_plan_digest(plan)
+    dims = [8, 12, 4]
+    meta["dims"] = dims
+    runs = {}
+    for dtype, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        for mode in planner.MODES:
+            losses, weights, snaps, rep = _epochs(g, pr, plan, ds, dims, mode, dtype, kind="gat")
+            runs[f"{tag}_{mode}"] = {"losses": losses, "totals": rep["totals"],
+                                     "peaks": rep["peak_live_slots"],
+                                     "consistent": bool(rep["planner_consistent"])}
+            if mode == "full":
+                for l, w in enumerate(weights):
+                    arrays[f"{tag}_W{l}_after2"] = w
+                for l, w in enumerate(snaps["w_e0"]):
+                    arrays[f"{tag}_W{l}_after1"] = w
+                for l, a in enumerate(snaps["a_e0"]):
+                    arrays[f"{tag}_a{l}_after1"] = a
+                for l, a in enumerate(snaps["a_after"]):
+                    arrays[f"{tag}_a{l}_after2"] = a
+                arrays[f"{tag}_hL_e0"] = snaps["hL"]
+                arrays[f"{tag}_gh0_e0"] = snaps["gh0"]
+                arrays[f"{tag}_gh1_e0"] = snaps["gh1"]
+    meta["runs"] = runs
+    model = engine.init_model("gat", dims, seed=5, lr=0.1)
+    mono = reference.reference_train(g, model, ds.features, ds.labels, ds.mask, epochs=2)
+    meta["mono_losses"] = [float(x) for x in mono]
+    for l, (w, a) in enumerate(zip(model.weights, model.attn)):
+        arrays[f"mono_W{l}_after2"] = w
+        arrays[f"mono_a{l}_after2"] = a
+    # single-chunk kernel vectors: chunk (1, 2) of the reorganized grid
+    ch = pr.chunks[1][2]
+    rng = np.random.default_rng(21)
+    d_in, d_out = 8, 12
+    h_nbr = rng.standard_normal((ch.sources.size, d_in))
+    h_dst = rng.standard_normal((ch.num_vertices, d_in))
+    W = rng.standard_normal((d_in, d_out)) * 0.5
+    av = rng.standard_normal(2 * d_out) * 0.5
+    R = rng.standard_normal((ch.num_vertices, d_out))
+    h, st = engine.gat_layer_forward(ch, h_nbr, h_dst, W, av)
+    gn, gd, gW, ga = engine.gat_layer_backward_recompute(ch, h_nbr, h_dst, R, W, av)
+    for k, v in (("h_nbr", h_nbr), ("h_dst", h_dst), ("W", W), ("a", av), ("R", R), ("h", h),
+                 ("alpha", st.alpha), ("t", st.t), ("s", st.s), ("g_nbr", gn), ("g_dst", gd),
+                 ("g_W", gW), ("g_a", ga)):
+        arrays["k_" + k] = v
+    meta["kernel_chunk"] = [1, 2]
+
+
 def set_instances(count=200, seed=123):
     rng = np.random.default_rng(seed)
     out = []
@@ -269,7 +336,16 @@ def cfg1(arrays, meta):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-cfg1", action="store_true")
+    ap.add_argument("--only-gat", action="store_true")
     args = ap.parse_args()
+    arrays, meta = {}, {}
+    gat(arrays, meta)
+    np.savez_compressed(os.path.join(HERE, "gat.npz"), **arrays)
+    with open(os.path.join(HERE, "gat.json"), "w") as fh:
+        json.dump(meta, fh, indent=0, sort_keys=True)
+    if args.only_gat:
+        print("GAT golden vectors written to", HERE)
+        return
     with open(os.path.join(HERE, "toy.json"), "w") as fh:
         json.dump(toy(), fh, indent=0, sort_keys=True)
     arrays, meta = {}, {}

@@ -186,3 +186,107 @@ def test_set_instances_plan_digests(golden_sets):
         assert _digest(pl) == gold["digest"]
         for mode, pred in gold["predicted"].items():
             assert O.expected_rows(pl, mode) == pred
+
+
+# ---------------------------------------------------------------------------
+# GAT: kernel vectors and 2-epoch runs of the reference
+# ---------------------------------------------------------------------------
+
+
+def _gat_grid(golden_small):
+    meta, arr = golden_small
+    g, owner, grid = _small_grid(meta, arr)
+    grid, _, _ = O.reorganize_grid(grid)
+    return arr, owner, grid
+
+
+def test_gat_chunk_kernels(golden_small, golden_gat):
+    meta, ga = golden_gat
+    arr, owner, grid = _gat_grid(golden_small)
+    i, j = meta["kernel_chunk"]
+    ch = grid[i][j]
+    h, st = O.gat_chunk_forward(ch, ga["k_h_nbr"], ga["k_h_dst"], ga["k_W"], ga["k_a"])
+    # the reference's softmax denominator uses reduceat (numpy-internal
+    # association): tolerance, not bitwise
+    assert O.rel_err(h, ga["k_h"]) < 1e-13
+    assert O.rel_err(st["alpha"], ga["k_alpha"]) < 1e-13
+    np.testing.assert_array_equal(st["t"], ga["k_t"])
+    out = O.gat_chunk_backward(ch, ga["k_h_nbr"], ga["k_h_dst"], ga["k_R"], ga["k_W"], ga["k_a"])
+    for k, v in zip(("g_nbr", "g_dst", "g_W", "g_a"), out):
+        assert O.rel_err(v, ga["k_" + k]) < 1e-12, k
+
+
+def test_gat_single_edge_and_empty_destination():
+    """Known answers of the reference's tests (tests/test_engine.py:181-222):
+    one in-edge => alpha 1, h = ReLU(h_nbr W), zero attention gradient; a
+    destination without in-edges gets a zero row and finite gradients."""
+    rng = np.random.default_rng(3)
+    ch = {"csc_offsets": np.array([0, 1]), "csc_local_src": np.array([0])}
+    hn, hd = rng.standard_normal((1, 3)), rng.standard_normal((1, 3))
+    W, a = rng.standard_normal((3, 2)), rng.standard_normal(4)
+    h, st = O.gat_chunk_forward(ch, hn, hd, W, a)
+    np.testing.assert_array_equal(st["alpha"], [1.0])
+    np.testing.assert_array_equal(h, np.maximum(hn @ W, 0.0))
+    _, _, _, g_a = O.gat_chunk_backward(ch, hn, hd, rng.standard_normal((1, 2)), W, a)
+    np.testing.assert_array_equal(g_a, np.zeros(4))
+    ch = {"csc_offsets": np.array([0, 1, 1, 2]), "csc_local_src": np.array([0, 1])}
+    hn, hd = rng.standard_normal((2, 4)), rng.standard_normal((3, 4))
+    W, a = rng.standard_normal((4, 2)), rng.standard_normal(4)
+    h, _ = O.gat_chunk_forward(ch, hn, hd, W, a)
+    np.testing.assert_array_equal(h[1], 0.0)
+    out = O.gat_chunk_backward(ch, hn, hd, rng.standard_normal(h.shape), W, a)
+    assert all(np.isfinite(x).all() for x in out)
+
+
+@pytest.mark.parametrize("tag,dtype", [("f64", np.float64), ("f32", np.float32)])
+@pytest.mark.parametrize("mode", ["baseline", "p2p", "full"])
+def test_gat_partitioned_epochs(golden_small, golden_gat, tag, dtype, mode):
+    meta, ga = golden_gat
+    arr, owner, grid = _gat_grid(golden_small)
+    pl = O.plan_of_grid(grid, owner)
+    assert _digest(pl) == meta["plan_digest_reorg"]
+    W, A = O.glorot_weights(meta["dims"], 5, dtype=dtype, gat=True)
+    run = meta["runs"][f"{tag}_{mode}"]
+    tot, losses = None, []
+    tol = 1e-12 if dtype == np.float64 else 2e-6
+    for e in range(2):
+        res = O.partitioned_epoch(grid, pl, W, arr["X"], arr["labels"], arr["mask"], mode=mode,
+                                  dtype=dtype, kind="gat", attn=A)
+        W, A = res["weights"], res["attn"]
+        losses.append(res["loss"])
+        tot = res["meters"] if tot is None else [
+            {k: a[k] + b[k] for k in a} for a, b in zip(tot, res["meters"])]
+        if e == 0 and mode == "full":
+            assert O.rel_err(res["h"][-1], ga[f"{tag}_hL_e0"]) < tol
+            assert O.rel_err(res["grad_h"][0], ga[f"{tag}_gh0_e0"]) < tol
+            assert O.rel_err(res["grad_h"][1], ga[f"{tag}_gh1_e0"]) < tol
+            for l in range(2):
+                assert O.rel_err(W[l], ga[f"{tag}_W{l}_after1"]) < tol
+                assert O.rel_err(A[l], ga[f"{tag}_a{l}_after1"]) < tol
+    np.testing.assert_allclose(losses, run["losses"], rtol=1e-12 if dtype == np.float64 else 1e-6)
+    totals = {k: sum(d[k] for d in tot) for k in O.METER_KEYS}
+    assert totals == run["totals"]
+    assert res["peaks"] == run["peaks"]
+    if mode == "full":
+        for l in range(2):
+            assert O.rel_err(W[l], ga[f"{tag}_W{l}_after2"]) < tol
+            assert O.rel_err(A[l], ga[f"{tag}_a{l}_after2"]) < tol
+
+
+def test_gat_partitioned_matches_monolithic_reference(golden_small, golden_gat):
+    """The reference's own acceptance bar (tests/test_acceptance.py:154-156):
+    the partitioned fp64 GAT epoch equals the monolithic trainer."""
+    meta, ga = golden_gat
+    arr, owner, grid = _gat_grid(golden_small)
+    pl = O.plan_of_grid(grid, owner)
+    W, A = O.glorot_weights(meta["dims"], 5, dtype=np.float64, gat=True)
+    losses = []
+    for _ in range(2):
+        res = O.partitioned_epoch(grid, pl, W, arr["X"], arr["labels"], arr["mask"],
+                                  dtype=np.float64, kind="gat", attn=A)
+        W, A = res["weights"], res["attn"]
+        losses.append(res["loss"])
+    np.testing.assert_allclose(losses, meta["mono_losses"], rtol=1e-10)
+    for l in range(2):
+        assert O.rel_err(W[l], ga[f"mono_W{l}_after2"]) < 1e-8
+        assert O.rel_err(A[l], ga[f"mono_a{l}_after2"]) < 1e-8
