@@ -215,6 +215,32 @@ int ht_sgd(ht_fleet* f, int L, const int* dims, float* const* W, float lr,
            float* const* grads_out);
 int ht_fleet_sync(ht_fleet* f);
 
+/* ---- GAT epoch kernels (engine.py:196-289, 409-476; config 5) ---------- */
+/* Replaces gat_layer_forward / gat_layer_backward_recompute and the GAT
+ * branches of train_epoch (engine.py:418-423, 455-470) together with
+ * DeviceFleet.load_dest_rows / add_dest_grads / load_recomp_chkpt("gat")
+ * (devices.py:361-385, 427-432).  Widths must be multiples of 4 (<= 256
+ * for HT_PREC_TF32).  A = attention vector [a_dst | a_src] (2 d_out). */
+int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims);
+/* One forward layer over all batches: dedup comm of h_in rows, destination
+ * input rows, q = h_nbr.W / p = h_dst.W (3xTF32), edge softmax
+ * aggregation, ReLU, destination rows stored to h_out (host.h[l+1]). */
+int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
+                         const float* A, float slope, const void* h_in, void* h_out,
+                         int precision);
+/* One recompute-backward layer over all batches: inputs re-staged through
+ * the forward machinery, destination inputs and gradients loaded, layer
+ * recomputed and differentiated; destination-input gradients added into
+ * grad_in (host.grad_h[l]), neighbour gradients pushed to owners and
+ * flushed (read-modify-write: grad_in must be zero at epoch start). */
+int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, const float* W,
+                          const float* A, float slope, const void* h_in,
+                          const void* grad_out, void* grad_in, int precision);
+/* ht_sgd plus the attention vectors (engine.py:339-343); A, gW_out, gA_out
+ * may be NULL. */
+int ht_sgd2(ht_fleet* f, int L, const int* dims, float* const* W, float* const* A, float lr,
+            float* const* gW_out, float* const* gA_out);
+
 /* ---- timing of the dominant kernels (bench roofline) ------------------- */
 /* Enables CUDA-event timing of the aggregation kernels; ht_kernel_stats
  * returns launches, summed milliseconds and summed algorithmic bytes of

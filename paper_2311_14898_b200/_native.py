@@ -77,6 +77,10 @@ _SIGS = {
     "ht_loss_value": (i32, [vp, P_F64]),
     "ht_backward_layer": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, i32]),
     "ht_sgd": (i32, [vp, i32, vp, vp, f32, vp]),
+    "ht_sgd2": (i32, [vp, i32, vp, vp, vp, f32, vp, vp]),
+    "ht_gat_epoch_begin": (i32, [vp, i32, vp]),
+    "ht_gat_forward_layer": (i32, [vp, i32, i32, i32, vp, vp, f32, vp, vp, i32]),
+    "ht_gat_backward_layer": (i32, [vp, i32, i32, i32, vp, vp, f32, vp, vp, vp, i32]),
     "ht_fleet_sync": (i32, [vp]),
     "ht_set_timing": (i32, [vp, i32]),
     "ht_kernel_stats": (i32, [vp, i32, P_I64, P_F64, P_F64]),

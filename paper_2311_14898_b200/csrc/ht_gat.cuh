@@ -1,0 +1,311 @@
+// GAT layer kernels (src/engine.py:196-289) for sm_100a.
+//
+// Per chunk (i, j), with q = h_nbr.W (|N_ij| rows), p = h_dst.W (|V_ij|
+// rows), both produced by the tcgen05 GEMM:
+//
+//   k_rowdot      el_src[u] = q_u . a_src (one warp per row)
+//   k_gat_dst     one warp per destination v over its CSC in-edges:
+//                 t_e = p_v.a_dst + el_src[u], LeakyReLU, max-subtracted
+//                 softmax (lane-parallel over edges), s_v = sum_e alpha_e q_u
+//                 (sequential multiply-then-add in CSC order, the np.add.at
+//                 of src/engine.py:236), h_v = ReLU(s_v).
+//                 BWD (recompute backward, src/engine.py:240-289): also
+//                 gs = g_v * (s_v > 0), per-edge g_alpha = gs . q_u,
+//                 g_t = alpha (g_alpha - sum alpha g_alpha) * LeakyReLU'(t),
+//                 writes gs rows, alpha / g_t per edge (CSC order), the
+//                 segment sum of g_t and the rank-1 gp_v = seg_gt_v * a_dst.
+//   k_gat_src     BWD, one warp per source u over its CSR out-edges:
+//                 gq_u = sum_e (alpha_e gs_{dst e} + g_t_e a_src) in edge
+//                 order (the np.add.at of src/engine.py:275/280), and
+//                 gts_u = sum_e g_t_e.
+//   k_wcolsum / k_colsum_reduce
+//                 out[c] += sum_r w_r X[r][c] (attention-vector gradients),
+//                 block partials reduced in a fixed order (deterministic).
+//
+// Feature widths are multiples of 4 (float4 rows) and at most 512.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace ht {
+namespace gat {
+
+constexpr int kW = 32;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int NV>
+__device__ __forceinline__ void load4(float4 (&r)[NV], const float* __restrict__ row, int d4,
+                                      int lane) {
+  const float4* p = reinterpret_cast<const float4*>(row);
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int c = lane + t * kW;
+    r[t] = c < d4 ? __ldg(p + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void store4(float* __restrict__ row, const float4 (&r)[NV], int d4,
+                                       int lane) {
+  float4* p = reinterpret_cast<float4*>(row);
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    const int c = lane + t * kW;
+    if (c < d4) p[c] = r[t];
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ float dot4(const float4 (&a)[NV], const float4 (&b)[NV]) {
+  float s = 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    s = fmaf(a[t].x, b[t].x, s);
+    s = fmaf(a[t].y, b[t].y, s);
+    s = fmaf(a[t].z, b[t].z, s);
+    s = fmaf(a[t].w, b[t].w, s);
+  }
+  return s;
+}
+
+// acc += a * x, product rounded before the add (np.add.at semantics)
+__device__ __forceinline__ void axpy_rn(float4& acc, float a, const float4& x) {
+  acc.x = __fadd_rn(acc.x, __fmul_rn(a, x.x));
+  acc.y = __fadd_rn(acc.y, __fmul_rn(a, x.y));
+  acc.z = __fadd_rn(acc.z, __fmul_rn(a, x.z));
+  acc.w = __fadd_rn(acc.w, __fmul_rn(a, x.w));
+}
+
+__device__ __forceinline__ float leaky(float t, float slope) { return t > 0.f ? t : slope * t; }
+
+// out[r] = X[r] . a   (one warp per row)
+template <int NV>
+__global__ void __launch_bounds__(256) k_rowdot(float* __restrict__ out, const float* __restrict__ X,
+                                                int64_t ldx, const float* __restrict__ a, int d,
+                                                int64_t rows) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  float4 av[NV];
+  load4<NV>(av, a, d4, lane);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+    float4 x[NV];
+    load4<NV>(x, X + r * ldx, d4, lane);
+    const float s = warp_sum(dot4<NV>(x, av));
+    if (lane == 0) out[r] = s;
+  }
+}
+
+// One warp per destination segment of a chunk's CSC view.  `idx` are
+// chunk-local source ids (rows of Q / el_src), rows are d floats wide.
+template <int NV, bool BWD>
+__global__ void __launch_bounds__(256) k_gat_dst(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
+    const float* __restrict__ Q, const float* __restrict__ P, const float* __restrict__ el_src,
+    const float* __restrict__ a_dst, int d, float slope, float* __restrict__ H,
+    const float* __restrict__ G, float* __restrict__ GS, float* __restrict__ GP,
+    float* __restrict__ AL, float* __restrict__ GT, float* __restrict__ SGT) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  float4 ad[NV];
+  load4<NV>(ad, a_dst, d4, lane);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nseg; v += nw) {
+    const int64_t e0 = off[v], e1 = off[v + 1];
+    float4 pv[NV];
+    load4<NV>(pv, P + v * (int64_t)d, d4, lane);
+    const float el_d = warp_sum(dot4<NV>(pv, ad));
+    // segment max and softmax denominator, lane-parallel over edges
+    float mx = -CUDART_INF_F;
+    for (int64_t e = e0 + lane; e < e1; e += kW)
+      mx = fmaxf(mx, leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope));
+    mx = warp_max(mx);
+    float den = 0.f;
+    for (int64_t e = e0 + lane; e < e1; e += kW)
+      den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
+    den = warp_sum(den);
+    // s_v = sum alpha_e q_u, sequential in edge order
+    float4 acc[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t base = e0; base < e1; base += kW) {
+      const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
+      int my_i = 0;
+      float my_a = 0.f;
+      if (lane < cnt) {
+        my_i = __ldg(idx + base + lane);
+        my_a = expf(leaky(el_d + __ldg(el_src + my_i), slope) - mx) / den;
+        if (BWD) AL[base + lane] = my_a;
+      }
+      int k = 0;
+      for (; k + 4 <= cnt; k += 4) {  // four rows in flight
+        float4 x[4][NV];
+        float a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int s = __shfl_sync(0xffffffffu, my_i, k + u);
+          a[u] = __shfl_sync(0xffffffffu, my_a, k + u);
+          load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a[u], x[u][t]);
+      }
+      for (; k < cnt; ++k) {
+        const int s = __shfl_sync(0xffffffffu, my_i, k);
+        const float a = __shfl_sync(0xffffffffu, my_a, k);
+        float4 x[NV];
+        load4<NV>(x, Q + (int64_t)s * d, d4, lane);
+#pragma unroll
+        for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a, x[t]);
+      }
+    }
+    if (!BWD) {
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        acc[t].x = fmaxf(acc[t].x, 0.f);
+        acc[t].y = fmaxf(acc[t].y, 0.f);
+        acc[t].z = fmaxf(acc[t].z, 0.f);
+        acc[t].w = fmaxf(acc[t].w, 0.f);
+      }
+      store4<NV>(H + v * (int64_t)d, acc, d4, lane);
+      continue;
+    }
+    // ---- backward: gs = g * (s > 0) ----
+    float4 gs[NV];
+    load4<NV>(gs, G + v * (int64_t)d, d4, lane);
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      gs[t].x = acc[t].x > 0.f ? gs[t].x : 0.f;
+      gs[t].y = acc[t].y > 0.f ? gs[t].y : 0.f;
+      gs[t].z = acc[t].z > 0.f ? gs[t].z : 0.f;
+      gs[t].w = acc[t].w > 0.f ? gs[t].w : 0.f;
+    }
+    store4<NV>(GS + v * (int64_t)d, gs, d4, lane);
+    // g_alpha_e = gs . q_u (kept in GT for now), sum alpha_e g_alpha_e
+    float sdot = 0.f;
+    for (int64_t base = e0; base < e1; base += kW) {
+      const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
+      const int my_i = lane < cnt ? __ldg(idx + base + lane) : 0;
+      float my_g = 0.f;
+      for (int k = 0; k < cnt; ++k) {
+        const int s = __shfl_sync(0xffffffffu, my_i, k);
+        float4 x[NV];
+        load4<NV>(x, Q + (int64_t)s * d, d4, lane);
+        const float g = warp_sum(dot4<NV>(gs, x));
+        if (lane == k) my_g = g;
+      }
+      if (lane < cnt) {
+        GT[base + lane] = my_g;
+        sdot += AL[base + lane] * my_g;
+      }
+    }
+    sdot = warp_sum(sdot);
+    float sgt = 0.f;
+    for (int64_t e = e0 + lane; e < e1; e += kW) {
+      const float t = el_d + __ldg(el_src + __ldg(idx + e));
+      const float gt = AL[e] * (GT[e] - sdot) * (t > 0.f ? 1.f : slope);
+      GT[e] = gt;
+      sgt += gt;
+    }
+    sgt = warp_sum(sgt);
+    if (lane == 0) SGT[v] = sgt;
+    float4 gp[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t)
+      gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
+    store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+  }
+}
+
+// One warp per source segment of a chunk's CSR view: dst = chunk-local
+// destination rows of GS, perm = CSC edge id (index into AL / GT).
+template <int NV>
+__global__ void __launch_bounds__(256) k_gat_src(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ dst,
+    const int32_t* __restrict__ perm, int64_t nseg, const float* __restrict__ GS,
+    const float* __restrict__ AL, const float* __restrict__ GT, const float* __restrict__ a_src,
+    int d, float* __restrict__ GQ, float* __restrict__ GTS) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  float4 as[NV];
+  load4<NV>(as, a_src, d4, lane);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nseg; u += nw) {
+    const int64_t e0 = off[u], e1 = off[u + 1];
+    float4 acc[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float gts = 0.f;
+    for (int64_t base = e0; base < e1; base += kW) {
+      const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
+      int my_d = 0;
+      float my_a = 0.f, my_t = 0.f;
+      if (lane < cnt) {
+        my_d = __ldg(dst + base + lane);
+        const int32_t pe = __ldg(perm + base + lane);
+        my_a = AL[pe];
+        my_t = GT[pe];
+        gts += my_t;
+      }
+      for (int k = 0; k < cnt; ++k) {
+        const int r = __shfl_sync(0xffffffffu, my_d, k);
+        const float a = __shfl_sync(0xffffffffu, my_a, k);
+        const float g = __shfl_sync(0xffffffffu, my_t, k);
+        float4 x[NV];
+        load4<NV>(x, GS + (int64_t)r * d, d4, lane);
+#pragma unroll
+        for (int t = 0; t < NV; ++t) {
+          // per-edge value (alpha gs + g_t a_src), then the add
+          acc[t].x = __fadd_rn(acc[t].x, __fadd_rn(__fmul_rn(a, x[t].x), __fmul_rn(g, as[t].x)));
+          acc[t].y = __fadd_rn(acc[t].y, __fadd_rn(__fmul_rn(a, x[t].y), __fmul_rn(g, as[t].y)));
+          acc[t].z = __fadd_rn(acc[t].z, __fadd_rn(__fmul_rn(a, x[t].z), __fmul_rn(g, as[t].z)));
+          acc[t].w = __fadd_rn(acc[t].w, __fadd_rn(__fmul_rn(a, x[t].w), __fmul_rn(g, as[t].w)));
+        }
+      }
+    }
+    store4<NV>(GQ + u * (int64_t)d, acc, d4, lane);
+    gts = warp_sum(gts);
+    if (lane == 0) GTS[u] = gts;
+  }
+}
+
+// partial[b][c] = sum over block b's rows r of w[r] * X[r][c]
+__global__ void __launch_bounds__(256) k_wcolsum(float* __restrict__ partial,
+                                                 const float* __restrict__ X, int64_t ldx,
+                                                 const float* __restrict__ w, int64_t rows, int d,
+                                                 int64_t rows_per_block) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float s = 0.f;
+    for (int64_t r = r0; r < r1; ++r) s = fmaf(__ldg(w + r), __ldg(X + r * ldx + c), s);
+    partial[(int64_t)blockIdx.x * d + c] = s;
+  }
+}
+
+// out[c] += sum_b partial[b][c], b ascending
+__global__ void k_colsum_reduce(float* __restrict__ out, const float* __restrict__ partial,
+                                int nb, int d) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  float s = 0.f;
+  for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * d + c];
+  out[c] += s;
+}
+
+}  // namespace gat
+}  // namespace ht

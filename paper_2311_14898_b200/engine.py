@@ -98,7 +98,8 @@ class EpochResult:
     loss: float
     model: ModelConfig
     tracker: ActivationTracker = field(default_factory=ActivationTracker)
-    grads: list | None = None   # summed weight gradients of this epoch (new)
+    grads: list | None = None        # summed weight gradients of this epoch (new)
+    attn_grads: list | None = None   # GAT: summed attention-vector gradients (new)
 
 
 def sync_and_update(model: ModelConfig, device_grads: list, lr: float | None = None) -> ModelConfig:
@@ -123,21 +124,43 @@ def comm_passes_per_epoch(model: ModelConfig) -> tuple:
     return (2 * L, L) if model.kind == "gat" else (L, L)
 
 
-def _epoch_reset(host: HostStore, fleet: DeviceFleet) -> None:
+def _epoch_reset(host: HostStore, fleet: DeviceFleet, kind: str = "gcn") -> None:
     """reset_epoch with the same observable result but without rewriting
     rows the epoch overwrites anyway: the loss writes every row of
-    grad_h[L], and in p2p/full mode the first flush of a row stores it, so
-    only rows no chunk ever reads need explicit zeros."""
+    grad_h[L], and in p2p/full GCN mode the first flush of a row stores it,
+    so only rows no chunk ever reads need explicit zeros.  GAT adds
+    destination-input gradients into the host rows before the flushes, so
+    every flush is a read-modify-write there and all rows are zeroed."""
     L = len(host.dims) - 1
     for l in range(1, len(host.h)):
         host.h_valid[l] = False
     host.agg_written.clear()
     for l in range(L):
         g = host.grad_h[l]
-        if isinstance(g, DeviceArray) or fleet.mode == "baseline":
+        if isinstance(g, DeviceArray) or fleet.mode == "baseline" or kind == "gat":
             _zero_rows(g, None)
         else:
             _zero_rows(g, fleet._untouched)
+
+
+def _loss(h_, host: HostStore, dims: list, labels, mask) -> None:
+    mask_b = np.ascontiguousarray(np.asarray(mask, dtype=bool))
+    labels_i = np.ascontiguousarray(np.asarray(labels, dtype=np.int64))
+    count = int(mask_b.sum())
+    if count == 0:
+        warnings.warn("training mask is empty; loss is 0", stacklevel=3)
+    L = len(dims) - 1
+    N.call("ht_loss", h_, dims[L], N.ptr(labels_i), N.ptr(mask_b.view(np.uint8)),
+           int(host.num_vertices), count, N.ptr(host.grad_h[L]), None)  # value read after SGD
+
+
+def _f32_params(params: list, shapes: list) -> list:
+    out = []
+    for k, (x, shp) in enumerate(zip(params, shapes)):
+        if x.dtype != np.float32 or not x.flags.c_contiguous or x.shape != shp:
+            params[k] = np.ascontiguousarray(x, dtype=np.float32).reshape(shp)
+        out.append(params[k])
+    return out
 
 
 def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, host: HostStore,
@@ -145,18 +168,23 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
                 tracker: ActivationTracker | None = None) -> EpochResult:
     """One full-graph epoch over the chunk grid on the GPU (engine.py:387-480).
 
-    Forward: per layer, every batch stages its deduplicated neighbour rows
-    (host loads, barrier, peer fetches, barrier), aggregates them, applies
-    z = agg.W and ReLU, and writes h^{l+1} and the agg checkpoint rows to
-    the host store.  Loss on the last layer.  Backward: checkpoint and
-    dest-gradient reload, hybrid recompute, transposed aggregation, owner
-    push and flush into grad_h[l].  Then the ascending-device gradient sum
-    and the SGD step, in place on model.weights.
+    GCN forward: per layer, every batch stages its deduplicated neighbour
+    rows (host loads, barrier, peer fetches, barrier), aggregates them,
+    applies z = agg.W and ReLU, and writes h^{l+1} and the agg checkpoint
+    rows to the host store.  Loss on the last layer.  Backward: checkpoint
+    and dest-gradient reload, hybrid recompute, transposed aggregation,
+    owner push and flush into grad_h[l].  GAT (engine.py:418-423, 455-470):
+    the forward also loads destination inputs and aggregates with edge
+    softmax attention; no checkpoints; the backward re-stages the layer
+    inputs through the forward machinery, recomputes, adds the
+    destination-input gradients to the host and then pushes/flushes the
+    neighbour gradients.  Then the ascending-device gradient sum and the
+    SGD step (W, and the attention vectors for GAT), in place.
     """
     if tracker is None:
         tracker = ActivationTracker()
-    if model.kind != "gcn":
-        raise SimulationError(f"model kind {model.kind!r} is not on the B200 path yet (gcn only)")
+    if model.kind not in KINDS:
+        raise SimulationError(f"unknown model kind {model.kind!r}")
     if not host.h_valid[0]:
         raise SimulationError("host features not set; call set_features first")
     if host.dtype != np.float32 or fleet.dtype != np.float32:
@@ -166,74 +194,96 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     dims = [int(d) for d in model.dims]
     if list(host.dims) != dims:
         raise SimulationError("host store widths do not match the model")
-    W = []
-    for l, w in enumerate(model.weights):
-        if w.dtype != np.float32 or not w.flags.c_contiguous or w.shape != (dims[l], dims[l + 1]):
-            model.weights[l] = np.ascontiguousarray(w, dtype=np.float32).reshape(dims[l], dims[l + 1])
-        W.append(model.weights[l])
+    gat = model.kind == "gat"
+    W = _f32_params(model.weights, [(dims[l], dims[l + 1]) for l in range(L)])
+    A = _f32_params(model.attn, [(2 * dims[l + 1],) for l in range(L)]) if gat else None
     prec = PRECISIONS[fleet.precision]
     fleet.attach_partition(p)
-    _epoch_reset(host, fleet)
+    _epoch_reset(host, fleet, model.kind)
     h_ = fleet._handle
     item = host.dtype.itemsize
     dims_c = (C.c_int * (L + 1))(*dims)
-    N.call("ht_epoch_begin", h_, L, dims_c)
+    N.call("ht_gat_epoch_begin" if gat else "ht_epoch_begin", h_, L, dims_c)
     fleet.connect_peers()  # rank mode: IPC handles, once
+    slope = C.c_float(model.leaky_slope)
+
+    def chunks(kind_tag, l):
+        for j in range(n):
+            for i in range(m):
+                tag = (kind_tag, l, i, j)
+                tracker.acquire(tag)
+                tracker.release(tag)
 
     # ---- forward (Alg. 1 lines 4-9) ----
     for l in range(L):
         fleet._dim = dims[l]
         fleet._fwd_next = None
-        agg = host.agg_array(l)
-        N.call("ht_forward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(host.h[l]),
-               N.ptr(host.h[l + 1]), N.ptr(agg), prec)
-        for j in range(n):
-            fleet._meter_fwd(j, dims[l] * item)
-            for i in range(m):
-                tag = ("fwd", l, i, j)
-                tracker.acquire(tag)
-                tracker.release(tag)
-                host.agg_written.add((l, i, j))
-            fleet._meter_dest(j, dims[l + 1] * item, "d2h")
-            fleet._meter_dest(j, dims[l] * item, "d2h", "chkpt")
+        if gat:
+            N.call("ht_gat_forward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(A[l]),
+                   slope, N.ptr(host.h[l]), N.ptr(host.h[l + 1]), prec)
+            for j in range(n):
+                fleet._meter_fwd(j, dims[l] * item)
+                fleet._meter_dest(j, dims[l] * item, "h2d")
+                fleet._meter_dest(j, dims[l + 1] * item, "d2h")
+        else:
+            agg = host.agg_array(l)
+            N.call("ht_forward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(host.h[l]),
+                   N.ptr(host.h[l + 1]), N.ptr(agg), prec)
+            for j in range(n):
+                fleet._meter_fwd(j, dims[l] * item)
+                for i in range(m):
+                    host.agg_written.add((l, i, j))
+                fleet._meter_dest(j, dims[l + 1] * item, "d2h")
+                fleet._meter_dest(j, dims[l] * item, "d2h", "chkpt")
+        chunks("fwd", l)
         host.h_valid[l + 1] = True
 
     # ---- loss ----
-    mask_b = np.ascontiguousarray(np.asarray(mask, dtype=bool))
-    labels_i = np.ascontiguousarray(np.asarray(labels, dtype=np.int64))
-    count = int(mask_b.sum())
-    if count == 0:
-        warnings.warn("training mask is empty; loss is 0", stacklevel=2)
-    loss = C.c_double(0.0)
-    N.call("ht_loss", h_, dims[L], N.ptr(labels_i), N.ptr(mask_b.view(np.uint8)),
-           int(host.num_vertices), count, N.ptr(host.grad_h[L]), None)  # value read after SGD
+    _loss(h_, host, dims, labels, mask)
 
     # ---- backward (Alg. 1 lines 12-20) ----
     for l in reversed(range(L)):
         fleet._dim = dims[l]
-        N.call("ht_backward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(host.agg[l]),
-               N.ptr(host.grad_h[l + 1]), N.ptr(host.grad_h[l]), prec)
-        for j in range(n):
-            fleet._meter_dest(j, dims[l] * item, "h2d", "chkpt")
-            fleet._meter_dest(j, dims[l + 1] * item, "h2d")
-            for i in range(m):
-                tag = ("bwd", l, i, j)
-                tracker.acquire(tag)
-                tracker.release(tag)
-            fleet._meter_bwd(j, dims[l] * item)
+        if gat:
+            N.call("ht_gat_backward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(A[l]),
+                   slope, N.ptr(host.h[l]), N.ptr(host.grad_h[l + 1]), N.ptr(host.grad_h[l]),
+                   prec)
+            for j in range(n):
+                fleet._meter_fwd(j, dims[l] * item)          # inputs re-staged
+                fleet._meter_dest(j, dims[l] * item, "h2d")  # destination inputs
+                fleet._meter_dest(j, dims[l + 1] * item, "h2d")
+                fleet._meter_dest(j, dims[l] * item, "d2h")  # add_dest_grads
+                fleet._meter_bwd(j, dims[l] * item)
+        else:
+            N.call("ht_backward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]),
+                   N.ptr(host.agg[l]), N.ptr(host.grad_h[l + 1]), N.ptr(host.grad_h[l]), prec)
+            for j in range(n):
+                fleet._meter_dest(j, dims[l] * item, "h2d", "chkpt")
+                fleet._meter_dest(j, dims[l + 1] * item, "h2d")
+                fleet._meter_bwd(j, dims[l] * item)
+        chunks("bwd", l)
     fleet._fwd_next = fleet._bwd_next = None
 
     # ---- replica gradient sum + SGD (engine.py:479) ----
     grads = [np.empty_like(w) for w in W]
     wp = (C.c_void_p * L)(*[N.ptr(w) for w in W])
     gp = (C.c_void_p * L)(*[N.ptr(g) for g in grads])
-    N.call("ht_sgd", h_, L, dims_c, wp, C.c_float(model.lr), gp)
+    attn_grads = None
+    if gat:
+        attn_grads = [np.empty_like(a) for a in A]
+        ap = (C.c_void_p * L)(*[N.ptr(a) for a in A])
+        agp = (C.c_void_p * L)(*[N.ptr(g) for g in attn_grads])
+        N.call("ht_sgd2", h_, L, dims_c, wp, ap, C.c_float(model.lr), gp, agp)
+    else:
+        N.call("ht_sgd", h_, L, dims_c, wp, C.c_float(model.lr), gp)
+    loss = C.c_double(0.0)
     N.call("ht_loss_value", h_, C.byref(loss))
     value = float(loss.value)
     if fleet.rank is not None and fleet.m > 1:  # per-rank partials of the mean
         from . import dist
         value = dist.allreduce_sum(value)
-    return EpochResult(loss=value, model=model, tracker=tracker, grads=grads)
+    return EpochResult(loss=value, model=model, tracker=tracker, grads=grads,
+                       attn_grads=attn_grads)
 
 
 _MATRIX_MAGIC = b"HTF1"

@@ -1,0 +1,156 @@
+"""GAT epochs (BASELINE config 5's model) on the GPU
+through the C ABI, against the reference's golden vectors
+(tests/golden/gat.*, written by the unmodified reference) and the CPU
+oracle.  FP32 validation mode: 1e-5 relative (max-normalised, as in the
+reference's tests/test_engine.py:122-124); TF32 production mode: 1e-3
+against the fp64 oracle from the same starting state."""
+
+import numpy as np
+import pytest
+
+import paper_2311_14898_b200 as H
+from oracle import hongtu_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _small(golden_small):
+    meta, arr = golden_small
+    s = meta["synth"]
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=s["num_vertices"], avg_degree=s["avg_degree"],
+                                     seed=s["seed"]), s["feature_dim"], s["num_classes"])
+    a = H.PartitionAssignment(owner=arr["owner_m3"].astype(np.int64), m=3)
+    p = H.reorganize(H.split_chunks(ds.graph, a, 4)).partition
+    return ds, a, p
+
+
+def _run(p, ds, dims, mode="full", precision="fp32", epochs=2, seed=5, model=None):
+    plan = H.plan_for_partition(p)
+    if model is None:
+        model = H.init_model("gat", dims, seed=seed, lr=0.1, dtype=np.float32)
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+    host.set_features(ds.features)
+    fleet = H.DeviceFleet(plan, mode=mode, dtype=np.float32, precision=precision)
+    losses, snaps = [], []
+    for _ in range(epochs):
+        res = H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+        losses.append(res.loss)
+        snaps.append({"hL": np.array(host.h[-1]), "h1": np.array(host.h[1]),
+                      "gh0": np.array(host.grad_h[0]), "gh1": np.array(host.grad_h[1]),
+                      "W": [w.copy() for w in model.weights], "A": [a.copy() for a in model.attn],
+                      "grads": res.grads, "attn_grads": res.attn_grads})
+    return losses, snaps, fleet, model
+
+
+@pytest.mark.parametrize("mode", ["baseline", "p2p", "full"])
+def test_gat_epochs_match_reference(golden_small, golden_gat, mode):
+    meta, ga = golden_gat
+    ds, a, p = _small(golden_small)
+    assert H.plan_for_partition(p) is not None
+    losses, snaps, fleet, model = _run(p, ds, meta["dims"], mode=mode)
+    run = meta["runs"][f"f32_{mode}"]
+    np.testing.assert_allclose(losses, run["losses"], rtol=1e-5)
+    # two epochs of (2L, L) communication sweeps, exactly the reference's meters
+    rep = fleet.transfer_report(*(2 * x for x in H.comm_passes_per_epoch(model)))
+    assert rep["totals"] == run["totals"]
+    assert rep["peak_live_slots"] == run["peaks"]
+    assert rep["planner_consistent"]
+    if mode == "full":
+        assert O.rel_err(snaps[0]["hL"], ga["f32_hL_e0"]) < 1e-5
+        assert O.rel_err(snaps[0]["gh0"], ga["f32_gh0_e0"]) < 1e-5
+        assert O.rel_err(snaps[0]["gh1"], ga["f32_gh1_e0"]) < 1e-5
+        for l in range(2):
+            assert O.rel_err(snaps[0]["W"][l], ga[f"f32_W{l}_after1"]) < 1e-5
+            assert O.rel_err(snaps[0]["A"][l], ga[f"f32_a{l}_after1"]) < 1e-5
+            assert O.rel_err(snaps[1]["W"][l], ga[f"f32_W{l}_after2"]) < 1e-5
+            assert O.rel_err(snaps[1]["A"][l], ga[f"f32_a{l}_after2"]) < 1e-5
+
+
+def _oracle(p, a, ds, w0, a0, dtype, mode="full"):
+    grid = [[vars(c) for c in row] for row in p.chunks]
+    return O.partitioned_epoch(grid, O.plan_of_grid(grid, a.owner), [w.copy() for w in w0],
+                               ds.features, ds.labels, ds.mask, dtype=dtype, mode=mode,
+                               kind="gat", attn=[x.copy() for x in a0])
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 3), (4, 2)])
+def test_gat_epoch_matches_oracle(m, n):
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=3000, avg_degree=7.0, seed=11), 20, 8)
+    a = H.partition_vertices(ds.graph, m, seed=11)
+    p = H.split_chunks(ds.graph, a, n)
+    dims = [20, 32, 8]
+    m0 = H.init_model("gat", dims, seed=2, dtype=np.float32)
+    w0, a0 = [w.copy() for w in m0.weights], [x.copy() for x in m0.attn]
+    losses, snaps, _, _ = _run(p, ds, dims, epochs=1, model=m0)
+    ref = _oracle(p, a, ds, w0, a0, np.float32)
+    assert abs(losses[0] - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+    assert O.rel_err(snaps[0]["h1"], ref["h"][1]) < 1e-5
+    assert O.rel_err(snaps[0]["hL"], ref["h"][2]) < 1e-5
+    for l in range(2):
+        assert O.rel_err(snaps[0]["grads"][l], ref["grads"][l]) < 1e-5
+        assert O.rel_err(snaps[0]["attn_grads"][l], ref["attn_grads"][l]) < 1e-5
+        assert O.rel_err(snaps[0]["W"][l], ref["weights"][l]) < 1e-5
+        assert O.rel_err(snaps[0]["A"][l], ref["attn"][l]) < 1e-5
+    assert O.rel_err(snaps[0]["gh0"], ref["grad_h"][0]) < 1e-5
+    assert O.rel_err(snaps[0]["gh1"], ref["grad_h"][1]) < 1e-5
+
+
+def test_gat_tf32_within_contract_of_fp64_oracle():
+    """Production precision (q, p in 3xTF32; gradient GEMMs in TF32) against
+    the fp64 oracle, one epoch from the same state: 1e-3 (north star)."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=4000, avg_degree=9.0, seed=3), 32, 8)
+    a = H.partition_vertices(ds.graph, 2, seed=3)
+    p = H.split_chunks(ds.graph, a, 2)
+    dims = [32, 64, 8]
+    m0 = H.init_model("gat", dims, seed=7, dtype=np.float32)
+    w0 = [w.astype(np.float64) for w in m0.weights]
+    a0 = [x.astype(np.float64) for x in m0.attn]
+    losses, snaps, _, _ = _run(p, ds, dims, precision="tf32", epochs=1, model=m0)
+    ref = _oracle(p, a, ds, w0, a0, np.float64)
+    assert abs(losses[0] - ref["loss"]) <= 1e-3 * abs(ref["loss"])
+    assert O.rel_err(snaps[0]["hL"], ref["h"][2]) < 1e-3
+    for l in range(2):
+        assert O.rel_err(snaps[0]["grads"][l], ref["grads"][l]) < 1e-3
+        assert O.rel_err(snaps[0]["attn_grads"][l], ref["attn_grads"][l]) < 1e-3
+
+
+def test_gat_zero_in_degree_and_hub_segments():
+    """Destinations without in-edges get zero rows (src/engine.py:217-221);
+    a hub source with thousands of out-edges and a hub destination with
+    thousands of in-edges run through the warp-per-segment kernels."""
+    rng = np.random.default_rng(9)
+    V = 6000
+    src = np.concatenate([np.zeros(5000, np.int64), rng.integers(0, V, 12000),
+                          rng.integers(0, V, 5000)])
+    dst = np.concatenate([rng.integers(0, V // 2, 5000), rng.integers(0, V // 2, 12000),
+                          np.full(5000, 7, np.int64)])  # vertices >= V/2 (but 7) have no in-edges
+    g = H.from_edges(src, dst, V)
+    X = rng.standard_normal((V, 12))
+    labels = rng.integers(0, 4, V)
+    mask = rng.random(V) < 0.5
+    a = H.PartitionAssignment(owner=(np.arange(V) % 2).astype(np.int64), m=2)
+    p = H.split_chunks(g, a, 2)
+    ds = H.SynthDataset(graph=g, features=X, labels=labels, mask=mask)
+    dims = [12, 16, 4]
+    m0 = H.init_model("gat", dims, seed=4, dtype=np.float32)
+    w0, a0 = [w.copy() for w in m0.weights], [x.copy() for x in m0.attn]
+    losses, snaps, _, _ = _run(p, ds, dims, epochs=1, model=m0)
+    ref = _oracle(p, a, ds, w0, a0, np.float32)
+    assert np.all(snaps[0]["h1"][V // 2 + 1:] == 0)
+    assert abs(losses[0] - ref["loss"]) <= 1e-5 * abs(ref["loss"])
+    assert O.rel_err(snaps[0]["gh0"], ref["grad_h"][0]) < 1e-5
+    for l in range(2):
+        assert O.rel_err(snaps[0]["grads"][l], ref["grads"][l]) < 1e-5
+        assert O.rel_err(snaps[0]["attn_grads"][l], ref["attn_grads"][l]) < 1e-5
+
+
+def test_gat_width_must_be_multiple_of_four(golden_small):
+    ds, a, p = _small(golden_small)
+    dims = [8, 10, 4]
+    plan = H.plan_for_partition(p)
+    model = H.init_model("gat", dims, seed=5, dtype=np.float32)
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+    host.set_features(ds.features)
+    fleet = H.DeviceFleet(plan, dtype=np.float32, precision="fp32")
+    with pytest.raises(H.ChunktrainError, match="multiples of 4"):
+        H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
