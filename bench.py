@@ -206,19 +206,21 @@ def reference_cpu_sample(ds, dims, budget_edges=1_500_000, threads=None):
 # ---------------------------------------------------------------------------
 # timed epochs
 # ---------------------------------------------------------------------------
-def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed, rank=None):
+def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed, rank=None,
+               kind="gcn", features=None, labels=None):
     import paper_2311_14898_b200 as H
     from paper_2311_14898_b200 import _native as N
     dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count()) if rank is not None else 0
     host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement,
                        device=dev)
-    host.set_features(ds.features)
+    host.set_features(ds.features if features is None else features)
+    labels = ds.labels if labels is None else labels
     fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision, rank=rank,
                           devices=[dev] if rank is not None else None)
-    model = H.init_model("gcn", dims, seed=seed, lr=0.1, dtype=np.float32)
+    model = H.init_model(kind, dims, seed=seed, lr=0.1, dtype=np.float32)
     losses = []
     for _ in range(warmup):
-        losses.append(H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss)
+        losses.append(H.train_epoch(p, fleet, model, host, labels, ds.mask).loss)
     fleet.set_timing(timing)
     for d in fleet.devices:  # meters of the timed region only
         for k, v in d.counter_dict().items():
@@ -227,7 +229,7 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     N.call("ht_fleet_mark", fleet._handle, 0)
     t0 = time.perf_counter()
     for _ in range(steps):
-        losses.append(H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss)
+        losses.append(H.train_epoch(p, fleet, model, host, labels, ds.mask).loss)
     N.call("ht_fleet_mark", fleet._handle, 1)
     ms = C.c_double(0)
     N.call("ht_fleet_elapsed", fleet._handle, C.byref(ms))
@@ -235,9 +237,50 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     launches = N.lib().ht_launches() - l0
     stats = {w: fleet.kernel_stats(w) for w in range(4)} if timing else {}
     rep = fleet.transfer_report()
+    fleet.close()  # device memory back before the next measurement
     del host
     return {"ms_total": ms.value, "wall_s": wall, "losses": losses, "launches": launches,
-            "stats": stats, "report": rep, "fleet": fleet}
+            "stats": stats, "report": rep}
+
+
+GAT_DIMS = [256, 128, 128, 64]  # it-2004 / config 5 widths
+
+
+def gat_measure(p, plan, ds, steps, warmup, precision, seed, rank, slowest):
+    """BASELINE config 5's model (3-layer GAT 256-128-128-64) on the bench
+    graph: config 5's 41M-vertex graph needs ~190 GB of pinned host rows,
+    beyond one box's host memory, so the GAT path is measured on the same
+    2.4M-vertex graph (synthetic 256-wide features, 64 classes)."""
+    V = ds.graph.num_vertices
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((V, GAT_DIMS[0]), dtype=np.float32)
+    y = (np.asarray(ds.labels) % GAT_DIMS[-1]).astype(np.int64)
+    L = len(GAT_DIMS) - 1
+    E = ds.graph.num_edges
+    out = {"workload": f"3-layer GAT {'-'.join(map(str, GAT_DIMS))} on the bench graph "
+                       f"({V} V / {E} E), m=n=1, mode full",
+           "metric": METRIC.replace("GCN", "GAT"), "unit": "GTEPS"}
+    val = run_epochs(p, plan, ds, GAT_DIMS, "device", steps, warmup, precision, True, seed,
+                     rank=rank, kind="gat", features=X, labels=y)
+    ms_v = slowest(val["ms_total"]) / steps
+    e2e = run_epochs(p, plan, ds, GAT_DIMS, "host", steps, warmup, precision, True, seed,
+                     rank=rank, kind="gat", features=X, labels=y)
+    ms_e = slowest(e2e["ms_total"]) / steps
+    lf, msf, bf = val["stats"][0]
+    lb, msb, bb = val["stats"][1]
+    lg, msg, flops = val["stats"][2]
+    out.update({
+        "value": L * E / (ms_v / 1e3) / 1e9, "ms_per_step": ms_v,
+        "e2e": {"value": L * E / (ms_e / 1e3) / 1e9, "ms_per_step": ms_e},
+        "edge_kernels": {"fwd_ms_per_step": msf / steps, "bwd_ms_per_step": msb / steps,
+                         "fwd_gbs": bf / (msf / 1e3) / 1e9 if msf else None,
+                         "bwd_gbs": bb / (msb / 1e3) / 1e9 if msb else None,
+                         "share_of_step": (msf + msb) / val["ms_total"] if val["ms_total"] else None},
+        "gemm": {"ms_per_step": msg / steps, "tflops": flops / (msg / 1e3) / 1e12 if msg else None},
+        "gpu_launches": int(val["launches"]),
+        "losses": {"value": val["losses"][-1], "e2e": e2e["losses"][-1]},
+    })
+    return out
 
 
 def main():
@@ -250,6 +293,9 @@ def main():
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--only-value", action="store_true", help="profiling: HBM-resident run only")
+    ap.add_argument("--no-gat", action="store_true", help="skip the GAT (config 5 model) line")
+    ap.add_argument("--kind", default="gcn", choices=["gcn", "gat"],
+                    help="profiling: model of the --only-value run")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -313,6 +359,11 @@ def main():
             return hd.allreduce_max(ms)
         return ms
 
+    if args.only_value and args.kind == "gat":  # profiling aid
+        r = gat_measure(p, plan, ds, args.steps, args.warmup, args.precision, cfg["seed"], rk,
+                        slowest)
+        log(f"[bench] GAT: {json.dumps(r)}")
+        return
     # ---- value: HBM-resident vertex store ----
     with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk_v:
         val = run_epochs(p, plan, ds, dims, "device", args.steps, args.warmup, args.precision,
@@ -326,6 +377,12 @@ def main():
         e2e = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,
                          True, cfg["seed"], rank=rk)
     ms_e = slowest(e2e["ms_total"]) / args.steps
+    gat = None
+    if not args.no_gat:
+        with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk_g:
+            gat = gat_measure(p, plan, ds, args.steps, args.warmup, args.precision, cfg["seed"],
+                              rk, slowest)
+        gat["clocks"] = clk_g.summary()
     if rank != 0:
         dist.barrier()
         dist.destroy_process_group()
@@ -386,6 +443,7 @@ def main():
         "clocks": clk_e.summary(),
         "clocks_value_run": clk_v.summary(),
         "losses": {"value": val["losses"][-1], "e2e": e2e["losses"][-1]},
+        "gat": gat,
     }
     print(json.dumps(out), flush=True)
     if world > 1:

@@ -202,6 +202,7 @@ struct Device {
   // GAT staging (sized by ht_gat_epoch_begin): neighbour / destination
   // inputs, projections q / p, scores, backward rows and per-edge values
   DBuf g_hn, g_hd[2], g_q, g_p, g_els, g_gs, g_gp, g_al, g_gt, g_sgt, g_gq, g_gts, g_ghd, g_gin[2];
+  DBuf g_pgts;                         // per-piece g_t sums of split source segments
   DBuf g_cpart;                        // column partials of the attention gradients
   std::vector<int64_t> gA_off;         // attention gradients: gWall + gW_off[L] + gA_off[l]
   cudaEvent_t e_gcomp[2] = {nullptr, nullptr};
@@ -795,7 +796,7 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
       for (DBuf* b : {&w.W, &w.Wt, &w.Wp, &w.Wt_hi, &w.Wt_lo, &w.Wp_hi, &w.Wp_lo, &w.A}) b->release();
     for (DBuf* b : {&d.g_hn, &d.g_hd[0], &d.g_hd[1], &d.g_q, &d.g_p, &d.g_els, &d.g_gs, &d.g_gp,
                     &d.g_al, &d.g_gt, &d.g_sgt, &d.g_gq, &d.g_gts, &d.g_ghd, &d.g_gin[0],
-                    &d.g_gin[1], &d.g_cpart})
+                    &d.g_gin[1], &d.g_cpart, &d.g_pgts})
       b->release();
     for (cudaEvent_t e : {d.e_gcomp[0], d.e_gcomp[1]})
       if (e) cudaEventDestroy(e);
@@ -1774,15 +1775,21 @@ int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const floa
 }
 
 int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const float* AL,
-                   const float* GT, const float* a_src, int d, float* GQ, float* GTS) {
+                   const float* GT, const float* a_src, int d, float* GQ, float* GTS, float* part,
+                   float* pgts) {
   if (c.nn <= 0) return HT_OK;
   const int g = grid_for(c.nn);
   const int64_t* off = c.csr_off.as<int64_t>();
   const int32_t* dst = c.csr_dst.as<int32_t>();
   const int32_t* perm = c.csr_perm.as<int32_t>();
-  count_launch();
-#define GATS(NV) \
-  ht::gat::k_gat_src<NV><<<g, kThreads, 0, s>>>(off, dst, perm, c.nn, GS, AL, GT, a_src, d, GQ, GTS)
+  count_launch(1 + (c.bw_np ? 1 : 0) + (c.bw_nf ? 1 : 0));
+#define GATS(NV)                                                                                \
+  ht::gat::k_gat_src<NV><<<g, kThreads, 0, s>>>(off, dst, perm, c.nn, kSplit, GS, AL, GT, a_src, \
+                                                d, GQ, GTS);                                     \
+  if (c.bw_np)                                                                                  \
+    ht::gat::k_gat_src_pieces<NV><<<grid_for(c.bw_np), kThreads, 0, s>>>(                       \
+        c.bw_lo.as<int64_t>(), c.bw_hi.as<int64_t>(), c.bw_np, dst, perm, GS, AL, GT, a_src, d,  \
+        part, pgts)
   switch (nv_of(d)) {
     case 1: GATS(1); break;
     case 2: GATS(2); break;
@@ -1791,6 +1798,12 @@ int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const flo
   }
 #undef GATS
   CU(cudaGetLastError());
+  if (c.bw_nf) {
+    ht::gat::k_gat_src_fixup<<<grid_for(c.bw_nf), kThreads, 0, s>>>(
+        GQ, GTS, part, pgts, d, c.bw_seg.as<int64_t>(), c.bw_first.as<int64_t>(),
+        c.bw_cnt.as<int64_t>(), c.bw_nf);
+    CU(cudaGetLastError());
+  }
   return HT_OK;
 }
 
@@ -1996,6 +2009,9 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
     HT_TRY(d.g_gts.ensure(mn * 4));
     HT_TRY(d.g_ghd.ensure(mv * dmax * 4));
     HT_TRY(d.g_cpart.ensure((int64_t)kColBlocks * dmax * 4));
+    int64_t np = 1;
+    for (int j = 0; j < f->n; ++j) np = std::max(np, d.chunks[j].bw_np);
+    HT_TRY(d.g_pgts.ensure(np * 4));
     for (int s = 0; s < 2; ++s) {
       HT_TRY(d.g_hd[s].ensure(mv * dmax * 4));
       HT_TRY(d.g_gin[s].ensure(mv * dmax * 4));
@@ -2129,7 +2145,8 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, d.g_els.as<float>(), a_dst, d_out, slope,
                                   nullptr, d.g_gin[s].as<float>(), GS, GP, AL, GT,
                                   d.g_sgt.as<float>()));
-      HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>()));
+      HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
+                            d.partial.as<float>(), d.g_pgts.as<float>()));
       timer_end(f, d, tr, 1,
                 (double)c.ne * (28.0 + 12.0 * d_out) + (double)c.nv * (16.0 * d_out + 16.0) +
                     (double)c.nn * (4.0 * d_out + 12.0),

@@ -17,7 +17,9 @@
 //   k_gat_src     BWD, one warp per source u over its CSR out-edges:
 //                 gq_u = sum_e (alpha_e gs_{dst e} + g_t_e a_src) in edge
 //                 order (the np.add.at of src/engine.py:275/280), and
-//                 gts_u = sum_e g_t_e.
+//                 gts_u = sum_e g_t_e.  Power-law hubs (> 4096 out-edges)
+//                 are split into pieces (k_gat_src_pieces) summed in piece
+//                 order (k_gat_src_fixup), as in the GCN transposed path.
 //   k_wcolsum / k_colsum_reduce
 //                 out[c] += sum_r w_r X[r][c] (attention-vector gradients),
 //                 block partials reduced in a fixed order (deterministic).
@@ -89,6 +91,15 @@ __device__ __forceinline__ void axpy_rn(float4& acc, float a, const float4& x) {
 }
 
 __device__ __forceinline__ float leaky(float t, float slope) { return t > 0.f ? t : slope * t; }
+
+// acc += (a x + g b), the per-edge value rounded before the add
+__device__ __forceinline__ void edge_add(float4& acc, float a, const float4& x, float g,
+                                         const float4& b) {
+  acc.x = __fadd_rn(acc.x, __fadd_rn(__fmul_rn(a, x.x), __fmul_rn(g, b.x)));
+  acc.y = __fadd_rn(acc.y, __fadd_rn(__fmul_rn(a, x.y), __fmul_rn(g, b.y)));
+  acc.z = __fadd_rn(acc.z, __fadd_rn(__fmul_rn(a, x.z), __fmul_rn(g, b.z)));
+  acc.w = __fadd_rn(acc.w, __fadd_rn(__fmul_rn(a, x.w), __fmul_rn(g, b.w)));
+}
 
 // out[r] = X[r] . a   (one warp per row)
 template <int NV>
@@ -231,12 +242,62 @@ __global__ void __launch_bounds__(256) k_gat_dst(
   }
 }
 
+// gq / gts contribution of CSR edges [e0, e1) of one source (one warp):
+// per edge (alpha gs_dst + g_t a_src), added in edge order; four rows in
+// flight.
+template <int NV>
+__device__ __forceinline__ void src_sum(float4 (&acc)[NV], float& gts, int64_t e0, int64_t e1,
+                                        const int32_t* __restrict__ dst,
+                                        const int32_t* __restrict__ perm,
+                                        const float* __restrict__ GS, const float* __restrict__ AL,
+                                        const float* __restrict__ GT, const float4 (&as)[NV],
+                                        int d, int d4, int lane) {
+  for (int64_t base = e0; base < e1; base += kW) {
+    const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
+    int my_d = 0;
+    float my_a = 0.f, my_t = 0.f;
+    if (lane < cnt) {
+      my_d = __ldg(dst + base + lane);
+      const int32_t pe = __ldg(perm + base + lane);
+      my_a = __ldg(AL + pe);
+      my_t = __ldg(GT + pe);
+      gts += my_t;
+    }
+    int k = 0;
+    for (; k + 4 <= cnt; k += 4) {
+      float4 x[4][NV];
+      float a[4], g[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = __shfl_sync(0xffffffffu, my_d, k + u);
+        a[u] = __shfl_sync(0xffffffffu, my_a, k + u);
+        g[u] = __shfl_sync(0xffffffffu, my_t, k + u);
+        load4<NV>(x[u], GS + (int64_t)r * d, d4, lane);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int t = 0; t < NV; ++t) edge_add(acc[t], a[u], x[u][t], g[u], as[t]);
+    }
+    for (; k < cnt; ++k) {
+      const int r = __shfl_sync(0xffffffffu, my_d, k);
+      const float a = __shfl_sync(0xffffffffu, my_a, k);
+      const float g = __shfl_sync(0xffffffffu, my_t, k);
+      float4 x[NV];
+      load4<NV>(x, GS + (int64_t)r * d, d4, lane);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) edge_add(acc[t], a, x[t], g, as[t]);
+    }
+  }
+}
+
 // One warp per source segment of a chunk's CSR view: dst = chunk-local
 // destination rows of GS, perm = CSC edge id (index into AL / GT).
+// Segments longer than `split` edges are left to k_gat_src_pieces.
 template <int NV>
 __global__ void __launch_bounds__(256) k_gat_src(
     const int64_t* __restrict__ off, const int32_t* __restrict__ dst,
-    const int32_t* __restrict__ perm, int64_t nseg, const float* __restrict__ GS,
+    const int32_t* __restrict__ perm, int64_t nseg, int64_t split, const float* __restrict__ GS,
     const float* __restrict__ AL, const float* __restrict__ GT, const float* __restrict__ a_src,
     int d, float* __restrict__ GQ, float* __restrict__ GTS) {
   const int lane = threadIdx.x & 31;
@@ -246,40 +307,61 @@ __global__ void __launch_bounds__(256) k_gat_src(
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nseg; u += nw) {
     const int64_t e0 = off[u], e1 = off[u + 1];
+    if (e1 - e0 > split) continue;
     float4 acc[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     float gts = 0.f;
-    for (int64_t base = e0; base < e1; base += kW) {
-      const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
-      int my_d = 0;
-      float my_a = 0.f, my_t = 0.f;
-      if (lane < cnt) {
-        my_d = __ldg(dst + base + lane);
-        const int32_t pe = __ldg(perm + base + lane);
-        my_a = AL[pe];
-        my_t = GT[pe];
-        gts += my_t;
-      }
-      for (int k = 0; k < cnt; ++k) {
-        const int r = __shfl_sync(0xffffffffu, my_d, k);
-        const float a = __shfl_sync(0xffffffffu, my_a, k);
-        const float g = __shfl_sync(0xffffffffu, my_t, k);
-        float4 x[NV];
-        load4<NV>(x, GS + (int64_t)r * d, d4, lane);
-#pragma unroll
-        for (int t = 0; t < NV; ++t) {
-          // per-edge value (alpha gs + g_t a_src), then the add
-          acc[t].x = __fadd_rn(acc[t].x, __fadd_rn(__fmul_rn(a, x[t].x), __fmul_rn(g, as[t].x)));
-          acc[t].y = __fadd_rn(acc[t].y, __fadd_rn(__fmul_rn(a, x[t].y), __fmul_rn(g, as[t].y)));
-          acc[t].z = __fadd_rn(acc[t].z, __fadd_rn(__fmul_rn(a, x[t].z), __fmul_rn(g, as[t].z)));
-          acc[t].w = __fadd_rn(acc[t].w, __fadd_rn(__fmul_rn(a, x[t].w), __fmul_rn(g, as[t].w)));
-        }
-      }
-    }
+    src_sum<NV>(acc, gts, e0, e1, dst, perm, GS, AL, GT, as, d, d4, lane);
     store4<NV>(GQ + u * (int64_t)d, acc, d4, lane);
     gts = warp_sum(gts);
     if (lane == 0) GTS[u] = gts;
+  }
+}
+
+// pieces [lo, hi) of long source segments -> partial rows / gts partials
+template <int NV>
+__global__ void __launch_bounds__(256) k_gat_src_pieces(
+    const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, int64_t np,
+    const int32_t* __restrict__ dst, const int32_t* __restrict__ perm,
+    const float* __restrict__ GS, const float* __restrict__ AL, const float* __restrict__ GT,
+    const float* __restrict__ a_src, int d, float* __restrict__ part, float* __restrict__ pgts) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  float4 as[NV];
+  load4<NV>(as, a_src, d4, lane);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < np; q += nw) {
+    float4 acc[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float gts = 0.f;
+    src_sum<NV>(acc, gts, lo[q], hi[q], dst, perm, GS, AL, GT, as, d, d4, lane);
+    store4<NV>(part + q * (int64_t)d, acc, d4, lane);
+    gts = warp_sum(gts);
+    if (lane == 0) pgts[q] = gts;
+  }
+}
+
+// long segment s: GQ / GTS = sum of its pieces in piece order
+__global__ void __launch_bounds__(256) k_gat_src_fixup(
+    float* __restrict__ GQ, float* __restrict__ GTS, const float* __restrict__ part,
+    const float* __restrict__ pgts, int d, const int64_t* __restrict__ seg,
+    const int64_t* __restrict__ first, const int64_t* __restrict__ cnt, int64_t nf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < nf; f += nw) {
+    const int64_t q0 = first[f], qn = cnt[f];
+    for (int c = lane; c < d; c += kW) {
+      float s = 0.f;
+      for (int64_t q = 0; q < qn; ++q) s = __fadd_rn(s, part[(q0 + q) * d + c]);
+      GQ[seg[f] * (int64_t)d + c] = s;
+    }
+    if (lane == 0) {
+      float s = 0.f;
+      for (int64_t q = 0; q < qn; ++q) s += pgts[q0 + q];
+      GTS[seg[f]] = s;
+    }
   }
 }
 

@@ -265,7 +265,7 @@ class DeviceFleet:
             ords = (C.c_int * self.m)(*self.ordinals)
             N.call("ht_fleet_create", self.m, self.n, ords, _MODE_ID[self.mode], flush, C.byref(h))
         self._handle = h.value
-        weakref.finalize(self, N.lib().ht_fleet_destroy, self._handle)
+        self._finalizer = weakref.finalize(self, N.lib().ht_fleet_destroy, self._handle)
         keep = []
 
         def arr(a):
@@ -329,6 +329,12 @@ class DeviceFleet:
         c = C.c_int64(0)
         N.call("ht_fleet_capacity", self._handle, i, C.byref(c))
         return int(c.value)
+
+    def close(self) -> None:
+        """Release the fleet's device buffers now (otherwise at garbage
+        collection)."""
+        if self._handle is not None and self._finalizer.alive:
+            self._finalizer()
 
     # -- meters ---------------------------------------------------------------
     def _meter_fwd(self, j: int, row_bytes: int):

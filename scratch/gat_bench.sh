@@ -1,0 +1,6 @@
+#!/bin/bash
+OUT=gpurun_out
+timeout 900 python bench.py --no-cpu-baseline > $OUT/bench_gat.json 2> $OUT/bench_gat.err; echo "rc $?" >> $OUT/bench_gat.err
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed \
+  --clock-control none --csv --log-file $OUT/gat_launches.csv \
+  timeout 600 python bench.py --only-value --kind gat --steps 1 --warmup 1 --no-cpu-baseline > $OUT/gat_prof.log 2>&1
