@@ -154,14 +154,23 @@ def dedup_report():
             "volumes": {"v_ori": v.v_ori, "v_p2p": v.v_p2p, "v_ru": v.v_ru}}
 
 
-def host_bytes_per_epoch(plan, dims, mode="full"):
+def host_bytes_per_epoch(plan, dims, mode="full", cached=False, kind="gcn"):
     """Host<->GPU bytes of one epoch from the plan (SURVEY 8(d) formulas,
     fp32): neighbour loads/flushes + destination + checkpoint rows, plus the
-    loss gradient rows this path writes to host.grad_h[L]."""
+    loss gradient rows this path writes to host.grad_h[L].  With the HBM
+    owner cache the host is read once (the owned h^0 rows) and written once
+    per produced row: h^{l+1} and agg^l per forward layer, grad_h^l per
+    backward layer, grad_h^L after the loss."""
     import paper_2311_14898_b200 as H
     L = len(dims) - 1
-    pred = H.predicted_transfers(plan, mode)
     V = int(plan.owner.shape[0])
+    if cached:
+        h2d = 4 * V * dims[0] + V * 9
+        d2h = 4 * V * (sum(dims[1:]) + sum(dims[:L]) + dims[L])
+        if kind == "gcn":
+            d2h += 4 * V * sum(dims[:L])
+        return h2d, d2h
+    pred = H.predicted_transfers(plan, mode)
     h2d = d2h = 0
     for l in range(L):
         h2d += 4 * (pred["fwd_h2d_rows"] * dims[l] + V * (dims[l] + dims[l + 1]))
@@ -237,10 +246,11 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     launches = N.lib().ht_launches() - l0
     stats = {w: fleet.kernel_stats(w) for w in range(4)} if timing else {}
     rep = fleet.transfer_report()
+    cache = fleet.cache_active
     fleet.close()  # device memory back before the next measurement
     del host
     return {"ms_total": ms.value, "wall_s": wall, "losses": losses, "launches": launches,
-            "stats": stats, "report": rep}
+            "stats": stats, "report": rep, "cache": cache}
 
 
 GAT_DIMS = [256, 128, 128, 64]  # it-2004 / config 5 widths
@@ -271,7 +281,12 @@ def gat_measure(p, plan, ds, steps, warmup, precision, seed, rank, slowest):
     lg, msg, flops = val["stats"][2]
     out.update({
         "value": L * E / (ms_v / 1e3) / 1e9, "ms_per_step": ms_v,
-        "e2e": {"value": L * E / (ms_e / 1e3) / 1e9, "ms_per_step": ms_e},
+        "e2e": {"value": L * E / (ms_e / 1e3) / 1e9, "ms_per_step": ms_e,
+                "hbm_owner_cache": bool(e2e["cache"]),
+                "h2d_bytes_per_step": host_bytes_per_epoch(plan, GAT_DIMS, cached=e2e["cache"],
+                                                           kind="gat")[0] if e2e["cache"] else None,
+                "d2h_bytes_per_step": host_bytes_per_epoch(plan, GAT_DIMS, cached=e2e["cache"],
+                                                           kind="gat")[1] if e2e["cache"] else None},
         "edge_kernels": {"fwd_ms_per_step": msf / steps, "bwd_ms_per_step": msb / steps,
                          "fwd_gbs": bf / (msf / 1e3) / 1e9 if msf else None,
                          "bwd_gbs": bb / (msb / 1e3) / 1e9 if msb else None,
@@ -387,7 +402,9 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
         return
-    h2d, d2h = host_bytes_per_epoch(plan, dims)
+    cached = e2e["cache"]
+    h2d, d2h = host_bytes_per_epoch(plan, dims, cached=cached)
+    plan_h2d, plan_d2h = host_bytes_per_epoch(plan, dims)
     base_h2d, base_d2h = host_bytes_per_epoch(plan, dims, "baseline")
     dedup = dedup_report()
     pcie = pcie_peaks()
@@ -420,11 +437,13 @@ def main():
         "data": "synthetic (seeded clustered power-law graph, random-init Glorot weights)",
         "config": config,
         "e2e": {"value": e2e_v, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e,
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e, "hbm_owner_cache": bool(cached),
                 "pcie_gbs": (h2d + d2h) / (ms_e / 1e3) / 1e9,
                 "transfer_kernel_ms_per_step": mst / args.steps},
         "epoch_s": {"hbm_resident": ms_v / 1e3, "host_resident": ms_e / 1e3},
-        "host_gb_per_epoch": {"dedup_full": (h2d + d2h) / 1e9,
+        "host_gb_per_epoch": {"measured_path": (h2d + d2h) / 1e9,
+                              "hbm_owner_cache": bool(cached),
+                              "dedup_full_plan": (plan_h2d + plan_d2h) / 1e9,
                               "non_dedup_baseline_plan": (base_h2d + base_d2h) / 1e9},
         "gpu_launches": int(val["launches"]),
         "gpu_launches_e2e": int(e2e["launches"]),
@@ -434,6 +453,7 @@ def main():
         "cpu_baseline": cpu,
         "roofline_pcie": {
             "bound": "pcie", "what": "all host<->GPU bytes of the e2e epoch / epoch time",
+            "d2h_bound_frac": (d2h / (ms_e / 1e3) / 1e9) / pcie[1] if pcie else None,
             "achieved": (h2d + d2h) / (ms_e / 1e3) / 1e9, "unit": "GB/s",
             "peak": pcie_bidir, "peak_source": "measured (copy engines, both directions at once)",
             "frac": ((h2d + d2h) / (ms_e / 1e3) / 1e9) / pcie_bidir if pcie_bidir else None,

@@ -188,6 +188,14 @@ int ht_dest_rows(ht_fleet* f, int op, int batch, int dim, int elem_size,
 #define HT_PREC_FP32 0   /* SIMT FP32 GEMMs: FP32 validation mode (1e-5)      */
 #define HT_PREC_TF32 1   /* tcgen05 TF32, 3xTF32 for z = agg.W (1e-3)         */
 
+/* HBM owner cache: mode 0 off, 1 on (error if the
+ * plan or free HBM does not allow it), 2 auto.  With it each device keeps
+ * HBM mirrors of the host rows it owns (h^l, agg^l, grad_h^l) and the layer
+ * calls read those instead of the host arrays; every produced row is still
+ * written through to the host arrays.  Decided at each ht_epoch_begin;
+ * ht_fleet_cache_state reports whether every local device uses it. */
+int ht_fleet_set_cache(ht_fleet* f, int mode);
+int ht_fleet_cache_state(ht_fleet* f, int* on);
 /* Zero the per-device weight-gradient accumulators (engine.py:441-448). */
 int ht_epoch_begin(ht_fleet* f, int L, const int* dims);
 /* One forward layer over all batches (engine.py:409-434): dedup comm,

@@ -142,6 +142,10 @@ struct DevChunk {
   // CSR edge; uploaded by the first GAT epoch
   DBuf csc_loc, csr_perm;            // int32 [ne], int32 [ne]
   bool gat_ready = false;
+  // HBM owner cache: the destination rows are the contiguous mirror rows
+  // [dest_m0, dest_m0 + nv); h2d / flush rows as mirror positions
+  int64_t dest_m0 = -1;
+  DBuf h2d_m, flush_m;               // int64 [h2d.n], int64 [flush.n]
 };
 
 struct LayerW {
@@ -206,6 +210,17 @@ struct Device {
   DBuf g_cpart;                        // column partials of the attention gradients
   std::vector<int64_t> gA_off;         // attention gradients: gWall + gW_off[L] + gA_off[l]
   cudaEvent_t e_gcomp[2] = {nullptr, nullptr};
+  // HBM owner cache: HBM mirrors of the host rows this
+  // device owns - h^l (l < L), agg^l (GCN), grad_h^l (l <= L) - read by the
+  // layer drivers instead of the host; every row produced is written
+  // through to the host store, which stays the reference's complete copy.
+  bool cache = false;
+  int64_t mcount = 0;                  // owned rows (mirror rows)
+  std::vector<int64_t> mrows;          // host row of each mirror position, ascending
+  DBuf mrows_d;                        // same, on the device
+  CopyList own;                        // runs of (host row, mirror position)
+  std::vector<DBuf> mh, ma, mg;
+  cudaEvent_t e_up = nullptr, e_mg = nullptr;
 };
 
 }  // namespace
@@ -226,6 +241,8 @@ struct ht_fleet {
   int64_t loss_count = 0;
   bool prefetch = true;  // checkpoint prefetch (HT_CKPT_PREFETCH=0 disables)
   bool gat = false;      // buffers sized by ht_gat_epoch_begin
+  int cache_req = 0;     // HBM owner cache: 0 off, 1 on (fail if impossible), 2 auto
+  bool cache_ok = false; // the plan admits the cache (p2p/full, contiguous dest rows)
   int64_t nrows = 0;  // host rows addressed by the plan (max vertex id + 1)
   // rank mode (one process per GPU): index of the local device, barrier
   // sequence, device array of every rank's barrier counter
@@ -382,7 +399,11 @@ int launch_acc(cudaStream_t s, int elem, void* dst, void* src, const int64_t* di
   if (rows <= 0) return HT_OK;
   const int g = grid_for(rows);
   count_launch();
-  if (elem == 4)
+  const uintptr_t al = (uintptr_t)dst | (uintptr_t)src;
+  if (elem == 4 && d % 4 == 0 && (al & 15) == 0)
+    ht::k_acc_rows4<<<grid_for((rows + 1) / 2), kThreads, 0, s>>>(
+        (float*)dst, (float*)src, didx, sidx, first, rows, d, zero_src, sbase);
+  else if (elem == 4)
     ht::k_acc_rows<float><<<g, kThreads, 0, s>>>((float*)dst, (float*)src, didx, sidx, first, rows,
                                                 d, zero_src, sbase);
   else
@@ -772,7 +793,7 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
       for (auto* b : {&c.nbr_slot, &c.dest_rows, &c.csc_off, &c.csc_slot, &c.csc_w, &c.csr_off,
                       &c.csr_dst, &c.csr_w, &c.fw_lo, &c.fw_hi, &c.fw_seg, &c.fw_first, &c.fw_cnt,
                       &c.bw_lo, &c.bw_hi, &c.bw_seg, &c.bw_first, &c.bw_cnt, &c.csc_loc,
-                      &c.csr_perm})
+                      &c.csr_perm, &c.h2d_m, &c.flush_m})
         b->release();
       for (CopyList* cl : {&c.h2d, &c.flush, &c.base_bwd})
         cl->src.release(), cl->dst.release(), cl->flag.release();
@@ -798,8 +819,11 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
                     &d.g_al, &d.g_gt, &d.g_sgt, &d.g_gq, &d.g_gts, &d.g_ghd, &d.g_gin[0],
                     &d.g_gin[1], &d.g_cpart, &d.g_pgts})
       b->release();
-    for (cudaEvent_t e : {d.e_gcomp[0], d.e_gcomp[1]})
+    for (cudaEvent_t e : {d.e_gcomp[0], d.e_gcomp[1], d.e_up, d.e_mg})
       if (e) cudaEventDestroy(e);
+    for (auto* v : {&d.mh, &d.ma, &d.mg})
+      for (auto& b : *v) b.release();
+    d.mrows_d.release();
     if (d.wpin) cudaFreeHost(d.wpin);
     if (d.lpin) cudaFreeHost(d.lpin);
     if (d.stream) cudaStreamDestroy(d.stream);
@@ -969,6 +993,55 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
       }
     }
   }
+  // HBM owner cache structure: mirror rows = the owned rows (the union of
+  // the destination sets, ascending); every destination set must be a
+  // contiguous mirror range and every host-loaded row an owned row
+  f->cache_ok = !base;
+  for (int i = 0; i < m && f->cache_ok; ++i) {
+    Device& d = f->dev[i];
+    if (!d.local) continue;
+    d.mrows.clear();
+    for (int j = 0; j < n; ++j) {
+      if (!f->sets[i][j].has_dest) { f->cache_ok = false; break; }
+      d.mrows.insert(d.mrows.end(), f->sets[i][j].dest.begin(), f->sets[i][j].dest.end());
+    }
+    std::sort(d.mrows.begin(), d.mrows.end());
+    d.mrows.erase(std::unique(d.mrows.begin(), d.mrows.end()), d.mrows.end());
+    d.mcount = (int64_t)d.mrows.size();
+    auto pos_of = [&](int64_t v, int64_t* out) {
+      auto it = std::lower_bound(d.mrows.begin(), d.mrows.end(), v);
+      if (it == d.mrows.end() || *it != v) return false;
+      *out = it - d.mrows.begin();
+      return true;
+    };
+    for (int j = 0; j < n && f->cache_ok; ++j) {
+      HostSets& h = f->sets[i][j];
+      DevChunk& c = d.chunks[j];
+      c.dest_m0 = -1;
+      if (!h.dest.empty()) {
+        int64_t p0;
+        if (!pos_of(h.dest[0], &p0) || p0 + (int64_t)h.dest.size() > d.mcount ||
+            !std::equal(h.dest.begin(), h.dest.end(), d.mrows.begin() + p0)) {
+          f->cache_ok = false;
+          break;
+        }
+        c.dest_m0 = p0;
+      } else {
+        c.dest_m0 = 0;
+      }
+      const auto& rows = f->mode == HT_MODE_FULL ? h.load : h.owned;
+      std::vector<int64_t> pm(rows.size());
+      for (size_t q = 0; q < rows.size(); ++q)
+        if (!pos_of(rows[q], &pm[q])) { f->cache_ok = false; break; }
+      if (f->cache_ok) HT_TRY(upload(c.h2d_m, pm, d.stream));
+    }
+    if (!f->cache_ok) break;
+    HT_TRY(upload(d.mrows_d, d.mrows, d.stream));
+    std::vector<int64_t> pos(d.mcount);
+    std::iota(pos.begin(), pos.end(), 0);
+    make_runs(d.own, d.mrows, pos, nullptr);
+  }
+
   // owner-side push and flush lists
   if (!base) {
     std::vector<uint8_t> flushed;
@@ -1008,6 +1081,15 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         }
         HT_TRY(upload_list(c.flush, slot, fl, s, &first));
         make_runs(c.flush, fl, slot, &first);
+        if (f->cache_ok) {  // flush rows as mirror positions
+          std::vector<int64_t> fm(fl.size());
+          for (size_t q = 0; q < fl.size(); ++q) {
+            auto it = std::lower_bound(d.mrows.begin(), d.mrows.end(), fl[q]);
+            if (it == d.mrows.end() || *it != fl[q]) { f->cache_ok = false; break; }
+            fm[q] = it - d.mrows.begin();
+          }
+          HT_TRY(upload(c.flush_m, fm, s));
+        }
       }
     }
   }
@@ -1082,7 +1164,8 @@ int stage_batch(ht_fleet* f, int j, const void* host_rows_dev) {
 
 // push views (device-resident, per device in d.se at row stride dim) to the
 // owners, then flush.  assume_zero: first flush of a row stores.
-int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero) {
+// layer >= 0 and the device caches: flush into its grad mirror of `layer`
+int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero, int layer = -1) {
   const int dim = f->dim;
   if (f->mode == HT_MODE_BASELINE) {
     // host_grad[N_ij] += view_i in ascending device order
@@ -1117,7 +1200,13 @@ int push_flush(ht_fleet* f, int j, void* host_grad_dev, bool assume_zero) {
     const CopyList& fl = c.flush;
     const int64_t rb = (int64_t)dim * f->elem;
     const bool lastb = j == f->n - 1;
-    if (assume_zero && fl.dma) {
+    if (layer >= 0 && d.cache) {
+      // mirror zeroed at layer start: first flushes store, re-flushes add;
+      // the host copy is written through once per layer
+      HT_TRY(launch_acc(d.stream, f->elem, d.mg[layer].p, d.grad.p, c.flush_m.as<int64_t>(),
+                        fl.src.as<int64_t>(), assume_zero ? fl.flag.as<uint8_t>() : nullptr, fl.n,
+                        dim, 1));
+    } else if (assume_zero && fl.dma) {
       // every row is a first flush (a store): copy engines, chunked so the
       // next layer can start loading finished chunks
       for (int g = 0; g < kChunks; ++g) {
@@ -1263,6 +1352,26 @@ int check_chunks(ht_fleet* f) {
   return HT_OK;
 }
 
+// HBM owner cache: owned rows of a host array -> mirror (on `s`)
+int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
+                 int64_t rb) {
+  if (d.own.dma)
+    return xfer(s, d.own, false, const_cast<void*>(host), rb, mirror, rb, rb, 0, f->nrows);
+  return launch_copy(s, mirror, host, nullptr, d.mrows_d.as<int64_t>(), d.mcount, rb, rb, rb, 0,
+                     kHostGrid);
+}
+
+// HBM owner cache: write a mirror through to the host rows (on tout, after
+// everything enqueued so far on the compute stream)
+int cache_writeback(ht_fleet* f, Device& d, void* host, const float* mirror, int64_t rb) {
+  HT_TRY(ev_rec(d.e_mg, d.stream));
+  HT_TRY(ev_wait(d.tout, d.e_mg));
+  if (d.own.dma)
+    return xfer(d.tout, d.own, true, host, rb, const_cast<float*>(mirror), rb, rb, 0, f->nrows);
+  return launch_copy(d.tout, host, mirror, d.mrows_d.as<int64_t>(), nullptr, d.mcount, rb, rb, rb,
+                     0, kHostGrid);
+}
+
 // K6, early: reload the checkpoint rows of `layer` into their per-layer
 // device buffer on the low-priority prefetch stream, chunk by chunk as the
 // stores land.  The backward then reads them from HBM.
@@ -1289,7 +1398,7 @@ int prefetch_checkpoints(ht_fleet* f, Device& d, int layer, void* aout, int64_t 
 
 // extra_grad: floats of further parameter gradients kept behind the weight
 // gradients in the (IPC-shared) accumulator (GAT attention vectors)
-int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad) {
+int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bool gat) {
   if (!f->finalized) return fail(HT_ESTATE, "fleet not finalized");
   HT_TRY(check_chunks(f));
   HT_TRY(sync_all(f));
@@ -1332,7 +1441,37 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad) {
     HT_TRY(d.partial.ensure(np * dmax * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
-    if (f->prefetch) {
+    // HBM owner cache: decided per epoch (requested mode, plan, free HBM)
+    d.cache = false;
+    if (f->cache_req != 0) {
+      if (!f->cache_ok) {
+        if (f->cache_req == 1)
+          return fail(HT_EINVAL, "HBM owner cache needs mode p2p/full and destination sets that "
+                                 "are contiguous ranges of each device's owned rows");
+      } else {
+        int64_t per_row = 0;
+        for (int l = 0; l < L; ++l) per_row += dims[l] * (gat ? 1 : 2);  // h (+ agg)
+        for (int l = 0; l <= L; ++l) per_row += dims[l];                // grad
+        const int64_t need = d.mcount * per_row * 4;
+        size_t fr = 0, tot = 0;
+        CU(cudaMemGetInfo(&fr, &tot));
+        const bool fits = need + ((int64_t)4 << 30) <= (int64_t)fr;
+        if (!fits && f->cache_req == 1)
+          return fail(HT_ENOMEM, "HBM owner cache needs %lld bytes, %lld free", (long long)need,
+                      (long long)fr);
+        d.cache = fits;
+      }
+    }
+    if (d.cache) {
+      d.mh.resize(L);
+      d.ma.resize(gat ? 0 : L);
+      d.mg.resize(L + 1);
+      for (int l = 0; l < L; ++l) HT_TRY(d.mh[l].ensure(std::max<int64_t>(1, d.mcount) * dims[l] * 4));
+      for (int l = 0; l < (gat ? 0 : L); ++l)
+        HT_TRY(d.ma[l].ensure(std::max<int64_t>(1, d.mcount) * dims[l] * 4));
+      for (int l = 0; l <= L; ++l) HT_TRY(d.mg[l].ensure(std::max<int64_t>(1, d.mcount) * dims[l] * 4));
+    }
+    if (f->prefetch && !d.cache) {
       if ((int)d.ck.size() < L) d.ck.resize(L);
       if ((int)d.e_ck.size() < L) d.e_ck.resize(L, nullptr);
       for (int l = 0; l < L; ++l)
@@ -1358,8 +1497,26 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad) {
 
 }  // namespace
 
+extern "C" int ht_fleet_set_cache(ht_fleet* f, int mode) {
+  if (mode < 0 || mode > 2) return fail(HT_EINVAL, "cache mode must be 0 (off), 1 (on) or 2 (auto)");
+  f->cache_req = mode;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_cache_state(ht_fleet* f, int* on) {
+  *on = 1;
+  int any = 0;
+  for (auto& d : f->dev)
+    if (d.local) {
+      any = 1;
+      if (!d.cache) *on = 0;
+    }
+  if (!any) *on = 0;
+  return HT_OK;
+}
+
 extern "C" int ht_epoch_begin(ht_fleet* f, int L, const int* dims) {
-  HT_TRY(epoch_begin_impl(f, L, dims, 0));
+  HT_TRY(epoch_begin_impl(f, L, dims, 0, false));
   f->gat = false;
   return HT_OK;
 }
@@ -1391,6 +1548,18 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       if (!d.local) continue;  // rank mode: a peer process drives it
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
+      if (d.cache) {  // owned rows come from the HBM mirror (compute stream)
+        if (layer == 0 && j == 0) {
+          HT_TRY(cache_upload(f, d, d.tin, hin, d.mh[0].as<float>(), rbi));
+          HT_TRY(ev_rec(d.e_up, d.tin));
+          HT_TRY(ev_wait(d.stream, d.e_up));
+        }
+        for (auto& o : f->dev) HT_TRY(ev_wait(d.stream, o.e_fetch));  // peers done with our slots
+        HT_TRY(launch_copy(d.stream, d.value.p, d.mh[layer].p, c.h2d.dst.as<int64_t>(),
+                           c.h2d_m.as<int64_t>(), c.h2d.n, rbi, rbi, rbi));
+        HT_TRY(ev_rec(d.e_in, d.stream));
+        continue;
+      }
       if (d.fwd_count > 0) {  // slots of the previous batch no longer read
         HT_TRY(ev_wait(d.tin, d.e_agg));
         for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_fetch));
@@ -1442,8 +1611,9 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
       const int s = (int)(d.fwd_count & 1);
-      if (d.fwd_count >= 2) HT_TRY(ev_wait(d.stream, d.e_out[s]));  // staging set s drained
-      float* agg = d.fa[s].as<float>();
+      if (d.fwd_count >= 2 && !d.cache) HT_TRY(ev_wait(d.stream, d.e_out[s]));  // staging set s drained
+      // cache: the aggregation and h rows land in their mirrors directly
+      float* agg = d.cache ? d.ma[layer].as<float>() + c.dest_m0 * d_in : d.fa[s].as<float>();
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
       HT_TRY(launch_seg(d.stream, agg, d.value.as<float>(), d_in, d_in, c.csc_off.as<int64_t>(),
@@ -1452,7 +1622,9 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nv * (4.0 * d_in + 4.0),
                 d.stream);
       HT_TRY(ev_rec(d.e_agg, d.stream));
-      float* hdst = last ? d.hL.as<float>() + d.hL_off[j] * d_out : d.fb[s].as<float>();
+      float* hdst = last     ? d.hL.as<float>() + d.hL_off[j] * d_out
+                    : d.cache ? d.mh[layer + 1].as<float>() + c.dest_m0 * d_out
+                              : d.fb[s].as<float>();
       LayerW& w = d.lw[layer];
       const int64_t* rows = c.dest_rows.as<int64_t>();
       const bool lastb = j == f->n - 1;
@@ -1510,7 +1682,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
           for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
       }
       HT_TRY(ev_rec(d.e_out[s], d.tout));
-      if (lastb && f->prefetch) HT_TRY(prefetch_checkpoints(f, d, layer, aout, rbi));
+      if (lastb && f->prefetch && !d.cache) HT_TRY(prefetch_checkpoints(f, d, layer, aout, rbi));
       d.fwd_count++;
     }
   }
@@ -1548,10 +1720,15 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
         count_launch();
         ht::k_loss<<<blocks, 256, 0, d.stream>>>(
             d.hL.as<float>() + d.hL_off[j] * d_last, c.nv, d_last, d.labels.as<int64_t>(),
-            d.mask.as<uint8_t>(), c.dest_rows.as<int64_t>(), (float*)gout, (float)count,
-            d.loss_part.as<double>() + (int64_t)j * blocks);
+            d.mask.as<uint8_t>(), c.dest_rows.as<int64_t>(),
+            d.cache ? d.mg[f->L].as<float>() : (float*)gout, d.cache ? c.dest_m0 : -1,
+            (float)count, d.loss_part.as<double>() + (int64_t)j * blocks);
         CU(cudaGetLastError());
       }
+    if (d.cache) {  // grad_h[L] rows live in the mirror; write them through
+      if (count <= 0) CU(cudaMemsetAsync(d.mg[f->L].p, 0, d.mcount * (int64_t)d_last * 4, d.stream));
+      HT_TRY(cache_writeback(f, d, gout, d.mg[f->L].as<float>(), (int64_t)d_last * 4));
+    }
     HT_TRY(ev_rec(d.e_loss, d.stream));
   }
   if (loss) return ht_loss_value(f, loss);
@@ -1594,6 +1771,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
     if (!d.lw[layer].valid) HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
     if (f->mode != HT_MODE_BASELINE)  // begin_backward_layer: zeroed gradient slots
       CU(cudaMemsetAsync(d.grad.p, 0, d.cap * rbi, d.stream));
+    if (d.cache) CU(cudaMemsetAsync(d.mg[layer].p, 0, d.mcount * rbi, d.stream));
   }
   for (int j = 0; j < f->n; ++j) {
     for (int i = 0; i < f->m; ++i) {
@@ -1604,6 +1782,10 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       const int s = (int)(d.bwd_count & 1);
       const int64_t* rows = c.dest_rows.as<int64_t>();
       float *A = d.ba[s].as<float>(), *G = d.bb[s].as<float>();
+      if (d.cache) {  // checkpoint and gradient rows straight from the mirrors
+        A = d.ma[layer].as<float>() + c.dest_m0 * d_in;
+        G = d.mg[layer + 1].as<float>() + c.dest_m0 * d_out;
+      } else {
       // K6 on tin: checkpoint rows (ready since the forward), then the
       // destination gradients (ready once the layer above has flushed)
       if (d.bwd_count >= 2) HT_TRY(ev_wait(d.tin, d.e_bcomp[s]));
@@ -1648,6 +1830,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // K7 on the compute stream
       HT_TRY(ev_wait(d.stream, d.e_bin));
       if (f->prefetch && j == 0) HT_TRY(ev_wait(d.stream, d.e_ck[layer]));
+      }
       float *GZ = d.sc.as<float>(), *GA = d.sd.as<float>();
       LayerW& w = d.lw[layer];
       TimerRec tg;
@@ -1700,11 +1883,13 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       d.bwd_count++;
     }
     // K9/K10: owner push (ascending source device) + flush into host grads
-    HT_TRY(push_flush(f, j, gin, true));
+    // (into the mirror with the cache)
+    HT_TRY(push_flush(f, j, gin, true, layer));
   }
   for (auto& d : f->dev) {
     if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
+    if (d.cache) HT_TRY(cache_writeback(f, d, gin, d.mg[layer].as<float>(), rbi));
     HT_TRY(ev_rec(d.e_flush, d.stream));
   }
   return HT_OK;
@@ -1907,8 +2092,8 @@ int gat_dest_load(ht_fleet* f, Device& d, DevChunk& c, const void* host, float* 
 // Stage batch j's neighbour rows of layer input `hin` on every device and
 // gather them into N_ij order (g_hn); destination rows of `hin` into
 // g_hd[s] (and, when gsrc != null, destination rows of gsrc into g_gin[s]).
-int gat_stage(ht_fleet* f, int j, const void* hin, int d_in, const void* gsrc, int d_out,
-              bool first_of_layer, bool bwd) {
+int gat_stage(ht_fleet* f, int layer, int j, const void* hin, int d_in, const void* gsrc,
+              int d_out, bool first_of_layer, bool bwd) {
   const int64_t rbi = (int64_t)d_in * 4, rbo = (int64_t)d_out * 4;
   for (int i = 0; i < f->m; ++i) {
     Device& d = f->dev[i];
@@ -1917,6 +2102,18 @@ int gat_stage(ht_fleet* f, int j, const void* hin, int d_in, const void* gsrc, i
     DevChunk& c = d.chunks[j];
     int64_t& cnt = bwd ? d.bwd_count : d.fwd_count;
     const int s = (int)(cnt & 1);
+    if (d.cache) {  // owned rows from the HBM mirror; destination rows are read in place
+      if (!bwd && layer == 0 && j == 0) {
+        HT_TRY(cache_upload(f, d, d.tin, hin, d.mh[0].as<float>(), rbi));
+        HT_TRY(ev_rec(d.e_up, d.tin));
+        HT_TRY(ev_wait(d.stream, d.e_up));
+      }
+      for (auto& o : f->dev) HT_TRY(ev_wait(d.stream, o.e_fetch));  // peers done with our slots
+      HT_TRY(launch_copy(d.stream, d.value.p, d.mh[layer].p, c.h2d.dst.as<int64_t>(),
+                         c.h2d_m.as<int64_t>(), c.h2d.n, rbi, rbi, rbi));
+      HT_TRY(ev_rec(d.e_in, d.stream));
+      continue;
+    }
     if (!first_of_layer) {  // slots of the previous batch gathered everywhere
       HT_TRY(ev_wait(d.tin, d.e_agg));
       for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_fetch));
@@ -1968,7 +2165,7 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
   for (int l = 0; l <= L; ++l) HT_TRY(gat_width_ok(dims[l]));
   int64_t extra = 0;  // attention gradients live behind the weight gradients
   for (int l = 0; l < L; ++l) extra += 2 * (int64_t)dims[l + 1];
-  HT_TRY(epoch_begin_impl(f, L, dims, extra));
+  HT_TRY(epoch_begin_impl(f, L, dims, extra, true));
   int dmax = 0;
   for (int l = 0; l <= L; ++l) dmax = std::max(dmax, dims[l]);
   for (int i = 0; i < f->m; ++i) {
@@ -2051,7 +2248,7 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
   }
   if (last) f->hL_dim = d_out;
   for (int j = 0; j < f->n; ++j) {
-    HT_TRY(gat_stage(f, j, hin, d_in, nullptr, d_out, j == 0, false));
+    HT_TRY(gat_stage(f, layer, j, hin, d_in, nullptr, d_out, j == 0, false));
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
       if (!d.local) continue;
@@ -2059,12 +2256,15 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
       DevChunk& c = d.chunks[j];
       const int s = (int)(d.fwd_count & 1);
       LayerW& w = d.lw[layer];
-      if (d.fwd_count >= 2) HT_TRY(ev_wait(d.stream, d.e_out[s]));  // output set s drained
-      float* H = last ? d.hL.as<float>() + d.hL_off[j] * d_out : d.fb[s].as<float>();
+      if (d.fwd_count >= 2 && !d.cache) HT_TRY(ev_wait(d.stream, d.e_out[s]));  // output set s drained
+      float* H = last     ? d.hL.as<float>() + d.hL_off[j] * d_out
+                 : d.cache ? d.mh[layer + 1].as<float>() + c.dest_m0 * d_out
+                           : d.fb[s].as<float>();
+      const float* HD = d.cache ? d.mh[layer].as<float>() + c.dest_m0 * d_in : d.g_hd[s].as<float>();
       TimerRec tg;
       timer_begin(f, d, tg, d.stream);
       HT_TRY(gat_proj(d, precision, d.g_hn.as<float>(), c.nn, d_in, d_out, d.g_q.as<float>(), w));
-      HT_TRY(gat_proj(d, precision, d.g_hd[s].as<float>(), c.nv, d_in, d_out, d.g_p.as<float>(), w));
+      HT_TRY(gat_proj(d, precision, HD, c.nv, d_in, d_out, d.g_p.as<float>(), w));
       timer_end(f, d, tg, 2, 2.0 * (double)(c.nn + c.nv) * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_gcomp[s], d.stream));  // destination inputs of set s consumed
       HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), d.g_q.as<float>(), w.A.as<float>() + d_out,
@@ -2115,11 +2315,12 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
     HT_TRY(upload_attn(d, layer, A, d_out));
     if (f->mode != HT_MODE_BASELINE)  // begin_backward_layer: zeroed gradient slots
       CU(cudaMemsetAsync(d.grad.p, 0, d.cap * (int64_t)d_in * 4, d.stream));
+    if (d.cache) CU(cudaMemsetAsync(d.mg[layer].p, 0, d.mcount * (int64_t)d_in * 4, d.stream));
   }
   for (int j = 0; j < f->n; ++j) {
     // load_recomp_chkpt("gat"): inputs re-staged through the forward
     // machinery, destination inputs, then the destination gradients
-    HT_TRY(gat_stage(f, j, hin, d_in, gout, d_out, j == 0, true));
+    HT_TRY(gat_stage(f, layer, j, hin, d_in, gout, d_out, j == 0, true));
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
       if (!d.local) continue;
@@ -2130,7 +2331,9 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       const float* a_dst = w.A.as<float>();
       const float* a_src = a_dst + d_out;
       float* HN = d.g_hn.as<float>();
-      float* HD = d.g_hd[s].as<float>();
+      float* HD = d.cache ? d.mh[layer].as<float>() + c.dest_m0 * d_in : d.g_hd[s].as<float>();
+      const float* Gin = d.cache ? d.mg[layer + 1].as<float>() + c.dest_m0 * d_out
+                                 : d.g_gin[s].as<float>();
       float *Q = d.g_q.as<float>(), *P = d.g_p.as<float>();
       float *GS = d.g_gs.as<float>(), *GP = d.g_gp.as<float>(), *GQ = d.g_gq.as<float>();
       float *AL = d.g_al.as<float>(), *GT = d.g_gt.as<float>();
@@ -2143,7 +2346,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
       HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, d.g_els.as<float>(), a_dst, d_out, slope,
-                                  nullptr, d.g_gin[s].as<float>(), GS, GP, AL, GT,
+                                  nullptr, Gin, GS, GP, AL, GT,
                                   d.g_sgt.as<float>()));
       HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
                             d.partial.as<float>(), d.g_pgts.as<float>()));
@@ -2176,15 +2379,20 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       if (!d.local) continue;
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
-      HT_TRY(launch_acc(d.stream, 4, gin, d.g_ghd.p, c.dest_rows.as<int64_t>(), nullptr, nullptr,
-                        c.nv, d_in, 0));
+      if (d.cache)  // contiguous mirror rows of the destinations
+        HT_TRY(launch_acc(d.stream, 4, d.mg[layer].as<float>() + c.dest_m0 * d_in, d.g_ghd.p,
+                          nullptr, nullptr, nullptr, c.nv, d_in, 0));
+      else
+        HT_TRY(launch_acc(d.stream, 4, gin, d.g_ghd.p, c.dest_rows.as<int64_t>(), nullptr,
+                          nullptr, c.nv, d_in, 0));
     }
     if (f->mode == HT_MODE_BASELINE) HT_TRY(barrier(f));
-    HT_TRY(push_flush(f, j, gin, false));
+    HT_TRY(push_flush(f, j, gin, false, layer));
   }
   for (auto& d : f->dev) {
     if (!d.local) continue;
     HT_TRY(set_dev(d));
+    if (d.cache) HT_TRY(cache_writeback(f, d, gin, d.mg[layer].as<float>(), (int64_t)d_in * 4));
     HT_TRY(ev_rec(d.e_flush, d.stream));
   }
   return HT_OK;

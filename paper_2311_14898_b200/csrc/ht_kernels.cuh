@@ -85,6 +85,59 @@ __global__ void __launch_bounds__(256) k_acc_rows(T* __restrict__ dst, T* __rest
   }
 }
 
+// float4 rows (d % 4 == 0, 16-byte aligned rows): two rows per warp in
+// flight, so every lane has four independent 16-byte loads outstanding
+__global__ void __launch_bounds__(256) k_acc_rows4(float* __restrict__ dst, float* __restrict__ src,
+                                                   const int64_t* __restrict__ didx,
+                                                   const int64_t* __restrict__ sidx,
+                                                   const uint8_t* __restrict__ store_first,
+                                                   int64_t rows, int d, int zero_src,
+                                                   int64_t sbase) {
+  const int lane = lane_id();
+  const int d4 = d >> 2;
+  const int64_t nw = num_warps();
+  for (int64_t r0 = global_warp() * 2; r0 < rows; r0 += nw * 2) {
+    float4* s[2];
+    float4* o[2];
+    bool st[2], ok[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t r = r0 + q;
+      ok[q] = r < rows;
+      const int64_t rr = ok[q] ? r : r0;
+      s[q] = reinterpret_cast<float4*>(src + ((sidx ? sidx[rr] : rr) + sbase) * d);
+      o[q] = reinterpret_cast<float4*>(dst + (didx ? didx[rr] : rr) * d);
+      st[q] = store_first && store_first[rr];
+    }
+    for (int c = lane; c < d4; c += 2 * kWarp) {
+      float4 a[2][2], b[2][2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int cc = c + u * kWarp;
+          if (ok[q] && cc < d4) {
+            a[q][u] = s[q][cc];
+            b[q][u] = st[q] ? make_float4(0.f, 0.f, 0.f, 0.f) : o[q][cc];
+          }
+        }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int cc = c + u * kWarp;
+          if (ok[q] && cc < d4) {
+            float4 v = a[q][u];
+            if (!st[q]) v = make_float4(b[q][u].x + v.x, b[q][u].y + v.y, b[q][u].z + v.z,
+                                        b[q][u].w + v.w);
+            o[q][cc] = v;
+            if (zero_src) s[q][cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // segment gather-sum: out[seg] = sum_{e in [lo, hi)} w[e] * X[idx[e]]
 // sequential in e, product rounded before the add (no FMA contraction)
@@ -383,15 +436,16 @@ __global__ void k_reduce_splits(float* __restrict__ acc, const float* __restrict
 
 // ---------------------------------------------------------------------------
 // K11 loss: rows of H (ld = d); labels/mask aligned with rows; gradient rows
-// written to out (host or device) at out_rows[r] (stride d).  One warp per
+// written to out (host or device) at out_rows[r] (stride d), or at
+// out_base + r when out_base >= 0.  One warp per
 // row; per-block partial loss sums in double, fixed order.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64_t rows, int d,
                                               const int64_t* __restrict__ labels,
                                               const uint8_t* __restrict__ mask,
                                               const int64_t* __restrict__ out_rows,
-                                              float* __restrict__ out, float count,
-                                              double* __restrict__ block_loss) {
+                                              float* __restrict__ out, int64_t out_base,
+                                              float count, double* __restrict__ block_loss) {
   __shared__ double wsum[8];
   const int lane = lane_id(), wib = threadIdx.x >> 5;
   double my = 0.0;
@@ -399,8 +453,10 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64
   const int64_t stride = (int64_t)gridDim.x * 8;
   for (int64_t r = warp; r < rows; r += stride) {
     const int64_t v = out_rows[r];
+    // gradient row: host row v, or mirror row out_base + r (HBM owner cache)
+    const int64_t orow = out_base >= 0 ? out_base + r : v;
     if (!mask[v]) {  // rows off the mask get a zero gradient (engine.py:305, 319)
-      for (int c = lane; c < d; c += kWarp) out[v * d + c] = 0.f;
+      for (int c = lane; c < d; c += kWarp) out[orow * d + c] = 0.f;
       continue;
     }
     const float* z = H + r * d;
@@ -413,7 +469,7 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     const int64_t y = labels[v];
-    float* g = out + v * d;
+    float* g = out + orow * d;
     for (int c = lane; c < d; c += kWarp) {
       const float p = __fdiv_rn(expf(z[c] - mx), s);
       if (c == y) my += -(double)logf(p);

@@ -208,21 +208,33 @@ class BufferInfo:
         self.dtype = np.dtype(dtype)
 
 
+# HBM owner cache: each device keeps HBM mirrors of the
+# host rows it owns (layer inputs, checkpoints, gradients) and reads those
+# instead of the host; every row produced is still written through to the
+# HostStore.  "auto" enables it for host-resident stores in p2p/full mode
+# when the mirrors fit in free HBM.
+_CACHE_MODES = {"off": 0, "on": 1, "auto": 2}
+
+
 class DeviceFleet:
     """Executes a DedupPlan over m virtual devices on the GPU(s)
     (devices.py:129-488).  ``devices[i]`` maps virtual device i to a CUDA
     ordinal (default: round-robin over the visible GPUs)."""
 
     def __init__(self, plan: DedupPlan, mode: str = "full", flush_policy: str = "on_eviction",
-                 dtype=np.float64, devices=None, precision: str = "tf32", rank: int | None = None):
+                 dtype=np.float64, devices=None, precision: str = "tf32", rank: int | None = None,
+                 cache: str = "auto"):
         if mode not in _MODES:
             raise SimulationError(f"unknown mode {mode!r}")
         if flush_policy not in _FLUSH_POLICIES:
             raise SimulationError(f"unknown flush policy {flush_policy!r}")
         if precision not in PRECISIONS:
             raise SimulationError(f"unknown precision {precision!r}, expected one of {list(PRECISIONS)}")
+        if cache not in _CACHE_MODES:
+            raise SimulationError(f"unknown cache mode {cache!r}, expected one of {list(_CACHE_MODES)}")
         self.plan = plan
         self.mode = mode
+        self.cache = cache
         self.flush_policy = flush_policy
         self.dtype = np.dtype(dtype)
         self.precision = precision
@@ -245,6 +257,7 @@ class DeviceFleet:
         else:
             self.ordinals = list(devices) if devices is not None else [i % ngpu for i in range(self.m)]
         self._ipc_ready = rank is None or self.m == 1
+        self.cache_active = False  # set per epoch by train_epoch
         self._handle = None
         self._create_native()
         self._precompute_meters()

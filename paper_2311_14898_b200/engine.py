@@ -124,17 +124,22 @@ def comm_passes_per_epoch(model: ModelConfig) -> tuple:
     return (2 * L, L) if model.kind == "gat" else (L, L)
 
 
-def _epoch_reset(host: HostStore, fleet: DeviceFleet, kind: str = "gcn") -> None:
+def _epoch_reset(host: HostStore, fleet: DeviceFleet, kind: str = "gcn",
+                 cached: bool = False) -> None:
     """reset_epoch with the same observable result but without rewriting
     rows the epoch overwrites anyway: the loss writes every row of
     grad_h[L], and in p2p/full GCN mode the first flush of a row stores it,
     so only rows no chunk ever reads need explicit zeros.  GAT adds
     destination-input gradients into the host rows before the flushes, so
-    every flush is a read-modify-write there and all rows are zeroed."""
+    every flush is a read-modify-write there and all rows are zeroed.  With
+    the HBM owner cache every owned row of every gradient array is written
+    through from a zeroed mirror, so nothing needs zeroing."""
     L = len(host.dims) - 1
     for l in range(1, len(host.h)):
         host.h_valid[l] = False
     host.agg_written.clear()
+    if cached:
+        return
     for l in range(L):
         g = host.grad_h[l]
         if isinstance(g, DeviceArray) or fleet.mode == "baseline" or kind == "gat":
@@ -199,11 +204,21 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     A = _f32_params(model.attn, [(2 * dims[l + 1],) for l in range(L)]) if gat else None
     prec = PRECISIONS[fleet.precision]
     fleet.attach_partition(p)
-    _epoch_reset(host, fleet, model.kind)
     h_ = fleet._handle
     item = host.dtype.itemsize
     dims_c = (C.c_int * (L + 1))(*dims)
+    # HBM owner cache ("auto": host-resident stores only - an HBM store needs
+    # no mirror; the native side refuses plans that do not admit it)
+    from .devices import _CACHE_MODES
+    want = _CACHE_MODES[fleet.cache]
+    if fleet.cache == "auto" and host.placement != "host":
+        want = 0
+    N.call("ht_fleet_set_cache", h_, want)
     N.call("ht_gat_epoch_begin" if gat else "ht_epoch_begin", h_, L, dims_c)
+    on = C.c_int(0)
+    N.call("ht_fleet_cache_state", h_, C.byref(on))
+    fleet.cache_active = bool(on.value)
+    _epoch_reset(host, fleet, model.kind, fleet.cache_active)
     fleet.connect_peers()  # rank mode: IPC handles, once
     slope = C.c_float(model.leaky_slope)
 

@@ -1,0 +1,64 @@
+"""HBM owner cache: with the cache the layer drivers
+read owned rows from HBM mirrors instead of the host store and write every
+produced row through.  The arithmetic is unchanged, so an epoch with the
+cache must equal the cache-off epoch bitwise - host arrays (h, agg,
+grad_h), weights, attention vectors, loss and meters - for GCN and GAT,
+single and multiple devices and batches (re-flushes)."""
+
+import numpy as np
+import pytest
+
+import paper_2311_14898_b200 as H
+
+pytestmark = pytest.mark.gpu
+
+
+def _epochs(p, ds, dims, kind, cache, mode="full", precision="tf32", epochs=2):
+    plan = H.plan_for_partition(p)
+    model = H.init_model(kind, dims, seed=3, lr=0.1, dtype=np.float32)
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+    host.set_features(ds.features)
+    fleet = H.DeviceFleet(plan, mode=mode, dtype=np.float32, precision=precision, cache=cache)
+    out = []
+    for _ in range(epochs):
+        r = H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+        snap = {"loss": r.loss, "W": [w.copy() for w in model.weights],
+                "h": [np.array(x) for x in host.h], "gh": [np.array(x) for x in host.grad_h],
+                "agg": {k: np.array(v) for k, v in host.agg.items()}}
+        if kind == "gat":
+            snap["A"] = [a.copy() for a in model.attn]
+        out.append(snap)
+    rep = fleet.transfer_report(*H.comm_passes_per_epoch(model))
+    return out, rep, fleet.cache_active
+
+
+@pytest.mark.parametrize("kind", ["gcn", "gat"])
+@pytest.mark.parametrize("m,n,mode", [(1, 1, "full"), (1, 3, "full"), (3, 2, "full"),
+                                      (2, 3, "p2p")])
+def test_cache_bitwise_equals_host_path(kind, m, n, mode):
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=2500, avg_degree=8.0, seed=4), 16, 8)
+    a = H.partition_vertices(ds.graph, m, seed=4)
+    p = H.split_chunks(ds.graph, a, n)
+    if n > 1:
+        p = H.reorganize(p).partition
+    dims = [16, 24, 8]
+    off, rep_off, act_off = _epochs(p, ds, dims, kind, "off", mode)
+    on, rep_on, act_on = _epochs(p, ds, dims, kind, "on", mode)
+    assert not act_off and act_on
+    assert rep_on["totals"] == rep_off["totals"]
+    for a_, b_ in zip(off, on):
+        assert a_["loss"] == b_["loss"]
+        for key in ("W", "h", "gh") + (("A",) if kind == "gat" else ()):
+            for x, y in zip(a_[key], b_[key]):
+                np.testing.assert_array_equal(x, y, err_msg=key)
+        for l in a_["agg"]:
+            np.testing.assert_array_equal(a_["agg"][l], b_["agg"][l])
+
+
+def test_cache_refused_in_baseline_mode():
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=800, avg_degree=6.0, seed=1), 8, 4)
+    p = H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 2, seed=1), 2)
+    with pytest.raises(H.ChunktrainError, match="cache"):
+        _epochs(p, ds, [8, 8, 4], "gcn", "on", mode="baseline", epochs=1)
+    _, _, active = _epochs(p, ds, [8, 8, 4], "gcn", "auto", mode="baseline", epochs=1)
+    assert not active
