@@ -238,6 +238,10 @@ struct ht_fleet {
   double t_ms[4] = {0, 0, 0, 0}, t_bytes[4] = {0, 0, 0, 0};
   int L = 0;
   std::vector<int> dims;
+  // h^l arrays passed to the forward layers (device-usable) and whether they
+  // are HBM: the backward takes ReLU' from h^{l+1} when it is device-resident
+  std::vector<void*> hptr;
+  std::vector<char> hdev;
   int64_t loss_count = 0;
   bool prefetch = true;  // checkpoint prefetch (HT_CKPT_PREFETCH=0 disables)
   bool gat = false;      // buffers sized by ht_gat_epoch_begin
@@ -342,6 +346,15 @@ int dev_ptr(const void* p, void** out) {
     return HT_OK;
   }
   return fail(HT_EINVAL, "array at %p is pageable host memory; pin it first", p);
+}
+
+bool is_dev_mem(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice;
 }
 
 // Row copy with the widest vector the row size and alignment permit.
@@ -1352,6 +1365,23 @@ int check_chunks(ht_fleet* f) {
   return HT_OK;
 }
 
+// The output rows h^{layer+1} of chunk j as they sit in HBM (the last
+// layer's device copy, the owner-cache mirror, or an HBM host store), or
+// nullptr when only pinned host memory holds them.  *rows: row indices
+// into the returned array (nullptr = consecutive).
+const float* hbm_outputs(ht_fleet* f, Device& d, int j, int layer, int d_out,
+                         const int64_t** rows) {
+  *rows = nullptr;
+  DevChunk& c = d.chunks[j];
+  if (layer + 1 == f->L) return d.hL.as<float>() + d.hL_off[j] * d_out;
+  if (d.cache) return d.mh[layer + 1].as<float>() + c.dest_m0 * d_out;
+  if ((int)f->hdev.size() > layer + 1 && f->hdev[layer + 1]) {
+    *rows = c.dest_rows.as<int64_t>();
+    return static_cast<const float*>(f->hptr[layer + 1]);
+  }
+  return nullptr;
+}
+
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
 int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
                  int64_t rb) {
@@ -1404,6 +1434,8 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
   HT_TRY(sync_all(f));
   f->L = L;
   f->dims.assign(dims, dims + L + 1);
+  f->hptr.assign(L + 1, nullptr);
+  f->hdev.assign(L + 1, 0);
   int dmax = 0;
   for (int l = 0; l <= L; ++l) dmax = std::max(dmax, pad4(dims[l]));
   for (auto& d : f->dev) {
@@ -1535,6 +1567,8 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
   f->elem = 4;
   const bool last = layer == f->L - 1;
   const int64_t rbi = (int64_t)d_in * 4, rbo = (int64_t)d_out * 4;
+  f->hptr[layer + 1] = hout;
+  f->hdev[layer + 1] = is_dev_mem(hout);
   for (auto& d : f->dev) {
     if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
@@ -1837,9 +1871,17 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       timer_begin(f, d, tg, d.stream);
       const int64_t M = c.nv;
       const int64_t nw = (int64_t)d_in * d_out;
+      const int64_t* hrows = nullptr;
+      const float* HO = hbm_outputs(f, d, j, layer, d_out, &hrows);
+      if (HO && M > 0) {  // gz = g * (h > 0): z need not be recomputed
+        count_launch();
+        ht::k_relu_mask<<<grid_for(M), kThreads, 0, d.stream>>>(GZ, ldz, G, HO, hrows, M, d_out);
+        CU(cudaGetLastError());
+      }
       if (precision == HT_PREC_TF32) {
-        HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, w.Wt_hi.as<float>(),
-                                             w.Wt_lo.as<float>(), d_in, d_out, GZ, ldz, G, d_out));
+        if (!HO)
+          HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, w.Wt_hi.as<float>(),
+                                               w.Wt_lo.as<float>(), d_in, d_out, GZ, ldz, G, d_out));
         HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
                                               w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
                                               nullptr, 0));
@@ -1856,8 +1898,9 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
         int splits = (int)std::min<int64_t>(kSplitsMax, std::max<int64_t>(1, M / 2048));
         int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
         splits = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
-        HT_TRY((gemm<false, false, ht::EPI_MASK>(d.stream, A, d_in, w.W.as<float>(), d_out, GZ,
-                                                 ldz, G, d_out, M, d_out, d_in, 1, d_in)));
+        if (!HO)
+          HT_TRY((gemm<false, false, ht::EPI_MASK>(d.stream, A, d_in, w.W.as<float>(), d_out, GZ,
+                                                   ldz, G, d_out, M, d_out, d_in, 1, d_in)));
         if (M > 0) {
           HT_TRY((gemm<true, false, ht::EPI_STORE>(d.stream, A, d_in, GZ, ldz,
                                                    d.gemm_ws.as<float>(), d_out, nullptr, 0, d_in,
@@ -1913,7 +1956,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
 // ===========================================================================
 namespace {
 
-constexpr int kColBlocks = 296;
+constexpr int kColBlocks = 1184;  // 148 SMs x 8
 
 int gat_width_ok(int d) {
   if (d % 4 == 0 && d >= 4 && d <= 512) return HT_OK;
@@ -1939,7 +1982,8 @@ int launch_rowdot(cudaStream_t s, float* out, const float* X, const float* a, in
 template <bool BWD>
 int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const float* P,
                    const float* els, const float* a_dst, int d, float slope, float* H,
-                   const float* G, float* GS, float* GP, float* AL, float* GT, float* SGT) {
+                   const float* G, float* GS, float* GP, float* AL, float* GT, float* SGT,
+                   const float* HO = nullptr, const int64_t* ho_rows = nullptr) {
   if (c.nv <= 0) return HT_OK;
   const int g = grid_for(c.nv);
   const int64_t* off = c.csc_off.as<int64_t>();
@@ -1947,7 +1991,7 @@ int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const floa
   count_launch();
 #define GATD(NV)                                                                              \
   ht::gat::k_gat_dst<NV, BWD><<<g, kThreads, 0, s>>>(off, idx, c.nv, Q, P, els, a_dst, d, slope, \
-                                                     H, G, GS, GP, AL, GT, SGT)
+                                                     H, G, GS, GP, AL, GT, SGT, HO, ho_rows)
   switch (nv_of(d)) {
     case 1: GATD(1); break;
     case 2: GATD(2); break;
@@ -1996,11 +2040,16 @@ int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const flo
 int launch_wcolsum(cudaStream_t s, float* acc, const float* X, const float* w, int64_t rows, int d,
                    float* partial) {
   if (rows <= 0) return HT_OK;
-  int64_t nb = std::min<int64_t>(kColBlocks, (rows + 31) / 32);
+  int64_t nb = std::min<int64_t>(kColBlocks, (rows + 63) / 64);
   const int64_t rpb = (rows + nb - 1) / nb;
   nb = (rows + rpb - 1) / rpb;
   count_launch(2);
-  ht::gat::k_wcolsum<<<(int)nb, 256, 0, s>>>(partial, X, d, w, rows, d, rpb);
+  switch (nv_of(d)) {
+    case 1: ht::gat::k_wcolsum<1><<<(int)nb, 256, 0, s>>>(partial, X, d, w, rows, d, rpb); break;
+    case 2: ht::gat::k_wcolsum<2><<<(int)nb, 256, 0, s>>>(partial, X, d, w, rows, d, rpb); break;
+    case 3: ht::gat::k_wcolsum<3><<<(int)nb, 256, 0, s>>>(partial, X, d, w, rows, d, rpb); break;
+    default: ht::gat::k_wcolsum<4><<<(int)nb, 256, 0, s>>>(partial, X, d, w, rows, d, rpb); break;
+  }
   ht::gat::k_colsum_reduce<<<(d + 127) / 128, 128, 0, s>>>(acc, partial, (int)nb, d);
   CU(cudaGetLastError());
   return HT_OK;
@@ -2240,6 +2289,8 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
   f->elem = 4;
   const bool last = layer == f->L - 1;
   const int64_t rbo = (int64_t)d_out * 4;
+  f->hptr[layer + 1] = hout;
+  f->hdev[layer + 1] = is_dev_mem(hout);
   for (auto& d : f->dev) {
     if (!d.local) continue;
     HT_TRY(set_dev(d));
@@ -2345,9 +2396,10 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), Q, a_src, d_out, c.nn));
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
+      const int64_t* hrows = nullptr;
+      const float* HO = hbm_outputs(f, d, j, layer, d_out, &hrows);
       HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, d.g_els.as<float>(), a_dst, d_out, slope,
-                                  nullptr, Gin, GS, GP, AL, GT,
-                                  d.g_sgt.as<float>()));
+                                  nullptr, Gin, GS, GP, AL, GT, d.g_sgt.as<float>(), HO, hrows));
       HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
                             d.partial.as<float>(), d.g_pgts.as<float>()));
       timer_end(f, d, tr, 1,

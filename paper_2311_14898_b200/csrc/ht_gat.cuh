@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     const float* __restrict__ Q, const float* __restrict__ P, const float* __restrict__ el_src,
     const float* __restrict__ a_dst, int d, float slope, float* __restrict__ H,
     const float* __restrict__ G, float* __restrict__ GS, float* __restrict__ GP,
-    float* __restrict__ AL, float* __restrict__ GT, float* __restrict__ SGT) {
+    float* __restrict__ AL, float* __restrict__ GT, float* __restrict__ SGT,
+    const float* __restrict__ HO, const int64_t* __restrict__ ho_rows) {
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
   float4 ad[NV];
@@ -147,11 +148,18 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     for (int64_t e = e0 + lane; e < e1; e += kW)
       den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
     den = warp_sum(den);
-    // s_v = sum alpha_e q_u, sequential in edge order
+    // s_v = sum alpha_e q_u, sequential in edge order.  Backward with the
+    // layer output h = ReLU(s) in HBM (HO): (s > 0) == (h > 0) bitwise, so
+    // only alpha is recomputed, not s (one row gather per edge saved)
     float4 acc[NV];
 #pragma unroll
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int64_t base = e0; base < e1; base += kW) {
+    if (BWD && HO) {
+      load4<NV>(acc, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
+      for (int64_t e = e0 + lane; e < e1; e += kW)
+        AL[e] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
+    }
+    for (int64_t base = e0; base < ((BWD && HO) ? e0 : e1); base += kW) {
       const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
       int my_i = 0;
       float my_a = 0.f;
@@ -212,7 +220,26 @@ __global__ void __launch_bounds__(256) k_gat_dst(
       const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
       const int my_i = lane < cnt ? __ldg(idx + base + lane) : 0;
       float my_g = 0.f;
-      for (int k = 0; k < cnt; ++k) {
+      int k = 0;
+      for (; k + 4 <= cnt; k += 4) {  // four rows in flight, four interleaved reductions
+        float4 x[4][NV];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int s = __shfl_sync(0xffffffffu, my_i, k + u);
+          load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
+        }
+        float g[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) g[u] = dot4<NV>(gs, x[u]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) g[u] += __shfl_xor_sync(0xffffffffu, g[u], o);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (lane == k + u) my_g = g[u];
+      }
+      for (; k < cnt; ++k) {
         const int s = __shfl_sync(0xffffffffu, my_i, k);
         float4 x[NV];
         load4<NV>(x, Q + (int64_t)s * d, d4, lane);
@@ -365,17 +392,46 @@ __global__ void __launch_bounds__(256) k_gat_src_fixup(
   }
 }
 
-// partial[b][c] = sum over block b's rows r of w[r] * X[r][c]
+// partial[b][c] = sum over block b's rows r of w[r] * X[r][c]: warps take
+// rows, lanes float4 columns, the block's 8 warp sums combined in shared
+// memory in warp order (deterministic)
+template <int NV>
 __global__ void __launch_bounds__(256) k_wcolsum(float* __restrict__ partial,
                                                  const float* __restrict__ X, int64_t ldx,
                                                  const float* __restrict__ w, int64_t rows, int d,
                                                  int64_t rows_per_block) {
+  __shared__ float4 red[8][NV * kW];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int d4 = d >> 2;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = min(rows, r0 + rows_per_block);
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    float s = 0.f;
-    for (int64_t r = r0; r < r1; ++r) s = fmaf(__ldg(w + r), __ldg(X + r * ldx + c), s);
-    partial[(int64_t)blockIdx.x * d + c] = s;
+  float4 acc[NV];
+#pragma unroll
+  for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t r = r0 + wib; r < r1; r += 8) {
+    const float wr = __ldg(w + r);
+    float4 x[NV];
+    load4<NV>(x, X + r * ldx, d4, lane);
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      acc[t].x = fmaf(wr, x[t].x, acc[t].x);
+      acc[t].y = fmaf(wr, x[t].y, acc[t].y);
+      acc[t].z = fmaf(wr, x[t].z, acc[t].z);
+      acc[t].w = fmaf(wr, x[t].w, acc[t].w);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < NV; ++t) red[wib][lane + t * kW] = acc[t];
+  __syncthreads();
+  for (int c4 = threadIdx.x; c4 < d4; c4 += blockDim.x) {
+    float4 s = red[0][c4];
+    for (int q = 1; q < 8; ++q) {
+      s.x += red[q][c4].x;
+      s.y += red[q][c4].y;
+      s.z += red[q][c4].z;
+      s.w += red[q][c4].w;
+    }
+    reinterpret_cast<float4*>(partial + (int64_t)blockIdx.x * d)[c4] = s;
   }
 }
 

@@ -434,6 +434,23 @@ __global__ void k_reduce_splits(float* __restrict__ acc, const float* __restrict
   }
 }
 
+// ReLU' from the stored layer output: gz[r] = g[r] * (h[row(r)] > 0).  h =
+// max(z, 0) was produced from the same z by the forward, so (h > 0) == (z >
+// 0) bitwise: the backward needs no recompute of z when h is in HBM.
+__global__ void __launch_bounds__(256) k_relu_mask(float* __restrict__ gz, int64_t ldz,
+                                                   const float* __restrict__ g,
+                                                   const float* __restrict__ h,
+                                                   const int64_t* __restrict__ hrows,
+                                                   int64_t rows, int d) {
+  const int lane = lane_id();
+  for (int64_t r = global_warp(); r < rows; r += num_warps()) {
+    const float* hr = h + (hrows ? hrows[r] : r) * (int64_t)d;
+    const float* gr = g + r * (int64_t)d;
+    float* o = gz + r * ldz;
+    for (int c = lane; c < d; c += kWarp) o[c] = __ldg(hr + c) > 0.f ? __ldg(gr + c) : 0.f;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K11 loss: rows of H (ld = d); labels/mask aligned with rows; gradient rows
 // written to out (host or device) at out_rows[r] (stride d), or at
