@@ -146,6 +146,10 @@ struct DevChunk {
   // [dest_m0, dest_m0 + nv); h2d / flush rows as mirror positions
   int64_t dest_m0 = -1;
   DBuf h2d_m, flush_m;               // int64 [h2d.n], int64 [flush.n]
+  // single device (m = 1): sources by global row, so the gathers read an
+  // HBM-resident h^l (mirror or HBM store) in place, without slot loads
+  DBuf csc_gid;                      // int32 [ne]: global row of each CSC source
+  DBuf nbr_gid;                      // int64 [nn]: global row of each neighbour
 };
 
 struct LayerW {
@@ -170,6 +174,7 @@ struct Device {
   int64_t cap = 0;
   DBuf value, grad;                    // cap x dim slot buffers
   DBuf sa, sb, sc, sd, se, partial;    // staging
+  DBuf tT;                             // A^T gz in d_out space (narrow-side backward)
   DBuf gemm_ws;
   DBuf W, Wt, Wp;                      // current layer weights, transpose, padded
   DBuf Wt_hi, Wt_lo, Wp_hi, Wp_lo;     // TF32 hi/lo halves for tcgen05
@@ -464,6 +469,22 @@ void seg_variant(int g, cudaStream_t s, float* out, const float* X, int64_t ldx,
     const char* e = getenv("HT_SEG_VARIANT");
     return e ? atoi(e) : 0;
   }();
+  static int v1 = [] {  // narrow rows (<= 128 floats): separate tuning knob
+    const char* e = getenv("HT_SEG_VARIANT1");
+    return e ? atoi(e) : 0;
+  }();
+  if (NV == 1) {
+    switch (v1) {
+      case 1: ht::k_seg_gather_v4<NV, 4, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
+      case 2: ht::k_seg_gather_v4<NV, 8, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
+      case 3: ht::k_seg_gather_v4<NV, 8, 6><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
+      case 4: ht::k_seg_gather_v4<NV, 16, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
+      case 5: ht::k_seg_gather_v4<NV, 4, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
+      case 6: ht::k_seg_gather_v4<NV, 8, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
+      case 7: ht::k_seg_gather_v4<NV, 2, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
+      default: ht::k_seg_gather_v4<NV, 8, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;  // measured best (sweep, r1)
+    }
+  }
   switch (v) {
     case 1: ht::k_seg_gather_v4<NV, 4, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
     case 2: ht::k_seg_gather_v4<NV, 8, 2><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
@@ -702,7 +723,8 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
     }
     CU(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
     d.chunks.resize(n);
-    for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
+    for (auto& c : d.chunks) c.csc_gid.release(), c.nbr_gid.release();
+    for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.tT, &d.partial, &d.gemm_ws,
                     &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo, &d.hL,
                     &d.labels, &d.mask, &d.loss_part})
       b->dev = d.ordinal;
@@ -981,6 +1003,12 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         }
         HT_TRY(upload(c.csc_off, h.csc_off, s));
         HT_TRY(upload(c.csc_slot, slot32, s));
+        if (m == 1 && f->nrows < ((int64_t)1 << 31)) {
+          std::vector<int32_t> gid(h.ne);
+          for (int64_t e = 0; e < h.ne; ++e) gid[e] = (int32_t)h.nbr[h.csc_src[e]];
+          HT_TRY(upload(c.csc_gid, gid, s));
+          HT_TRY(upload(c.nbr_gid, h.nbr, s));
+        }
         HT_TRY(upload(c.csc_w, w32, s));
         HT_TRY(upload(c.csr_off, h.csr_off, s));
         HT_TRY(upload(c.csr_dst, dst32, s));
@@ -1382,6 +1410,17 @@ const float* hbm_outputs(ht_fleet* f, Device& d, int j, int layer, int d_out,
   return nullptr;
 }
 
+// m = 1: the layer input h^l as an HBM array indexed by global row (the
+// owner-cache mirror when it is the identity map, or an HBM host store),
+// or nullptr.  The gathers then read it in place: no slot loads.
+const float* hbm_inputs(ht_fleet* f, Device& d, int layer, const void* hin) {
+  if (f->m != 1 || !d.chunks[0].csc_gid.p || getenv("HT_NO_DIRECT_READ")) return nullptr;
+  if (d.cache && d.mcount == f->nrows && (d.mrows.empty() || d.mrows.back() == d.mcount - 1))
+    return d.mh[layer].as<float>();
+  if (is_dev_mem(hin)) return static_cast<const float*>(hin);
+  return nullptr;
+}
+
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
 int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
                  int64_t rb) {
@@ -1470,6 +1509,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     HT_TRY(d.sc.ensure(mv * dmax * 4));
     HT_TRY(d.sd.ensure(mv * dmax * 4));
     HT_TRY(d.se.ensure(mn * dmax * 4));
+    HT_TRY(d.tT.ensure(mn * dmax * 4));
     HT_TRY(d.partial.ensure(np * dmax * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
@@ -1589,8 +1629,13 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
           HT_TRY(ev_wait(d.stream, d.e_up));
         }
         for (auto& o : f->dev) HT_TRY(ev_wait(d.stream, o.e_fetch));  // peers done with our slots
-        HT_TRY(launch_copy(d.stream, d.value.p, d.mh[layer].p, c.h2d.dst.as<int64_t>(),
-                           c.h2d_m.as<int64_t>(), c.h2d.n, rbi, rbi, rbi));
+        if (!hbm_inputs(f, d, layer, hin))  // else K3 reads the mirror in place
+          HT_TRY(launch_copy(d.stream, d.value.p, d.mh[layer].p, c.h2d.dst.as<int64_t>(),
+                             c.h2d_m.as<int64_t>(), c.h2d.n, rbi, rbi, rbi));
+        HT_TRY(ev_rec(d.e_in, d.stream));
+        continue;
+      }
+      if (hbm_inputs(f, d, layer, hin)) {  // HBM store, one device: K3 reads it in place
         HT_TRY(ev_rec(d.e_in, d.stream));
         continue;
       }
@@ -1650,8 +1695,11 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       float* agg = d.cache ? d.ma[layer].as<float>() + c.dest_m0 * d_in : d.fa[s].as<float>();
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
-      HT_TRY(launch_seg(d.stream, agg, d.value.as<float>(), d_in, d_in, c.csc_off.as<int64_t>(),
-                        c.csc_slot.as<int32_t>(), c.csc_w.as<float>(), c.nv, c.fw_np, c.fw_lo,
+      const float* Xd = hbm_inputs(f, d, layer, hin);
+      HT_TRY(launch_seg(d.stream, agg, Xd ? Xd : d.value.as<float>(), d_in, d_in,
+                        c.csc_off.as<int64_t>(),
+                        Xd ? c.csc_gid.as<int32_t>() : c.csc_slot.as<int32_t>(), c.csc_w.as<float>(),
+                        c.nv, c.fw_np, c.fw_lo,
                         c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt, d.partial.as<float>()));
       timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nv * (4.0 * d_in + 4.0),
                 d.stream);
@@ -1873,6 +1921,10 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       const int64_t nw = (int64_t)d_in * d_out;
       const int64_t* hrows = nullptr;
       const float* HO = hbm_outputs(f, d, j, layer, d_out, &hrows);
+      // narrow-side transposed aggregation: grad_h_nbr = (A^T gz) W^T when
+      // d_out < d_in (K8 gathers d_out-wide rows instead of d_in-wide ones;
+      // same product, reassociated).  Needs gz with zeroed pad columns.
+      const bool narrow = HO && d_out < d_in && !getenv("HT_NO_NARROW_BWD");
       if (HO && M > 0) {  // gz = g * (h > 0): z need not be recomputed
         count_launch();
         ht::k_relu_mask<<<grid_for(M), kThreads, 0, d.stream>>>(GZ, ldz, G, HO, hrows, M, d_out);
@@ -1882,9 +1934,10 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
         if (!HO)
           HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, w.Wt_hi.as<float>(),
                                                w.Wt_lo.as<float>(), d_in, d_out, GZ, ldz, G, d_out));
-        HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
-                                              w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
-                                              nullptr, 0));
+        if (!narrow)
+          HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
+                                                w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
+                                                nullptr, 0));
         if (M > 0) {
           int used = 1;
           HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, ldz, d_out, M, kSplitsMax,
@@ -1910,19 +1963,32 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
               d.gWall.as<float>() + d.gW_off[layer], d.gemm_ws.as<float>(), nw, splits);
           CU(cudaGetLastError());
         }
-        HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, ldz, w.W.as<float>(), d_out, GA,
-                                                 d_in, nullptr, 0, M, d_in, d_out, 1, d_out)));
+        if (!narrow)
+          HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, ldz, w.W.as<float>(), d_out, GA,
+                                                   d_in, nullptr, 0, M, d_in, d_out, 1, d_out)));
       }
       timer_end(f, d, tg, 2, 6.0 * c.nv * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_bcomp[s], d.stream));
       // K8: transposed aggregation over the CSR view -> neighbour-row grads
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
-      HT_TRY(launch_seg(d.stream, d.se.as<float>(), GA, d_in, d_in, c.csr_off.as<int64_t>(),
-                        c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), c.nn, c.bw_np, c.bw_lo,
-                        c.bw_hi, c.bw_nf, c.bw_seg, c.bw_first, c.bw_cnt, d.partial.as<float>()));
-      timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nn * (4.0 * d_in + 4.0),
+      const int kw = narrow ? ldz : d_in;  // width of the gathered rows
+      HT_TRY(launch_seg(d.stream, narrow ? d.tT.as<float>() : d.se.as<float>(), narrow ? GZ : GA,
+                        kw, kw, c.csr_off.as<int64_t>(), c.csr_dst.as<int32_t>(),
+                        c.csr_w.as<float>(), c.nn, c.bw_np, c.bw_lo, c.bw_hi, c.bw_nf, c.bw_seg,
+                        c.bw_first, c.bw_cnt, d.partial.as<float>()));
+      timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * kw) + (double)c.nn * (4.0 * kw + 4.0),
                 d.stream);
+      if (narrow && c.nn > 0) {  // views = (A^T gz) W^T
+        if (precision == HT_PREC_TF32)
+          HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, d.tT.as<float>(), ldz, c.nn, d_out,
+                                                w.Wp_hi.as<float>(), nullptr, ldz, d_in,
+                                                d.se.as<float>(), d_in, nullptr, 0));
+        else
+          HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, d.tT.as<float>(), ldz, w.W.as<float>(),
+                                                   d_out, d.se.as<float>(), d_in, nullptr, 0, c.nn,
+                                                   d_in, d_out, 1, d_out)));
+      }
       d.bwd_count++;
     }
     // K9/K10: owner push (ascending source device) + flush into host grads
@@ -2158,11 +2224,13 @@ int gat_stage(ht_fleet* f, int layer, int j, const void* hin, int d_in, const vo
         HT_TRY(ev_wait(d.stream, d.e_up));
       }
       for (auto& o : f->dev) HT_TRY(ev_wait(d.stream, o.e_fetch));  // peers done with our slots
-      HT_TRY(launch_copy(d.stream, d.value.p, d.mh[layer].p, c.h2d.dst.as<int64_t>(),
-                         c.h2d_m.as<int64_t>(), c.h2d.n, rbi, rbi, rbi));
+      if (!hbm_inputs(f, d, layer, hin))  // else the views are gathered from the mirror
+        HT_TRY(launch_copy(d.stream, d.value.p, d.mh[layer].p, c.h2d.dst.as<int64_t>(),
+                           c.h2d_m.as<int64_t>(), c.h2d.n, rbi, rbi, rbi));
       HT_TRY(ev_rec(d.e_in, d.stream));
       continue;
     }
+
     if (!first_of_layer) {  // slots of the previous batch gathered everywhere
       HT_TRY(ev_wait(d.tin, d.e_agg));
       for (auto& o : f->dev) HT_TRY(ev_wait(d.tin, o.e_fetch));
@@ -2176,10 +2244,12 @@ int gat_stage(ht_fleet* f, int layer, int j, const void* hin, int d_in, const vo
         }
       }
     if (cnt >= 2) HT_TRY(ev_wait(d.tin, d.e_gcomp[s]));  // staging set s consumed
-    TimerRec tr;
-    timer_begin(f, d, tr, d.tin);
-    HT_TRY(gat_host_loads(f, d, c, hin, rbi));
-    timer_end(f, d, tr, 3, (double)c.h2d.n * rbi, d.tin);
+    if (!hbm_inputs(f, d, layer, hin)) {  // else the views are gathered from the HBM store
+      TimerRec tr;
+      timer_begin(f, d, tr, d.tin);
+      HT_TRY(gat_host_loads(f, d, c, hin, rbi));
+      timer_end(f, d, tr, 3, (double)c.h2d.n * rbi, d.tin);
+    }
     HT_TRY(gat_dest_load(f, d, c, hin, d.g_hd[s].as<float>(), rbi));
     if (gsrc) HT_TRY(gat_dest_load(f, d, c, gsrc, d.g_gin[s].as<float>(), rbo));
     HT_TRY(ev_rec(d.e_in, d.tin));
@@ -2200,9 +2270,11 @@ int gat_stage(ht_fleet* f, int layer, int j, const void* hin, int d_in, const vo
       }
     if (f->rank >= 0 && f->m > 1) HT_TRY(xbarrier(f));
     HT_TRY(ev_rec(d.e_fetch, d.stream));
-    // the reference's views: value[slot(N_ij)] in N_ij order
-    HT_TRY(launch_copy(d.stream, d.g_hn.p, d.value.p, nullptr, c.nbr_slot.as<int64_t>(), c.nn, rbi,
-                       rbi, rbi));
+    // the reference's views: value[slot(N_ij)] in N_ij order (or h^l[N_ij]
+    // straight from an HBM-resident input on a single device)
+    const float* Xd = hbm_inputs(f, d, layer, hin);
+    HT_TRY(launch_copy(d.stream, d.g_hn.p, Xd ? (const void*)Xd : d.value.p, nullptr,
+                       Xd ? c.nbr_gid.as<int64_t>() : c.nbr_slot.as<int64_t>(), c.nn, rbi, rbi, rbi));
     HT_TRY(ev_rec(d.e_agg, d.stream));
   }
   return HT_OK;

@@ -448,6 +448,7 @@ __global__ void __launch_bounds__(256) k_relu_mask(float* __restrict__ gz, int64
     const float* gr = g + r * (int64_t)d;
     float* o = gz + r * ldz;
     for (int c = lane; c < d; c += kWarp) o[c] = __ldg(hr + c) > 0.f ? __ldg(gr + c) : 0.f;
+    for (int c = d + lane; c < ldz; c += kWarp) o[c] = 0.f;  // zero pad columns
   }
 }
 
