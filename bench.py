@@ -417,9 +417,19 @@ def main():
     achieved = (bf + bb) / (agg_ms / 1e3) / 1e9 if agg_ms > 0 else 0.0
     lg, msg, flops = val["stats"][2]
     lt, mst, tb = e2e["stats"][3]
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per bracket from the committed ncu launch list of this workload
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+            tj = json.load(fh)
+        if tj.get("config_id") == args.config and tj.get("m") == m:
+            traffic, traffic_src = tj["dram_bytes_per_launch"], tj["source"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "hbm", "kernel": "k_seg_gather (CSC forward + CSR backward aggregation)",
                 "achieved": achieved, "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
-                "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": (bf + bb) / (lf + lb) if lf + lb else None,
                 "launches_per_step": (lf + lb) / args.steps,
                 "share_of_step": agg_ms / val["ms_total"] if val["ms_total"] else None}
     cpu = None
