@@ -220,8 +220,11 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     import paper_2311_14898_b200 as H
     from paper_2311_14898_b200 import _native as N
     dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count()) if rank is not None else 0
+    # one process per GPU: a compact host store with only the rank's owned
+    # rows (host memory per process ~ V/N; every host copy contiguous)
+    rows = np.flatnonzero(plan.owner == rank) if rank is not None and placement == "host" else None
     host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement,
-                       device=dev)
+                       device=dev, rows=rows)
     host.set_features(ds.features if features is None else features)
     labels = ds.labels if labels is None else labels
     fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision, rank=rank,

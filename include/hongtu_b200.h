@@ -195,6 +195,12 @@ int ht_dest_rows(ht_fleet* f, int op, int batch, int dim, int elem_size,
  * written through to the host arrays.  Decided at each ht_epoch_begin;
  * ht_fleet_cache_state reports whether every local device uses it. */
 int ht_fleet_set_cache(ht_fleet* f, int mode);
+/* Compact host arrays (rank mode): the host arrays passed to the layer calls
+ * hold only the local device's owned rows, ascending (`rows`, n = their
+ * count; must equal the plan's owned rows); host row k = owned row k.  Needs
+ * the HBM owner cache; host transfers become single contiguous copies.
+ * rows == NULL restores full (V-row) host arrays. */
+int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t n);
 int ht_fleet_cache_state(ht_fleet* f, int* on);
 /* Zero the per-device weight-gradient accumulators (engine.py:441-448). */
 int ht_epoch_begin(ht_fleet* f, int L, const int* dims);

@@ -251,6 +251,7 @@ struct ht_fleet {
   bool prefetch = true;  // checkpoint prefetch (HT_CKPT_PREFETCH=0 disables)
   bool gat = false;      // buffers sized by ht_gat_epoch_begin
   int cache_req = 0;     // HBM owner cache: 0 off, 1 on (fail if impossible), 2 auto
+  bool host_compact = false;  // host arrays hold only the local device's owned rows
   bool cache_ok = false; // the plan admits the cache (p2p/full, contiguous dest rows)
   int64_t nrows = 0;  // host rows addressed by the plan (max vertex id + 1)
   // rank mode (one process per GPU): index of the local device, barrier
@@ -1424,6 +1425,10 @@ const float* hbm_inputs(ht_fleet* f, Device& d, int layer, const void* hin) {
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
 int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
                  int64_t rb) {
+  if (f->host_compact) {  // host array = owned rows in mirror order
+    if (d.mcount) CU(cudaMemcpyAsync(mirror, host, d.mcount * rb, cudaMemcpyDefault, s));
+    return HT_OK;
+  }
   if (d.own.dma)
     return xfer(s, d.own, false, const_cast<void*>(host), rb, mirror, rb, rb, 0, f->nrows);
   return launch_copy(s, mirror, host, nullptr, d.mrows_d.as<int64_t>(), d.mcount, rb, rb, rb, 0,
@@ -1435,10 +1440,47 @@ int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float
 int cache_writeback(ht_fleet* f, Device& d, void* host, const float* mirror, int64_t rb) {
   HT_TRY(ev_rec(d.e_mg, d.stream));
   HT_TRY(ev_wait(d.tout, d.e_mg));
+  if (f->host_compact) {
+    if (d.mcount) CU(cudaMemcpyAsync(host, mirror, d.mcount * rb, cudaMemcpyDefault, d.tout));
+    return HT_OK;
+  }
   if (d.own.dma)
     return xfer(d.tout, d.own, true, host, rb, const_cast<float*>(mirror), rb, rb, 0, f->nrows);
   return launch_copy(d.tout, host, mirror, d.mrows_d.as<int64_t>(), nullptr, d.mcount, rb, rb, rb,
                      0, kHostGrid);
+}
+
+// Destination rows of chunk c (in destination order at `dev`) -> the host
+// array: host-row chunk g (the GEMM / store pipelining unit), or all rows
+// for g < 0.  Copy-engine runs, the zero-copy kernel (all rows at g <= 0),
+// or - compact host arrays - one contiguous copy at the mirror position.
+int put_dest(ht_fleet* f, DevChunk& c, cudaStream_t s, void* host, const float* dev, int64_t rb,
+             int g) {
+  if (f->host_compact) {
+    int64_t r0 = 0, r1 = c.nv;
+    if (g >= 0) {
+      if (c.dest_pos.empty()) {
+        if (g > 0) return HT_OK;
+      } else {
+        r0 = c.dest_pos[g];
+        r1 = c.dest_pos[g + 1];
+      }
+    }
+    if (r1 > r0)
+      CU(cudaMemcpyAsync(static_cast<char*>(host) + (c.dest_m0 + r0) * rb,
+                         reinterpret_cast<const char*>(dev) + r0 * rb, (r1 - r0) * rb,
+                         cudaMemcpyDefault, s));
+    return HT_OK;
+  }
+  if (c.dest.dma) {
+    for (int gg = g < 0 ? 0 : g; gg < (g < 0 ? kChunks : g + 1); ++gg)
+      HT_TRY(xfer(s, c.dest, true, host, rb, const_cast<float*>(dev), rb, rb,
+                  chunk_bound(f->nrows, gg), chunk_bound(f->nrows, gg + 1)));
+    return HT_OK;
+  }
+  if (g > 0) return HT_OK;
+  return launch_copy(s, host, dev, c.dest_rows.as<int64_t>(), nullptr, c.nv, rb, rb, rb, 0,
+                     kHostGrid);
 }
 
 // K6, early: reload the checkpoint rows of `layer` into their per-layer
@@ -1534,6 +1576,9 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
         d.cache = fits;
       }
     }
+    if (f->host_compact && !d.cache)
+      return fail(HT_EINVAL, "compact host arrays need the HBM owner cache (mode on/auto, and "
+                             "enough free HBM for the mirrors)");
     if (d.cache) {
       d.mh.resize(L);
       d.ma.resize(gat ? 0 : L);
@@ -1572,6 +1617,25 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
 extern "C" int ht_fleet_set_cache(ht_fleet* f, int mode) {
   if (mode < 0 || mode > 2) return fail(HT_EINVAL, "cache mode must be 0 (off), 1 (on) or 2 (auto)");
   f->cache_req = mode;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t n) {
+  if (!rows || n <= 0) {
+    f->host_compact = false;
+    return HT_OK;
+  }
+  if (!f->finalized) return fail(HT_ESTATE, "fleet not finalized");
+  int local = 0;
+  for (auto& d : f->dev) local += d.local ? 1 : 0;
+  if (local != 1) return fail(HT_EINVAL, "compact host arrays need a fleet with one local device");
+  for (auto& d : f->dev)
+    if (d.local) {
+      if (!f->cache_ok || (int64_t)d.mrows.size() != n || !std::equal(rows, rows + n, d.mrows.begin()))
+        return fail(HT_EINVAL, "compact host arrays must hold exactly the owned rows of the "
+                               "fleet's device (ascending), and the plan must admit the cache");
+    }
+  f->host_compact = true;
   return HT_OK;
 }
 
@@ -1733,36 +1797,25 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
         if (nck > 1) {
           HT_TRY(ev_rec(d.e_gchunk[g], d.stream));
           HT_TRY(ev_wait(d.tout, d.e_gchunk[g]));
-          HT_TRY(xfer(d.tout, c.dest, true, hout, rbo, hdst, rbo, rbo, chunk_bound(f->nrows, g),
-                      chunk_bound(f->nrows, g + 1)));
+          HT_TRY(put_dest(f, c, d.tout, hout, hdst, rbo, g));
           if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
         }
       }
       HT_TRY(ev_rec(d.e_comp, d.stream));
       // K5: (remaining) destination rows, then checkpoint rows, to the host store
       HT_TRY(ev_wait(d.tout, d.e_comp));
-      if (c.dest.dma) {
-        if (nck == 1)
-          for (int g = 0; g < kChunks; ++g) {
-            HT_TRY(xfer(d.tout, c.dest, true, hout, rbo, hdst, rbo, rbo, chunk_bound(f->nrows, g),
-                        chunk_bound(f->nrows, g + 1)));
-            if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
-          }
-        // checkpoint rows, chunked: the first backward layer reloads the last
-        // forward layer's checkpoints chunk by chunk as they land
+      if (nck == 1)
         for (int g = 0; g < kChunks; ++g) {
-          HT_TRY(xfer(d.tout, c.dest, true, aout, rbi, agg, rbi, rbi, chunk_bound(f->nrows, g),
-                      chunk_bound(f->nrows, g + 1)));
-          if (lastb) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
+          HT_TRY(put_dest(f, c, d.tout, hout, hdst, rbo, g));
+          if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
         }
-      } else {
-        HT_TRY(launch_copy(d.tout, hout, hdst, rows, nullptr, c.nv, rbo, rbo, rbo, 0, kHostGrid));
-        if (lastb)
-          for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
-        HT_TRY(launch_copy(d.tout, aout, agg, rows, nullptr, c.nv, rbi, rbi, rbi, 0, kHostGrid));
-        if (lastb)
-          for (int g = 0; g < kChunks; ++g) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
+      // checkpoint rows, chunked: the first backward layer reloads the last
+      // forward layer's checkpoints chunk by chunk as they land
+      for (int g = 0; g < kChunks; ++g) {
+        HT_TRY(put_dest(f, c, d.tout, aout, agg, rbi, g));
+        if (lastb) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
       }
+      (void)rows;
       HT_TRY(ev_rec(d.e_out[s], d.tout));
       if (lastb && f->prefetch && !d.cache) HT_TRY(prefetch_checkpoints(f, d, layer, aout, rbi));
       d.fwd_count++;
@@ -2401,14 +2454,7 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
                 (double)c.ne * (12.0 + 4.0 * d_out) + (double)c.nv * (8.0 * d_out + 16.0), d.stream);
       HT_TRY(ev_rec(d.e_comp, d.stream));
       HT_TRY(ev_wait(d.tout, d.e_comp));
-      if (c.dest.dma) {
-        for (int g = 0; g < kChunks; ++g)
-          HT_TRY(xfer(d.tout, c.dest, true, hout, rbo, H, rbo, rbo, chunk_bound(f->nrows, g),
-                      chunk_bound(f->nrows, g + 1)));
-      } else {
-        HT_TRY(launch_copy(d.tout, hout, H, c.dest_rows.as<int64_t>(), nullptr, c.nv, rbo, rbo, rbo,
-                           0, kHostGrid));
-      }
+      HT_TRY(put_dest(f, c, d.tout, hout, H, rbo, -1));
       HT_TRY(ev_rec(d.e_out[s], d.tout));
       if (j == f->n - 1) HT_TRY(ev_rec(d.e_hst, d.tout));  // layer output complete
       d.fwd_count++;

@@ -124,7 +124,7 @@ class HostStore:
     the HongTu setting) or HBM (``placement="device"``, HongTu-IM)."""
 
     def __init__(self, num_vertices: int, dims: list, dtype=np.float64, placement: str = "host",
-                 device: int = 0):
+                 device: int = 0, rows=None):
         if placement not in ("host", "device"):
             raise SimulationError(f"unknown placement {placement!r}")
         self.num_vertices = int(num_vertices)
@@ -132,6 +132,16 @@ class HostStore:
         self.dtype = np.dtype(dtype)
         self.placement = placement
         self.device = device
+        # compact store (rank mode): only these vertices' rows, ascending -
+        # row k of every array is vertex rows[k] (new; the reference keeps
+        # all V rows in one process)
+        self.rows = None
+        if rows is not None:
+            r = np.ascontiguousarray(rows, dtype=np.int64)
+            if r.ndim != 1 or (r.size > 1 and np.any(r[1:] <= r[:-1])) or \
+                    (r.size and (r[0] < 0 or r[-1] >= self.num_vertices)):
+                raise SimulationError("HostStore rows must be ascending unique vertex ids")
+            self.rows = r
         self.h = [self._alloc(d) for d in self.dims]
         self.grad_h = [self._alloc(d) for d in self.dims]
         self.h_valid = [False] * len(self.dims)
@@ -139,7 +149,7 @@ class HostStore:
         self.agg_written = set()
 
     def _alloc(self, d):
-        shape = (self.num_vertices, d)
+        shape = (self.num_vertices if self.rows is None else self.rows.size, d)
         if self.placement == "device":
             return DeviceArray(shape, self.dtype, self.device)
         return N.pinned_zeros(shape, self.dtype)
@@ -150,7 +160,10 @@ class HostStore:
         return self.agg[layer]
 
     def set_features(self, features) -> None:
-        X = np.asarray(features, dtype=self.dtype)
+        X = np.asarray(features)
+        if self.rows is not None and X.ndim == 2 and X.shape[0] == self.num_vertices:
+            X = X[self.rows]  # a compact store takes its rows of the full matrix
+        X = np.asarray(X, dtype=self.dtype)
         if X.shape != tuple(self.h[0].shape):
             raise SimulationError(f"feature matrix shape {X.shape} does not match "
                                   f"(num_vertices, d0) = {tuple(self.h[0].shape)}")

@@ -213,6 +213,14 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     want = _CACHE_MODES[fleet.cache]
     if fleet.cache == "auto" and host.placement != "host":
         want = 0
+    if host.rows is not None:  # compact store: host row k = owned row k (needs the cache)
+        want = 1
+        if getattr(fleet, "_compact_for", None) is not host:
+            N.call("ht_fleet_set_host_rows", h_, N.ptr(host.rows), int(host.rows.size))
+            fleet._compact_for = host
+    elif getattr(fleet, "_compact_for", None) is not None:
+        N.call("ht_fleet_set_host_rows", h_, None, 0)
+        fleet._compact_for = None
     N.call("ht_fleet_set_cache", h_, want)
     N.call("ht_gat_epoch_begin" if gat else "ht_epoch_begin", h_, L, dims_c)
     on = C.c_int(0)

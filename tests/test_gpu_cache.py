@@ -66,3 +66,42 @@ def test_cache_refused_in_baseline_mode():
         _epochs(p, ds, [8, 8, 4], "gcn", "on", mode="baseline", epochs=1)
     _, _, active = _epochs(p, ds, [8, 8, 4], "gcn", "auto", mode="baseline", epochs=1)
     assert not active
+
+
+def test_compact_host_store_single_device():
+    """A compact store holding all rows (m = 1) is the full store; the
+    compact path (contiguous host copies) must give bitwise the same epoch."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=2000, avg_degree=8.0, seed=6), 16, 8)
+    a = H.partition_vertices(ds.graph, 1, seed=6)
+    p = H.split_chunks(ds.graph, a, 2)
+    dims = [16, 24, 8]
+    plan = H.plan_for_partition(p)
+    outs = []
+    for rows in (None, np.arange(ds.graph.num_vertices)):
+        model = H.init_model("gcn", dims, seed=3, lr=0.1, dtype=np.float32)
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, rows=rows)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, dtype=np.float32)
+        r = H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+        outs.append((r.loss, [w.copy() for w in model.weights], np.array(host.grad_h[0]),
+                     np.array(host.h[2]), np.array(host.agg[1])))
+    a_, b_ = outs
+    assert a_[0] == b_[0]
+    for x, y in zip(a_[1:], b_[1:]):
+        np.testing.assert_array_equal(x if not isinstance(x, list) else np.concatenate(
+            [w.ravel() for w in x]), y if not isinstance(y, list) else np.concatenate(
+            [w.ravel() for w in y]))
+
+
+def test_compact_host_store_rejected_for_multi_device_fleet():
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=1000, avg_degree=6.0, seed=2), 8, 4)
+    a = H.partition_vertices(ds.graph, 2, seed=2)
+    p = H.split_chunks(ds.graph, a, 1)
+    plan = H.plan_for_partition(p)
+    model = H.init_model("gcn", [8, 8, 4], seed=1, dtype=np.float32)
+    host = H.HostStore(ds.graph.num_vertices, [8, 8, 4], dtype=np.float32,
+                       rows=np.flatnonzero(a.owner == 0))
+    host.set_features(ds.features)
+    fleet = H.DeviceFleet(plan, dtype=np.float32)
+    with pytest.raises(H.ChunktrainError, match="one local device"):
+        H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)

@@ -22,7 +22,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir, mode, kind, cache):
+def _worker(rank, world, port, out_dir, mode, kind, cache, compact=False):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as tdist
@@ -35,7 +35,8 @@ def _worker(rank, world, port, out_dir, mode, kind, cache):
     plan = H.plan_for_partition(p)
     dims = [16, 24, 8]
     model = H.init_model(kind, dims, seed=3, lr=0.1, dtype=np.float32)
-    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+    own = np.flatnonzero(a.owner == rank) if compact else None
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, rows=own)
     host.set_features(ds.features)
     fleet = H.DeviceFleet(plan, mode=mode, dtype=np.float32, precision="fp32", rank=rank,
                           devices=[0], cache=cache)
@@ -43,10 +44,12 @@ def _worker(rank, world, port, out_dir, mode, kind, cache):
     for _ in range(2):
         losses.append(H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss)
     mine = np.concatenate(plan.dest_sets[rank])
+    gh0 = np.asarray(host.grad_h[0])
+    gh0 = gh0[np.searchsorted(own, mine)] if compact else gh0[mine]
     res = {"losses": losses, "W": [w.tolist() for w in model.weights],
            "A": [x.tolist() for x in model.attn] if kind == "gat" else None,
            "cache": fleet.cache_active,
-           "gh0_rows": mine.tolist(), "gh0": np.asarray(host.grad_h[0])[mine].tolist(),
+           "gh0_rows": mine.tolist(), "gh0": gh0.tolist(),
            "report": fleet.transfer_report(
                *(2 * x for x in H.comm_passes_per_epoch(model)))["planner_consistent"]}
     with open(os.path.join(out_dir, f"r{rank}.json"), "w") as fh:
@@ -54,10 +57,11 @@ def _worker(rank, world, port, out_dir, mode, kind, cache):
     tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,mode,cache", [("gcn", "full", "auto"), ("gcn", "p2p", "auto"),
-                                             ("gcn", "full", "off"), ("gat", "full", "auto"),
-                                             ("gat", "p2p", "off")])
-def test_two_ranks_share_one_gpu(tmp_path, kind, mode, cache):
+@pytest.mark.parametrize("kind,mode,cache,compact", [
+    ("gcn", "full", "auto", False), ("gcn", "p2p", "auto", False), ("gcn", "full", "off", False),
+    ("gcn", "full", "auto", True), ("gat", "full", "auto", False), ("gat", "p2p", "off", False),
+    ("gat", "full", "auto", True)])
+def test_two_ranks_share_one_gpu(tmp_path, kind, mode, cache, compact):
     import sys
     sys.path.insert(0, ROOT)
     import paper_2311_14898_b200 as H
@@ -65,7 +69,8 @@ def test_two_ranks_share_one_gpu(tmp_path, kind, mode, cache):
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
-    procs = [ctx.Process(target=_worker, args=(r, world, port, str(tmp_path), mode, kind, cache))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, str(tmp_path), mode, kind, cache,
+                                                    compact))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -76,7 +81,7 @@ def test_two_ranks_share_one_gpu(tmp_path, kind, mode, cache):
     assert out[0]["losses"] == out[1]["losses"]
     assert out[0]["W"] == out[1]["W"]
     assert out[0]["A"] == out[1]["A"]
-    assert out[0]["cache"] == out[1]["cache"] == (cache == "auto")
+    assert out[0]["cache"] == out[1]["cache"] == (cache == "auto" or compact)
     assert out[0]["report"] and out[1]["report"]
     # oracle: the same partitioned epochs in one process
     ds = H.synth_dataset(H.SynthSpec(num_vertices=4000, avg_degree=8.0, seed=9), 16, 8)
