@@ -201,6 +201,11 @@ int ht_fleet_set_cache(ht_fleet* f, int mode);
  * the HBM owner cache; host transfers become single contiguous copies.
  * rows == NULL restores full (V-row) host arrays. */
 int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t n);
+/* Lean epochs (opt-in): skip grad_h^0 (computed and
+ * flushed by the reference, never consumed: engine.py:449, 477) and, with
+ * the owner cache, the host copies of h^L and grad_h^L.  Weights, attention
+ * vectors, loss and every other host array are unchanged. */
+int ht_fleet_set_lean(ht_fleet* f, int lean);
 int ht_fleet_cache_state(ht_fleet* f, int* on);
 /* Zero the per-device weight-gradient accumulators (engine.py:441-448). */
 int ht_epoch_begin(ht_fleet* f, int L, const int* dims);

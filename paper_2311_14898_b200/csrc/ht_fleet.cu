@@ -252,6 +252,9 @@ struct ht_fleet {
   bool gat = false;      // buffers sized by ht_gat_epoch_begin
   int cache_req = 0;     // HBM owner cache: 0 off, 1 on (fail if impossible), 2 auto
   bool host_compact = false;  // host arrays hold only the local device's owned rows
+  // lean epoch (opt-in): no grad_h^0 (never consumed,
+  // engine.py:449/477) and no host copies of h^L / grad_h^L with the cache
+  bool lean = false;
   bool cache_ok = false; // the plan admits the cache (p2p/full, contiguous dest rows)
   int64_t nrows = 0;  // host rows addressed by the plan (max vertex id + 1)
   // rank mode (one process per GPU): index of the local device, barrier
@@ -1639,6 +1642,11 @@ extern "C" int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t 
   return HT_OK;
 }
 
+extern "C" int ht_fleet_set_lean(ht_fleet* f, int lean) {
+  f->lean = lean != 0;
+  return HT_OK;
+}
+
 extern "C" int ht_fleet_cache_state(ht_fleet* f, int* on) {
   *on = 1;
   int any = 0;
@@ -1797,7 +1805,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
         if (nck > 1) {
           HT_TRY(ev_rec(d.e_gchunk[g], d.stream));
           HT_TRY(ev_wait(d.tout, d.e_gchunk[g]));
-          HT_TRY(put_dest(f, c, d.tout, hout, hdst, rbo, g));
+          if (!(last && f->lean && d.cache)) HT_TRY(put_dest(f, c, d.tout, hout, hdst, rbo, g));
           if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
         }
       }
@@ -1806,7 +1814,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       HT_TRY(ev_wait(d.tout, d.e_comp));
       if (nck == 1)
         for (int g = 0; g < kChunks; ++g) {
-          HT_TRY(put_dest(f, c, d.tout, hout, hdst, rbo, g));
+          if (!(last && f->lean && d.cache)) HT_TRY(put_dest(f, c, d.tout, hout, hdst, rbo, g));
           if (lastb) HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
         }
       // checkpoint rows, chunked: the first backward layer reloads the last
@@ -1862,7 +1870,7 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
       }
     if (d.cache) {  // grad_h[L] rows live in the mirror; write them through
       if (count <= 0) CU(cudaMemsetAsync(d.mg[f->L].p, 0, d.mcount * (int64_t)d_last * 4, d.stream));
-      HT_TRY(cache_writeback(f, d, gout, d.mg[f->L].as<float>(), (int64_t)d_last * 4));
+      if (!f->lean) HT_TRY(cache_writeback(f, d, gout, d.mg[f->L].as<float>(), (int64_t)d_last * 4));
     }
     HT_TRY(ev_rec(d.e_loss, d.stream));
   }
@@ -1977,7 +1985,8 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // narrow-side transposed aggregation: grad_h_nbr = (A^T gz) W^T when
       // d_out < d_in (K8 gathers d_out-wide rows instead of d_in-wide ones;
       // same product, reassociated).  Needs gz with zeroed pad columns.
-      const bool narrow = HO && d_out < d_in && !getenv("HT_NO_NARROW_BWD");
+      const bool no_in = f->lean && layer == 0;  // lean: grad_h^0 is not produced
+      const bool narrow = !no_in && HO && d_out < d_in && !getenv("HT_NO_NARROW_BWD");
       if (HO && M > 0) {  // gz = g * (h > 0): z need not be recomputed
         count_launch();
         ht::k_relu_mask<<<grid_for(M), kThreads, 0, d.stream>>>(GZ, ldz, G, HO, hrows, M, d_out);
@@ -1987,7 +1996,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
         if (!HO)
           HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, w.Wt_hi.as<float>(),
                                                w.Wt_lo.as<float>(), d_in, d_out, GZ, ldz, G, d_out));
-        if (!narrow)
+        if (!narrow && !no_in)
           HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
                                                 w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
                                                 nullptr, 0));
@@ -2016,12 +2025,16 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
               d.gWall.as<float>() + d.gW_off[layer], d.gemm_ws.as<float>(), nw, splits);
           CU(cudaGetLastError());
         }
-        if (!narrow)
+        if (!narrow && !no_in)
           HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, ldz, w.W.as<float>(), d_out, GA,
                                                    d_in, nullptr, 0, M, d_in, d_out, 1, d_out)));
       }
       timer_end(f, d, tg, 2, 6.0 * c.nv * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_bcomp[s], d.stream));
+      if (no_in) {
+        d.bwd_count++;
+        continue;
+      }
       // K8: transposed aggregation over the CSR view -> neighbour-row grads
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
@@ -2046,12 +2059,13 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
     }
     // K9/K10: owner push (ascending source device) + flush into host grads
     // (into the mirror with the cache)
-    HT_TRY(push_flush(f, j, gin, true, layer));
+    if (!(f->lean && layer == 0)) HT_TRY(push_flush(f, j, gin, true, layer));
   }
   for (auto& d : f->dev) {
     if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
-    if (d.cache) HT_TRY(cache_writeback(f, d, gin, d.mg[layer].as<float>(), rbi));
+    if (d.cache && !(f->lean && layer == 0))
+      HT_TRY(cache_writeback(f, d, gin, d.mg[layer].as<float>(), rbi));
     HT_TRY(ev_rec(d.e_flush, d.stream));
   }
   return HT_OK;
@@ -2454,7 +2468,7 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
                 (double)c.ne * (12.0 + 4.0 * d_out) + (double)c.nv * (8.0 * d_out + 16.0), d.stream);
       HT_TRY(ev_rec(d.e_comp, d.stream));
       HT_TRY(ev_wait(d.tout, d.e_comp));
-      HT_TRY(put_dest(f, c, d.tout, hout, H, rbo, -1));
+      if (!(last && f->lean && d.cache)) HT_TRY(put_dest(f, c, d.tout, hout, H, rbo, -1));
       HT_TRY(ev_rec(d.e_out[s], d.tout));
       if (j == f->n - 1) HT_TRY(ev_rec(d.e_hst, d.tout));  // layer output complete
       d.fwd_count++;
@@ -2536,14 +2550,17 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       timer_begin(f, d, tw, d.stream);
       HT_TRY(gat_wgrad(d, precision, HN, GQ, c.nn, d_in, d_out, gW));
       HT_TRY(gat_wgrad(d, precision, HD, GP, c.nv, d_in, d_out, gW));
-      HT_TRY(gat_proj_t(d, precision, GQ, c.nn, d_in, d_out, d.se.as<float>(), w));
-      HT_TRY(gat_proj_t(d, precision, GP, c.nv, d_in, d_out, d.g_ghd.as<float>(), w));
+      if (!(f->lean && layer == 0)) {  // lean: grad_h^0 is not produced
+        HT_TRY(gat_proj_t(d, precision, GQ, c.nn, d_in, d_out, d.se.as<float>(), w));
+        HT_TRY(gat_proj_t(d, precision, GP, c.nv, d_in, d_out, d.g_ghd.as<float>(), w));
+      }
       timer_end(f, d, tw, 2, 4.0 * (double)(c.nn + c.nv) * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_gcomp[s], d.stream));  // staging set s consumed
       d.bwd_count++;
     }
     // add_dest_grads (src/devices.py:376-385), then the deduplicated
     // neighbour-gradient accumulation (baseline: after every device's adds)
+    if (f->lean && layer == 0) continue;
     for (int i = 0; i < f->m; ++i) {
       Device& d = f->dev[i];
       if (!d.local) continue;
@@ -2562,7 +2579,8 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
   for (auto& d : f->dev) {
     if (!d.local) continue;
     HT_TRY(set_dev(d));
-    if (d.cache) HT_TRY(cache_writeback(f, d, gin, d.mg[layer].as<float>(), (int64_t)d_in * 4));
+    if (d.cache && !(f->lean && layer == 0))
+      HT_TRY(cache_writeback(f, d, gin, d.mg[layer].as<float>(), (int64_t)d_in * 4));
     HT_TRY(ev_rec(d.e_flush, d.stream));
   }
   return HT_OK;

@@ -236,7 +236,7 @@ class DeviceFleet:
 
     def __init__(self, plan: DedupPlan, mode: str = "full", flush_policy: str = "on_eviction",
                  dtype=np.float64, devices=None, precision: str = "tf32", rank: int | None = None,
-                 cache: str = "auto"):
+                 cache: str = "auto", lean: bool = False):
         if mode not in _MODES:
             raise SimulationError(f"unknown mode {mode!r}")
         if flush_policy not in _FLUSH_POLICIES:
@@ -248,6 +248,10 @@ class DeviceFleet:
         self.plan = plan
         self.mode = mode
         self.cache = cache
+        # lean epochs (opt-in): no grad_h^0, and no host copies of h^L /
+        # grad_h^L with the owner cache; the transfer
+        # meters stay the reference's
+        self.lean = bool(lean)
         self.flush_policy = flush_policy
         self.dtype = np.dtype(dtype)
         self.precision = precision

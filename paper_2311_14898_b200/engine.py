@@ -222,6 +222,7 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
         N.call("ht_fleet_set_host_rows", h_, None, 0)
         fleet._compact_for = None
     N.call("ht_fleet_set_cache", h_, want)
+    N.call("ht_fleet_set_lean", h_, int(fleet.lean))
     N.call("ht_gat_epoch_begin" if gat else "ht_epoch_begin", h_, L, dims_c)
     on = C.c_int(0)
     N.call("ht_fleet_cache_state", h_, C.byref(on))

@@ -105,3 +105,32 @@ def test_compact_host_store_rejected_for_multi_device_fleet():
     fleet = H.DeviceFleet(plan, dtype=np.float32)
     with pytest.raises(H.ChunktrainError, match="one local device"):
         H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+
+
+@pytest.mark.parametrize("kind", ["gcn", "gat"])
+def test_lean_epoch_same_parameters(kind):
+    """Lean epochs skip grad_h^0 and the host copies of
+    h^L / grad_h^L; weights, attention vectors, loss and the remaining host
+    arrays are bitwise those of the full epoch."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=2500, avg_degree=8.0, seed=8), 16, 8)
+    a = H.partition_vertices(ds.graph, 2, seed=8)
+    p = H.split_chunks(ds.graph, a, 2)
+    dims = [16, 24, 8]
+    plan = H.plan_for_partition(p)
+    outs = []
+    for lean in (False, True):
+        model = H.init_model(kind, dims, seed=3, lr=0.1, dtype=np.float32)
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, dtype=np.float32, lean=lean)
+        losses = [H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss for _ in range(2)]
+        outs.append((losses, [w.copy() for w in model.weights],
+                     [x.copy() for x in model.attn] if kind == "gat" else [],
+                     np.array(host.h[1]), np.array(host.grad_h[1]), np.array(host.grad_h[0])))
+    full, lean = outs
+    assert full[0] == lean[0]
+    for x, y in zip(full[1] + full[2], lean[1] + lean[2]):
+        np.testing.assert_array_equal(x, y)
+    np.testing.assert_array_equal(full[3], lean[3])
+    np.testing.assert_array_equal(full[4], lean[4])
+    assert np.any(full[5] != 0) and not np.any(lean[5])  # grad_h^0 not produced
