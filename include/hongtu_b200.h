@@ -206,6 +206,12 @@ int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t n);
  * the owner cache, the host copies of h^L and grad_h^L.  Weights, attention
  * vectors, loss and every other host array are unchanged. */
 int ht_fleet_set_lean(ht_fleet* f, int lean);
+/* HBM-resident store (HongTu-IM) on a single device: its device arrays
+ * h[0..L], agg[0..L-1] (NULL for GAT), grad[0..L] are used as the owner
+ * cache's mirrors (the layers read and write them in place, no copies).
+ * h == NULL clears.  Takes effect at the next ht_(gat_)epoch_begin. */
+int ht_fleet_alias_store(ht_fleet* f, int L, void* const* h, void* const* agg,
+                         void* const* grad);
 int ht_fleet_cache_state(ht_fleet* f, int* on);
 /* Zero the per-device weight-gradient accumulators (engine.py:441-448). */
 int ht_epoch_begin(ht_fleet* f, int L, const int* dims);

@@ -39,7 +39,9 @@ struct DBuf {
   int64_t bytes = 0;
   int dev = 0;
   bool owned = true;  // false: a peer process's buffer mapped through CUDA IPC
+  bool alias = false; // true: a caller-owned device array (an HBM host store)
   int ensure(int64_t want) {
+    if (alias) p = nullptr, bytes = 0, alias = false;
     if (want <= bytes) return HT_OK;
     if (!owned) return fail(HT_ESTATE, "cannot grow a buffer shared with peer processes");
     if (p) cudaFree(p);
@@ -51,13 +53,19 @@ struct DBuf {
     return HT_OK;
   }
   void release() {
-    if (p) {
+    if (p && !alias) {
       if (owned) cudaFree(p);
       else cudaIpcCloseMemHandle(p);
     }
     p = nullptr;
     bytes = 0;
     owned = true;
+    alias = false;
+  }
+  void set_alias(void* q) {
+    release();
+    p = q;
+    alias = true;
   }
   template <class T>
   T* as() const { return static_cast<T*>(p); }
@@ -255,6 +263,9 @@ struct ht_fleet {
   // lean epoch (opt-in): no grad_h^0 (never consumed,
   // engine.py:449/477) and no host copies of h^L / grad_h^L with the cache
   bool lean = false;
+  // HBM store (placement "device") on a single device: its arrays serve as
+  // the owner-cache mirrors directly (h[0..L], agg[0..L-1], grad[0..L])
+  std::vector<void*> alias_h, alias_a, alias_g;
   bool cache_ok = false; // the plan admits the cache (p2p/full, contiguous dest rows)
   int64_t nrows = 0;  // host rows addressed by the plan (max vertex id + 1)
   // rank mode (one process per GPU): index of the local device, barrier
@@ -1428,6 +1439,7 @@ const float* hbm_inputs(ht_fleet* f, Device& d, int layer, const void* hin) {
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
 int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
                  int64_t rb) {
+  if (host == mirror) return HT_OK;  // an aliased HBM store is its own mirror
   if (f->host_compact) {  // host array = owned rows in mirror order
     if (d.mcount) CU(cudaMemcpyAsync(mirror, host, d.mcount * rb, cudaMemcpyDefault, s));
     return HT_OK;
@@ -1441,6 +1453,7 @@ int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float
 // HBM owner cache: write a mirror through to the host rows (on tout, after
 // everything enqueued so far on the compute stream)
 int cache_writeback(ht_fleet* f, Device& d, void* host, const float* mirror, int64_t rb) {
+  if (host == mirror) return HT_OK;  // aliased HBM store
   HT_TRY(ev_rec(d.e_mg, d.stream));
   HT_TRY(ev_wait(d.tout, d.e_mg));
   if (f->host_compact) {
@@ -1459,6 +1472,9 @@ int cache_writeback(ht_fleet* f, Device& d, void* host, const float* mirror, int
 // or - compact host arrays - one contiguous copy at the mirror position.
 int put_dest(ht_fleet* f, DevChunk& c, cudaStream_t s, void* host, const float* dev, int64_t rb,
              int g) {
+  // rows already in place (an aliased HBM store written directly)
+  if (c.dest_m0 >= 0 && reinterpret_cast<const char*>(dev) == static_cast<char*>(host) + c.dest_m0 * rb)
+    return HT_OK;
   if (f->host_compact) {
     int64_t r0 = 0, r1 = c.nv;
     if (g >= 0) {
@@ -1543,24 +1559,34 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
       np = std::max({np, d.chunks[j].fw_np, d.chunks[j].bw_np});
       d.hL_off[j + 1] = d.hL_off[j] + d.chunks[j].nv;
     }
-    HT_TRY(d.value.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
+    // sized for 180 GB of HBM: the buffers every path needs first, then
+    // either the owner-cache mirrors or the host-path staging sets
     HT_TRY(d.grad.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
-    for (int s = 0; s < 2; ++s) {
-      HT_TRY(d.fa[s].ensure(mv * dmax * 4));
-      HT_TRY(d.fb[s].ensure(mv * dmax * 4));
-      HT_TRY(d.ba[s].ensure(mv * dmax * 4));
-      HT_TRY(d.bb[s].ensure(mv * dmax * 4));
-    }
     HT_TRY(d.sc.ensure(mv * dmax * 4));
     HT_TRY(d.sd.ensure(mv * dmax * 4));
     HT_TRY(d.se.ensure(mn * dmax * 4));
-    HT_TRY(d.tT.ensure(mn * dmax * 4));
+    int narrow_w = 0;  // widest d_out of the layers whose backward runs narrow-side
+    for (int l = 0; l < L; ++l)
+      if (dims[l + 1] < dims[l]) narrow_w = std::max(narrow_w, pad4(dims[l + 1]));
+    if (narrow_w) HT_TRY(d.tT.ensure(mn * narrow_w * 4));
     HT_TRY(d.partial.ensure(np * dmax * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
-    // HBM owner cache: decided per epoch (requested mode, plan, free HBM)
+    // HBM owner cache: decided per epoch (requested mode, plan, free HBM).
+    // An HBM store on one device with the identity row map *is* the mirror.
     d.cache = false;
-    if (f->cache_req != 0) {
+    const bool alias = !f->alias_h.empty() && (int)f->alias_h.size() == L + 1 && f->cache_ok &&
+                       f->m == 1 && d.mcount == f->nrows &&
+                       (gat || (int)f->alias_a.size() == L);
+    if (alias) {
+      d.cache = true;
+      d.mh.resize(L);
+      d.ma.resize(gat ? 0 : L);
+      d.mg.resize(L + 1);
+      for (int l = 0; l < L; ++l) d.mh[l].set_alias(f->alias_h[l]);
+      for (int l = 0; l < (gat ? 0 : L); ++l) d.ma[l].set_alias(f->alias_a[l]);
+      for (int l = 0; l <= L; ++l) d.mg[l].set_alias(f->alias_g[l]);
+    } else if (f->alias_h.empty() && f->cache_req != 0) {  // (an HBM store needs no mirror)
       if (!f->cache_ok) {
         if (f->cache_req == 1)
           return fail(HT_EINVAL, "HBM owner cache needs mode p2p/full and destination sets that "
@@ -1569,7 +1595,12 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
         int64_t per_row = 0;
         for (int l = 0; l < L; ++l) per_row += dims[l] * (gat ? 1 : 2);  // h (+ agg)
         for (int l = 0; l <= L; ++l) per_row += dims[l];                // grad
-        const int64_t need = d.mcount * per_row * 4;
+        int64_t need = d.mcount * per_row * 4;
+        if (gat) {  // GAT staging allocated after this decision (ht_gat_epoch_begin)
+          int64_t me = 1;
+          for (int j = 0; j < f->n; ++j) me = std::max(me, d.chunks[j].ne);
+          need += (3 * mn + 4 * mv) * (int64_t)dmax * 4 + 2 * me * 4 + 2 * me * 4;
+        }
         size_t fr = 0, tot = 0;
         CU(cudaMemGetInfo(&fr, &tot));
         const bool fits = need + ((int64_t)4 << 30) <= (int64_t)fr;
@@ -1579,10 +1610,22 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
         d.cache = fits;
       }
     }
+    // the slot value buffer: not needed when a single device's gathers read
+    // the identity-mapped mirror in place (hbm_inputs)
+    const bool direct = d.cache && f->m == 1 && d.chunks[0].csc_gid.p &&
+                        d.mcount == f->nrows && !getenv("HT_NO_DIRECT_READ");
+    if (!direct) HT_TRY(d.value.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
+    if (!d.cache)
+      for (int s = 0; s < 2; ++s) {
+        HT_TRY(d.fa[s].ensure(mv * dmax * 4));
+        HT_TRY(d.fb[s].ensure(mv * dmax * 4));
+        HT_TRY(d.ba[s].ensure(mv * dmax * 4));
+        HT_TRY(d.bb[s].ensure(mv * dmax * 4));
+      }
     if (f->host_compact && !d.cache)
       return fail(HT_EINVAL, "compact host arrays need the HBM owner cache (mode on/auto, and "
                              "enough free HBM for the mirrors)");
-    if (d.cache) {
+    if (d.cache && !alias) {
       d.mh.resize(L);
       d.ma.resize(gat ? 0 : L);
       d.mg.resize(L + 1);
@@ -1639,6 +1682,22 @@ extern "C" int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t 
                                "fleet's device (ascending), and the plan must admit the cache");
     }
   f->host_compact = true;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_alias_store(ht_fleet* f, int L, void* const* h, void* const* agg,
+                                    void* const* grad) {
+  f->alias_h.clear();
+  f->alias_a.clear();
+  f->alias_g.clear();
+  if (!h) return HT_OK;
+  for (int l = 0; l <= L; ++l) {
+    if (!is_dev_mem(h[l]) || !is_dev_mem(grad[l]) || (agg && l < L && !is_dev_mem(agg[l])))
+      return fail(HT_EINVAL, "aliased store arrays must be device memory");
+  }
+  f->alias_h.assign(h, h + L + 1);
+  f->alias_g.assign(grad, grad + L + 1);
+  if (agg) f->alias_a.assign(agg, agg + L);
   return HT_OK;
 }
 
@@ -2397,10 +2456,11 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
     int64_t np = 1;
     for (int j = 0; j < f->n; ++j) np = std::max(np, d.chunks[j].bw_np);
     HT_TRY(d.g_pgts.ensure(np * 4));
-    for (int s = 0; s < 2; ++s) {
-      HT_TRY(d.g_hd[s].ensure(mv * dmax * 4));
-      HT_TRY(d.g_gin[s].ensure(mv * dmax * 4));
-    }
+    if (!d.cache)  // with the owner cache these rows are read in place
+      for (int s = 0; s < 2; ++s) {
+        HT_TRY(d.g_hd[s].ensure(mv * dmax * 4));
+        HT_TRY(d.g_gin[s].ensure(mv * dmax * 4));
+      }
     // pinned scratch: the weight slots of the epoch + the attention vectors
     const int64_t want = d.wpin_off[L] + d.gA_off[L];
     if (d.wpin_cap < want) {

@@ -221,6 +221,16 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     elif getattr(fleet, "_compact_for", None) is not None:
         N.call("ht_fleet_set_host_rows", h_, None, 0)
         fleet._compact_for = None
+    # an HBM store on one device is used in place as the owner-cache mirror
+    alias = host.placement == "device" and fleet.m == 1 and fleet.cache != "off" and \
+        host.rows is None and fleet.mode != "baseline"
+    if alias:
+        hp = (C.c_void_p * (L + 1))(*[N.ptr(x) for x in host.h])
+        gp_ = (C.c_void_p * (L + 1))(*[N.ptr(x) for x in host.grad_h])
+        ap_ = None if gat else (C.c_void_p * L)(*[N.ptr(host.agg_array(l)) for l in range(L)])
+        N.call("ht_fleet_alias_store", h_, L, hp, ap_, gp_)
+    else:
+        N.call("ht_fleet_alias_store", h_, L, None, None, None)
     N.call("ht_fleet_set_cache", h_, want)
     N.call("ht_fleet_set_lean", h_, int(fleet.lean))
     N.call("ht_gat_epoch_begin" if gat else "ht_epoch_begin", h_, L, dims_c)

@@ -134,3 +134,29 @@ def test_lean_epoch_same_parameters(kind):
     np.testing.assert_array_equal(full[3], lean[3])
     np.testing.assert_array_equal(full[4], lean[4])
     assert np.any(full[5] != 0) and not np.any(lean[5])  # grad_h^0 not produced
+
+
+@pytest.mark.parametrize("kind", ["gcn", "gat"])
+def test_hbm_store_in_place_equals_host_store(kind):
+    """An HBM-resident store (placement="device", one device) is used in place
+    as the owner-cache mirror: same epoch, bitwise, as the pinned host store."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=2500, avg_degree=8.0, seed=5), 16, 8)
+    a = H.partition_vertices(ds.graph, 1, seed=5)
+    p = H.split_chunks(ds.graph, a, 2)
+    dims = [16, 24, 8]
+    plan = H.plan_for_partition(p)
+    outs = []
+    for placement in ("host", "device"):
+        model = H.init_model(kind, dims, seed=3, lr=0.1, dtype=np.float32)
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, dtype=np.float32)
+        losses = [H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss for _ in range(2)]
+        assert fleet.cache_active
+        snap = [np.array(x) for x in host.h] + [np.array(x) for x in host.grad_h]
+        if kind == "gcn":
+            snap += [np.array(host.agg[l]) for l in range(2)]
+        outs.append((losses, [w.copy() for w in model.weights], snap))
+    assert outs[0][0] == outs[1][0]
+    for x, y in zip(outs[0][1] + outs[0][2], outs[1][1] + outs[1][2]):
+        np.testing.assert_array_equal(x, y)
