@@ -41,6 +41,11 @@ CONFIGS = {
                  name="2-layer GCN 64-128-16, synthetic power-law 100K V / ~1.87M E"),
     "cfg2": dict(V=2_400_000, avg_degree=26.8, dims=[100, 256, 256, 47], n=1, seed=0,
                  name="3-layer GCN 100-256-256-47, ogbn-products-shape synthetic 2.4M V / ~62M E"),
+    # one GPU's share of BASELINE config 3 (friendster-shape 65.6M V / 1.8B E
+    # over 8 GPUs): 8.2M V / ~227M E, 256-128-128-64, vertex data host-resident
+    "cfg3s": dict(V=8_200_000, avg_degree=28.5, dims=[256, 128, 128, 64], n=1, seed=0,
+                  name="3-layer GCN 256-128-128-64, per-GPU share of the friendster-shape config 3 "
+                       "(8.2M V / ~227M E synthetic)"),
 }
 METRIC = "full-graph GCN epoch GTEPS (L*|E|/epoch_s)"
 
