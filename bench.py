@@ -116,11 +116,17 @@ def build_inputs(cfg, m):
     t1 = time.time()
     a = H.partition_vertices(ds.graph, m, seed=cfg["seed"])
     p = H.split_chunks(ds.graph, a, cfg["n"])
-    plan = H.plan_for_partition(p)
+    # dedup plan on the GPU: sort/unique of the chunks' raw neighbour ids
+    # (ht_gplan_build, bit-identical with the host planner)
+    from paper_2311_14898_b200 import _native as N
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count())
+    tp = time.time()
+    plan = H.plan_for_partition(p, device=dev)
+    log(f"[bench] GPU dedup planner {time.time() - tp:.2f}s")
     chosen = "identity"
     if cfg["n"] > 1:
         r = H.reorganize(p)
-        plan_r = H.plan_for_partition(r.partition)
+        plan_r = H.plan_for_partition(r.partition, device=dev)
         if H.comm_cost(plan_r.volumes) <= H.comm_cost(plan.volumes):
             p, plan, chosen = r.partition, plan_r, "reorganized"
     t2 = time.time()
