@@ -17,7 +17,7 @@
 //   k_gat_src     BWD, one warp per source u over its CSR out-edges:
 //                 gq_u = sum_e (alpha_e gs_{dst e} + g_t_e a_src) in edge
 //                 order (the np.add.at of src/engine.py:275/280), and
-//                 gts_u = sum_e g_t_e.  Power-law hubs (> 4096 out-edges)
+//                 gts_u = sum_e g_t_e.  Power-law hubs (> 1024 out-edges)
 //                 are split into pieces (k_gat_src_pieces) summed in piece
 //                 order (k_gat_src_fixup), as in the GCN transposed path.
 //   k_wcolsum / k_colsum_reduce

@@ -81,7 +81,7 @@ def test_epoch_matches_oracle_grads(m, n):
 
 
 def test_long_segments_split_path():
-    """A hub source with > 4096 out-edges and a hub destination with > 4096
+    """A hub source and a hub destination with thousands of edges (> the 1024-edge piece length)
     in-edges exercise the piece + fixup kernels in both directions."""
     rng = np.random.default_rng(9)
     V = 12000
@@ -103,7 +103,7 @@ def test_long_segments_split_path():
     ref = O.partitioned_epoch(grid, O.plan_of_grid(grid, a.owner), [w.copy() for w in w0],
                               X, labels, mask, dtype=np.float32)
     assert abs(losses[0] - ref["loss"]) <= 1e-5 * abs(ref["loss"])
-    assert O.rel_err(snaps[0]["agg0"], ref["agg"][0]) < 1e-6
+    assert O.rel_err(snaps[0]["agg0"], ref["agg"][0]) < 1e-5  # hub pieces reassociate
     assert O.rel_err(snaps[0]["gh0"], ref["grad_h"][0]) < 1e-5
     for l in range(2):
         assert O.rel_err(snaps[0]["grads"][l], ref["grads"][l]) < 1e-5
