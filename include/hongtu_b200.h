@@ -63,6 +63,11 @@ int ht_build_graph(const int64_t* src, const int64_t* dst, int64_t E, int64_t V,
                    int64_t* csc_offsets, int64_t* csc_sources, int64_t* csr_offsets,
                    int64_t* csr_targets, int64_t* csr_edge_perm, double* weights);
 
+/* CSR -> canonical edge permutation rebuilt from CSC + CSR offsets in one
+ * counting pass (replaces the np.lexsort of graph.py:262-264 on HTG1 load). */
+int ht_csr_perm(int64_t V, int64_t E, const int64_t* csc_offsets, const int64_t* csc_sources,
+                const int64_t* csr_offsets, int64_t* perm);
+
 /* synth.py:154-157 parallel-edge removal: indices (into src/dst) of the
  * first occurrence of each distinct (dst, src) pair, ascending by (dst, src),
  * i.e. np.unique(dst*V + src, return_index=True)[1].  keep holds E entries. */

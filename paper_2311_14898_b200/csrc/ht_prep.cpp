@@ -154,6 +154,30 @@ void repair_empty(std::vector<int64_t>& sizes, int64_t* owner, int64_t V,
 
 }  // namespace
 
+// CSR -> canonical permutation of a graph given by its CSC (sorted by
+// (dst, src)): CSR position k holds canonical edge perm[k], the CSR order
+// being by (src, dst) with ties in canonical order - what
+// np.lexsort((dst, csc_sources)) gives (graph.py:117).  One counting pass
+// over the canonical edges (O(E), no sort): used when an HTG1 cache is
+// loaded (graph.py:224-266).
+extern "C" int ht_csr_perm(int64_t V, int64_t E, const int64_t* csc_offsets,
+                           const int64_t* csc_sources, const int64_t* csr_offsets,
+                           int64_t* perm) {
+  if (V < 0 || E < 0) return ht::fail(HT_EINVAL, "negative sizes");
+  if (csc_offsets[V] != E || csr_offsets[V] != E)
+    return ht::fail(HT_EINVAL, "offsets do not end at the edge count");
+  std::vector<int64_t> cur(csr_offsets, csr_offsets + V);
+  for (int64_t v = 0; v < V; ++v)
+    for (int64_t e = csc_offsets[v]; e < csc_offsets[v + 1]; ++e) {
+      const int64_t u = csc_sources[e];
+      if (u < 0 || u >= V) return ht::fail(HT_EINVAL, "source id out of range");
+      const int64_t k = cur[u]++;
+      if (k >= csr_offsets[u + 1]) return ht::fail(HT_EINVAL, "CSR offsets inconsistent with CSC");
+      perm[k] = e;
+    }
+  return HT_OK;
+}
+
 extern "C" int ht_ldg_partition(int64_t V, const int64_t* csc_offsets, const int64_t* csc_sources,
                                 const int64_t* csr_offsets, const int64_t* csr_targets,
                                 const int64_t* arrival, int64_t m, int64_t cap, int64_t* owner) {

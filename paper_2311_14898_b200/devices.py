@@ -118,6 +118,25 @@ def _parallel_zero(a: np.ndarray, threads: int = 8):
         t.join()
 
 
+def _parallel_rows(dst: np.ndarray, src, threads: int = 8):
+    """dst[:] = src (with dtype conversion) in row blocks on several threads:
+    no full-size temporary, and memory-mapped sources stream in."""
+    n = dst.shape[0]
+    if n * dst.shape[1] < (1 << 22):
+        dst[:] = src
+        return
+    step = (n + threads - 1) // threads
+
+    def work(t):
+        dst[t * step:(t + 1) * step] = src[t * step:(t + 1) * step]
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+
+
 class HostStore:
     """Per-layer representations h^l, gradients and aggregation checkpoints
     (devices.py:44-75).  Arrays are pinned host memory (``placement="host"``,
@@ -160,14 +179,16 @@ class HostStore:
         return self.agg[layer]
 
     def set_features(self, features) -> None:
-        X = np.asarray(features)
+        X = features if isinstance(features, np.ndarray) else np.asarray(features)
         if self.rows is not None and X.ndim == 2 and X.shape[0] == self.num_vertices:
             X = X[self.rows]  # a compact store takes its rows of the full matrix
-        X = np.asarray(X, dtype=self.dtype)
         if X.shape != tuple(self.h[0].shape):
             raise SimulationError(f"feature matrix shape {X.shape} does not match "
                                   f"(num_vertices, d0) = {tuple(self.h[0].shape)}")
-        self.h[0][:] = X
+        if isinstance(self.h[0], DeviceArray):
+            self.h[0][:] = np.asarray(X, dtype=self.dtype)
+        else:  # cast straight into the pinned rows, in parallel row blocks
+            _parallel_rows(self.h[0], X)
         self.h_valid[0] = True
 
     def reset_epoch(self) -> None:

@@ -334,12 +334,20 @@ def save_matrix(X: np.ndarray, path: str) -> None:
         fh.write(X.astype("<f8").tobytes())
 
 
-def load_matrix(path: str) -> np.ndarray:
+def load_matrix(path: str, mmap: bool = False) -> np.ndarray:
+    """HTF1 (engine.py:511-523).  ``mmap=True`` returns a read-only
+    memory-mapped view (feature matrices of 10^8 rows stream into
+    ``HostStore.set_features`` without a full in-memory copy)."""
+    import os
     with open(path, "rb") as fh:
         magic = fh.read(4)
         if magic != _MATRIX_MAGIC:
             raise GraphFormatError(f"{path}: bad magic {magic!r}, expected {_MATRIX_MAGIC!r}")
         rows, cols = struct.unpack("<QQ", fh.read(16))
+        if mmap:
+            if os.path.getsize(path) < 20 + rows * cols * 8:
+                raise GraphFormatError(f"{path}: truncated payload")
+            return np.memmap(path, dtype="<f8", mode="r", offset=20, shape=(rows, cols))
         raw = fh.read(rows * cols * 8)
         if len(raw) != rows * cols * 8:
             raise GraphFormatError(f"{path}: truncated payload")

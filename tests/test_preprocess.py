@@ -187,3 +187,49 @@ def test_cfg1_preprocessing_matches_reference():
     plan = H.plan_for_partition(r.partition)
     assert _digest(plan) == gold["plan_digest_reorg"]
     assert plan.layout.capacities == gold["caps"]
+
+
+def test_graph_cache_mmap_and_duplicate_edges(tmp_path):
+    """HTG1 memory-mapped load with the native CSR permutation equals the
+    lexsort of the reference (graph.py:262-264) - incl. duplicate edges and
+    self loops, where tie order matters - and the private-copy load."""
+    rng = np.random.default_rng(4)
+    V = 500
+    src = rng.integers(0, V, 4000)
+    dst = rng.integers(0, V, 4000)
+    src = np.concatenate([src, src[:300], np.arange(20)])   # duplicates + self loops
+    dst = np.concatenate([dst, dst[:300], np.arange(20)])
+    g = H.from_edges(src, dst, V)
+    path = str(tmp_path / "g.htg")
+    H.save_graph_cache(g, path)
+    for mm in (True, False):
+        g2 = H.load_graph_cache(path, mmap=mm)
+        assert g2.content_hash() == g.content_hash()
+        np.testing.assert_array_equal(g2.csr_edge_perm, g.csr_edge_perm)
+        dstc = np.repeat(np.arange(V), np.diff(g.csc_offsets))
+        np.testing.assert_array_equal(g2.csr_edge_perm, np.lexsort((dstc, g.csc_sources)))
+
+
+def test_feature_matrix_mmap_into_host_store(tmp_path):
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((3000, 24))
+    path = str(tmp_path / "x.htf")
+    H.save_matrix(X, path)
+    Xm = H.load_matrix(path, mmap=True)
+    np.testing.assert_array_equal(np.asarray(Xm), X)
+
+
+@pytest.mark.gpu  # pinned host memory needs the driver
+def test_feature_matrix_mmap_into_pinned_host_store(tmp_path):
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((3000, 24))
+    path = str(tmp_path / "x.htf")
+    H.save_matrix(X, path)
+    Xm = H.load_matrix(path, mmap=True)
+    host = H.HostStore(3000, [24, 8], dtype=np.float32)
+    host.set_features(Xm)
+    np.testing.assert_array_equal(host.h[0], X.astype(np.float32))
+    big = rng.standard_normal((200_000, 24))  # the threaded row-block cast
+    hb = H.HostStore(200_000, [24, 8], dtype=np.float32)
+    hb.set_features(big)
+    np.testing.assert_array_equal(hb.h[0], big.astype(np.float32))
