@@ -119,10 +119,11 @@ def build_inputs(cfg, m):
     # dedup plan on the GPU: sort/unique of the chunks' raw neighbour ids
     # (ht_gplan_build, bit-identical with the host planner)
     from paper_2311_14898_b200 import _native as N
-    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count())
+    ngpu = N.device_count()
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, ngpu) if ngpu else None
     tp = time.time()
     plan = H.plan_for_partition(p, device=dev)
-    log(f"[bench] GPU dedup planner {time.time() - tp:.2f}s")
+    log(f"[bench] {'GPU' if ngpu else 'host'} dedup planner {time.time() - tp:.2f}s")
     chosen = "identity"
     if cfg["n"] > 1:
         r = H.reorganize(p)
