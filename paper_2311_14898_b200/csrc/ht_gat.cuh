@@ -139,15 +139,23 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     float4 pv[NV];
     load4<NV>(pv, P + v * (int64_t)d, d4, lane);
     const float el_d = warp_sum(dot4<NV>(pv, ad));
+    // the first 32 in-edges (most destinations have fewer) stay in
+    // registers across the passes: source id i0 and attention input t0
+    const int c0 = (e1 - e0) < (int64_t)kW ? (int)(e1 - e0) : kW;
+    const bool in0 = lane < c0;
+    const int i0 = in0 ? __ldg(idx + e0 + lane) : 0;
+    const float t0 = in0 ? el_d + __ldg(el_src + i0) : 0.f;
     // segment max and softmax denominator, lane-parallel over edges
-    float mx = -CUDART_INF_F;
-    for (int64_t e = e0 + lane; e < e1; e += kW)
+    float mx = in0 ? leaky(t0, slope) : -CUDART_INF_F;
+    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
       mx = fmaxf(mx, leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope));
     mx = warp_max(mx);
-    float den = 0.f;
-    for (int64_t e = e0 + lane; e < e1; e += kW)
+    const float x0 = in0 ? expf(leaky(t0, slope) - mx) : 0.f;
+    float den = x0;
+    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
       den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
     den = warp_sum(den);
+    const float a0 = in0 ? x0 / den : 0.f;  // alpha of the first chunk
     // s_v = sum alpha_e q_u, sequential in edge order.  Backward with the
     // layer output h = ReLU(s) in HBM (HO): (s > 0) == (h > 0) bitwise, so
     // only alpha is recomputed, not s (one row gather per edge saved)
@@ -156,18 +164,19 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (BWD && HO) {
       load4<NV>(acc, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
-      for (int64_t e = e0 + lane; e < e1; e += kW)
+      if (in0) AL[e0 + lane] = a0;
+      for (int64_t e = e0 + kW + lane; e < e1; e += kW)
         AL[e] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
     }
     for (int64_t base = e0; base < ((BWD && HO) ? e0 : e1); base += kW) {
       const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
-      int my_i = 0;
-      float my_a = 0.f;
-      if (lane < cnt) {
+      int my_i = i0;
+      float my_a = a0;
+      if (base != e0 && lane < cnt) {
         my_i = __ldg(idx + base + lane);
         my_a = expf(leaky(el_d + __ldg(el_src + my_i), slope) - mx) / den;
-        if (BWD) AL[base + lane] = my_a;
       }
+      if (BWD && lane < cnt) AL[base + lane] = my_a;
       int k = 0;
       for (; k + 4 <= cnt; k += 4) {  // four rows in flight
         float4 x[4][NV];
@@ -214,11 +223,12 @@ __global__ void __launch_bounds__(256) k_gat_dst(
       gs[t].w = acc[t].w > 0.f ? gs[t].w : 0.f;
     }
     store4<NV>(GS + v * (int64_t)d, gs, d4, lane);
-    // g_alpha_e = gs . q_u (kept in GT for now), sum alpha_e g_alpha_e
-    float sdot = 0.f;
+    // g_alpha_e = gs . q_u, sum alpha_e g_alpha_e; the first chunk keeps
+    // its g_alpha in a register (g0), later chunks park it in GT
+    float sdot = 0.f, g0 = 0.f;
     for (int64_t base = e0; base < e1; base += kW) {
       const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
-      const int my_i = lane < cnt ? __ldg(idx + base + lane) : 0;
+      const int my_i = base == e0 ? i0 : (lane < cnt ? __ldg(idx + base + lane) : 0);
       float my_g = 0.f;
       int k = 0;
       for (; k + 4 <= cnt; k += 4) {  // four rows in flight, four interleaved reductions
@@ -247,13 +257,23 @@ __global__ void __launch_bounds__(256) k_gat_dst(
         if (lane == k) my_g = g;
       }
       if (lane < cnt) {
-        GT[base + lane] = my_g;
-        sdot += AL[base + lane] * my_g;
+        if (base == e0) {
+          g0 = my_g;
+          sdot += a0 * my_g;
+        } else {
+          GT[base + lane] = my_g;
+          sdot += AL[base + lane] * my_g;
+        }
       }
     }
     sdot = warp_sum(sdot);
     float sgt = 0.f;
-    for (int64_t e = e0 + lane; e < e1; e += kW) {
+    if (in0) {
+      const float gt = a0 * (g0 - sdot) * (t0 > 0.f ? 1.f : slope);
+      GT[e0 + lane] = gt;
+      sgt = gt;
+    }
+    for (int64_t e = e0 + kW + lane; e < e1; e += kW) {
       const float t = el_d + __ldg(el_src + __ldg(idx + e));
       const float gt = AL[e] * (GT[e] - sdot) * (t > 0.f ? 1.f : slope);
       GT[e] = gt;
