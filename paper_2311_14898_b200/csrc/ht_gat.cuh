@@ -292,6 +292,10 @@ __global__ void __launch_bounds__(256) k_gat_dst(
 // gq / gts contribution of CSR edges [e0, e1) of one source (one warp):
 // per edge (alpha gs_dst + g_t a_src), added in edge order; four rows in
 // flight.
+#ifndef HT_GAT_SU
+#define HT_GAT_SU 8
+#endif
+constexpr int SU = HT_GAT_SU;  // CSR rows in flight per warp
 template <int NV>
 __device__ __forceinline__ void src_sum(float4 (&acc)[NV], float& gts, int64_t e0, int64_t e1,
                                         const int32_t* __restrict__ dst,
@@ -311,18 +315,18 @@ __device__ __forceinline__ void src_sum(float4 (&acc)[NV], float& gts, int64_t e
       gts += my_t;
     }
     int k = 0;
-    for (; k + 4 <= cnt; k += 4) {
-      float4 x[4][NV];
-      float a[4], g[4];
+    for (; k + SU <= cnt; k += SU) {
+      float4 x[SU][NV];
+      float a[SU], g[SU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < SU; ++u) {
         const int r = __shfl_sync(0xffffffffu, my_d, k + u);
         a[u] = __shfl_sync(0xffffffffu, my_a, k + u);
         g[u] = __shfl_sync(0xffffffffu, my_t, k + u);
         load4<NV>(x[u], GS + (int64_t)r * d, d4, lane);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < SU; ++u)
 #pragma unroll
         for (int t = 0; t < NV; ++t) edge_add(acc[t], a[u], x[u][t], g[u], as[t]);
     }
