@@ -1442,6 +1442,16 @@ const float* hbm_inputs(ht_fleet* f, Device& d, int layer, const void* hin) {
   return nullptr;
 }
 
+// One device, one batch, identity-mapped mirror: the neighbour-gradient
+// views go straight to their grad mirror rows (scatter by global row) - the
+// owner push into the slot buffer and the flush out of it would move the
+// same rows twice.  Bitwise the reference's order: each row's first flush
+// is a store (GCN), or follows the destination-gradient add (GAT).
+bool direct_bwd(ht_fleet* f, Device& d) {
+  return f->m == 1 && f->n == 1 && d.cache && d.chunks[0].nbr_gid.p && d.mcount == f->nrows &&
+         (d.mrows.empty() || d.mrows.back() == d.mcount - 1) && !getenv("HT_NO_DIRECT_BWD");
+}
+
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
 int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
                  int64_t rb) {
@@ -1977,7 +1987,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
     if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     if (!d.lw[layer].valid) HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
-    if (f->mode != HT_MODE_BASELINE)  // begin_backward_layer: zeroed gradient slots
+    if (f->mode != HT_MODE_BASELINE && !direct_bwd(f, d))  // zeroed gradient slots
       CU(cudaMemsetAsync(d.grad.p, 0, d.cap * rbi, d.stream));
     if (d.cache) CU(cudaMemsetAsync(d.mg[layer].p, 0, d.mcount * rbi, d.stream));
   }
@@ -2120,11 +2130,15 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
                                                    d_out, d.se.as<float>(), d_in, nullptr, 0, c.nn,
                                                    d_in, d_out, 1, d_out)));
       }
+      if (direct_bwd(f, d))  // views -> grad mirror rows (the only, first flush: a store)
+        HT_TRY(launch_copy(d.stream, d.mg[layer].p, d.se.p, c.nbr_gid.as<int64_t>(), nullptr, c.nn,
+                           rbi, rbi, rbi));
       d.bwd_count++;
     }
     // K9/K10: owner push (ascending source device) + flush into host grads
     // (into the mirror with the cache)
-    if (!(f->lean && layer == 0)) HT_TRY(push_flush(f, j, gin, true, layer));
+    if (!(f->lean && layer == 0) && !direct_bwd(f, f->dev[f->rank >= 0 ? f->rank : 0]))
+      HT_TRY(push_flush(f, j, gin, true, layer));
   }
   for (auto& d : f->dev) {
     if (!d.local) continue;  // rank mode: a peer process drives it
@@ -2566,6 +2580,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       CU(cudaMemsetAsync(d.grad.p, 0, d.cap * (int64_t)d_in * 4, d.stream));
     if (d.cache) CU(cudaMemsetAsync(d.mg[layer].p, 0, d.mcount * (int64_t)d_in * 4, d.stream));
   }
+  Device& d0 = f->dev[f->rank >= 0 ? f->rank : 0];
   for (int j = 0; j < f->n; ++j) {
     // load_recomp_chkpt("gat"): inputs re-staged through the forward
     // machinery, destination inputs, then the destination gradients
@@ -2640,7 +2655,13 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
                           nullptr, c.nv, d_in, 0));
     }
     if (f->mode == HT_MODE_BASELINE) HT_TRY(barrier(f));
-    HT_TRY(push_flush(f, j, gin, false, layer));
+    if (direct_bwd(f, d0)) {  // views added straight into the grad mirror rows
+      HT_TRY(set_dev(d0));
+      HT_TRY(launch_acc(d0.stream, 4, d0.mg[layer].p, d0.se.p, d0.chunks[j].nbr_gid.as<int64_t>(),
+                        nullptr, nullptr, d0.chunks[j].nn, d_in, 0));
+    } else {
+      HT_TRY(push_flush(f, j, gin, false, layer));
+    }
   }
   for (auto& d : f->dev) {
     if (!d.local) continue;
