@@ -1,0 +1,13 @@
+#!/bin/bash
+# bench line + launch lists + full captures of the top kernels (r1 refresh)
+OUT=gpurun_out
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "rc $?" >> $OUT/bench.err
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed
+ncu --metrics $M --clock-control none --csv --log-file $OUT/gcn_launches.csv \
+  timeout 600 python bench.py --only-value --steps 1 --warmup 3 --no-cpu-baseline > $OUT/gcn_prof.log 2>&1
+ncu --metrics $M --clock-control none --csv --log-file $OUT/gat_launches.csv \
+  timeout 600 python bench.py --only-value --kind gat --steps 1 --warmup 1 --no-cpu-baseline > $OUT/gat_prof.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:k_seg_gather_v4" -s 2 -c 1 -o $OUT/full_seg -f \
+  timeout 600 python bench.py --only-value --steps 1 --warmup 1 --no-cpu-baseline > $OUT/full_seg.log 2>&1
+ncu --set full --clock-control none --import-source on -k "regex:k_gat_dst" -s 4 -c 1 -o $OUT/full_gat_dst_bwd -f \
+  timeout 600 python bench.py --only-value --kind gat --steps 1 --warmup 1 --no-cpu-baseline > $OUT/full_gat.log 2>&1
