@@ -166,20 +166,21 @@ def dedup_report():
             "volumes": {"v_ori": v.v_ori, "v_p2p": v.v_p2p, "v_ru": v.v_ru}}
 
 
-def host_bytes_per_epoch(plan, dims, mode="full", cached=False, kind="gcn"):
+def host_bytes_per_epoch(plan, dims, mode="full", cached=False, kind="gcn", ckpt_hbm=False):
     """Host<->GPU bytes of one epoch from the plan (SURVEY 8(d) formulas,
     fp32): neighbour loads/flushes + destination + checkpoint rows, plus the
     loss gradient rows this path writes to host.grad_h[L].  With the HBM
     owner cache the host is read once (the owned h^0 rows) and written once
     per produced row: h^{l+1} and agg^l per forward layer, grad_h^l per
-    backward layer, grad_h^L after the loss."""
+    backward layer, grad_h^L after the loss; with the checkpoint tier in HBM
+    (``checkpoints="auto"``) the agg^l rows are not written."""
     import paper_2311_14898_b200 as H
     L = len(dims) - 1
     V = int(plan.owner.shape[0])
     if cached:
         h2d = 4 * V * dims[0] + V * 9
         d2h = 4 * V * (sum(dims[1:]) + sum(dims[:L]) + dims[L])
-        if kind == "gcn":
+        if kind == "gcn" and not ckpt_hbm:
             d2h += 4 * V * sum(dims[:L])
         return h2d, d2h
     pred = H.predicted_transfers(plan, mode)
@@ -228,7 +229,7 @@ def reference_cpu_sample(ds, dims, budget_edges=1_500_000, threads=None):
 # timed epochs
 # ---------------------------------------------------------------------------
 def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed, rank=None,
-               kind="gcn", features=None, labels=None, lean=False):
+               kind="gcn", features=None, labels=None, lean=False, checkpoints="auto"):
     import paper_2311_14898_b200 as H
     from paper_2311_14898_b200 import _native as N
     dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count()) if rank is not None else 0
@@ -240,7 +241,8 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     host.set_features(ds.features if features is None else features)
     labels = ds.labels if labels is None else labels
     fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision, rank=rank,
-                          devices=[dev] if rank is not None else None, lean=lean)
+                          devices=[dev] if rank is not None else None, lean=lean,
+                          checkpoints=checkpoints)
     model = H.init_model(kind, dims, seed=seed, lr=0.1, dtype=np.float32)
     losses = []
     for _ in range(warmup):
@@ -262,10 +264,11 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     stats = {w: fleet.kernel_stats(w) for w in range(4)} if timing else {}
     rep = fleet.transfer_report()
     cache = fleet.cache_active
+    ckpt_hbm = bool(host.agg.pending)
     fleet.close()  # device memory back before the next measurement
     del host
     return {"ms_total": ms.value, "wall_s": wall, "losses": losses, "launches": launches,
-            "stats": stats, "report": rep, "cache": cache}
+            "stats": stats, "report": rep, "cache": cache, "ckpt_hbm": ckpt_hbm}
 
 
 GAT_DIMS = [256, 128, 128, 64]  # it-2004 / config 5 widths
@@ -411,6 +414,10 @@ def main():
     e2e_lean = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,
                           False, cfg["seed"], rank=rk, lean=True)
     ms_el = slowest(e2e_lean["ms_total"]) / args.steps
+    # the reference's host-side checkpoint cache (agg rows written through)
+    e2e_hc = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,
+                        False, cfg["seed"], rank=rk, checkpoints="host")
+    ms_hc = slowest(e2e_hc["ms_total"]) / args.steps
     gat = None
     if not args.no_gat:
         with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk_g:
@@ -422,7 +429,9 @@ def main():
         dist.destroy_process_group()
         return
     cached = e2e["cache"]
-    h2d, d2h = host_bytes_per_epoch(plan, dims, cached=cached)
+    ckpt_hbm = e2e["ckpt_hbm"]
+    h2d, d2h = host_bytes_per_epoch(plan, dims, cached=cached, ckpt_hbm=ckpt_hbm)
+    hc_h2d, hc_d2h = host_bytes_per_epoch(plan, dims, cached=e2e_hc["cache"])
     plan_h2d, plan_d2h = host_bytes_per_epoch(plan, dims)
     base_h2d, base_d2h = host_bytes_per_epoch(plan, dims, "baseline")
     dedup = dedup_report()
@@ -467,13 +476,19 @@ def main():
         "config": config,
         "e2e": {"value": e2e_v, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e, "hbm_owner_cache": bool(cached),
+                "checkpoints_in_hbm": bool(ckpt_hbm),
                 "pcie_gbs": (h2d + d2h) / (ms_e / 1e3) / 1e9,
                 "transfer_kernel_ms_per_step": mst / args.steps},
         "e2e_lean": {"value": L * E / (ms_el / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": ms_el,
                      "d2h_bytes_per_step": d2h - 4 * int(plan.owner.shape[0]) * (2 * dims[L] + dims[0])
-                     if cached else None,
+                     if cached and e2e_lean["ckpt_hbm"] == ckpt_hbm else None,
                      "what": "DeviceFleet(lean=True): grad_h^0 not produced, no host copies of "
                              "h^L / grad_h^L (opt-in; not the reference's host contents)"},
+        "e2e_host_checkpoints": {
+            "value": L * E / (ms_hc / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": ms_hc,
+            "h2d_bytes_per_step": hc_h2d, "d2h_bytes_per_step": hc_d2h,
+            "what": "DeviceFleet(checkpoints='host'): agg checkpoints written through to "
+                    "host.agg every epoch (the reference's host-side checkpoint cache)"},
         "epoch_s": {"hbm_resident": ms_v / 1e3, "host_resident": ms_e / 1e3},
         "host_gb_per_epoch": {"measured_path": (h2d + d2h) / 1e9,
                               "hbm_owner_cache": bool(cached),

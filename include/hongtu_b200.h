@@ -211,6 +211,15 @@ int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t n);
  * the owner cache, the host copies of h^L and grad_h^L.  Weights, attention
  * vectors, loss and every other host array are unchanged. */
 int ht_fleet_set_lean(ht_fleet* f, int lean);
+/* Checkpoint tier of the recompute-cache hybrid (replaces the host-side
+ * cache of store_checkpoint / load_recomp_chkpt, devices.py:391-425): with
+ * hbm = 1 and the owner cache active, a GCN forward keeps the agg
+ * checkpoints in the HBM mirrors the backward reads and does not write them
+ * to agg_out.  ht_fleet_checkpoint_read then fills host_agg (the layer's
+ * (V, d_layer) host array) from the mirrors; valid until the next forward
+ * of that layer. */
+int ht_fleet_set_checkpoints(ht_fleet* f, int hbm);
+int ht_fleet_checkpoint_read(ht_fleet* f, int layer, void* host_agg);
 /* HBM-resident store (HongTu-IM) on a single device: its device arrays
  * h[0..L], agg[0..L-1] (NULL for GAT), grad[0..L] are used as the owner
  * cache's mirrors (the layers read and write them in place, no copies).

@@ -83,6 +83,8 @@ _SIGS = {
     "ht_fleet_set_cache": (i32, [vp, i32]),
     "ht_fleet_set_host_rows": (i32, [vp, vp, i64]),
     "ht_fleet_set_lean": (i32, [vp, i32]),
+    "ht_fleet_set_checkpoints": (i32, [vp, i32]),
+    "ht_fleet_checkpoint_read": (i32, [vp, i32, vp]),
     "ht_fleet_alias_store": (i32, [vp, i32, vp, vp, vp]),
     "ht_fleet_cache_state": (i32, [vp, C.POINTER(i32)]),
     "ht_gat_forward_layer": (i32, [vp, i32, i32, i32, vp, vp, f32, vp, vp, i32]),

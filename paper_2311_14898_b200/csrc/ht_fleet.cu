@@ -269,6 +269,11 @@ struct ht_fleet {
   // lean epoch (opt-in): no grad_h^0 (never consumed,
   // engine.py:449/477) and no host copies of h^L / grad_h^L with the cache
   bool lean = false;
+  // checkpoint tier (the recompute-cache hybrid sized to HBM): with the owner
+  // cache active, the GCN agg checkpoints stay in their HBM mirrors and are
+  // not written through to host.agg; ht_fleet_checkpoint_read materializes
+  // them on demand
+  bool ckpt_hbm = false;
   // HBM store (placement "device") on a single device: its arrays serve as
   // the owner-cache mirrors directly (h[0..L], agg[0..L-1], grad[0..L])
   std::vector<void*> alias_h, alias_a, alias_g;
@@ -1722,6 +1727,31 @@ extern "C" int ht_fleet_set_lean(ht_fleet* f, int lean) {
   return HT_OK;
 }
 
+extern "C" int ht_fleet_set_checkpoints(ht_fleet* f, int hbm) {
+  f->ckpt_hbm = hbm != 0;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_checkpoint_read(ht_fleet* f, int layer, void* host_agg) {
+  if (layer < 0 || layer >= f->L || f->gat) return fail(HT_EINVAL, "no GCN checkpoint for that layer");
+  void* hp;
+  HT_TRY(dev_ptr(host_agg, &hp));
+  const int64_t rb = (int64_t)f->dims[layer] * 4;
+  for (auto& d : f->dev) {
+    if (!d.local) continue;
+    if (!d.cache || (int)d.ma.size() <= layer || !d.ma[layer].p)
+      return fail(HT_ESTATE, "checkpoints are not held in HBM mirrors");
+    HT_TRY(set_dev(d));
+    HT_TRY(cache_writeback(f, d, hp, d.ma[layer].as<float>(), rb));
+  }
+  for (auto& d : f->dev)
+    if (d.local) {
+      HT_TRY(set_dev(d));
+      CU(cudaStreamSynchronize(d.tout));
+    }
+  return HT_OK;
+}
+
 extern "C" int ht_fleet_cache_state(ht_fleet* f, int* on) {
   *on = 1;
   int any = 0;
@@ -1895,7 +1925,7 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       // checkpoint rows, chunked: the first backward layer reloads the last
       // forward layer's checkpoints chunk by chunk as they land
       for (int g = 0; g < kChunks; ++g) {
-        HT_TRY(put_dest(f, c, d.tout, aout, agg, rbi, g));
+        if (!(d.cache && f->ckpt_hbm)) HT_TRY(put_dest(f, c, d.tout, aout, agg, rbi, g));
         if (lastb) HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
       }
       (void)rows;
@@ -1913,7 +1943,7 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
   void* gout;
   HT_TRY(dev_ptr(grad_out, &gout));
   f->loss_count = count;
-  const int blocks = 148 * 4;
+  const int blocks = 148 * 8;  // one full wave of 8 resident 256-thread blocks per SM
   for (int i = 0; i < f->m; ++i) {
     Device& d = f->dev[i];
     if (!d.local) continue;  // rank mode: a peer process drives it

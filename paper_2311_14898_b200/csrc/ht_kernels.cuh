@@ -478,6 +478,31 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64
       continue;
     }
     const float* z = H + r * d;
+    const int64_t y = labels[v];
+    float* g = out + orow * d;
+    if (d <= 2 * kWarp) {  // the row in registers: one read, exp once per element
+      const float z0 = lane < d ? z[lane] : -INFINITY;
+      const float z1 = lane + kWarp < d ? z[lane + kWarp] : -INFINITY;
+      float mx = fmaxf(z0, z1);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float e0 = lane < d ? expf(z0 - mx) : 0.f;
+      const float e1 = lane + kWarp < d ? expf(z1 - mx) : 0.f;
+      float s = e0 + e1;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane < d) {
+        const float p = __fdiv_rn(e0, s);
+        if (lane == y) my += -(double)logf(p);
+        g[lane] = __fdiv_rn(lane == y ? __fsub_rn(p, 1.f) : p, count);
+      }
+      if (lane + kWarp < d) {
+        const float p = __fdiv_rn(e1, s);
+        if (lane + kWarp == y) my += -(double)logf(p);
+        g[lane + kWarp] = __fdiv_rn(lane + kWarp == y ? __fsub_rn(p, 1.f) : p, count);
+      }
+      continue;
+    }
     float mx = -INFINITY;
     for (int c = lane; c < d; c += kWarp) mx = fmaxf(mx, z[c]);
 #pragma unroll
@@ -486,8 +511,6 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64
     for (int c = lane; c < d; c += kWarp) s += expf(z[c] - mx);
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const int64_t y = labels[v];
-    float* g = out + orow * d;
     for (int c = lane; c < d; c += kWarp) {
       const float p = __fdiv_rn(expf(z[c] - mx), s);
       if (c == y) my += -(double)logf(p);

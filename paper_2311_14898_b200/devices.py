@@ -137,6 +137,43 @@ def _parallel_rows(dst: np.ndarray, src, threads: int = 8):
         t.join()
 
 
+class _Checkpoints(dict):
+    """``HostStore.agg``: layer -> (V, d_l) checkpoint array.  When a fleet
+    keeps an epoch's checkpoints in its HBM mirrors (``checkpoints="hbm"``),
+    the host array is filled on first access, so readers see exactly the
+    reference's contents (devices.py:391-404) without the epoch paying the
+    device-to-host copy."""
+
+    def __init__(self):
+        super().__init__()
+        self.pending = {}  # layer -> fleet holding that layer's checkpoints
+
+    def _materialize(self, layer):
+        fleet = self.pending.pop(layer, None)
+        if fleet is not None:
+            N.call("ht_fleet_checkpoint_read", fleet._handle, int(layer),
+                   N.ptr(dict.__getitem__(self, layer)), kind=DeviceError)
+
+    def materialize_all(self):
+        for layer in list(self.pending):
+            self._materialize(layer)
+
+    def __getitem__(self, layer):
+        self._materialize(layer)
+        return dict.__getitem__(self, layer)
+
+    def get(self, layer, default=None):
+        return self[layer] if layer in self else default
+
+    def values(self):
+        self.materialize_all()
+        return dict.values(self)
+
+    def items(self):
+        self.materialize_all()
+        return dict.items(self)
+
+
 class HostStore:
     """Per-layer representations h^l, gradients and aggregation checkpoints
     (devices.py:44-75).  Arrays are pinned host memory (``placement="host"``,
@@ -164,7 +201,7 @@ class HostStore:
         self.h = [self._alloc(d) for d in self.dims]
         self.grad_h = [self._alloc(d) for d in self.dims]
         self.h_valid = [False] * len(self.dims)
-        self.agg = {}
+        self.agg = _Checkpoints()
         self.agg_written = set()
 
     def _alloc(self, d):
@@ -174,9 +211,11 @@ class HostStore:
         return N.pinned_zeros(shape, self.dtype)
 
     def agg_array(self, layer: int):
+        """The checkpoint array of `layer` (allocated on first use), without
+        materializing HBM-held checkpoints."""
         if layer not in self.agg:
             self.agg[layer] = self._alloc(self.dims[layer])
-        return self.agg[layer]
+        return dict.__getitem__(self.agg, layer)
 
     def set_features(self, features) -> None:
         X = features if isinstance(features, np.ndarray) else np.asarray(features)
@@ -198,6 +237,7 @@ class HostStore:
         for g in self.grad_h:
             _zero_rows(g, None)
         self.agg_written.clear()
+        self.agg.pending.clear()
 
 
 # ---------------------------------------------------------------------------
@@ -248,6 +288,7 @@ class BufferInfo:
 # HostStore.  "auto" enables it for host-resident stores in p2p/full mode
 # when the mirrors fit in free HBM.
 _CACHE_MODES = {"off": 0, "on": 1, "auto": 2}
+_CKPT_MODES = ("auto", "host")
 
 
 class DeviceFleet:
@@ -257,7 +298,7 @@ class DeviceFleet:
 
     def __init__(self, plan: DedupPlan, mode: str = "full", flush_policy: str = "on_eviction",
                  dtype=np.float64, devices=None, precision: str = "tf32", rank: int | None = None,
-                 cache: str = "auto", lean: bool = False):
+                 cache: str = "auto", lean: bool = False, checkpoints: str = "auto"):
         if mode not in _MODES:
             raise SimulationError(f"unknown mode {mode!r}")
         if flush_policy not in _FLUSH_POLICIES:
@@ -266,9 +307,17 @@ class DeviceFleet:
             raise SimulationError(f"unknown precision {precision!r}, expected one of {list(PRECISIONS)}")
         if cache not in _CACHE_MODES:
             raise SimulationError(f"unknown cache mode {cache!r}, expected one of {list(_CACHE_MODES)}")
+        if checkpoints not in _CKPT_MODES:
+            raise SimulationError(f"unknown checkpoint placement {checkpoints!r}, expected one "
+                                  f"of {list(_CKPT_MODES)}")
         self.plan = plan
         self.mode = mode
         self.cache = cache
+        # GCN agg checkpoints: "auto" keeps them in the owner cache's HBM
+        # mirrors when it is active (host.agg filled on first read), "host"
+        # always writes them through (devices.py:391-404)
+        self.checkpoints = checkpoints
+        self._ckpt_hosts = weakref.WeakSet()
         # lean epochs (opt-in): no grad_h^0, and no host copies of h^L /
         # grad_h^L with the owner cache; the transfer
         # meters stay the reference's
@@ -385,6 +434,10 @@ class DeviceFleet:
         """Release the fleet's device buffers now (otherwise at garbage
         collection)."""
         if self._handle is not None and self._finalizer.alive:
+            for host in list(self._ckpt_hosts):  # HBM-held checkpoints -> host first
+                for layer, fl in list(host.agg.pending.items()):
+                    if fl is self:
+                        host.agg._materialize(layer)
             self._finalizer()
 
     # -- meters ---------------------------------------------------------------

@@ -138,6 +138,7 @@ def _epoch_reset(host: HostStore, fleet: DeviceFleet, kind: str = "gcn",
     for l in range(1, len(host.h)):
         host.h_valid[l] = False
     host.agg_written.clear()
+    host.agg.pending.clear()
     if cached:
         return
     for l in range(L):
@@ -237,6 +238,10 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     on = C.c_int(0)
     N.call("ht_fleet_cache_state", h_, C.byref(on))
     fleet.cache_active = bool(on.value)
+    # checkpoint tier: with the owner cache the agg checkpoints stay in HBM
+    # (the hybrid sized to 180 GB); host.agg is filled from there on read
+    ckpt_hbm = fleet.cache_active and fleet.checkpoints == "auto" and not gat
+    N.call("ht_fleet_set_checkpoints", h_, int(ckpt_hbm))
     _epoch_reset(host, fleet, model.kind, fleet.cache_active)
     fleet.connect_peers()  # rank mode: IPC handles, once
     slope = C.c_float(model.leaky_slope)
@@ -263,6 +268,9 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
             agg = host.agg_array(l)
             N.call("ht_forward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]), N.ptr(host.h[l]),
                    N.ptr(host.h[l + 1]), N.ptr(agg), prec)
+            if ckpt_hbm:
+                host.agg.pending[l] = fleet
+                fleet._ckpt_hosts.add(host)
             for j in range(n):
                 fleet._meter_fwd(j, dims[l] * item)
                 for i in range(m):
@@ -290,7 +298,8 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
                 fleet._meter_bwd(j, dims[l] * item)
         else:
             N.call("ht_backward_layer", h_, l, dims[l], dims[l + 1], N.ptr(W[l]),
-                   N.ptr(host.agg[l]), N.ptr(host.grad_h[l + 1]), N.ptr(host.grad_h[l]), prec)
+                   N.ptr(host.agg_array(l)), N.ptr(host.grad_h[l + 1]), N.ptr(host.grad_h[l]),
+                   prec)
             for j in range(n):
                 fleet._meter_dest(j, dims[l] * item, "h2d", "chkpt")
                 fleet._meter_dest(j, dims[l + 1] * item, "h2d")

@@ -160,3 +160,38 @@ def test_hbm_store_in_place_equals_host_store(kind):
     assert outs[0][0] == outs[1][0]
     for x, y in zip(outs[0][1] + outs[0][2], outs[1][1] + outs[1][2]):
         np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (1, 3), (3, 2)])
+def test_hbm_checkpoints_equal_host_checkpoints(m, n):
+    """Checkpoint tier: with the owner cache the GCN agg checkpoints stay in
+    HBM (checkpoints="auto") instead of being written through ("host").
+    The epochs must be bitwise equal, and host.agg - filled from HBM on first
+    read, here after two epochs and after the fleet is closed - must equal
+    the written-through arrays."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=2500, avg_degree=8.0, seed=5), 16, 8)
+    a = H.partition_vertices(ds.graph, m, seed=5)
+    p = H.split_chunks(ds.graph, a, n)
+    if n > 1:
+        p = H.reorganize(p).partition
+    dims = [16, 24, 8]
+    plan = H.plan_for_partition(p)
+    res = {}
+    for ck in ("host", "auto"):
+        model = H.init_model("gcn", dims, seed=3, lr=0.1, dtype=np.float32)
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, cache="on", checkpoints=ck)
+        losses = [H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss for _ in range(2)]
+        held = dict(host.agg.pending)
+        assert bool(held) == (ck == "auto")
+        fleet.close()  # HBM-held checkpoints are materialized before the buffers go
+        assert not host.agg.pending
+        res[ck] = (losses, [w.copy() for w in model.weights], [np.array(g) for g in host.grad_h],
+                   {l: np.array(host.agg[l]) for l in range(len(dims) - 1)})
+    assert res["host"][0] == res["auto"][0]
+    for x, y in zip(res["host"][1] + res["host"][2], res["auto"][1] + res["auto"][2]):
+        np.testing.assert_array_equal(x, y)
+    for l in res["host"][3]:
+        np.testing.assert_array_equal(res["host"][3][l], res["auto"][3][l])
+        assert np.abs(res["auto"][3][l]).sum() > 0
