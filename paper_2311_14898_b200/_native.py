@@ -18,7 +18,8 @@ import numpy as np
 from .errors import ChunktrainError, DeviceError, PlanError, SimulationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhongtu_b200.so")
+# HT_LIB: an alternative build of the same library (same-box A/B timing)
+LIB_PATH = os.environ.get("HT_LIB") or os.path.join(_HERE, "lib", "libhongtu_b200.so")
 
 HT_OK, HT_EINVAL, HT_ECUDA, HT_ESTATE, HT_ELIVE, HT_ENOMEM = 0, -1, -2, -3, -4, -5
 

@@ -173,7 +173,7 @@ struct LayerW {
 };
 
 constexpr int kHostGrid = 128;    // CTAs of a zero-copy host transfer kernel
-constexpr int kSplitsMax = 64;    // row slices of the weight-gradient GEMM
+constexpr int kSplitsMax = 148;   // row slices of the weight-gradient GEMM (one per SM)
 
 struct TimerRec {
   cudaEvent_t a, b;

@@ -458,6 +458,27 @@ __global__ void __launch_bounds__(256) k_relu_mask(float* __restrict__ gz, int64
 // out_base + r when out_base >= 0.  One warp per
 // row; per-block partial loss sums in double, fixed order.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void loss_row(const float* __restrict__ z, float* __restrict__ g, int d,
+                                         int64_t y, float count, int lane, double& my) {
+  float mx = -INFINITY;
+  for (int c = lane; c < d; c += kWarp) mx = fmaxf(mx, z[c]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float s = 0.f;
+  for (int c = lane; c < d; c += kWarp) s += expf(z[c] - mx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int c = lane; c < d; c += kWarp) {
+    const float p = __fdiv_rn(expf(z[c] - mx), s);
+    if (c == y) my += -(double)logf(p);
+    g[c] = __fdiv_rn(c == y ? __fsub_rn(p, 1.f) : p, count);
+  }
+}
+
+// Rows are taken 32 at a time per warp: their vertex ids, mask bits and
+// labels are loaded lane-parallel (one latency per 32 rows); rows of width
+// <= 64 are held in registers and the next row's values are requested
+// before the current one is reduced.
 __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64_t rows, int d,
                                               const int64_t* __restrict__ labels,
                                               const uint8_t* __restrict__ mask,
@@ -467,54 +488,62 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64
   __shared__ double wsum[8];
   const int lane = lane_id(), wib = threadIdx.x >> 5;
   double my = 0.0;
-  const int64_t warp = blockIdx.x * 8 + wib;
-  const int64_t stride = (int64_t)gridDim.x * 8;
-  for (int64_t r = warp; r < rows; r += stride) {
-    const int64_t v = out_rows[r];
-    // gradient row: host row v, or mirror row out_base + r (HBM owner cache)
-    const int64_t orow = out_base >= 0 ? out_base + r : v;
-    if (!mask[v]) {  // rows off the mask get a zero gradient (engine.py:305, 319)
-      for (int c = lane; c < d; c += kWarp) out[orow * d + c] = 0.f;
-      continue;
+  const int64_t nblk = (rows + kWarp - 1) / kWarp;
+  for (int64_t blk = blockIdx.x * 8 + wib; blk < nblk; blk += (int64_t)gridDim.x * 8) {
+    const int64_t r0 = blk * kWarp;
+    const int nr = (int)((rows - r0) < (int64_t)kWarp ? (rows - r0) : (int64_t)kWarp);
+    const int64_t my_v = lane < nr ? out_rows[r0 + lane] : 0;
+    const int my_m = lane < nr ? (int)mask[my_v] : 0;
+    const int my_y = lane < nr && my_m ? (int)labels[my_v] : 0;
+    const bool reg = d <= 2 * kWarp;
+    float z0 = 0.f, z1 = 0.f;
+    if (reg && nr > 0) {
+      z0 = lane < d ? H[r0 * d + lane] : -INFINITY;
+      z1 = lane + kWarp < d ? H[r0 * d + lane + kWarp] : -INFINITY;
     }
-    const float* z = H + r * d;
-    const int64_t y = labels[v];
-    float* g = out + orow * d;
-    if (d <= 2 * kWarp) {  // the row in registers: one read, exp once per element
-      const float z0 = lane < d ? z[lane] : -INFINITY;
-      const float z1 = lane + kWarp < d ? z[lane + kWarp] : -INFINITY;
-      float mx = fmaxf(z0, z1);
+    for (int j = 0; j < nr; ++j) {
+      const int64_t r = r0 + j;
+      const int64_t v = __shfl_sync(0xffffffffu, my_v, j);
+      const int m = __shfl_sync(0xffffffffu, my_m, j);
+      const int y = __shfl_sync(0xffffffffu, my_y, j);
+      // gradient row: host row v, or mirror row out_base + r (HBM owner cache)
+      float* g = out + (out_base >= 0 ? out_base + r : v) * d;
+      if (!reg) {
+        if (!m) {  // rows off the mask get a zero gradient (engine.py:305, 319)
+          for (int c = lane; c < d; c += kWarp) g[c] = 0.f;
+        } else {
+          loss_row(H + r * d, g, d, y, count, lane, my);
+        }
+        continue;
+      }
+      const float c0 = z0, c1 = z1;
+      if (j + 1 < nr) {  // next row in flight while this one is reduced
+        z0 = lane < d ? H[(r + 1) * d + lane] : -INFINITY;
+        z1 = lane + kWarp < d ? H[(r + 1) * d + lane + kWarp] : -INFINITY;
+      }
+      if (!m) {
+        if (lane < d) g[lane] = 0.f;
+        if (lane + kWarp < d) g[lane + kWarp] = 0.f;
+        continue;
+      }
+      float mx = fmaxf(c0, c1);
 #pragma unroll
       for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float e0 = lane < d ? expf(z0 - mx) : 0.f;
-      const float e1 = lane + kWarp < d ? expf(z1 - mx) : 0.f;
-      float s = e0 + e1;
+      const float e0 = lane < d ? expf(c0 - mx) : 0.f;
+      const float e1 = lane + kWarp < d ? expf(c1 - mx) : 0.f;
+      float sum = e0 + e1;
 #pragma unroll
-      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       if (lane < d) {
-        const float p = __fdiv_rn(e0, s);
+        const float p = __fdiv_rn(e0, sum);
         if (lane == y) my += -(double)logf(p);
         g[lane] = __fdiv_rn(lane == y ? __fsub_rn(p, 1.f) : p, count);
       }
       if (lane + kWarp < d) {
-        const float p = __fdiv_rn(e1, s);
+        const float p = __fdiv_rn(e1, sum);
         if (lane + kWarp == y) my += -(double)logf(p);
         g[lane + kWarp] = __fdiv_rn(lane + kWarp == y ? __fsub_rn(p, 1.f) : p, count);
       }
-      continue;
-    }
-    float mx = -INFINITY;
-    for (int c = lane; c < d; c += kWarp) mx = fmaxf(mx, z[c]);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float s = 0.f;
-    for (int c = lane; c < d; c += kWarp) s += expf(z[c] - mx);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    for (int c = lane; c < d; c += kWarp) {
-      const float p = __fdiv_rn(expf(z[c] - mx), s);
-      if (c == y) my += -(double)logf(p);
-      g[c] = __fdiv_rn(c == y ? __fsub_rn(p, 1.f) : p, count);
     }
   }
 #pragma unroll

@@ -17,13 +17,10 @@
 //   Two TMEM accumulators (2 x BN columns) let the epilogue of tile t
 //   overlap the MMAs of tile t+1.
 //
-// k_tc_wgrad (dW) - per CTA a slice of rows: TMA brings raw row-major tiles
-// (32 rows x 128 features of agg, 32 x BN of gz); transposer warps write
-// them K-major (feature rows, 32 reduction values per 128-byte row); the MMA
-// warp accumulates one 128 x BN tile in TMEM; a partial tile per slice is
-// reduced in a fixed order afterwards.  (MN-major TF32 operands read back as
-// zeros on sm_100a - measured, scratch/wgrad_dbg2.cu - hence the
-// transposition.)
+// k_tc_wgrad (dW) - one CTA per row slice: both operands read MN-major
+// straight from the row-major matrices (TMA SWIZZLE_128B_ATOM_32B boxes),
+// rounded to TF32 in place, all of K x N accumulated in TMEM; the slices'
+// partial tiles are reduced in a fixed order afterwards.
 //
 // Shared-memory operand layouts are the canonical SWIZZLE_128B K-major UMMA
 // layouts (cute/arch/mma_sm100_desc.hpp): 8-row x 128-byte atoms, 16-byte
@@ -373,49 +370,76 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
-// k_tc_wgrad: P[z][k][n] = sum_{m in slice z} A[m][k] G[m][n], tile 128 x BN
-// grid (ceil(K/128), ceil(N/BN), slices); rows_per_slice multiple of 32.
+// k_tc_wgrad: P[z][k][n] = sum_{m in slice z} A[m][k] G[m][n] for all
+// k < K <= 256, n < N <= 256 in one CTA per row slice (grid = slices).
+//
+// Both operands are consumed MN-major straight from their row-major HBM
+// layout: A^T (features k x rows m) has k contiguous, so a TMA box of 32
+// features x 32 rows lands as 32 rows of 128 B - the UMMA MN-major
+// SWIZZLE_128B_BASE32B canonical layout (CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+// the only MN-major smem layout for TF32, cutlass sm100_common.inl).  Each
+// 32-feature block is one box; LBO = block stride (4 KB), SBO = 4-row group
+// stride (512 B); one K=8 MMA step covers 8 rows (1 KB).  KT = ceil(K/128)
+// accumulators of 128 x BN in TMEM (KT * BN <= 512 columns).
+//   warp 0     TMA producer (KT*4 + BN/32 boxes per stage, in-bounds only)
+//   warps 2-7  round the landed stage to TF32 in place (RNA; the tensor core
+//              would truncate - a systematic 2^-11 bias per operand)
+//   warp 1     MMA issuer
+//   warps 4-7  epilogue: TMEM -> the slice's partial tile
 // ---------------------------------------------------------------------------
-template <int BN>
+template <int KT, int BN>
 struct WgradCfg {
-  static constexpr int RA = 32 * 128 * 4;     // raw A: 32 rows x 128 floats
-  static constexpr int RG = 32 * BN * 4;      // raw G: 32 rows x BN floats
-  static constexpr int KA = 128 * 128;        // K-major A: 128 rows x 128 B
-  static constexpr int KG = BN * 128;         // K-major G: BN rows x 128 B
-  static constexpr int RAW = RA + RG;
-  static constexpr int KM = KA + KG;
-  static constexpr size_t SMEM = 1024 + 2 * (size_t)RAW + 2 * (size_t)KM + 256;
+  static constexpr int R = 32;                       // reduction rows per stage
+  static constexpr int BOX = 32 * R * 4;             // one 32-feature x R-row box
+  static constexpr int ABYTES = KT * 4 * BOX;
+  static constexpr int GBYTES = (BN / 32) * BOX;
+  static constexpr int STAGE = ABYTES + GBYTES;
+  static constexpr int S0 = (200 * 1024) / STAGE;
+  static constexpr int STAGES = S0 > 6 ? 6 : S0;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256;
 };
 
-template <int BN>
+// UMMA shared-memory descriptor, MN-major SWIZZLE_128B_BASE32B, version 1
+__device__ __forceinline__ uint64_t sdesc_mn32(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;  // MN block stride
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;  // 4-row K group stride
+  d |= (uint64_t)1 << 46;                       // version
+  d |= (uint64_t)1 << 61;                       // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+// instruction descriptor: A,B = TF32 MN-major, D = F32, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc_tf32_mn(int n) {
+  return idesc_tf32(n) | (1u << 15) | (1u << 16);
+}
+
+template <int KT, int BN>
 __global__ void __launch_bounds__(256, 1)
     k_tc_wgrad(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmG,
                int K, int N, int64_t M, int64_t rows_per_slice, float* __restrict__ P) {
-  using Cfg = WgradCfg<BN>;
+  using Cfg = WgradCfg<KT, BN>;
+  constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* km = smem;                  // [2][KA + KG]  (1024-aligned stages)
-  uint8_t* raw = smem + 2 * Cfg::KM;   // [2][RA + RG]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(raw + 2 * Cfg::RAW);
-  uint64_t* rfull = bar;       // [2] TMA landed
-  uint64_t* rempty = bar + 2;  // [2] transposers done reading raw
-  uint64_t* kfull = bar + 4;   // [2] K-major tiles written
-  uint64_t* kempty = bar + 6;  // [2] MMAs done
-  uint64_t* accf = bar + 8;
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 9);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + ST * Cfg::STAGE);
+  uint64_t* full = bar;            // [ST] TMA landed
+  uint64_t* conv = bar + ST;       // [ST] rounded in place
+  uint64_t* empty = bar + 2 * ST;  // [ST] MMAs done
+  uint64_t* accf = bar + 3 * ST;
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 3 * ST + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
-  const int64_t r0 = (int64_t)blockIdx.z * rows_per_slice;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_slice;
   const int64_t r1 = min(M, r0 + rows_per_slice);
-  const int nst = r1 > r0 ? (int)((r1 - r0 + 31) / 32) : 0;
-  constexpr uint32_t NCOL = tmem_cols(BN);
+  const int nst = r1 > r0 ? (int)((r1 - r0 + Cfg::R - 1) / Cfg::R) : 0;
+  constexpr uint32_t NCOL = tmem_cols(KT * BN);
   if (warp == 1) tmem_alloc(slot, NCOL);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], 192);
-      mbar_init(&kfull[s], 192);
-      mbar_init(&kempty[s], 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 192);
+      mbar_init(&empty[s], 1);
     }
     mbar_init(accf, 1);
     fence_barrier_init();
@@ -425,86 +449,83 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem = *slot;
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer
+    if (lane == 0) {  // TMA producer: only boxes that start inside the matrix
+      const int na = (K + 31) / 32, ng = (N + 31) / 32;
+      const uint32_t tx = (uint32_t)(na + ng) * Cfg::BOX;
       for (int it = 0; it < nst; ++it) {
-        const int s = it & 1;
-        mbar_wait(&rempty[s], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&rfull[s], Cfg::RAW);
-        uint8_t* ra = raw + s * Cfg::RAW;
-        const int row = (int)(r0 + it * 32);
-        tma_load_2d(ra, &tmA, &rfull[s], k0, row);
-        tma_load_2d(ra + Cfg::RA, &tmG, &rfull[s], n0, row);
+        const int s = it % ST;
+        mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+        mbar_expect_tx(&full[s], tx);
+        uint8_t* st = smem + s * Cfg::STAGE;
+        const int row = (int)(r0 + (int64_t)it * Cfg::R);
+        for (int b = 0; b < na; ++b) tma_load_2d(st + b * Cfg::BOX, &tmA, &full[s], b * 32, row);
+        for (int b = 0; b < ng; ++b)
+          tma_load_2d(st + Cfg::ABYTES + b * Cfg::BOX, &tmG, &full[s], b * 32, row);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      const uint32_t idesc = idesc_tf32(BN);
+      constexpr uint32_t idesc = idesc_tf32_mn(BN);
       for (int it = 0; it < nst; ++it) {
-        const int s = it & 1;
-        mbar_wait(&kfull[s], (it >> 1) & 1);
+        const int s = it % ST;
+        mbar_wait(&conv[s], (it / ST) & 1);
         tc_fence_after();
-        const uint32_t a = smem_u32(km + s * Cfg::KM), b = a + Cfg::KA;
+        const uint32_t a = smem_u32(smem + s * Cfg::STAGE), g = a + Cfg::ABYTES;
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          mma_tf32(tmem, sdesc(a + ks * 32), sdesc(b + ks * 32), idesc, (it | ks) != 0);
-        mma_commit(&kempty[s]);
+        for (int t = 0; t < KT; ++t)
+#pragma unroll
+          for (int ks = 0; ks < Cfg::R / 8; ++ks)
+            mma_tf32(tmem + (uint32_t)(t * BN),
+                     sdesc_mn32(a + t * 4 * Cfg::BOX + ks * 1024, Cfg::BOX, 512),
+                     sdesc_mn32(g + ks * 1024, Cfg::BOX, 512), idesc, (it | ks) != 0);
+        mma_commit(&empty[s]);
       }
       mma_commit(accf);
     }
-  } else {  // transposers (warps 2-7, 192 threads); epilogue on warps 4-7
+  } else {  // converters (warps 2-7, 192 threads); epilogue on warps 4-7
     const int tt = threadIdx.x - 64;
     for (int it = 0; it < nst; ++it) {
-      const int s = it & 1;
-      mbar_wait(&rfull[s], (it >> 1) & 1);
-      mbar_wait(&kempty[s], ((it >> 1) & 1) ^ 1);
-      const float* ra = reinterpret_cast<const float*>(raw + s * Cfg::RAW);
-      const float* rg = ra + 32 * 128;
-      uint8_t* ka = km + s * Cfg::KM;
-      uint8_t* kg = ka + Cfg::KA;
-      // each thread: one feature row x 4 reduction rows (float4 store)
-      for (int w = tt; w < (128 + BN) * 8; w += 192) {
-        const int f = w % (128 + BN), rq = w / (128 + BN);  // rq: which 4-row group
-        float4 v;
-        if (f < 128) {
-          const float* p = ra + (rq * 4) * 128 + f;
-          v = make_float4(tf32_rna(p[0]), tf32_rna(p[128]), tf32_rna(p[256]), tf32_rna(p[384]));
-          *reinterpret_cast<float4*>(ka + sw128(f, rq)) = v;
-        } else {
-          const int g = f - 128;
-          const float* p = rg + (rq * 4) * BN + g;
-          v = make_float4(tf32_rna(p[0]), tf32_rna(p[BN]), tf32_rna(p[2 * BN]), tf32_rna(p[3 * BN]));
-          *reinterpret_cast<float4*>(kg + sw128(g, rq)) = v;
-        }
+      const int s = it % ST;
+      mbar_wait(&full[s], (it / ST) & 1);
+      float4* st = reinterpret_cast<float4*>(smem + s * Cfg::STAGE);
+#pragma unroll 4
+      for (int w = tt; w < Cfg::STAGE / 16; w += 192) {
+        float4 v = st[w];
+        v.x = tf32_rna(v.x);
+        v.y = tf32_rna(v.y);
+        v.z = tf32_rna(v.z);
+        v.w = tf32_rna(v.w);
+        st[w] = v;
       }
       fence_proxy_async();
-      mbar_arrive(&rempty[s]);
-      mbar_arrive(&kfull[s]);
+      mbar_arrive(&conv[s]);
     }
-    // epilogue: drain the 128 x BN accumulator into the slice's partial tile
-    if (warp < 4) goto done;
-    {
-    const int q4 = warp & 3;
-    const int k = k0 + q4 * 32 + lane;
-    float* out = P + (int64_t)blockIdx.z * K * N;
-    if (nst > 0) {
-      mbar_wait(accf, 0);
-      tc_fence_after();
-    }
+    if (warp >= 4) {  // epilogue: the KT accumulators -> the slice's partial tile
+      const int q4 = warp & 3;
+      float* out = P + (int64_t)blockIdx.x * K * N;
+      if (nst > 0) {
+        mbar_wait(accf, 0);
+        tc_fence_after();
+      }
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      if (nst > 0) tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0, v);
-      if (k < K) {
+      for (int t = 0; t < KT; ++t) {
+        const int k = t * 128 + q4 * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          if (nst > 0)
+            tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(t * BN + c0), v);
+          if (k < K) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int n = n0 + c0 + j;
-          if (n < N) out[(int64_t)k * N + n] = nst > 0 ? v[j] : 0.f;
+            for (int j = 0; j < 16; ++j) {
+              const int n = c0 + j;
+              if (n < N) out[(int64_t)k * N + n] = nst > 0 ? v[j] : 0.f;
+            }
+          }
         }
       }
     }
-    }
   }
-done:
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -549,7 +570,8 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 2-D fp32 tensor map: inner dim `cols` (contiguous), outer `rows`, row
 // stride `ld` floats; box = box_cols x box_rows.
 inline int tmap(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
-                int box_cols, int box_rows, bool swizzle) {
+                int box_cols, int box_rows, bool swizzle,
+                CUtensorMapSwizzle mode = CU_TENSOR_MAP_SWIZZLE_NONE) {
   auto fn = encode_fn();
   if (!fn) return fail(HT_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if (((uintptr_t)base & 15) || (ld * 4) % 16)
@@ -561,7 +583,7 @@ inline int tmap(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, i
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : mode,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(HT_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return HT_OK;
@@ -619,39 +641,45 @@ int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t M, int
   return launch_gemm_t<256, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
 }
 
-template <int BN>
+template <int KT, int BN>
 int launch_wgrad_t(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
                    int N, int64_t M, int splits, int64_t rps, float* P) {
-  using Cfg = WgradCfg<BN>;
+  using Cfg = WgradCfg<KT, BN>;
   CUtensorMap ta, tg;
-  HT_TRY(tmap(&ta, A, M, K, lda, 128, 32, false));
-  HT_TRY(tmap(&tg, G, M, N, ldg, BN, 32, false));
-  auto kern = k_tc_wgrad<BN>;
+  HT_TRY(tmap(&ta, A, M, K, lda, 32, Cfg::R, false, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  HT_TRY(tmap(&tg, G, M, N, ldg, 32, Cfg::R, false, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
+  auto kern = k_tc_wgrad<KT, BN>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
   if (e != cudaSuccess) return fail(HT_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
-  dim3 grid((unsigned)((K + 127) / 128), (unsigned)((N + BN - 1) / BN), (unsigned)splits);
-  kern<<<grid, 256, Cfg::SMEM, s>>>(ta, tg, K, N, M, rps, P);
+  kern<<<(unsigned)splits, 256, Cfg::SMEM, s>>>(ta, tg, K, N, M, rps, P);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HT_ECUDA, "k_tc_wgrad launch: %s", cudaGetErrorString(e));
   return HT_OK;
 }
 
-// P[z] = partial A^T G over row slice z; *splits_out = number of slices.
+template <int KT>
+int wgrad_kt(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
+             int N, int64_t M, int splits, int64_t rps, float* P) {
+  if (N <= 32) return launch_wgrad_t<KT, 32>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
+  if (N <= 64) return launch_wgrad_t<KT, 64>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
+  if (N <= 128) return launch_wgrad_t<KT, 128>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
+  return launch_wgrad_t<KT, 256>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
+}
+
+// P[z] = partial A^T G over row slice z (one CTA per slice, up to one per
+// SM); *splits_out = number of slices.
 inline int wgrad(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
                  int N, int64_t M, int max_splits, float* P, int* splits_out) {
   if (K > 256 || N > 256) return fail(HT_EINVAL, "tcgen05 wgrad supports K, N <= 256");
-  const int gx = (K + 127) / 128;
-  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((M + 31) / 32, sm_count() / gx));
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((M + 31) / 32, sm_count()));
   splits = std::max(1, std::min(splits, max_splits));
   int64_t rps = ((M + splits - 1) / splits + 31) / 32 * 32;
   if (rps < 32) rps = 32;
   splits = (int)std::max<int64_t>(1, (M + rps - 1) / rps);
   *splits_out = splits;
-  if (N <= 32) return launch_wgrad_t<32>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
-  if (N <= 64) return launch_wgrad_t<64>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
-  if (N <= 128) return launch_wgrad_t<128>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
-  return launch_wgrad_t<256>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
+  if (K <= 128) return wgrad_kt<1>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
+  return wgrad_kt<2>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
 }
 
 inline int split_weights(cudaStream_t s, const float* W, float* hi, float* lo, int64_t n) {
