@@ -293,6 +293,9 @@ int ht_kernel_stats(ht_fleet* f, int which, int64_t* launches, double* ms, doubl
  * stop - start in milliseconds (bench.py's CUDA-event timing). */
 int ht_fleet_mark(ht_fleet* f, int which);
 int ht_fleet_elapsed(ht_fleet* f, double* ms);
+/* Marks 0..15 may be recorded; elapsed time from mark a to mark b (max over
+ * devices) - per-phase device timing. */
+int ht_fleet_elapsed_between(ht_fleet* f, int a, int b, double* ms);
 /* Number of kernels this library has launched (process-wide). */
 int64_t ht_launches(void);
 

@@ -95,6 +95,7 @@ _SIGS = {
     "ht_kernel_stats": (i32, [vp, i32, P_I64, P_F64, P_F64]),
     "ht_fleet_mark": (i32, [vp, i32]),
     "ht_fleet_elapsed": (i32, [vp, P_F64]),
+    "ht_fleet_elapsed_between": (i32, [vp, i32, i32, P_F64]),
     "ht_launches": (i64, []),
     "ht_gemm_test": (i32, [i32, i32, vp, vp, vp, vp, i64, i32, i32]),
     "ht_pcie_probe": (i32, [i32, i64, vp]),

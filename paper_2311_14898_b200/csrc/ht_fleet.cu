@@ -36,6 +36,7 @@ const int64_t kSplit = [] {
   return (int64_t)(v >= 64 ? v : 1024);  // r1 sweep: 4096 -> 1024 saved 3 ms (GCN), 6 ms (GAT)
 }();
 constexpr int kThreads = 256;
+constexpr int kMarks = 16;
 std::atomic<int64_t> g_launches{0};  // kernels launched by this library
 inline void count_launch(int64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
@@ -200,7 +201,7 @@ struct Device {
   std::vector<int64_t> hL_off;         // row offset of batch j inside hL
   DBuf labels, mask, loss_part;
   std::vector<DevChunk> chunks;
-  cudaEvent_t mark[2] = {nullptr, nullptr};
+  cudaEvent_t mark[kMarks] = {};  // ht_fleet_mark slots (compute stream)
   // epoch pipeline: transfer streams, double-buffered staging, events
   cudaStream_t tin = nullptr, tout = nullptr;
   // checkpoint prefetch: agg rows of layer l come back from the host as
@@ -222,6 +223,9 @@ struct Device {
   int64_t wpin_cap = 0;
   uint8_t* lpin = nullptr;           // pinned labels + mask
   int64_t lpin_cap = 0;
+  DBuf sgd_p, sgd_w, sgd_t;          // SGD: pointer table, parameters, summed gradients
+  uint8_t* sgd_pin = nullptr;        // pinned staging of the SGD step
+  int64_t sgd_pin_cap = 0;
   // GAT staging (sized by ht_gat_epoch_begin): neighbour / destination
   // inputs, projections q / p, scores, backward rows and per-edge values
   DBuf g_hn, g_hd[2], g_q, g_p, g_els, g_gs, g_gp, g_al, g_gt, g_sgt, g_gq, g_gts, g_ghd, g_gin[2];
@@ -531,7 +535,34 @@ int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, c
   if (nseg <= 0) return HT_OK;
   const int g = grid_for(nseg);
   count_launch(1 + (np ? 1 : 0) + (nf ? 1 : 0));
-  if (d % 4 == 0 && d <= 512) {
+  static const bool sub_ok = [] {  // HT_NO_SUBWARP=1: narrow rows on the warp kernels
+    const char* e = getenv("HT_NO_SUBWARP");
+    return !(e && atoi(e));
+  }();
+  if (d % 4 == 0 && d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
+    static const int sv = [] {
+      const char* e = getenv("HT_SUB_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
+    if (d <= 32) {
+      ht::k_seg_gather_sub<8><<<grid_for((nseg + 3) / 4), kThreads, 0, s>>>(out, X, ldx, d, off, idx,
+                                                                           w, nseg, kSplit);
+      if (np) ht::k_seg_pieces_sub<8><<<grid_for((np + 3) / 4), kThreads, 0, s>>>(
+          partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
+    } else {
+      const int g2 = grid_for((nseg + 1) / 2);
+      if (sv == 1)
+        ht::k_seg_gather_sub<16, 4, 4><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
+      else if (sv == 2)
+        ht::k_seg_gather_sub<16, 8, 3><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
+      else if (sv == 3)
+        ht::k_seg_gather_sub<16, 16, 2><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
+      else
+        ht::k_seg_gather_sub<16, 8, 4><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
+      if (np) ht::k_seg_pieces_sub<16><<<grid_for((np + 1) / 2), kThreads, 0, s>>>(
+          partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
+    }
+  } else if (d % 4 == 0 && d <= 512) {
     const int nv = (d / 4 + 31) / 32;
 #define SEGV(NV)                                                                               \
   seg_variant<NV>(g, s, out, X, ldx, d, off, idx, w, nseg);                                \
@@ -885,8 +916,10 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (auto* v : {&d.mh, &d.ma, &d.mg})
       for (auto& b : *v) b.release();
     d.mrows_d.release();
+    for (DBuf* b : {&d.sgd_p, &d.sgd_w, &d.sgd_t}) b->release();
     if (d.wpin) cudaFreeHost(d.wpin);
     if (d.lpin) cudaFreeHost(d.lpin);
+    if (d.sgd_pin) cudaFreeHost(d.sgd_pin);
     if (d.stream) cudaStreamDestroy(d.stream);
     if (d.tin) cudaStreamDestroy(d.tin);
     if (d.tout) cudaStreamDestroy(d.tout);
@@ -2706,28 +2739,14 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
 namespace {
 // param -= lr * sum_i grads_i (ascending device), on device d0; the summed
 // gradient optionally copied out
-int sgd_one(Device& d0, const std::vector<const float*>& ptrs, int64_t nw, float* param, float lr,
-            float* grad_out) {
-  DBuf pbuf, wbuf, tbuf;
-  HT_TRY(upload(pbuf, ptrs, d0.stream));
-  HT_TRY(wbuf.ensure(nw * 4));
-  HT_TRY(tbuf.ensure(nw * 4));
-  CU(cudaMemcpyAsync(wbuf.p, param, nw * 4, cudaMemcpyHostToDevice, d0.stream));
-  count_launch();
-  ht::k_sgd<<<grid_for(nw / 32 + 1), 256, 0, d0.stream>>>(wbuf.as<float>(), tbuf.as<float>(),
-                                                         pbuf.as<const float*>(), (int)ptrs.size(),
-                                                         nw, lr);
-  CU(cudaGetLastError());
-  CU(cudaMemcpyAsync(param, wbuf.p, nw * 4, cudaMemcpyDeviceToHost, d0.stream));
-  if (grad_out) CU(cudaMemcpyAsync(grad_out, tbuf.p, nw * 4, cudaMemcpyDeviceToHost, d0.stream));
-  CU(cudaStreamSynchronize(d0.stream));
-  pbuf.release();
-  wbuf.release();
-  tbuf.release();
-  return HT_OK;
-}
 }  // namespace
 
+// ascending-device gradient sum + SGD for every parameter block of the
+// epoch (W per layer, then the GAT attention vector of that layer) in one
+// pass: the parameters and the pointer table go up in one pinned copy, one
+// k_sgd per block, updated parameters and summed gradients come back in one
+// pinned copy.  Persistent buffers: no allocation (and none of its implicit
+// synchronization) per epoch.
 extern "C" int ht_sgd2(ht_fleet* f, int L, const int* dims, float* const* W, float* const* A,
                        float lr, float* const* gW_out, float* const* gA_out) {
   // rank mode: every rank sums all ranks' accumulators (IPC views) in
@@ -2737,16 +2756,63 @@ extern "C" int ht_sgd2(ht_fleet* f, int L, const int* dims, float* const* W, flo
   if (f->rank >= 0 && f->m > 1) HT_TRY(xbarrier(f));  // every rank's dW complete
   HT_TRY(sync_all(f));
   HT_TRY(set_dev(d0));
-  std::vector<const float*> ptrs(f->m);
+  std::vector<float*> prm, grd;
+  std::vector<int64_t> cnt, goff;  // block sizes, offsets into each device's gWall
   for (int l = 0; l < L; ++l) {
-    const int64_t nw = (int64_t)dims[l] * dims[l + 1];
-    for (int i = 0; i < f->m; ++i) ptrs[i] = f->dev[i].gWall.as<float>() + f->dev[i].gW_off[l];
-    HT_TRY(sgd_one(d0, ptrs, nw, W[l], lr, gW_out ? gW_out[l] : nullptr));
-    if (A) {  // GAT attention vectors (engine.py:341-343)
-      for (int i = 0; i < f->m; ++i)
-        ptrs[i] = f->dev[i].gWall.as<float>() + f->dev[i].gW_off[L] + f->dev[i].gA_off[l];
-      HT_TRY(sgd_one(d0, ptrs, 2 * (int64_t)dims[l + 1], A[l], lr, gA_out ? gA_out[l] : nullptr));
+    prm.push_back(W[l]);
+    grd.push_back(gW_out ? gW_out[l] : nullptr);
+    cnt.push_back((int64_t)dims[l] * dims[l + 1]);
+    goff.push_back(-1 - l);  // resolved per device below
+    if (A) {
+      prm.push_back(A[l]);
+      grd.push_back(gA_out ? gA_out[l] : nullptr);
+      cnt.push_back(2 * (int64_t)dims[l + 1]);
+      goff.push_back(l);
     }
+  }
+  const int nb = (int)cnt.size();
+  int64_t total = 0;
+  std::vector<int64_t> off(nb);
+  for (int k = 0; k < nb; ++k) off[k] = total, total += cnt[k];
+  const int64_t ptr_bytes = (int64_t)nb * f->m * 8;
+  const int64_t pin_bytes = ptr_bytes + 3 * total * 4;
+  if (d0.sgd_pin_cap < pin_bytes) {
+    if (d0.sgd_pin) cudaFreeHost(d0.sgd_pin);
+    d0.sgd_pin = nullptr;
+    d0.sgd_pin_cap = 0;
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&d0.sgd_pin), pin_bytes, cudaHostAllocPortable));
+    d0.sgd_pin_cap = pin_bytes;
+  }
+  const float** ptab = reinterpret_cast<const float**>(d0.sgd_pin);
+  float* pin_in = reinterpret_cast<float*>(d0.sgd_pin + ptr_bytes);
+  float* pin_w = pin_in + total;
+  float* pin_g = pin_w + total;
+  for (int k = 0; k < nb; ++k) {
+    std::memcpy(pin_in + off[k], prm[k], cnt[k] * 4);
+    for (int i = 0; i < f->m; ++i) {
+      const Device& di = f->dev[i];
+      const int64_t o = goff[k] < 0 ? di.gW_off[-1 - goff[k]] : di.gW_off[L] + di.gA_off[goff[k]];
+      ptab[(int64_t)k * f->m + i] = di.gWall.as<float>() + o;
+    }
+  }
+  HT_TRY(d0.sgd_p.ensure(ptr_bytes));
+  HT_TRY(d0.sgd_w.ensure(total * 4));
+  HT_TRY(d0.sgd_t.ensure(total * 4));
+  CU(cudaMemcpyAsync(d0.sgd_p.p, ptab, ptr_bytes, cudaMemcpyHostToDevice, d0.stream));
+  CU(cudaMemcpyAsync(d0.sgd_w.p, pin_in, total * 4, cudaMemcpyHostToDevice, d0.stream));
+  for (int k = 0; k < nb; ++k) {
+    count_launch();
+    ht::k_sgd<<<grid_for(cnt[k] / 32 + 1), 256, 0, d0.stream>>>(
+        d0.sgd_w.as<float>() + off[k], d0.sgd_t.as<float>() + off[k],
+        d0.sgd_p.as<const float*>() + (int64_t)k * f->m, f->m, cnt[k], lr);
+    CU(cudaGetLastError());
+  }
+  CU(cudaMemcpyAsync(pin_w, d0.sgd_w.p, total * 4, cudaMemcpyDeviceToHost, d0.stream));
+  CU(cudaMemcpyAsync(pin_g, d0.sgd_t.p, total * 4, cudaMemcpyDeviceToHost, d0.stream));
+  CU(cudaStreamSynchronize(d0.stream));
+  for (int k = 0; k < nb; ++k) {
+    std::memcpy(prm[k], pin_w + off[k], cnt[k] * 4);
+    if (grd[k]) std::memcpy(grd[k], pin_g + off[k], cnt[k] * 4);
   }
   if (f->rank >= 0 && f->m > 1) {  // nobody zeroes its dW while a peer still reads it
     HT_TRY(xbarrier(f));
@@ -2782,13 +2848,29 @@ extern "C" int ht_kernel_stats(ht_fleet* f, int which, int64_t* launches, double
 // device-timeline marks for the benchmark: events on every device stream
 // ---------------------------------------------------------------------------
 extern "C" int ht_fleet_mark(ht_fleet* f, int which) {
-  if (which < 0 || which > 1) return fail(HT_EINVAL, "mark index must be 0 or 1");
+  if (which < 0 || which >= kMarks) return fail(HT_EINVAL, "mark index must be in [0, %d)", kMarks);
   for (auto& d : f->dev) {
     if (!d.local) continue;  // rank mode: a peer process drives it
     HT_TRY(set_dev(d));
     if (!d.mark[which]) CU(cudaEventCreate(&d.mark[which]));
     CU(cudaEventRecord(d.mark[which], d.stream));
   }
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_elapsed_between(ht_fleet* f, int a, int b, double* ms) {
+  if (a < 0 || b < 0 || a >= kMarks || b >= kMarks) return fail(HT_EINVAL, "mark index out of range");
+  double mx = 0.0;
+  for (auto& d : f->dev) {
+    if (!d.local) continue;
+    HT_TRY(set_dev(d));
+    if (!d.mark[a] || !d.mark[b]) return fail(HT_ESTATE, "marks not recorded");
+    CU(cudaEventSynchronize(d.mark[b]));
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, d.mark[a], d.mark[b]));
+    mx = std::max(mx, (double)t);
+  }
+  *ms = mx;
   return HT_OK;
 }
 

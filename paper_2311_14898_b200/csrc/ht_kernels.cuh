@@ -281,6 +281,101 @@ __global__ void __launch_bounds__(256) k_seg_gather_s(float* __restrict__ out,
   }
 }
 
+// Narrow rows (d4 = d/4 <= G float4 words): a warp is split into 32/G
+// sub-groups of G lanes and each sub-group sums its own segment (or piece),
+// sequentially in edge order as above - so one load instruction moves
+// 32/G rows and a 48-float row no longer leaves 20 of 32 lanes idle.
+template <int G, int U>
+__device__ __forceinline__ void seg_sum_sub(float4& acc, const float* __restrict__ X, int64_t ldx,
+                                            int d4, const int32_t* __restrict__ idx,
+                                            const float* __restrict__ w, int64_t e0, int64_t e1,
+                                            int sl, unsigned gmask) {
+  // sub-groups of one warp run different segment lengths: every lane keeps
+  // executing the loop until the longest segment of the warp is done
+  int64_t len = e1 - e0;
+  int64_t lmax = len;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t t = __shfl_xor_sync(0xffffffffu, lmax, o);
+    lmax = t > lmax ? t : lmax;
+  }
+  for (int64_t b = 0; b < lmax; b += G) {
+    const int cnt = (int)((len - b) < (int64_t)G ? ((len - b) > 0 ? (len - b) : 0) : (int64_t)G);
+    const int my_i = sl < cnt ? __ldg(idx + e0 + b + sl) : 0;
+    const float my_w = sl < cnt ? __ldg(w + e0 + b + sl) : 0.f;
+    for (int k = 0; k < G; k += U) {
+      float4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = __shfl_sync(0xffffffffu, my_i, k + u, G);
+        const float4* row = reinterpret_cast<const float4*>(X + (int64_t)s * ldx);
+        x[u] = (k + u < cnt && sl < d4) ? __ldg(row + sl) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float wk = __shfl_sync(0xffffffffu, my_w, k + u, G);
+        if (k + u < cnt) {
+          acc.x = __fadd_rn(acc.x, __fmul_rn(wk, x[u].x));
+          acc.y = __fadd_rn(acc.y, __fmul_rn(wk, x[u].y));
+          acc.z = __fadd_rn(acc.z, __fmul_rn(wk, x[u].z));
+          acc.w = __fadd_rn(acc.w, __fmul_rn(wk, x[u].w));
+        }
+      }
+    }
+  }
+  (void)gmask;
+}
+
+template <int G, int U = 8, int MINB = 4>
+__global__ void __launch_bounds__(256, MINB) k_seg_gather_sub(float* __restrict__ out,
+                                                              const float* __restrict__ X,
+                                                              int64_t ldx, int d,
+                                                              const int64_t* __restrict__ off,
+                                                              const int32_t* __restrict__ idx,
+                                                              const float* __restrict__ w,
+                                                              int64_t nseg, int64_t split) {
+  constexpr int S = 32 / G;  // segments per warp
+  const int lane = lane_id(), sl = lane % G, sub = lane / G;
+  const int d4 = d >> 2;
+  const int64_t ngrp = (nseg + S - 1) / S;
+  for (int64_t gi = global_warp(); gi < ngrp; gi += num_warps()) {
+    const int64_t sg = gi * S + sub;
+    int64_t e0 = 0, e1 = 0;
+    const bool mine = sg < nseg;
+    if (mine) {
+      e0 = off[sg];
+      e1 = off[sg + 1];
+    }
+    const bool skip = !mine || e1 - e0 > split;  // long: k_seg_pieces
+    if (skip) e1 = e0;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    seg_sum_sub<G, U>(acc, X, ldx, d4, idx, w, e0, e1, sl, 0u);
+    if (!skip && sl < d4) reinterpret_cast<float4*>(out + sg * (int64_t)d)[sl] = acc;
+  }
+}
+
+template <int G, int U = 8>
+__global__ void __launch_bounds__(256) k_seg_pieces_sub(float* __restrict__ partial,
+                                                        const float* __restrict__ X, int64_t ldx,
+                                                        int d, const int64_t* __restrict__ lo,
+                                                        const int64_t* __restrict__ hi,
+                                                        const int32_t* __restrict__ idx,
+                                                        const float* __restrict__ w,
+                                                        int64_t npieces) {
+  constexpr int S = 32 / G;
+  const int lane = lane_id(), sl = lane % G, sub = lane / G;
+  const int d4 = d >> 2;
+  const int64_t ngrp = (npieces + S - 1) / S;
+  for (int64_t gi = global_warp(); gi < ngrp; gi += num_warps()) {
+    const int64_t p = gi * S + sub;
+    const bool mine = p < npieces;
+    const int64_t e0 = mine ? lo[p] : 0, e1 = mine ? hi[p] : 0;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    seg_sum_sub<G, U>(acc, X, ldx, d4, idx, w, e0, e1, sl, 0u);
+    if (mine && sl < d4) reinterpret_cast<float4*>(partial + p * (int64_t)d)[sl] = acc;
+  }
+}
+
 // Pieces of long segments: piece p sums edges [lo[p], hi[p]) into
 // partial row p.
 template <int NV>
