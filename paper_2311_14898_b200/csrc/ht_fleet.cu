@@ -153,6 +153,11 @@ struct DevChunk {
   int64_t fw_np = 0, fw_nf = 0, bw_np = 0, bw_nf = 0;
   DBuf fw_lo, fw_hi, fw_seg, fw_first, fw_cnt;  // long-segment pieces (forward)
   DBuf bw_lo, bw_hi, bw_seg, bw_first, bw_cnt;  // (backward)
+  // one device, one batch: the CSR offsets expanded to every host row
+  // (empty segments for rows without out-edges) so the transposed
+  // aggregation writes the dense grad mirror directly; pieces re-indexed
+  DBuf bx_off, bx_lo, bx_hi, bx_seg, bx_first, bx_cnt;
+  int64_t bx_np = 0, bx_nf = 0, bx_rows = -1;
   // GAT: chunk-local CSC sources (rows of q) and the CSC edge id of each
   // CSR edge; uploaded by the first GAT epoch
   DBuf csc_loc, csr_perm;            // int32 [ne], int32 [ne]
@@ -884,7 +889,8 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (auto& c : d.chunks) {
       for (auto* b : {&c.nbr_slot, &c.dest_rows, &c.csc_off, &c.csc_slot, &c.csc_w, &c.csr_off,
                       &c.csr_dst, &c.csr_w, &c.fw_lo, &c.fw_hi, &c.fw_seg, &c.fw_first, &c.fw_cnt,
-                      &c.bw_lo, &c.bw_hi, &c.bw_seg, &c.bw_first, &c.bw_cnt, &c.csc_loc,
+                      &c.bw_lo, &c.bw_hi, &c.bw_seg, &c.bw_first, &c.bw_cnt, &c.bx_off, &c.bx_lo,
+                      &c.bx_hi, &c.bx_seg, &c.bx_first, &c.bx_cnt, &c.csc_loc,
                       &c.csr_perm, &c.h2d_m, &c.flush_m})
         b->release();
       for (CopyList* cl : {&c.h2d, &c.flush, &c.base_bwd})
@@ -1085,6 +1091,23 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         c.bw_nf = (int64_t)sg.size();
         HT_TRY(upload(c.bw_lo, lo, s)); HT_TRY(upload(c.bw_hi, hi, s));
         HT_TRY(upload(c.bw_seg, sg, s)); HT_TRY(upload(c.bw_first, fi, s)); HT_TRY(upload(c.bw_cnt, cn, s));
+        c.bx_rows = -1;
+        if (m == 1 && n == 1 && f->nrows < ((int64_t)1 << 31)) {
+          std::vector<int64_t> offx(f->nrows + 1);
+          int64_t q = 0;
+          for (int64_t g = 0; g <= f->nrows; ++g) {
+            while (q < h.nn && h.nbr[q] < g) ++q;
+            offx[g] = h.csr_off[q];
+          }
+          lo.clear(); hi.clear(); sg.clear(); fi.clear(); cn.clear();
+          make_pieces(offx, lo, hi, sg, fi, cn);
+          c.bx_np = (int64_t)lo.size();
+          c.bx_nf = (int64_t)sg.size();
+          HT_TRY(upload(c.bx_off, offx, s));
+          HT_TRY(upload(c.bx_lo, lo, s)); HT_TRY(upload(c.bx_hi, hi, s));
+          HT_TRY(upload(c.bx_seg, sg, s)); HT_TRY(upload(c.bx_first, fi, s)); HT_TRY(upload(c.bx_cnt, cn, s));
+          c.bx_rows = f->nrows;
+        }
       }
       if (base) {
         std::vector<int64_t> pos(h.nbr.size());
@@ -1622,7 +1645,8 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     int narrow_w = 0;  // widest d_out of the layers whose backward runs narrow-side
     for (int l = 0; l < L; ++l)
       if (dims[l + 1] < dims[l]) narrow_w = std::max(narrow_w, pad4(dims[l + 1]));
-    if (narrow_w) HT_TRY(d.tT.ensure(mn * narrow_w * 4));
+    if (narrow_w)  // (the expanded CSR of one device / one batch has a row per host row)
+      HT_TRY(d.tT.ensure(std::max<int64_t>(mn, f->m == 1 && f->n == 1 ? f->nrows : 0) * narrow_w * 4));
     HT_TRY(d.partial.ensure(np * dmax * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
@@ -2177,23 +2201,32 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
       const int kw = narrow ? ldz : d_in;  // width of the gathered rows
-      HT_TRY(launch_seg(d.stream, narrow ? d.tT.as<float>() : d.se.as<float>(), narrow ? GZ : GA,
-                        kw, kw, c.csr_off.as<int64_t>(), c.csr_dst.as<int32_t>(),
-                        c.csr_w.as<float>(), c.nn, c.bw_np, c.bw_lo, c.bw_hi, c.bw_nf, c.bw_seg,
-                        c.bw_first, c.bw_cnt, d.partial.as<float>()));
+      // one device, one batch: the expanded CSR writes the grad mirror rows
+      // (every host row; zero rows for sources without out-edges) in place
+      // of the views - the only flush of each row, a store
+      const bool dx = direct_bwd(f, d) && c.bx_rows == d.mcount;
+      const int64_t nseg = dx ? c.bx_rows : c.nn;
+      float* views = dx ? d.mg[layer].as<float>() : d.se.as<float>();
+      HT_TRY(launch_seg(d.stream, narrow ? d.tT.as<float>() : views, narrow ? GZ : GA, kw, kw,
+                        dx ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>(),
+                        c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), nseg,
+                        dx ? c.bx_np : c.bw_np, dx ? c.bx_lo : c.bw_lo, dx ? c.bx_hi : c.bw_hi,
+                        dx ? c.bx_nf : c.bw_nf, dx ? c.bx_seg : c.bw_seg,
+                        dx ? c.bx_first : c.bw_first, dx ? c.bx_cnt : c.bw_cnt,
+                        d.partial.as<float>()));
       timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * kw) + (double)c.nn * (4.0 * kw + 4.0),
                 d.stream);
-      if (narrow && c.nn > 0) {  // views = (A^T gz) W^T
+      if (narrow && nseg > 0) {  // views = (A^T gz) W^T
         if (precision == HT_PREC_TF32)
-          HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, d.tT.as<float>(), ldz, c.nn, d_out,
-                                                w.Wp_hi.as<float>(), nullptr, ldz, d_in,
-                                                d.se.as<float>(), d_in, nullptr, 0));
+          HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, d.tT.as<float>(), ldz, nseg, d_out,
+                                                w.Wp_hi.as<float>(), nullptr, ldz, d_in, views,
+                                                d_in, nullptr, 0));
         else
           HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, d.tT.as<float>(), ldz, w.W.as<float>(),
-                                                   d_out, d.se.as<float>(), d_in, nullptr, 0, c.nn,
-                                                   d_in, d_out, 1, d_out)));
+                                                   d_out, views, d_in, nullptr, 0, nseg, d_in,
+                                                   d_out, 1, d_out)));
       }
-      if (direct_bwd(f, d))  // views -> grad mirror rows (the only, first flush: a store)
+      if (direct_bwd(f, d) && !dx)  // views -> grad mirror rows (the only, first flush: a store)
         HT_TRY(launch_copy(d.stream, d.mg[layer].p, d.se.p, c.nbr_gid.as<int64_t>(), nullptr, c.nn,
                            rbi, rbi, rbi));
       d.bwd_count++;
