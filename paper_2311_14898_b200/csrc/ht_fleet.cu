@@ -1513,6 +1513,19 @@ bool direct_bwd(ht_fleet* f, Device& d) {
          (d.mrows.empty() || d.mrows.back() == d.mcount - 1) && !getenv("HT_NO_DIRECT_BWD");
 }
 
+// GAT with one device, one batch and the identity-mapped mirror: N_ij is a
+// subset of V_ij = every host row, so q = h_nbr.W is p = h.W row for row
+// (bitwise: the same input row times the same W).  The projections run once
+// over all rows, the edge kernels index p by global row, the CSR pass runs
+// over the expanded offsets (gq / gts in global row order, zero rows for
+// rows without out-edges) and the input gradients land in the grad mirror
+// directly.  ∇W and ∇a sum over all rows (rows without out-edges add zeros):
+// the same sums in a different association than the staged path.
+bool gat_direct(ht_fleet* f, Device& d) {
+  const DevChunk& c = d.chunks[0];
+  return !getenv("HT_NO_GAT_DIRECT") && direct_bwd(f, d) && c.bx_rows == d.mcount && c.nv == d.mcount && c.dest_m0 == 0;
+}
+
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
 int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
                  int64_t rb) {
@@ -2291,11 +2304,13 @@ template <bool BWD>
 int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const float* P,
                    const float* els, const float* a_dst, int d, float slope, float* H,
                    const float* G, float* GS, float* GP, float* AL, float* GT, float* SGT,
-                   const float* HO = nullptr, const int64_t* ho_rows = nullptr) {
+                   const float* HO = nullptr, const int64_t* ho_rows = nullptr,
+                   bool global_src = false) {
   if (c.nv <= 0) return HT_OK;
   const int g = grid_for(c.nv);
   const int64_t* off = c.csc_off.as<int64_t>();
-  const int32_t* idx = c.csc_loc.as<int32_t>();
+  // sources as chunk-local rows of Q, or (direct) as global rows of P
+  const int32_t* idx = global_src ? c.csc_gid.as<int32_t>() : c.csc_loc.as<int32_t>();
   count_launch();
 #define GATD(NV)                                                                              \
   ht::gat::k_gat_dst<NV, BWD><<<g, kThreads, 0, s>>>(off, idx, c.nv, Q, P, els, a_dst, d, slope, \
@@ -2313,20 +2328,23 @@ int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const floa
 
 int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const float* AL,
                    const float* GT, const float* a_src, int d, float* GQ, float* GTS, float* part,
-                   float* pgts) {
-  if (c.nn <= 0) return HT_OK;
-  const int g = grid_for(c.nn);
-  const int64_t* off = c.csr_off.as<int64_t>();
+                   float* pgts, bool expanded = false) {
+  // expanded: segments over every host row (gat_direct), outputs in row order
+  const int64_t nseg = expanded ? c.bx_rows : c.nn;
+  const int64_t np = expanded ? c.bx_np : c.bw_np, nf = expanded ? c.bx_nf : c.bw_nf;
+  const DBuf &lo = expanded ? c.bx_lo : c.bw_lo, &hi = expanded ? c.bx_hi : c.bw_hi;
+  if (nseg <= 0) return HT_OK;
+  const int g = grid_for(nseg);
+  const int64_t* off = expanded ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>();
   const int32_t* dst = c.csr_dst.as<int32_t>();
   const int32_t* perm = c.csr_perm.as<int32_t>();
-  count_launch(1 + (c.bw_np ? 1 : 0) + (c.bw_nf ? 1 : 0));
+  count_launch(1 + (np ? 1 : 0) + (nf ? 1 : 0));
 #define GATS(NV)                                                                                \
-  ht::gat::k_gat_src<NV><<<g, kThreads, 0, s>>>(off, dst, perm, c.nn, kSplit, GS, AL, GT, a_src, \
+  ht::gat::k_gat_src<NV><<<g, kThreads, 0, s>>>(off, dst, perm, nseg, kSplit, GS, AL, GT, a_src, \
                                                 d, GQ, GTS);                                     \
-  if (c.bw_np)                                                                                  \
-    ht::gat::k_gat_src_pieces<NV><<<grid_for(c.bw_np), kThreads, 0, s>>>(                       \
-        c.bw_lo.as<int64_t>(), c.bw_hi.as<int64_t>(), c.bw_np, dst, perm, GS, AL, GT, a_src, d,  \
-        part, pgts)
+  if (np)                                                                                       \
+    ht::gat::k_gat_src_pieces<NV><<<grid_for(np), kThreads, 0, s>>>(                            \
+        lo.as<int64_t>(), hi.as<int64_t>(), np, dst, perm, GS, AL, GT, a_src, d, part, pgts)
   switch (nv_of(d)) {
     case 1: GATS(1); break;
     case 2: GATS(2); break;
@@ -2335,10 +2353,11 @@ int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const flo
   }
 #undef GATS
   CU(cudaGetLastError());
-  if (c.bw_nf) {
-    ht::gat::k_gat_src_fixup<<<grid_for(c.bw_nf), kThreads, 0, s>>>(
-        GQ, GTS, part, pgts, d, c.bw_seg.as<int64_t>(), c.bw_first.as<int64_t>(),
-        c.bw_cnt.as<int64_t>(), c.bw_nf);
+  if (nf) {
+    const DBuf &sg = expanded ? c.bx_seg : c.bw_seg, &fi = expanded ? c.bx_first : c.bw_first,
+               &cn = expanded ? c.bx_cnt : c.bw_cnt;
+    ht::gat::k_gat_src_fixup<<<grid_for(nf), kThreads, 0, s>>>(
+        GQ, GTS, part, pgts, d, sg.as<int64_t>(), fi.as<int64_t>(), cn.as<int64_t>(), nf);
     CU(cudaGetLastError());
   }
   return HT_OK;
@@ -2515,8 +2534,10 @@ int gat_stage(ht_fleet* f, int layer, int j, const void* hin, int d_in, const vo
     // the reference's views: value[slot(N_ij)] in N_ij order (or h^l[N_ij]
     // straight from an HBM-resident input on a single device)
     const float* Xd = hbm_inputs(f, d, layer, hin);
-    HT_TRY(launch_copy(d.stream, d.g_hn.p, Xd ? (const void*)Xd : d.value.p, nullptr,
-                       Xd ? c.nbr_gid.as<int64_t>() : c.nbr_slot.as<int64_t>(), c.nn, rbi, rbi, rbi));
+    if (!gat_direct(f, d))  // (direct: the layer reads its input rows in place)
+      HT_TRY(launch_copy(d.stream, d.g_hn.p, Xd ? (const void*)Xd : d.value.p, nullptr,
+                         Xd ? c.nbr_gid.as<int64_t>() : c.nbr_slot.as<int64_t>(), c.nn, rbi, rbi,
+                         rbi));
     HT_TRY(ev_rec(d.e_agg, d.stream));
   }
   return HT_OK;
@@ -2555,6 +2576,10 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
         CU(cudaStreamSynchronize(d.stream));  // host vectors go out of scope
         c.gat_ready = true;
       }
+    }
+    if (f->m == 1 && f->n == 1) {  // gat_direct: row-order GQ / gts / views
+      mn = std::max(mn, mv);
+      HT_TRY(d.se.ensure(mn * dmax * 4));
     }
     HT_TRY(d.g_hn.ensure(mn * dmax * 4));
     HT_TRY(d.g_q.ensure(mn * dmax * 4));
@@ -2627,19 +2652,22 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
                  : d.cache ? d.mh[layer + 1].as<float>() + c.dest_m0 * d_out
                            : d.fb[s].as<float>();
       const float* HD = d.cache ? d.mh[layer].as<float>() + c.dest_m0 * d_in : d.g_hd[s].as<float>();
+      const bool dir = gat_direct(f, d);  // q = p row for row: one projection
+      const float* Q = dir ? d.g_p.as<float>() : d.g_q.as<float>();
       TimerRec tg;
       timer_begin(f, d, tg, d.stream);
-      HT_TRY(gat_proj(d, precision, d.g_hn.as<float>(), c.nn, d_in, d_out, d.g_q.as<float>(), w));
+      if (!dir)
+        HT_TRY(gat_proj(d, precision, d.g_hn.as<float>(), c.nn, d_in, d_out, d.g_q.as<float>(), w));
       HT_TRY(gat_proj(d, precision, HD, c.nv, d_in, d_out, d.g_p.as<float>(), w));
-      timer_end(f, d, tg, 2, 2.0 * (double)(c.nn + c.nv) * d_in * d_out, d.stream);
+      timer_end(f, d, tg, 2, 2.0 * (double)((dir ? 0 : c.nn) + c.nv) * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_gcomp[s], d.stream));  // destination inputs of set s consumed
-      HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), d.g_q.as<float>(), w.A.as<float>() + d_out,
-                           d_out, c.nn));
+      HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), Q, w.A.as<float>() + d_out, d_out,
+                           dir ? c.nv : c.nn));
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
-      HT_TRY(launch_gat_dst<false>(d.stream, c, d.g_q.as<float>(), d.g_p.as<float>(),
-                                   d.g_els.as<float>(), w.A.as<float>(), d_out, slope, H, nullptr,
-                                   nullptr, nullptr, nullptr, nullptr, nullptr));
+      HT_TRY(launch_gat_dst<false>(d.stream, c, Q, d.g_p.as<float>(), d.g_els.as<float>(),
+                                   w.A.as<float>(), d_out, slope, H, nullptr, nullptr, nullptr,
+                                   nullptr, nullptr, nullptr, nullptr, nullptr, dir));
       timer_end(f, d, tr, 0,
                 (double)c.ne * (12.0 + 4.0 * d_out) + (double)c.nv * (8.0 * d_out + 16.0), d.stream);
       HT_TRY(ev_rec(d.e_comp, d.stream));
@@ -2690,27 +2718,30 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       LayerW& w = d.lw[layer];
       const float* a_dst = w.A.as<float>();
       const float* a_src = a_dst + d_out;
-      float* HN = d.g_hn.as<float>();
+      const bool dir = gat_direct(f, d);
       float* HD = d.cache ? d.mh[layer].as<float>() + c.dest_m0 * d_in : d.g_hd[s].as<float>();
+      float* HN = dir ? HD : d.g_hn.as<float>();
+      const int64_t nq = dir ? c.nv : c.nn;  // rows of Q / GQ / gts
       const float* Gin = d.cache ? d.mg[layer + 1].as<float>() + c.dest_m0 * d_out
                                  : d.g_gin[s].as<float>();
-      float *Q = d.g_q.as<float>(), *P = d.g_p.as<float>();
+      float *P = d.g_p.as<float>(), *Q = dir ? P : d.g_q.as<float>();
       float *GS = d.g_gs.as<float>(), *GP = d.g_gp.as<float>(), *GQ = d.g_gq.as<float>();
       float *AL = d.g_al.as<float>(), *GT = d.g_gt.as<float>();
       TimerRec tg;
       timer_begin(f, d, tg, d.stream);
-      HT_TRY(gat_proj(d, precision, HN, c.nn, d_in, d_out, Q, w));
+      if (!dir) HT_TRY(gat_proj(d, precision, HN, c.nn, d_in, d_out, Q, w));
       HT_TRY(gat_proj(d, precision, HD, c.nv, d_in, d_out, P, w));
-      timer_end(f, d, tg, 2, 2.0 * (double)(c.nn + c.nv) * d_in * d_out, d.stream);
-      HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), Q, a_src, d_out, c.nn));
+      timer_end(f, d, tg, 2, 2.0 * (double)((dir ? 0 : c.nn) + c.nv) * d_in * d_out, d.stream);
+      HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), Q, a_src, d_out, nq));
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
       const int64_t* hrows = nullptr;
       const float* HO = hbm_outputs(f, d, j, layer, d_out, &hrows);
       HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, d.g_els.as<float>(), a_dst, d_out, slope,
-                                  nullptr, Gin, GS, GP, AL, GT, d.g_sgt.as<float>(), HO, hrows));
+                                  nullptr, Gin, GS, GP, AL, GT, d.g_sgt.as<float>(), HO, hrows,
+                                  dir));
       HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
-                            d.partial.as<float>(), d.g_pgts.as<float>()));
+                            d.partial.as<float>(), d.g_pgts.as<float>(), dir));
       timer_end(f, d, tr, 1,
                 (double)c.ne * (28.0 + 12.0 * d_out) + (double)c.nv * (16.0 * d_out + 16.0) +
                     (double)c.nn * (4.0 * d_out + 12.0),
@@ -2719,17 +2750,20 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       float* gA = d.gWall.as<float>() + d.gW_off[f->L] + d.gA_off[layer];
       HT_TRY(launch_wcolsum(d.stream, gA, P, d.g_sgt.as<float>(), c.nv, d_out,
                             d.g_cpart.as<float>()));
-      HT_TRY(launch_wcolsum(d.stream, gA + d_out, Q, d.g_gts.as<float>(), c.nn, d_out,
+      HT_TRY(launch_wcolsum(d.stream, gA + d_out, Q, d.g_gts.as<float>(), nq, d_out,
                             d.g_cpart.as<float>()));
       // dW += h_nbr^T gq + h_dst^T gp; input gradients gq W^T, gp W^T
       float* gW = d.gWall.as<float>() + d.gW_off[layer];
       TimerRec tw;
       timer_begin(f, d, tw, d.stream);
-      HT_TRY(gat_wgrad(d, precision, HN, GQ, c.nn, d_in, d_out, gW));
+      HT_TRY(gat_wgrad(d, precision, HN, GQ, nq, d_in, d_out, gW));
       HT_TRY(gat_wgrad(d, precision, HD, GP, c.nv, d_in, d_out, gW));
       if (!(f->lean && layer == 0)) {  // lean: grad_h^0 is not produced
-        HT_TRY(gat_proj_t(d, precision, GQ, c.nn, d_in, d_out, d.se.as<float>(), w));
-        HT_TRY(gat_proj_t(d, precision, GP, c.nv, d_in, d_out, d.g_ghd.as<float>(), w));
+        HT_TRY(gat_proj_t(d, precision, GQ, nq, d_in, d_out, d.se.as<float>(), w));
+        // direct: the destination-input gradients are the first (and only
+        // store) into the zeroed grad mirror - 0 + x = x bitwise
+        HT_TRY(gat_proj_t(d, precision, GP, c.nv, d_in, d_out,
+                          dir ? d.mg[layer].as<float>() : d.g_ghd.as<float>(), w));
       }
       timer_end(f, d, tw, 2, 4.0 * (double)(c.nn + c.nv) * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_gcomp[s], d.stream));  // staging set s consumed
@@ -2743,6 +2777,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       if (!d.local) continue;
       HT_TRY(set_dev(d));
       DevChunk& c = d.chunks[j];
+      if (gat_direct(f, d)) continue;  // written by the projection above
       if (d.cache)  // contiguous mirror rows of the destinations
         HT_TRY(launch_acc(d.stream, 4, d.mg[layer].as<float>() + c.dest_m0 * d_in, d.g_ghd.p,
                           nullptr, nullptr, nullptr, c.nv, d_in, 0));
@@ -2751,7 +2786,11 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
                           nullptr, c.nv, d_in, 0));
     }
     if (f->mode == HT_MODE_BASELINE) HT_TRY(barrier(f));
-    if (direct_bwd(f, d0)) {  // views added straight into the grad mirror rows
+    if (gat_direct(f, d0)) {  // views in row order (zero rows for rows without out-edges)
+      HT_TRY(set_dev(d0));
+      HT_TRY(launch_acc(d0.stream, 4, d0.mg[layer].p, d0.se.p, nullptr, nullptr, nullptr,
+                        d0.chunks[j].bx_rows, d_in, 0));
+    } else if (direct_bwd(f, d0)) {  // views added straight into the grad mirror rows
       HT_TRY(set_dev(d0));
       HT_TRY(launch_acc(d0.stream, 4, d0.mg[layer].p, d0.se.p, d0.chunks[j].nbr_gid.as<int64_t>(),
                         nullptr, nullptr, d0.chunks[j].nn, d_in, 0));
