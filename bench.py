@@ -458,6 +458,11 @@ def main():
                 "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
                 "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": (bf + bb) / (lf + lb) if lf + lb else None,
+                # DRAM view of the same brackets: ncu DRAM bytes per bracket over the
+                # bracket's average event time (L2 hits make `frac` exceed 1)
+                "dram_gbs": traffic / (agg_ms / (lf + lb) / 1e3) / 1e9 if traffic and lf + lb else None,
+                "dram_frac": traffic / (agg_ms / (lf + lb) / 1e3) / 1e9 / hbm_peak
+                if traffic and lf + lb and hbm_peak else None,
                 "launches_per_step": (lf + lb) / args.steps,
                 "share_of_step": agg_ms / val["ms_total"] if val["ms_total"] else None}
     cpu = None
