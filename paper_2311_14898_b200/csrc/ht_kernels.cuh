@@ -289,7 +289,7 @@ template <int G, int U>
 __device__ __forceinline__ void seg_sum_sub(float4& acc, const float* __restrict__ X, int64_t ldx,
                                             int d4, const int32_t* __restrict__ idx,
                                             const float* __restrict__ w, int64_t e0, int64_t e1,
-                                            int sl, unsigned gmask) {
+                                            int sl) {
   // sub-groups of one warp run different segment lengths: every lane keeps
   // executing the loop until the longest segment of the warp is done
   int64_t len = e1 - e0;
@@ -323,7 +323,6 @@ __device__ __forceinline__ void seg_sum_sub(float4& acc, const float* __restrict
       }
     }
   }
-  (void)gmask;
 }
 
 template <int G, int U = 8, int MINB = 4>
@@ -349,7 +348,7 @@ __global__ void __launch_bounds__(256, MINB) k_seg_gather_sub(float* __restrict_
     const bool skip = !mine || e1 - e0 > split;  // long: k_seg_pieces
     if (skip) e1 = e0;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    seg_sum_sub<G, U>(acc, X, ldx, d4, idx, w, e0, e1, sl, 0u);
+    seg_sum_sub<G, U>(acc, X, ldx, d4, idx, w, e0, e1, sl);
     if (!skip && sl < d4) reinterpret_cast<float4*>(out + sg * (int64_t)d)[sl] = acc;
   }
 }
@@ -371,7 +370,7 @@ __global__ void __launch_bounds__(256) k_seg_pieces_sub(float* __restrict__ part
     const bool mine = p < npieces;
     const int64_t e0 = mine ? lo[p] : 0, e1 = mine ? hi[p] : 0;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    seg_sum_sub<G, U>(acc, X, ldx, d4, idx, w, e0, e1, sl, 0u);
+    seg_sum_sub<G, U>(acc, X, ldx, d4, idx, w, e0, e1, sl);
     if (mine && sl < d4) reinterpret_cast<float4*>(partial + p * (int64_t)d)[sl] = acc;
   }
 }
