@@ -166,6 +166,27 @@ def dedup_report():
             "volumes": {"v_ori": v.v_ori, "v_p2p": v.v_p2p, "v_ru": v.v_ru}}
 
 
+def dedup_at_scale(ds, dims, m=8, n=1, seed=0, device=None):
+    """The same plan comparison on the bench graph itself, partitioned for m
+    GPUs (the north star's 8-GPU layout): host bytes of one epoch through the
+    deduplicated plan vs the non-deduplicated one, all classes and the
+    neighbour class alone (SURVEY 8(d) formulas, fp32)."""
+    import paper_2311_14898_b200 as H
+    g = ds.graph
+    p = H.split_chunks(g, H.partition_vertices(g, m, seed=seed), n)
+    plan = H.plan_for_partition(p, device=device)
+    f = sum(host_bytes_per_epoch(plan, dims, "full"))
+    b = sum(host_bytes_per_epoch(plan, dims, "baseline"))
+    v = plan.volumes
+    nb = 4 * sum(dims[:-1])  # bytes per neighbour row over all layers (load + flush)
+    return {"config": f"bench graph m={m} n={n}", "host_gb_full": f / 1e9,
+            "host_gb_baseline": b / 1e9, "reduction": 1.0 - f / b,
+            "neighbour_gb_full": 2 * v.v_ru * nb / 1e9,
+            "neighbour_gb_baseline": 2 * v.v_ori * nb / 1e9,
+            "neighbour_reduction": 1.0 - v.v_ru / v.v_ori,
+            "volumes": {"v_ori": v.v_ori, "v_p2p": v.v_p2p, "v_ru": v.v_ru}}
+
+
 def host_bytes_per_epoch(plan, dims, mode="full", cached=False, kind="gcn", ckpt_hbm=False):
     """Host<->GPU bytes of one epoch from the plan (SURVEY 8(d) formulas,
     fp32): neighbour loads/flushes + destination + checkpoint rows, plus the
@@ -435,6 +456,10 @@ def main():
     plan_h2d, plan_d2h = host_bytes_per_epoch(plan, dims)
     base_h2d, base_d2h = host_bytes_per_epoch(plan, dims, "baseline")
     dedup = dedup_report()
+    try:
+        dedup["at_scale"] = dedup_at_scale(ds, dims, device=int(os.environ.get("LOCAL_RANK", "0")))
+    except Exception as exc:  # noqa: BLE001 - report, do not fail the bench
+        log(f"[bench] dedup at scale failed: {exc}")
     pcie = pcie_peaks()
     pcie_bidir = pcie[2] if pcie else None
 
