@@ -2328,7 +2328,8 @@ int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const floa
 
 int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const float* AL,
                    const float* GT, const float* a_src, int d, float* GQ, float* GTS, float* part,
-                   float* pgts, bool expanded = false) {
+                   float* pgts, bool expanded = false, const float* sgt_add = nullptr,
+                   const float* a_dst = nullptr) {
   // expanded: segments over every host row (gat_direct), outputs in row order
   const int64_t nseg = expanded ? c.bx_rows : c.nn;
   const int64_t np = expanded ? c.bx_np : c.bw_np, nf = expanded ? c.bx_nf : c.bw_nf;
@@ -2341,7 +2342,7 @@ int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const flo
   count_launch(1 + (np ? 1 : 0) + (nf ? 1 : 0));
 #define GATS(NV)                                                                                \
   ht::gat::k_gat_src<NV><<<g, kThreads, 0, s>>>(off, dst, perm, nseg, kSplit, GS, AL, GT, a_src, \
-                                                d, GQ, GTS);                                     \
+                                                d, GQ, GTS, sgt_add, a_dst);                     \
   if (np)                                                                                       \
     ht::gat::k_gat_src_pieces<NV><<<grid_for(np), kThreads, 0, s>>>(                            \
         lo.as<int64_t>(), hi.as<int64_t>(), np, dst, perm, GS, AL, GT, a_src, d, part, pgts)
@@ -2357,7 +2358,8 @@ int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const flo
     const DBuf &sg = expanded ? c.bx_seg : c.bw_seg, &fi = expanded ? c.bx_first : c.bw_first,
                &cn = expanded ? c.bx_cnt : c.bw_cnt;
     ht::gat::k_gat_src_fixup<<<grid_for(nf), kThreads, 0, s>>>(
-        GQ, GTS, part, pgts, d, sg.as<int64_t>(), fi.as<int64_t>(), cn.as<int64_t>(), nf);
+        GQ, GTS, part, pgts, d, sg.as<int64_t>(), fi.as<int64_t>(), cn.as<int64_t>(), nf, sgt_add,
+        a_dst);
     CU(cudaGetLastError());
   }
   return HT_OK;
@@ -2737,11 +2739,15 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       timer_begin(f, d, tr, d.stream);
       const int64_t* hrows = nullptr;
       const float* HO = hbm_outputs(f, d, j, layer, d_out, &hrows);
+      // direct: gp_v = sgt_v a_dst (rank 1) is added into gq_v by the CSR pass
+      // (rows are the same vertices), so dW and the input gradients take one
+      // GEMM each over gq + gp instead of two plus an add
       HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, d.g_els.as<float>(), a_dst, d_out, slope,
-                                  nullptr, Gin, GS, GP, AL, GT, d.g_sgt.as<float>(), HO, hrows,
-                                  dir));
+                                  nullptr, Gin, GS, dir ? nullptr : GP, AL, GT, d.g_sgt.as<float>(),
+                                  HO, hrows, dir));
       HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
-                            d.partial.as<float>(), d.g_pgts.as<float>(), dir));
+                            d.partial.as<float>(), d.g_pgts.as<float>(), dir,
+                            dir ? d.g_sgt.as<float>() : nullptr, a_dst));
       timer_end(f, d, tr, 1,
                 (double)c.ne * (28.0 + 12.0 * d_out) + (double)c.nv * (16.0 * d_out + 16.0) +
                     (double)c.nn * (4.0 * d_out + 12.0),
@@ -2757,13 +2763,13 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       TimerRec tw;
       timer_begin(f, d, tw, d.stream);
       HT_TRY(gat_wgrad(d, precision, HN, GQ, nq, d_in, d_out, gW));
-      HT_TRY(gat_wgrad(d, precision, HD, GP, c.nv, d_in, d_out, gW));
+      if (!dir) HT_TRY(gat_wgrad(d, precision, HD, GP, c.nv, d_in, d_out, gW));
       if (!(f->lean && layer == 0)) {  // lean: grad_h^0 is not produced
-        HT_TRY(gat_proj_t(d, precision, GQ, nq, d_in, d_out, d.se.as<float>(), w));
-        // direct: the destination-input gradients are the first (and only
-        // store) into the zeroed grad mirror - 0 + x = x bitwise
-        HT_TRY(gat_proj_t(d, precision, GP, c.nv, d_in, d_out,
-                          dir ? d.mg[layer].as<float>() : d.g_ghd.as<float>(), w));
+        // direct: (gq + gp) W^T is the only store into the zeroed grad mirror
+        HT_TRY(gat_proj_t(d, precision, GQ, nq, d_in, d_out,
+                          dir ? d.mg[layer].as<float>() : d.se.as<float>(), w));
+        if (!dir)
+          HT_TRY(gat_proj_t(d, precision, GP, c.nv, d_in, d_out, d.g_ghd.as<float>(), w));
       }
       timer_end(f, d, tw, 2, 4.0 * (double)(c.nn + c.nv) * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_gcomp[s], d.stream));  // staging set s consumed
@@ -2786,10 +2792,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
                           nullptr, c.nv, d_in, 0));
     }
     if (f->mode == HT_MODE_BASELINE) HT_TRY(barrier(f));
-    if (gat_direct(f, d0)) {  // views in row order (zero rows for rows without out-edges)
-      HT_TRY(set_dev(d0));
-      HT_TRY(launch_acc(d0.stream, 4, d0.mg[layer].p, d0.se.p, nullptr, nullptr, nullptr,
-                        d0.chunks[j].bx_rows, d_in, 0));
+    if (gat_direct(f, d0)) {  // written in place by the projection above
     } else if (direct_bwd(f, d0)) {  // views added straight into the grad mirror rows
       HT_TRY(set_dev(d0));
       HT_TRY(launch_acc(d0.stream, 4, d0.mg[layer].p, d0.se.p, d0.chunks[j].nbr_gid.as<int64_t>(),

@@ -281,11 +281,13 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     }
     sgt = warp_sum(sgt);
     if (lane == 0) SGT[v] = sgt;
-    float4 gp[NV];
+    if (GP) {  // (null: the rank-1 gp = sgt a_dst is folded into gq by k_gat_src)
+      float4 gp[NV];
 #pragma unroll
-    for (int t = 0; t < NV; ++t)
-      gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
-    store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+      for (int t = 0; t < NV; ++t)
+        gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
+      store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+    }
   }
 }
 
@@ -350,7 +352,8 @@ __global__ void __launch_bounds__(256) k_gat_src(
     const int64_t* __restrict__ off, const int32_t* __restrict__ dst,
     const int32_t* __restrict__ perm, int64_t nseg, int64_t split, const float* __restrict__ GS,
     const float* __restrict__ AL, const float* __restrict__ GT, const float* __restrict__ a_src,
-    int d, float* __restrict__ GQ, float* __restrict__ GTS) {
+    int d, float* __restrict__ GQ, float* __restrict__ GTS, const float* __restrict__ sgt_add,
+    const float* __restrict__ a_dst) {
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
   float4 as[NV];
@@ -363,7 +366,22 @@ __global__ void __launch_bounds__(256) k_gat_src(
 #pragma unroll
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     float gts = 0.f;
+    const float g = sgt_add ? __ldg(sgt_add + u) : 0.f;  // requested before the edge loop
     src_sum<NV>(acc, gts, e0, e1, dst, perm, GS, AL, GT, as, d, d4, lane);
+    if (sgt_add) {  // one device, one batch: row u's destination term gp_u = sgt_u a_dst
+      const float4* ad4 = reinterpret_cast<const float4*>(a_dst);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const int c = lane + t * kW;
+        if (c < d4) {
+          const float4 ad = __ldg(ad4 + c);
+          acc[t].x += g * ad.x;
+          acc[t].y += g * ad.y;
+          acc[t].z += g * ad.z;
+          acc[t].w += g * ad.w;
+        }
+      }
+    }
     store4<NV>(GQ + u * (int64_t)d, acc, d4, lane);
     gts = warp_sum(gts);
     if (lane == 0) GTS[u] = gts;
@@ -398,7 +416,8 @@ __global__ void __launch_bounds__(256) k_gat_src_pieces(
 __global__ void __launch_bounds__(256) k_gat_src_fixup(
     float* __restrict__ GQ, float* __restrict__ GTS, const float* __restrict__ part,
     const float* __restrict__ pgts, int d, const int64_t* __restrict__ seg,
-    const int64_t* __restrict__ first, const int64_t* __restrict__ cnt, int64_t nf) {
+    const int64_t* __restrict__ first, const int64_t* __restrict__ cnt, int64_t nf,
+    const float* __restrict__ sgt_add, const float* __restrict__ a_dst) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < nf; f += nw) {
@@ -406,6 +425,7 @@ __global__ void __launch_bounds__(256) k_gat_src_fixup(
     for (int c = lane; c < d; c += kW) {
       float s = 0.f;
       for (int64_t q = 0; q < qn; ++q) s = __fadd_rn(s, part[(q0 + q) * d + c]);
+      if (sgt_add) s += sgt_add[seg[f]] * a_dst[c];
       GQ[seg[f] * (int64_t)d + c] = s;
     }
     if (lane == 0) {
