@@ -234,6 +234,10 @@ struct Device {
   // GAT staging (sized by ht_gat_epoch_begin): neighbour / destination
   // inputs, projections q / p, scores, backward rows and per-edge values
   DBuf g_hn, g_hd[2], g_q, g_p, g_els, g_gs, g_gp, g_al, g_gt, g_sgt, g_gq, g_gts, g_ghd, g_gin[2];
+  // gat_direct: each layer's projection p = h.W and el_src = p.a_src kept
+  // from the forward for the backward (the recompute-cache hybrid sized to
+  // HBM: the backward skips the recompute GEMM, bitwise the same values)
+  std::vector<DBuf> g_pl, g_elsl;
   DBuf g_pgts;                         // per-piece g_t sums of split source segments
   DBuf g_cpart;                        // column partials of the attention gradients
   std::vector<int64_t> gA_off;         // attention gradients: gWall + gW_off[L] + gA_off[l]
@@ -917,6 +921,8 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
                     &d.g_al, &d.g_gt, &d.g_sgt, &d.g_gq, &d.g_gts, &d.g_ghd, &d.g_gin[0],
                     &d.g_gin[1], &d.g_cpart, &d.g_pgts})
       b->release();
+    for (auto* v : {&d.g_pl, &d.g_elsl})
+      for (auto& b : *v) b.release();
     for (cudaEvent_t e : {d.e_gcomp[0], d.e_gcomp[1], d.e_up, d.e_mg})
       if (e) cudaEventDestroy(e);
     for (auto* v : {&d.mh, &d.ma, &d.mg})
@@ -2586,6 +2592,14 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
     HT_TRY(d.g_hn.ensure(mn * dmax * 4));
     HT_TRY(d.g_q.ensure(mn * dmax * 4));
     HT_TRY(d.g_p.ensure(mv * dmax * 4));
+    if (f->m == 1 && f->n == 1) {  // per-layer projections for gat_direct (owner cache only)
+      d.g_pl.resize(L);
+      d.g_elsl.resize(L);
+      for (int l = 0; l < L; ++l) {
+        HT_TRY(d.g_pl[l].ensure(mv * dims[l + 1] * 4));
+        HT_TRY(d.g_elsl[l].ensure(mv * 4));
+      }
+    }
     HT_TRY(d.g_els.ensure(mn * 4));
     HT_TRY(d.g_gs.ensure(mv * dmax * 4));
     HT_TRY(d.g_gp.ensure(mv * dmax * 4));
@@ -2655,21 +2669,22 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
                            : d.fb[s].as<float>();
       const float* HD = d.cache ? d.mh[layer].as<float>() + c.dest_m0 * d_in : d.g_hd[s].as<float>();
       const bool dir = gat_direct(f, d);  // q = p row for row: one projection
-      const float* Q = dir ? d.g_p.as<float>() : d.g_q.as<float>();
+      float* P = dir ? d.g_pl[layer].as<float>() : d.g_p.as<float>();  // (kept for the backward)
+      float* els = dir ? d.g_elsl[layer].as<float>() : d.g_els.as<float>();
+      const float* Q = dir ? P : d.g_q.as<float>();
       TimerRec tg;
       timer_begin(f, d, tg, d.stream);
       if (!dir)
         HT_TRY(gat_proj(d, precision, d.g_hn.as<float>(), c.nn, d_in, d_out, d.g_q.as<float>(), w));
-      HT_TRY(gat_proj(d, precision, HD, c.nv, d_in, d_out, d.g_p.as<float>(), w));
+      HT_TRY(gat_proj(d, precision, HD, c.nv, d_in, d_out, P, w));
       timer_end(f, d, tg, 2, 2.0 * (double)((dir ? 0 : c.nn) + c.nv) * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_gcomp[s], d.stream));  // destination inputs of set s consumed
-      HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), Q, w.A.as<float>() + d_out, d_out,
-                           dir ? c.nv : c.nn));
+      HT_TRY(launch_rowdot(d.stream, els, Q, w.A.as<float>() + d_out, d_out, dir ? c.nv : c.nn));
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
-      HT_TRY(launch_gat_dst<false>(d.stream, c, Q, d.g_p.as<float>(), d.g_els.as<float>(),
-                                   w.A.as<float>(), d_out, slope, H, nullptr, nullptr, nullptr,
-                                   nullptr, nullptr, nullptr, nullptr, nullptr, dir));
+      HT_TRY(launch_gat_dst<false>(d.stream, c, Q, P, els, w.A.as<float>(), d_out, slope, H, nullptr,
+                                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                   dir));
       timer_end(f, d, tr, 0,
                 (double)c.ne * (12.0 + 4.0 * d_out) + (double)c.nv * (8.0 * d_out + 16.0), d.stream);
       HT_TRY(ev_rec(d.e_comp, d.stream));
@@ -2726,15 +2741,18 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       const int64_t nq = dir ? c.nv : c.nn;  // rows of Q / GQ / gts
       const float* Gin = d.cache ? d.mg[layer + 1].as<float>() + c.dest_m0 * d_out
                                  : d.g_gin[s].as<float>();
-      float *P = d.g_p.as<float>(), *Q = dir ? P : d.g_q.as<float>();
+      // direct: p and el_src as the forward left them (same weights: the
+      // update comes after the whole backward)
+      float *P = dir ? d.g_pl[layer].as<float>() : d.g_p.as<float>(), *Q = dir ? P : d.g_q.as<float>();
+      float* els = dir ? d.g_elsl[layer].as<float>() : d.g_els.as<float>();
       float *GS = d.g_gs.as<float>(), *GP = d.g_gp.as<float>(), *GQ = d.g_gq.as<float>();
       float *AL = d.g_al.as<float>(), *GT = d.g_gt.as<float>();
       TimerRec tg;
       timer_begin(f, d, tg, d.stream);
       if (!dir) HT_TRY(gat_proj(d, precision, HN, c.nn, d_in, d_out, Q, w));
-      HT_TRY(gat_proj(d, precision, HD, c.nv, d_in, d_out, P, w));
-      timer_end(f, d, tg, 2, 2.0 * (double)((dir ? 0 : c.nn) + c.nv) * d_in * d_out, d.stream);
-      HT_TRY(launch_rowdot(d.stream, d.g_els.as<float>(), Q, a_src, d_out, nq));
+      if (!dir) HT_TRY(gat_proj(d, precision, HD, c.nv, d_in, d_out, P, w));
+      timer_end(f, d, tg, 2, dir ? 0.0 : 2.0 * (double)(c.nn + c.nv) * d_in * d_out, d.stream);
+      if (!dir) HT_TRY(launch_rowdot(d.stream, els, Q, a_src, d_out, nq));
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
       const int64_t* hrows = nullptr;
@@ -2742,7 +2760,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       // direct: gp_v = sgt_v a_dst (rank 1) is added into gq_v by the CSR pass
       // (rows are the same vertices), so dW and the input gradients take one
       // GEMM each over gq + gp instead of two plus an add
-      HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, d.g_els.as<float>(), a_dst, d_out, slope,
+      HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, els, a_dst, d_out, slope,
                                   nullptr, Gin, GS, dir ? nullptr : GP, AL, GT, d.g_sgt.as<float>(),
                                   HO, hrows, dir));
       HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
