@@ -240,6 +240,13 @@ def host_bytes_per_epoch(plan, dims, mode="full", cached=False, kind="gcn", ckpt
     return h2d, d2h
 
 
+def host_threads():
+    """Threads the numpy/BLAS CPU path may use here (torchrun sets
+    OMP_NUM_THREADS=1 per rank unless told otherwise)."""
+    env = os.environ.get("OMP_NUM_THREADS")
+    return int(env) if env and env.isdigit() and int(env) > 0 else os.cpu_count()
+
+
 def reference_cpu_sample(ds, dims, budget_edges=1_500_000, threads=None):
     """Time the oracle port (numpy restatement of the reference's chunk
     kernels, the CPU implementation of this path) on a bounded sample:
@@ -269,7 +276,7 @@ def reference_cpu_sample(ds, dims, budget_edges=1_500_000, threads=None):
             "sample": (f"layer-0 forward+backward (oracle port, numpy fp32) over the first "
                        f"{verts.size} destinations ({es} edges, d={dims[0]}->{dims[1]}), "
                        f"extrapolated x{scale:.1f} by sum_l |E|*d_l"),
-            "cores": threads or os.cpu_count()}
+            "cores": threads or host_threads()}
 
 
 # ---------------------------------------------------------------------------
@@ -400,7 +407,7 @@ def main():
               "ordering": chosen, "l2": "inputs larger than L2 (no flush)"}
 
     if args.impl == "reference":
-        threads = os.cpu_count()
+        threads = host_threads()
         times = []
         for s in range(args.warmup + args.steps):
             r = reference_cpu_sample(ds, dims, threads=threads)
@@ -417,9 +424,8 @@ def main():
                "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
         print(json.dumps(out), flush=True)
-        if world > 1:
+        if world > 1:  # the other ranks left at once (no barrier to meet them at)
             import torch.distributed as dist
-            dist.barrier()
             dist.destroy_process_group()
         return
 
