@@ -195,6 +195,7 @@ struct Device {
   DBuf value, grad;                    // cap x dim slot buffers
   DBuf sa, sb, sc, sd, se, partial;    // staging
   DBuf tT;                             // A^T gz in d_out space (narrow-side backward)
+  DBuf pf_p, pf_z;                     // project-first layers: h.W and A.(h.W), pad4(d_out) wide
   DBuf gemm_ws;
   DBuf W, Wt, Wp;                      // current layer weights, transpose, padded
   DBuf Wt_hi, Wt_lo, Wp_hi, Wp_lo;     // TF32 hi/lo halves for tcgen05
@@ -287,6 +288,10 @@ struct ht_fleet {
   // not written through to host.agg; ht_fleet_checkpoint_read materializes
   // them on demand
   bool ckpt_hbm = false;
+  // project-first layers of this epoch (one device, one batch, d_out < d_in,
+  // HBM checkpoints): agg^l was never formed; ht_fleet_checkpoint_read
+  // aggregates it on demand
+  std::vector<char> agg_deferred;
   // HBM store (placement "device") on a single device: its arrays serve as
   // the owner-cache mirrors directly (h[0..L], agg[0..L-1], grad[0..L])
   std::vector<void*> alias_h, alias_a, alias_g;
@@ -928,7 +933,7 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (auto* v : {&d.mh, &d.ma, &d.mg})
       for (auto& b : *v) b.release();
     d.mrows_d.release();
-    for (DBuf* b : {&d.sgd_p, &d.sgd_w, &d.sgd_t}) b->release();
+    for (DBuf* b : {&d.sgd_p, &d.sgd_w, &d.sgd_t, &d.pf_p, &d.pf_z}) b->release();
     if (d.wpin) cudaFreeHost(d.wpin);
     if (d.lpin) cudaFreeHost(d.lpin);
     if (d.sgd_pin) cudaFreeHost(d.sgd_pin);
@@ -1532,6 +1537,19 @@ bool gat_direct(ht_fleet* f, Device& d) {
   return !getenv("HT_NO_GAT_DIRECT") && direct_bwd(f, d) && c.bx_rows == d.mcount && c.nv == d.mcount && c.dest_m0 == 0;
 }
 
+// Project-first GCN layer (d_out < d_in, one device, one batch, identity
+// mirror, HBM checkpoints): z = A.(h.W) instead of (A.h).W - the gather
+// moves pad4(d_out)-wide rows instead of d_in-wide ones (47 vs 256 floats
+// for the last cfg-2 layer).  The same product reassociated (TF32 3x GEMM,
+// FP32 sums); the backward then takes dW = h^T (A^T gz) (rows the narrow-side
+// pass computes anyway) and agg^l is only formed if host.agg[l] is read.
+bool project_first(ht_fleet* f, Device& d, int d_in, int d_out, int precision) {
+  const DevChunk& c = d.chunks[0];
+  return precision == HT_PREC_TF32 && d_out < d_in && f->ckpt_hbm && !f->gat &&
+         direct_bwd(f, d) && c.bx_rows == d.mcount && c.nv == d.mcount && c.dest_m0 == 0 &&
+         !getenv("HT_NO_PROJECT_FIRST");
+}
+
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
 int cache_upload(ht_fleet* f, Device& d, cudaStream_t s, const void* host, float* mirror,
                  int64_t rb) {
@@ -1632,6 +1650,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
   f->dims.assign(dims, dims + L + 1);
   f->hptr.assign(L + 1, nullptr);
   f->hdev.assign(L + 1, 0);
+  f->agg_deferred.assign(L, 0);
   int dmax = 0;
   for (int l = 0; l <= L; ++l) dmax = std::max(dmax, pad4(dims[l]));
   for (auto& d : f->dev) {
@@ -1813,16 +1832,27 @@ extern "C" int ht_fleet_checkpoint_read(ht_fleet* f, int layer, void* host_agg) 
   void* hp;
   HT_TRY(dev_ptr(host_agg, &hp));
   const int64_t rb = (int64_t)f->dims[layer] * 4;
+  const bool deferred = layer < (int)f->agg_deferred.size() && f->agg_deferred[layer];
   for (auto& d : f->dev) {
     if (!d.local) continue;
     if (!d.cache || (int)d.ma.size() <= layer || !d.ma[layer].p)
       return fail(HT_ESTATE, "checkpoints are not held in HBM mirrors");
     HT_TRY(set_dev(d));
+    if (deferred) {  // project-first layer: agg^l = A.h^l now, the forward's gather
+      const DevChunk& c = d.chunks[0];
+      const int din = f->dims[layer];
+      HT_TRY(launch_seg(d.stream, d.ma[layer].as<float>(), d.mh[layer].as<float>(), din, din,
+                        c.csc_off.as<int64_t>(), c.csc_gid.as<int32_t>(), c.csc_w.as<float>(), c.nv,
+                        c.fw_np, c.fw_lo, c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt,
+                        d.partial.as<float>()));
+    }
     HT_TRY(cache_writeback(f, d, hp, d.ma[layer].as<float>(), rb));
   }
+  if (deferred) f->agg_deferred[layer] = 0;
   for (auto& d : f->dev)
     if (d.local) {
       HT_TRY(set_dev(d));
+      CU(cudaStreamSynchronize(d.stream));
       CU(cudaStreamSynchronize(d.tout));
     }
   return HT_OK;
@@ -1944,6 +1974,50 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       DevChunk& c = d.chunks[j];
       const int s = (int)(d.fwd_count & 1);
       if (d.fwd_count >= 2 && !d.cache) HT_TRY(ev_wait(d.stream, d.e_out[s]));  // staging set s drained
+      const bool lastb = j == f->n - 1;
+      if (hbm_inputs(f, d, layer, hin) && project_first(f, d, d_in, d_out, precision)) {
+        // z = A.(h.W): the narrow projection of every row first, then the
+        // CSC gather over pad4(d_out)-wide rows, then ReLU into h^{l+1}
+        const int ldp = pad4(d_out);
+        const int64_t rows = d.mcount;
+        HT_TRY(d.pf_p.ensure(rows * ldp * 4));
+        HT_TRY(d.pf_z.ensure(rows * ldp * 4));
+        if (ldp != d_out) CU(cudaMemsetAsync(d.pf_p.p, 0, rows * ldp * 4, d.stream));  // pad column
+        LayerW& w = d.lw[layer];
+        TimerRec tg;
+        timer_begin(f, d, tg, d.stream);
+        HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, true, hbm_inputs(f, d, layer, hin), d_in,
+                                              rows, d_in, w.Wt_hi.as<float>(), w.Wt_lo.as<float>(),
+                                              d_in, d_out, d.pf_p.as<float>(), ldp, nullptr, 0));
+        timer_end(f, d, tg, 2, 2.0 * rows * d_in * d_out, d.stream);
+        TimerRec tr;
+        timer_begin(f, d, tr, d.stream);
+        HT_TRY(launch_seg(d.stream, d.pf_z.as<float>(), d.pf_p.as<float>(), ldp, ldp,
+                          c.csc_off.as<int64_t>(), c.csc_gid.as<int32_t>(), c.csc_w.as<float>(),
+                          c.nv, c.fw_np, c.fw_lo, c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt,
+                          d.partial.as<float>()));
+        timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * ldp) + (double)c.nv * (4.0 * ldp + 4.0),
+                  d.stream);
+        HT_TRY(ev_rec(d.e_agg, d.stream));
+        float* hdst = last ? d.hL.as<float>() + d.hL_off[j] * d_out
+                           : d.mh[layer + 1].as<float>() + c.dest_m0 * d_out;
+        count_launch(3);
+        ht::k_relu_rows<<<grid_for(c.nv * (int64_t)d_out / 32 + 1), kThreads, 0, d.stream>>>(
+            hdst, d_out, d.pf_z.as<float>(), ldp, c.nv, d_out);
+        CU(cudaGetLastError());
+        HT_TRY(ev_rec(d.e_comp, d.stream));
+        HT_TRY(ev_wait(d.tout, d.e_comp));
+        if (!(last && f->lean && d.cache)) HT_TRY(put_dest(f, c, d.tout, hout, hdst, rbo, -1));
+        if (lastb)
+          for (int g = 0; g < kChunks; ++g) {
+            HT_TRY(ev_rec(d.e_hchunk[g], d.tout));
+            HT_TRY(ev_rec(d.e_aggst[layer * kChunks + g], d.tout));
+          }
+        HT_TRY(ev_rec(d.e_out[s], d.tout));
+        f->agg_deferred[layer] = 1;  // agg^l formed only if host.agg[l] is read
+        d.fwd_count++;
+        continue;
+      }
       // cache: the aggregation and h rows land in their mirrors directly
       float* agg = d.cache ? d.ma[layer].as<float>() + c.dest_m0 * d_in : d.fa[s].as<float>();
       TimerRec tr;
@@ -1962,7 +2036,6 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
                               : d.fb[s].as<float>();
       LayerW& w = d.lw[layer];
       const int64_t* rows = c.dest_rows.as<int64_t>();
-      const bool lastb = j == f->n - 1;
       // K4 in host-row chunks when the destination rows are copy-engine
       // runs: chunk g's h rows go to the host (K5) while chunk g+1 computes
       const int nck = c.dest_pos.empty() ? 1 : kChunks;
@@ -2168,6 +2241,10 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // same product, reassociated).  Needs gz with zeroed pad columns.
       const bool no_in = f->lean && layer == 0;  // lean: grad_h^0 is not produced
       const bool narrow = !no_in && HO && d_out < d_in && !getenv("HT_NO_NARROW_BWD");
+      // project-first forward (agg^l never formed): the narrow-side rows
+      // A^T gz give dW = h^T (A^T gz); needs them in row order (expanded CSR)
+      const bool pfl = layer < (int)f->agg_deferred.size() && f->agg_deferred[layer] &&
+                       precision == HT_PREC_TF32;
       if (HO && M > 0) {  // gz = g * (h > 0): z need not be recomputed
         count_launch();
         ht::k_relu_mask<<<grid_for(M), kThreads, 0, d.stream>>>(GZ, ldz, G, HO, hrows, M, d_out);
@@ -2181,7 +2258,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
           HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
                                                 w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
                                                 nullptr, 0));
-        if (M > 0) {
+        if (M > 0 && !pfl) {  // (project-first layer: dW = h^T (A^T gz) after K8)
           int used = 1;
           HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, ldz, d_out, M, kSplitsMax,
                                d.gemm_ws.as<float>(), &used));
@@ -2212,7 +2289,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       }
       timer_end(f, d, tg, 2, 6.0 * c.nv * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_bcomp[s], d.stream));
-      if (no_in) {
+      if (no_in && !pfl) {
         d.bwd_count++;
         continue;
       }
@@ -2224,9 +2301,13 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // (every host row; zero rows for sources without out-edges) in place
       // of the views - the only flush of each row, a store
       const bool dx = direct_bwd(f, d) && c.bx_rows == d.mcount;
+      if (pfl && !(dx && HO && (narrow || no_in)))
+        return fail(HT_ESTATE, "project-first layer %d needs the one-device narrow backward", layer);
       const int64_t nseg = dx ? c.bx_rows : c.nn;
       float* views = dx ? d.mg[layer].as<float>() : d.se.as<float>();
-      HT_TRY(launch_seg(d.stream, narrow ? d.tT.as<float>() : views, narrow ? GZ : GA, kw, kw,
+      HT_TRY(launch_seg(d.stream, (narrow || pfl) ? d.tT.as<float>() : views,
+                        (narrow || pfl) ? GZ : GA, (narrow || pfl) ? ldz : kw,
+                        (narrow || pfl) ? ldz : kw,
                         dx ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>(),
                         c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), nseg,
                         dx ? c.bx_np : c.bw_np, dx ? c.bx_lo : c.bw_lo, dx ? c.bx_hi : c.bw_hi,
@@ -2235,6 +2316,20 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
                         d.partial.as<float>()));
       timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * kw) + (double)c.nn * (4.0 * kw + 4.0),
                 d.stream);
+      if (pfl && nseg > 0) {  // dW = h^T (A^T gz), rows in row order
+        int used = 1;
+        const int64_t nwl = (int64_t)d_in * d_out;
+        HT_TRY(ht::tc::wgrad(d.stream, d.mh[layer].as<float>(), d_in, d_in, d.tT.as<float>(), ldz,
+                             d_out, nseg, kSplitsMax, d.gemm_ws.as<float>(), &used));
+        count_launch(2);
+        ht::k_reduce_splits<<<grid_for(nwl / 32 + 1), 256, 0, d.stream>>>(
+            d.gWall.as<float>() + d.gW_off[layer], d.gemm_ws.as<float>(), nwl, used);
+        CU(cudaGetLastError());
+      }
+      if (no_in) {  // (lean, layer 0: grad_h^0 is not produced)
+        d.bwd_count++;
+        continue;
+      }
       if (narrow && nseg > 0) {  // views = (A^T gz) W^T
         if (precision == HT_PREC_TF32)
           HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, d.tT.as<float>(), ldz, nseg, d_out,

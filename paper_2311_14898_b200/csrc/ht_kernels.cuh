@@ -547,6 +547,19 @@ __global__ void __launch_bounds__(256) k_relu_mask(float* __restrict__ gz, int64
 }
 
 // ---------------------------------------------------------------------------
+// out[r][c] = max(in[r][c], 0) for c < d (row strides ldo / ldi floats)
+__global__ void __launch_bounds__(256) k_relu_rows(float* __restrict__ out, int64_t ldo,
+                                                   const float* __restrict__ in, int64_t ldi,
+                                                   int64_t rows, int d) {
+  const int64_t n = rows * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / d;
+    const int c = (int)(e - r * d);
+    out[r * ldo + c] = fmaxf(in[r * ldi + c], 0.f);
+  }
+}
+
 // K11 loss: rows of H (ld = d); labels/mask aligned with rows; gradient rows
 // written to out (host or device) at out_rows[r] (stride d), or at
 // out_base + r when out_base >= 0.  One warp per

@@ -43,6 +43,7 @@ def test_cache_bitwise_equals_host_path(kind, m, n, mode, monkeypatch):
     # likewise the one-device GAT path sums dW / da over all rows (rows
     # without out-edges add zeros: a different association of the same sums)
     monkeypatch.setenv("HT_NO_GAT_DIRECT", "1")
+    monkeypatch.setenv("HT_NO_PROJECT_FIRST", "1")  # (needs HBM checkpoints; reassociates)
     ds = H.synth_dataset(H.SynthSpec(num_vertices=2500, avg_degree=8.0, seed=4), 16, 8)
     a = H.partition_vertices(ds.graph, m, seed=4)
     p = H.split_chunks(ds.graph, a, n)
@@ -166,12 +167,13 @@ def test_hbm_store_in_place_equals_host_store(kind):
 
 
 @pytest.mark.parametrize("m,n", [(1, 1), (1, 3), (3, 2)])
-def test_hbm_checkpoints_equal_host_checkpoints(m, n):
+def test_hbm_checkpoints_equal_host_checkpoints(m, n, monkeypatch):
     """Checkpoint tier: with the owner cache the GCN agg checkpoints stay in
     HBM (checkpoints="auto") instead of being written through ("host").
     The epochs must be bitwise equal, and host.agg - filled from HBM on first
     read, here after two epochs and after the fleet is closed - must equal
     the written-through arrays."""
+    monkeypatch.setenv("HT_NO_PROJECT_FIRST", "1")  # same arithmetic on both sides
     ds = H.synth_dataset(H.SynthSpec(num_vertices=2500, avg_degree=8.0, seed=5), 16, 8)
     a = H.partition_vertices(ds.graph, m, seed=5)
     p = H.split_chunks(ds.graph, a, n)
@@ -198,3 +200,38 @@ def test_hbm_checkpoints_equal_host_checkpoints(m, n):
     for l in res["host"][3]:
         np.testing.assert_array_equal(res["host"][3][l], res["auto"][3][l])
         assert np.abs(res["auto"][3][l]).sum() > 0
+
+
+def test_project_first_layers(monkeypatch):
+    """One device, one batch, HBM checkpoints: layers with d_out < d_in run
+    z = A.(h.W) (narrow gather) and dW = h^T (A^T gz).  Against the
+    (A.h).W path: parameters and outputs within FP32 reassociation error,
+    and the deferred checkpoints - aggregated when host.agg is read - bitwise
+    equal where their inputs are (agg^0)."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=3000, avg_degree=9.0, seed=8), 32, 8)
+    p = H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 1, seed=8), 1)
+    plan = H.plan_for_partition(p)
+    dims = [32, 16, 8]  # both layers narrow
+    out = {}
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("HT_NO_PROJECT_FIRST", flag)
+        else:
+            monkeypatch.delenv("HT_NO_PROJECT_FIRST", raising=False)
+        model = H.init_model("gcn", dims, seed=3, lr=0.1, dtype=np.float32)
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, cache="on")
+        losses = [H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss for _ in range(2)]
+        out[flag] = (losses, [w.copy() for w in model.weights],
+                     [np.array(x) for x in host.h[1:]], [np.array(g) for g in host.grad_h],
+                     {l: np.array(host.agg[l]) for l in range(2)})
+        fleet.close()
+    a, b = out["1"], out[None]
+    np.testing.assert_allclose(a[0], b[0], rtol=1e-5)
+    for x, y in zip(a[1] + a[2] + a[3], b[1] + b[2] + b[3]):
+        assert np.abs(x - y).max() <= 1e-4 * max(np.abs(x).max(), 1e-30)
+    # agg^0 = A.h^0 reads the same features: bitwise; agg^1 aggregates h^1,
+    # which the two paths produce with different roundings
+    np.testing.assert_array_equal(a[4][0], b[4][0])
+    assert np.abs(a[4][1] - b[4][1]).max() <= 1e-4 * np.abs(b[4][1]).max()
