@@ -298,6 +298,14 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision, rank=rank,
                           devices=[dev] if rank is not None else None, lean=lean,
                           checkpoints=checkpoints, cache=cache)
+    try:
+        return _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind,
+                             labels)
+    finally:
+        fleet.close()  # device memory back before the next measurement (also on failure)
+
+
+def _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind, labels):
     model = H.init_model(kind, dims, seed=seed, lr=0.1, dtype=np.float32)
     losses = []
     for _ in range(warmup):
@@ -320,8 +328,6 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     rep = fleet.transfer_report()
     cache = fleet.cache_active
     ckpt_hbm = bool(host.agg.pending)
-    fleet.close()  # device memory back before the next measurement
-    del host
     return {"ms_total": ms.value, "wall_s": wall, "losses": losses, "launches": launches,
             "stats": stats, "report": rep, "cache": cache, "ckpt_hbm": ckpt_hbm}
 
@@ -489,7 +495,7 @@ def main():
     plan_h2d, plan_d2h = host_bytes_per_epoch(plan, dims)
     base_h2d, base_d2h = host_bytes_per_epoch(plan, dims, "baseline")
     virt = None
-    if world == 1:
+    if world == 1 and args.config == "cfg2":  # (8 virtual devices' staging fits cfg 2)
         try:
             virt = virtual_fleet_epochs(ds, dims, precision=args.precision, seed=cfg["seed"],
                                         device=int(os.environ.get("LOCAL_RANK", "0")))
@@ -500,6 +506,10 @@ def main():
         dedup["at_scale"] = dedup_at_scale(ds, dims, device=int(os.environ.get("LOCAL_RANK", "0")))
     except Exception as exc:  # noqa: BLE001 - report, do not fail the bench
         log(f"[bench] dedup at scale failed: {exc}")
+        try:  # the host planner gives the same sets (bit-identical)
+            dedup["at_scale"] = dedup_at_scale(ds, dims, device=None)
+        except Exception as exc2:  # noqa: BLE001
+            log(f"[bench] dedup at scale (host planner) failed: {exc2}")
     pcie = pcie_peaks()
     pcie_bidir = pcie[2] if pcie else None
 
