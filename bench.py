@@ -302,6 +302,7 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
         return _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind,
                              labels)
     finally:
+        host.agg.pending.clear()  # nobody reads these checkpoints: nothing to materialize
         fleet.close()  # device memory back before the next measurement (also on failure)
 
 

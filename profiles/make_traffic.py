@@ -33,8 +33,15 @@ def main(path, epochs, layers=3):
             per[d["ID"]]["name"] = d["Kernel Name"]
             if unit is not None:
                 per[d["ID"]][d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * unit
+    # kernels after the last SGD step belong to no epoch (e.g. a deferred
+    # checkpoint aggregated when the fleet is closed): not counted
+    ids = sorted(per, key=int)
+    last_sgd = max((int(k) for k in ids if "k_sgd" in per[k]["name"]), default=None)
     tot, n = 0.0, 0
-    for v in per.values():
+    for k in ids:
+        v = per[k]
+        if last_sgd is not None and int(k) > last_sgd:
+            continue
         if AGG.search(v["name"]):
             tot += v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)
             n += 1
