@@ -231,6 +231,17 @@ def test_project_first_layers(monkeypatch):
     np.testing.assert_allclose(a[0], b[0], rtol=1e-5)
     for x, y in zip(a[1] + a[2] + a[3], b[1] + b[2] + b[3]):
         assert np.abs(x - y).max() <= 1e-4 * max(np.abs(x).max(), 1e-30)
+    # lean epochs (no grad_h^0) on the project-first path: layer 0's dW
+    # still comes from the A^T gz rows - parameters bitwise the same
+    model = H.init_model("gcn", dims, seed=3, lr=0.1, dtype=np.float32)
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+    host.set_features(ds.features)
+    fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, cache="on", lean=True)
+    lean_losses = [H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss for _ in range(2)]
+    fleet.close()
+    assert lean_losses == b[0]
+    for x, y in zip(model.weights, b[1]):
+        np.testing.assert_array_equal(x, y)
     # agg^0 = A.h^0 reads the same features: bitwise; agg^1 aggregates h^1,
     # which the two paths produce with different roundings
     np.testing.assert_array_equal(a[4][0], b[4][0])
