@@ -217,7 +217,10 @@ int ht_fleet_set_lean(ht_fleet* f, int lean);
  * checkpoints in the HBM mirrors the backward reads and does not write them
  * to agg_out.  ht_fleet_checkpoint_read then fills host_agg (the layer's
  * (V, d_layer) host array) from the mirrors; valid until the next forward
- * of that layer. */
+ * of that layer.  With one device and one batch, TF32 layers with
+ * d_out < d_in then run project-first (z = A.(h.W)); their agg^l is never
+ * formed in the epoch and ht_fleet_checkpoint_read aggregates it on demand
+ * (same kernel and edge order as the forward gather). */
 int ht_fleet_set_checkpoints(ht_fleet* f, int hbm);
 int ht_fleet_checkpoint_read(ht_fleet* f, int layer, void* host_agg);
 /* HBM-resident store (HongTu-IM) on a single device: its device arrays
