@@ -233,3 +233,19 @@ def test_feature_matrix_mmap_into_pinned_host_store(tmp_path):
     hb = H.HostStore(200_000, [24, 8], dtype=np.float32)
     hb.set_features(big)
     np.testing.assert_array_equal(hb.h[0], big.astype(np.float32))
+
+
+def test_bench_dedup_report_matches_reference_numbers():
+    """bench.py's host-bytes accounting on config 1 against the reference's
+    own measurements: m=8, n=1 volumes (263217, 99968,
+    99968) and 422,350,848 host bytes per epoch through the 'full' plan
+    (plus the loss-gradient rows and the label/mask upload this path adds)."""
+    import bench
+    c = bench.CONFIGS["cfg1"]
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=c["V"], avg_degree=c["avg_degree"], seed=0),
+                         c["dims"][0], c["dims"][-1])
+    r = bench.dedup_at_scale(ds, c["dims"], m=8, n=1)
+    assert (r["volumes"]["v_ori"], r["volumes"]["v_p2p"], r["volumes"]["v_ru"]) == (263217, 99968, 99968)
+    V, dL = c["V"], c["dims"][-1]
+    assert round(r["host_gb_full"] * 1e9) == 422_350_848 + 4 * V * dL + 9 * V
+    assert r["reduction"] > 0.25  # the north star's >= 25 % host-byte reduction
