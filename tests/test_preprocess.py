@@ -249,3 +249,15 @@ def test_bench_dedup_report_matches_reference_numbers():
     V, dL = c["V"], c["dims"][-1]
     assert round(r["host_gb_full"] * 1e9) == 422_350_848 + 4 * V * dL + 9 * V
     assert r["reduction"] > 0.25  # the north star's >= 25 % host-byte reduction
+
+
+def test_bench_dedup_report_m4n4_matches_reference_numbers():
+    """Config 1 at m=4, n=4 (reorganized): 466,520,064 host bytes through the
+    'full' plan, 903,375,360 through the non-deduplicated one (SURVEY App. A
+    epoch meters), plus the loss-gradient rows and label/mask upload."""
+    import bench
+    r = bench.dedup_report()
+    extra = 4 * 100_000 * 16 + 9 * 100_000
+    assert round(r["host_gb_full"] * 1e9) == 466_520_064 + extra
+    assert round(r["host_gb_baseline"] * 1e9) == 903_375_360 + extra
+    assert (r["volumes"]["v_ori"], r["volumes"]["v_p2p"], r["volumes"]["v_ru"]) == (413135, 319160, 128724)
