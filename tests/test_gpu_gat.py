@@ -114,10 +114,13 @@ def test_gat_tf32_within_contract_of_fp64_oracle():
         assert O.rel_err(snaps[0]["attn_grads"][l], ref["attn_grads"][l]) < 1e-3
 
 
-def test_gat_zero_in_degree_and_hub_segments():
+@pytest.mark.parametrize("m,n", [(2, 2), (1, 1)])
+def test_gat_zero_in_degree_and_hub_segments(m, n):
     """Destinations without in-edges get zero rows (src/engine.py:217-221);
     a hub source with thousands of out-edges and a hub destination with
-    thousands of in-edges run through the warp-per-segment kernels."""
+    thousands of in-edges run through the warp-per-segment kernels.  (1, 1)
+    runs the one-device path: hub pieces over the expanded CSR with the
+    destination term folded into the fixup.)"""
     rng = np.random.default_rng(9)
     V = 6000
     src = np.concatenate([np.zeros(5000, np.int64), rng.integers(0, V, 12000),
@@ -128,8 +131,8 @@ def test_gat_zero_in_degree_and_hub_segments():
     X = rng.standard_normal((V, 12))
     labels = rng.integers(0, 4, V)
     mask = rng.random(V) < 0.5
-    a = H.PartitionAssignment(owner=(np.arange(V) % 2).astype(np.int64), m=2)
-    p = H.split_chunks(g, a, 2)
+    a = H.PartitionAssignment(owner=(np.arange(V) % m).astype(np.int64), m=m)
+    p = H.split_chunks(g, a, n)
     ds = H.SynthDataset(graph=g, features=X, labels=labels, mask=mask)
     dims = [12, 16, 4]
     m0 = H.init_model("gat", dims, seed=4, dtype=np.float32)
