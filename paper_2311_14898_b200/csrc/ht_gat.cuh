@@ -178,6 +178,33 @@ __global__ void __launch_bounds__(256) k_gat_dst(
       }
       if (BWD && lane < cnt) AL[base + lane] = my_a;
       int k = 0;
+      if (!BWD && NV == 1 && d4 <= 16) {
+        // rows of <= 64 floats: each half-warp loads one row, so one
+        // instruction brings two; the adds stay in edge order (lanes 0-15
+        // hold the sums, lanes 16-31 hand over the odd rows)
+        const int hl = lane >> 4, sl = lane & 15;
+        for (; k + 8 <= cnt; k += 8) {
+          float4 x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int s = __shfl_sync(0xffffffffu, my_i, k + 2 * u + hl);
+            x[u] = sl < d4 ? __ldg(reinterpret_cast<const float4*>(Q + (int64_t)s * d) + sl)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float4 y;
+            y.x = __shfl_down_sync(0xffffffffu, x[u].x, 16);
+            y.y = __shfl_down_sync(0xffffffffu, x[u].y, 16);
+            y.z = __shfl_down_sync(0xffffffffu, x[u].z, 16);
+            y.w = __shfl_down_sync(0xffffffffu, x[u].w, 16);
+            const float a0 = __shfl_sync(0xffffffffu, my_a, k + 2 * u);
+            const float a1 = __shfl_sync(0xffffffffu, my_a, k + 2 * u + 1);
+            axpy_rn(acc[0], a0, x[u]);
+            axpy_rn(acc[0], a1, y);
+          }
+        }
+      }
       for (; k + 4 <= cnt; k += 4) {  // four rows in flight
         float4 x[4][NV];
         float a[4];
