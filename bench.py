@@ -411,7 +411,9 @@ def main():
     E = ds.graph.num_edges
     config = {"workload": cfg["name"], "config_id": args.config, "vertices": cfg["V"],
               "edges": E, "dims": dims, "m": m, "n": cfg["n"], "mode": "full",
-              "ordering": chosen, "l2": "inputs larger than L2 (no flush)"}
+              "ordering": chosen,
+              "l2": ("inputs larger than L2 (no flush)" if 4 * cfg["V"] * sum(dims) > 126e6
+                     else "inputs fit in the 126 MB L2 (not flushed between steps)")}
 
     if args.impl == "reference":
         threads = host_threads()
