@@ -3,7 +3,8 @@
 training epoch: forward over every layer and batch, loss, backward, SGD).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
-    python bench.py --impl reference ...     # CPU reference arm (oracle port)
+    python bench.py --impl reference ...     # CPU reference arm (chunktrain from
+                                             # baseline/_ref, else the oracle port)
 
 Workload (N=1): BASELINE config 2 - 3-layer GCN 100-256-256-47 on an
 ogbn-products-shape synthetic graph (2.4M vertices, ~62M edges), m = N
@@ -247,36 +248,159 @@ def host_threads():
     return int(env) if env and env.isdigit() and int(env) > 0 else os.cpu_count()
 
 
-def reference_cpu_sample(ds, dims, budget_edges=1_500_000, threads=None):
-    """Time the oracle port (numpy restatement of the reference's chunk
-    kernels, the CPU implementation of this path) on a bounded sample:
-    layer-0 forward + hybrid backward over the first destination vertices
-    holding ~budget_edges in-edges; extrapolate to a full epoch by
-    sum_l |E| * d_l."""
-    from oracle import hongtu_oracle as O
-    g = ds.graph
-    gd = {k: getattr(g, k) for k in ("csc_offsets", "csc_sources", "edge_weights")}
-    gd["num_vertices"] = g.num_vertices
-    k = int(np.searchsorted(g.csc_offsets, budget_edges))
-    verts = np.arange(max(k, 1), dtype=np.int64)
-    ch = O.chunk_of(gd, verts)
-    X = np.asarray(ds.features[ch["sources"]], dtype=np.float32)
-    W = O.glorot_weights(dims[:2], 0, dtype=np.float32)[0]
-    gout = np.random.default_rng(0).standard_normal((verts.size, dims[1])).astype(np.float32)
-    t0 = time.perf_counter()
-    _, agg, _ = O.gcn_chunk_forward(ch, X, W)
-    O.gcn_chunk_backward(ch, agg, gout, W)
-    dt = time.perf_counter() - t0
-    es = int(ch["csc_local_src"].size)
-    L = len(dims) - 1
-    scale = sum(g.num_edges * dims[l] for l in range(L)) / (es * dims[0])
-    epoch_s = dt * scale
-    return {"epoch_s_extrapolated": epoch_s, "gteps": L * g.num_edges / epoch_s / 1e9,
-            "sample_s": dt, "sample_edges": es,
-            "sample": (f"layer-0 forward+backward (oracle port, numpy fp32) over the first "
-                       f"{verts.size} destinations ({es} edges, d={dims[0]}->{dims[1]}), "
-                       f"extrapolated x{scale:.1f} by sum_l |E|*d_l"),
-            "cores": threads or host_threads()}
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_impl():
+    """The CPU implementation of the path that the reference arm and the
+    cpu_baseline time: the unmodified reference package ``chunktrain`` from
+    ``baseline/_ref`` (kind "reference"), else the oracle port (kind "port").
+    Neither loads this repository's native library."""
+    if os.path.isdir(REF_DIR) and REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        from chunktrain import engine as E
+        from chunktrain import partition as P
+
+        def chunk(g, verts):
+            return P.chunk_from_vertices(g, verts, 0, 0)
+
+        def fwd(ch, h_nbr, W):
+            return E.gcn_layer_forward(ch, h_nbr, W)
+
+        def bwd(ch, agg, gout, W):
+            return E.gcn_layer_backward_hybrid(ch, agg, gout, W)
+
+        def src_of(ch):
+            return ch.sources
+
+        def nedges(ch):
+            return int(ch.num_edges)
+
+        return "reference", dict(chunk=chunk, fwd=fwd, bwd=bwd, loss=E.downstream_loss,
+                                 sources=src_of, edges=nedges,
+                                 what="chunktrain (unmodified reference, baseline/_ref)")
+    except ImportError:
+        from oracle import hongtu_oracle as O
+
+        def chunk(g, verts):
+            gd = {k: getattr(g, k) for k in ("csc_offsets", "csc_sources", "edge_weights")}
+            gd["num_vertices"] = g.num_vertices
+            return O.chunk_of(gd, verts)
+
+        return "port", dict(chunk=chunk, fwd=O.gcn_chunk_forward, bwd=O.gcn_chunk_backward,
+                            loss=O.softmax_xent, sources=lambda ch: ch["sources"],
+                            edges=lambda ch: int(ch["csc_local_src"].size),
+                            what="oracle port (oracle/hongtu_oracle.py, numpy)")
+
+
+def reference_graph(cfg):
+    """The workload's graph and node data built without this repository's
+    native library: chunktrain.synth when the reference is installed, else
+    the same draws (synth_edges, pure numpy) + numpy parallel-edge removal +
+    the oracle's graph builder."""
+    spec_kw = dict(num_vertices=cfg["V"], avg_degree=cfg["avg_degree"], seed=cfg["seed"])
+    if os.path.isdir(REF_DIR) and REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        from chunktrain import synth as S
+        ds = S.synth_dataset(S.SynthSpec(**spec_kw), cfg["dims"][0], cfg["dims"][-1])
+        return ds.graph, ds.labels, ds.mask
+    except ImportError:
+        from types import SimpleNamespace
+
+        from oracle import hongtu_oracle as O
+        from paper_2311_14898_b200 import synth as PS  # numpy draws only
+        spec = PS.SynthSpec(**spec_kw)
+        src, dst, cl = PS.synth_edges(spec)
+        _, keep = np.unique(dst * spec.num_vertices + src, return_index=True)
+        gd = O.build_graph(src[keep], dst[keep], spec.num_vertices)
+        _, y, mask = PS.synth_node_data(spec.num_vertices, cfg["dims"][0], cfg["dims"][-1],
+                                        spec.seed, cluster_of=cl)
+        return SimpleNamespace(**gd), y, mask
+
+
+class ReferenceSampler:
+    """One bounded sample of the epoch on the CPU reference path.
+
+    A step runs, for a window of consecutive destination vertices holding
+    ~``budget_edges`` in-edges (a different window each step, spread over
+    the vertex range), exactly what the reference's train_epoch does per
+    batch and layer (src/engine.py:409-477): gather h^l[N] from the full
+    (V, d_l) host array, gcn_layer_forward, the loss on the last layer,
+    gcn_layer_backward_hybrid from the agg checkpoint, and the flush of the
+    neighbour gradients into the full (V, d_l) host gradient array - for
+    every layer at its own width.  Nothing is extrapolated: the rate is the
+    edges actually traversed (each edge once per layer, as GTEPS counts
+    them) over the step's wall time."""
+
+    def __init__(self, graph, labels, mask, dims, budget_edges=250_000, windows=16, seed=0):
+        self.kind, self.api = reference_impl()
+        self.dims = dims
+        V = int(graph.num_vertices)
+        off = np.asarray(graph.csc_offsets)
+        self.chunks = []
+        for w in range(windows):
+            v0 = (V * w) // windows
+            v1 = int(np.searchsorted(off, off[v0] + budget_edges))
+            v1 = min(max(v1, v0 + 1), V)
+            verts = np.arange(v0, v1, dtype=np.int64)
+            self.chunks.append((verts, self.api["chunk"](graph, verts)))
+        rng = np.random.default_rng(seed)
+        L = len(dims) - 1
+        # host arrays of the layer inputs / input gradients (the HostStore)
+        self.h = [rng.standard_normal((V, dims[l]), dtype=np.float32) for l in range(L)]
+        self.g = [np.zeros((V, dims[l]), dtype=np.float32) for l in range(L)]
+        self.W = [(rng.standard_normal((dims[l], dims[l + 1])) *
+                   np.sqrt(2.0 / (dims[l] + dims[l + 1]))).astype(np.float32) for l in range(L)]
+        self.gup = [rng.standard_normal((budget_edges, dims[l + 1]), dtype=np.float32) * 1e-3
+                    for l in range(L)]
+        self.labels, self.mask = np.asarray(labels), np.asarray(mask)
+        self.step_i = 0
+
+    def step(self):
+        """One timed sample; returns (seconds, edges traversed)."""
+        verts, ch = self.chunks[self.step_i % len(self.chunks)]
+        self.step_i += 1
+        api, L = self.api, len(self.dims) - 1
+        src = api["sources"](ch)
+        nv = verts.size
+        t0 = time.perf_counter()
+        aggs = []
+        for l in range(L):
+            h_out, agg, _ = api["fwd"](ch, self.h[l][src], self.W[l])
+            aggs.append(agg)
+        _, grad = api["loss"](h_out, self.labels[verts], self.mask[verts])
+        for l in reversed(range(L)):
+            gout = grad if l == L - 1 else self.gup[l][:nv]
+            gnbr, _ = api["bwd"](ch, aggs[l], gout, self.W[l])
+            self.g[l][src] += gnbr
+        dt = time.perf_counter() - t0
+        return dt, L * api["edges"](ch)
+
+    def describe(self):
+        e = [self.api["edges"](c) for _, c in self.chunks]
+        return (f"{self.api['what']}: per step, one window of consecutive destinations "
+                f"(~{int(np.mean(e))} in-edges; {len(e)} windows spread over the vertex range, "
+                f"one per step in turn) through every layer: gather h^l[N] from the full "
+                f"(V, d_l) host array, gcn_layer_forward, downstream_loss, "
+                f"gcn_layer_backward_hybrid, flush into the (V, d_l) gradient array; "
+                f"GTEPS = edges traversed (once per layer) / step wall time, not extrapolated")
+
+
+def reference_cpu_baseline(graph, labels, mask, dims, steps=3, warmup=1):
+    """cpu_baseline of the ours-arm line: a few ReferenceSampler steps."""
+    rs = ReferenceSampler(graph, labels, mask, dims)
+    for _ in range(warmup):
+        rs.step()
+    t = e = 0.0
+    for _ in range(steps):
+        dt, ne = rs.step()
+        t, e = t + dt, e + ne
+    return {"value": e / t / 1e9, "unit": "GTEPS", "cores": host_threads(), "kind": rs.kind,
+            "sample": rs.describe() + f"; {steps} steps after {warmup} warm-up",
+            "seconds": t, "edges": int(e),
+            "note": "np.add.at / np.add.reduceat are single-threaded; BLAS may use all cores"}
 
 
 # ---------------------------------------------------------------------------
@@ -378,6 +502,46 @@ def gat_measure(p, plan, ds, steps, warmup, precision, seed, rank, slowest):
     return out
 
 
+def workload_config(config_id, cfg, E, m, ordering):
+    return {"workload": cfg["name"], "config_id": config_id, "vertices": cfg["V"],
+            "edges": E, "dims": cfg["dims"], "m": m, "n": cfg["n"], "mode": "full",
+            "ordering": ordering,
+            "l2": ("inputs larger than L2 (no flush)" if 4 * cfg["V"] * sum(cfg["dims"]) > 126e6
+                   else "inputs fit in the 126 MB L2 (not flushed between steps)")}
+
+
+def reference_arm(args, cfg, n_gpus):
+    """bench.py --impl reference: the reference's own CPU implementation of
+    the path (ReferenceSampler), W warm-up + K timed steps, each a bounded
+    sample of the workload; the JSON line reports exactly those K steps."""
+    dims = cfg["dims"]
+    t0 = time.time()
+    graph, labels, mask = reference_graph(cfg)
+    log(f"[bench-ref] graph {time.time() - t0:.1f}s |E|={graph.num_edges}")
+    rs = ReferenceSampler(graph, labels, mask, dims, seed=cfg["seed"])
+    # numpy has nothing to warm beyond the first touch of the host arrays:
+    # one warm-up sample (reported as executed) keeps the run to minutes
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        rs.step()
+    t = e = 0.0
+    for _ in range(args.steps):
+        dt, ne = rs.step()
+        t, e = t + dt, e + ne
+    v = e / t / 1e9
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GTEPS",
+           "n_gpus": n_gpus, "steps": args.steps, "warmup": warm,
+           "warmup_requested": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": workload_config(args.config, cfg, int(graph.num_edges), n_gpus, "identity"),
+           "edges_per_step": e / args.steps,
+           "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": host_threads(), "kind": rs.kind,
+                            "sample": rs.describe(),
+                            "note": "np.add.at / np.add.reduceat are single-threaded"},
+           "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -395,48 +559,24 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     N_gpus = args.gpus if world == 1 else world
+    cfg = CONFIGS[args.config]
+    dims = cfg["dims"]
+    L = len(dims) - 1
+    if args.impl == "reference":
+        # the CPU reference arm runs on rank 0 only; no process group, no GPU,
+        # no native library of this repository
+        if rank == 0:
+            reference_arm(args, cfg, N_gpus)
+        return
     if world > 1:
         # host plumbing only (IPC handles, loss partials, max-over-ranks
         # timing); the data path is CUDA IPC + device-side barriers
         import torch.distributed as dist
         dist.init_process_group("gloo")
-    cfg = CONFIGS[args.config]
-    dims = cfg["dims"]
-    L = len(dims) - 1
-    if args.impl == "reference" and rank != 0:
-        dist.destroy_process_group()  # the CPU reference arm runs on rank 0 only
-        return
     m = N_gpus
     ds, p, plan, chosen = build_inputs(cfg, m)
     E = ds.graph.num_edges
-    config = {"workload": cfg["name"], "config_id": args.config, "vertices": cfg["V"],
-              "edges": E, "dims": dims, "m": m, "n": cfg["n"], "mode": "full",
-              "ordering": chosen,
-              "l2": ("inputs larger than L2 (no flush)" if 4 * cfg["V"] * sum(dims) > 126e6
-                     else "inputs fit in the 126 MB L2 (not flushed between steps)")}
-
-    if args.impl == "reference":
-        threads = host_threads()
-        times = []
-        for s in range(args.warmup + args.steps):
-            r = reference_cpu_sample(ds, dims, threads=threads)
-            if s >= args.warmup:
-                times.append(r["epoch_s_extrapolated"])
-        epoch_s = statistics.mean(times)
-        v = L * E / epoch_s / 1e9
-        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GTEPS",
-               "n_gpus": N_gpus, "steps": args.steps, "warmup": args.warmup,
-               "ms_per_step": epoch_s * 1e3, "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
-               "cpu_baseline": {"value": v, "unit": "GTEPS", "cores": threads, "kind": "port",
-                                "sample": r["sample"]},
-               "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": 0}}
-        print(json.dumps(out), flush=True)
-        if world > 1:  # the other ranks left at once (no barrier to meet them at)
-            import torch.distributed as dist
-            dist.destroy_process_group()
-        return
+    config = workload_config(args.config, cfg, E, m, chosen)
 
     peaks = {}
     try:
@@ -545,20 +685,23 @@ def main():
                 "share_of_step": agg_ms / val["ms_total"] if val["ms_total"] else None}
     cpu = None
     if not args.no_cpu_baseline:
-        r = reference_cpu_sample(ds, dims)
-        cpu = {"value": r["gteps"], "unit": "GTEPS", "cores": r["cores"], "kind": "port",
-               "sample": r["sample"], "epoch_s_extrapolated": r["epoch_s_extrapolated"],
-               "note": "numpy np.add.at-style aggregation is single-threaded; BLAS uses all cores"}
+        cpu = reference_cpu_baseline(ds.graph, ds.labels, ds.mask, dims)
     value = L * E / (ms_v / 1e3) / 1e9
     e2e_v = L * E / (ms_e / 1e3) / 1e9
     out = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": N_gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_v,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": ("f32 aggregation / tf32 tcgen05 GEMMs (3xTF32 forward projections)"
+                  if args.precision == "tf32" else "f32"),
         "data": "synthetic (seeded clustered power-law graph, random-init Glorot weights)",
         "config": config,
         "e2e": {"value": e2e_v, "unit": "GTEPS", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e, "hbm_owner_cache": bool(cached),
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e,
+                "wall_ms_per_step": e2e["wall_s"] / args.steps * 1e3,
+                "timing": "ms_per_step: CUDA events on the fleet streams; wall_ms_per_step: "
+                          "host perf_counter around the same K train_epoch calls",
+                "hbm_owner_cache": bool(cached),
                 "checkpoints_in_hbm": bool(ckpt_hbm),
                 "pcie_gbs": (h2d + d2h) / (ms_e / 1e3) / 1e9,
                 "transfer_kernel_ms_per_step": mst / args.steps},
