@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256) k_gat_src_pieces(
 }
 
 // long segment s: GQ / GTS = sum of its pieces in piece order
-__global__ void __launch_bounds__(256) k_gat_src_fixup(
+static __global__ void __launch_bounds__(256) k_gat_src_fixup(
     float* __restrict__ GQ, float* __restrict__ GTS, const float* __restrict__ part,
     const float* __restrict__ pgts, int d, const int64_t* __restrict__ seg,
     const int64_t* __restrict__ first, const int64_t* __restrict__ cnt, int64_t nf,
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256) k_wcolsum(float* __restrict__ partial,
 }
 
 // out[c] += sum_b partial[b][c], b ascending
-__global__ void k_colsum_reduce(float* __restrict__ out, const float* __restrict__ partial,
+static __global__ void k_colsum_reduce(float* __restrict__ out, const float* __restrict__ partial,
                                 int nb, int d) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= d) return;

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(256) k_acc_rows(T* __restrict__ dst, T* __rest
 
 // float4 rows (d % 4 == 0, 16-byte aligned rows): two rows per warp in
 // flight, so every lane has four independent 16-byte loads outstanding
-__global__ void __launch_bounds__(256) k_acc_rows4(float* __restrict__ dst, float* __restrict__ src,
+static __global__ void __launch_bounds__(256) k_acc_rows4(float* __restrict__ dst, float* __restrict__ src,
                                                    const int64_t* __restrict__ didx,
                                                    const int64_t* __restrict__ sidx,
                                                    const uint8_t* __restrict__ store_first,
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(256) k_seg_pieces_s(float* __restrict__ partia
 }
 
 // out[seg[f]] = ((partial[first] + partial[first+1]) + ...) in piece order.
-__global__ void __launch_bounds__(256) k_seg_fixup(float* __restrict__ out,
+static __global__ void __launch_bounds__(256) k_seg_fixup(float* __restrict__ out,
                                                    const float* __restrict__ partial, int d,
                                                    const int64_t* __restrict__ seg,
                                                    const int64_t* __restrict__ first,
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(256) k_gemm(const float* __restrict__ A, int64
 }
 
 // acc[e] = acc[e] + ((slab0[e] + slab1[e]) + ...) over `splits` slabs.
-__global__ void k_reduce_splits(float* __restrict__ acc, const float* __restrict__ slabs,
+static __global__ void k_reduce_splits(float* __restrict__ acc, const float* __restrict__ slabs,
                                 int64_t n, int splits) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -531,7 +531,7 @@ __global__ void k_reduce_splits(float* __restrict__ acc, const float* __restrict
 // ReLU' from the stored layer output: gz[r] = g[r] * (h[row(r)] > 0).  h =
 // max(z, 0) was produced from the same z by the forward, so (h > 0) == (z >
 // 0) bitwise: the backward needs no recompute of z when h is in HBM.
-__global__ void __launch_bounds__(256) k_relu_mask(float* __restrict__ gz, int64_t ldz,
+static __global__ void __launch_bounds__(256) k_relu_mask(float* __restrict__ gz, int64_t ldz,
                                                    const float* __restrict__ g,
                                                    const float* __restrict__ h,
                                                    const int64_t* __restrict__ hrows,
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(256) k_relu_mask(float* __restrict__ gz, int64
 
 // ---------------------------------------------------------------------------
 // out[r][c] = max(in[r][c], 0) for c < d (row strides ldo / ldi floats)
-__global__ void __launch_bounds__(256) k_relu_rows(float* __restrict__ out, int64_t ldo,
+static __global__ void __launch_bounds__(256) k_relu_rows(float* __restrict__ out, int64_t ldo,
                                                    const float* __restrict__ in, int64_t ldi,
                                                    int64_t rows, int d) {
   const int64_t n = rows * d;
@@ -586,7 +586,7 @@ __device__ __forceinline__ void loss_row(const float* __restrict__ z, float* __r
 // labels are loaded lane-parallel (one latency per 32 rows); rows of width
 // <= 64 are held in registers and the next row's values are requested
 // before the current one is reduced.
-__global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64_t rows, int d,
+static __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64_t rows, int d,
                                               const int64_t* __restrict__ labels,
                                               const uint8_t* __restrict__ mask,
                                               const int64_t* __restrict__ out_rows,
@@ -668,7 +668,7 @@ __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H, int64
 // system-wide, publish `seq`, then spin (acquire) until every rank's
 // counter reached it.  Traps after 60 s so a dead peer fails loudly
 // instead of hanging the GPU.
-__global__ void k_xbarrier(uint32_t* self, uint32_t* const* peers, int m, uint32_t seq) {
+static __global__ void k_xbarrier(uint32_t* self, uint32_t* const* peers, int m, uint32_t seq) {
   __threadfence_system();
   __syncwarp();
   if (threadIdx.x == 0)
@@ -691,7 +691,7 @@ __global__ void k_xbarrier(uint32_t* self, uint32_t* const* peers, int m, uint32
 }
 
 // K12: total = ((0 + g_0) + g_1) + ...; W = W - lr * total (separate roundings)
-__global__ void k_sgd(float* __restrict__ W, float* __restrict__ total_out,
+static __global__ void k_sgd(float* __restrict__ W, float* __restrict__ total_out,
                       const float* const* __restrict__ grads, int ndev, int64_t n, float lr) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {

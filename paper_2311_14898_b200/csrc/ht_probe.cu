@@ -1,0 +1,141 @@
+// Measurement and unit-test entry points: PCIe probe, GEMM unit entry.
+
+#include "ht_fleet_internal.h"
+
+using ht::fail;
+
+// ---------------------------------------------------------------------------
+// PCIe peaks of this box (roofline denominators of the host-transfer
+// kernels): copy-engine H2D, D2H, both directions at once, and the
+// zero-copy row kernels reading / writing pinned memory (1 KB rows).
+// ---------------------------------------------------------------------------
+extern "C" int ht_pcie_probe(int device, int64_t bytes, double* out /* [5] GB/s */) {
+  CU(cudaSetDevice(device));
+  void *h0 = nullptr, *h1 = nullptr, *d0 = nullptr, *d1 = nullptr;
+  CU(cudaHostAlloc(&h0, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  CU(cudaHostAlloc(&h1, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
+  CU(cudaMalloc(&d0, bytes));
+  CU(cudaMalloc(&d1, bytes));
+  memset(h0, 1, bytes);
+  memset(h1, 2, bytes);
+  cudaStream_t s0, s1;
+  CU(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+  cudaEvent_t a, b, c;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  CU(cudaEventCreate(&c));
+  void *hd0 = nullptr, *hd1 = nullptr;
+  CU(cudaHostGetDevicePointer(&hd0, h0, 0));
+  CU(cudaHostGetDevicePointer(&hd1, h1, 0));
+  const int64_t rb = 1024, rows = bytes / rb;
+  for (int t = 0; t < 5; ++t) {
+    double best = 0;
+    for (int rep = 0; rep < 4; ++rep) {
+      CU(cudaEventRecord(a, s0));
+      if (t == 0) CU(cudaMemcpyAsync(d0, h0, bytes, cudaMemcpyHostToDevice, s0));
+      if (t == 1) CU(cudaMemcpyAsync(h0, d0, bytes, cudaMemcpyDeviceToHost, s0));
+      if (t == 2) {
+        CU(cudaStreamWaitEvent(s1, a, 0));
+        CU(cudaMemcpyAsync(d0, h0, bytes, cudaMemcpyHostToDevice, s0));
+        CU(cudaMemcpyAsync(h1, d1, bytes, cudaMemcpyDeviceToHost, s1));
+        CU(cudaEventRecord(c, s1));
+        CU(cudaStreamWaitEvent(s0, c, 0));
+      }
+      if (t == 3) HT_TRY(launch_copy(s0, d0, hd0, nullptr, nullptr, rows, rb, rb, rb));
+      if (t == 4) HT_TRY(launch_copy(s0, hd1, d1, nullptr, nullptr, rows, rb, rb, rb));
+      CU(cudaEventRecord(b, s0));
+      CU(cudaEventSynchronize(b));
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, a, b));
+      const double moved = (t == 2 ? 2.0 : 1.0) * (double)bytes;
+      best = std::max(best, moved / (ms * 1e-3) / 1e9);
+    }
+    out[t] = best;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaEventDestroy(c);
+  cudaStreamDestroy(s0);
+  cudaStreamDestroy(s1);
+  cudaFree(d0);
+  cudaFree(d1);
+  cudaFreeHost(h0);
+  cudaFreeHost(h1);
+  return HT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM unit entry (tests): the exact launchers the layer drivers use, on
+// host arrays.  op 0: C = relu(A W); 1: C = [A W > 0] * G; 2: C = A W^T
+// (A is M x N, W is K x N); 3: C = A^T G (A is M x K, G is M x N).
+// precision: HT_PREC_FP32 (SIMT) or HT_PREC_TF32 (tcgen05; 3xTF32 for ops
+// 0/1, 1xTF32 for ops 2/3).
+// ---------------------------------------------------------------------------
+extern "C" int ht_gemm_test(int op, int precision, const float* A, const float* W, const float* G,
+                            float* C, int64_t M, int K, int N) {
+  CU(cudaSetDevice(0));
+  cudaStream_t s = nullptr;
+  CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  // row operands are staged with row strides padded to 4 floats (the TMA
+  // alignment rule the layer drivers follow for their own staging)
+  const int ka = op == 2 ? N : K, lda = pad4(ka), ldn = pad4(N);
+  const int64_t c_rows = op == 3 ? K : M, c_cols = op == 2 ? K : N;
+  Device d;
+  d.stream = s;
+  DBuf dA, dG, dC, ws;
+  HT_TRY(dA.ensure(std::max<int64_t>(1, M * lda) * 4));
+  HT_TRY(dG.ensure(std::max<int64_t>(1, M * ldn) * 4));
+  HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * c_cols) * 4));
+  HT_TRY(ws.ensure((int64_t)148 * K * N * 4 + 4));
+  CU(cudaMemcpy2D(dA.p, lda * 4, A, ka * 4, ka * 4, M, cudaMemcpyHostToDevice));
+  if (G) CU(cudaMemcpy2D(dG.p, ldn * 4, G, N * 4, N * 4, M, cudaMemcpyHostToDevice));
+  if (W) HT_TRY(upload_weights(d, W, K, N));
+  CU(cudaMemset(dC.p, 0, c_rows * c_cols * 4));
+  const bool tc = precision == HT_PREC_TF32;
+  int rc = HT_OK;
+  if (op == 0) {
+    rc = tc ? ht::tc::rows<ht::tc::TC_RELU>(s, true, dA.as<float>(), lda, M, K, d.Wt_hi.as<float>(),
+                                            d.Wt_lo.as<float>(), K, N, dC.as<float>(), N, nullptr, 0)
+            : gemm<false, false, ht::EPI_RELU>(s, dA.as<float>(), lda, d.W.as<float>(), N,
+                                               dC.as<float>(), N, nullptr, 0, M, N, K, 1, K);
+  } else if (op == 1) {
+    rc = tc ? ht::tc::rows<ht::tc::TC_MASK>(s, true, dA.as<float>(), lda, M, K, d.Wt_hi.as<float>(),
+                                            d.Wt_lo.as<float>(), K, N, dC.as<float>(), N,
+                                            dG.as<float>(), ldn)
+            : gemm<false, false, ht::EPI_MASK>(s, dA.as<float>(), lda, d.W.as<float>(), N,
+                                               dC.as<float>(), N, dG.as<float>(), ldn, M, N, K, 1, K);
+  } else if (op == 2) {
+    rc = tc ? ht::tc::rows<ht::tc::TC_STORE>(s, false, dA.as<float>(), lda, M, N, d.Wp_hi.as<float>(),
+                                             nullptr, pad4(N), K, dC.as<float>(), K, nullptr, 0)
+            : gemm<false, true, ht::EPI_STORE>(s, dA.as<float>(), lda, d.W.as<float>(), N,
+                                               dC.as<float>(), K, nullptr, 0, M, K, N, 1, N);
+  } else if (op == 3) {
+    int used = 1;
+    if (tc) {
+      rc = ht::tc::wgrad(s, dA.as<float>(), lda, K, dG.as<float>(), ldn, N, M, 148, ws.as<float>(),
+                         &used);
+    } else {
+      int splits = (int)std::min<int64_t>(64, std::max<int64_t>(1, M / 2048));
+      int64_t kps = ((M + splits - 1) / splits + 15) / 16 * 16;
+      used = (int)std::max<int64_t>(1, (M + kps - 1) / kps);
+      rc = gemm<true, false, ht::EPI_STORE>(s, dA.as<float>(), lda, dG.as<float>(), ldn,
+                                            ws.as<float>(), N, nullptr, 0, K, N, M, used, kps);
+    }
+    if (rc == HT_OK) {
+      ht::k_reduce_splits<<<64, 256, 0, s>>>(dC.as<float>(), ws.as<float>(), (int64_t)K * N, used);
+      CU(cudaGetLastError());
+    }
+  } else {
+    rc = fail(HT_EINVAL, "unknown gemm op %d", op);
+  }
+  if (rc == HT_OK) {
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpy(C, dC.p, c_rows * c_cols * 4, cudaMemcpyDeviceToHost));
+  }
+  for (DBuf* b : {&dA, &dG, &dC, &ws, &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo})
+    b->release();
+  cudaStreamDestroy(s);
+  return rc;
+}
+

@@ -535,7 +535,7 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // W (rows x cols, ld) -> hi = rna_tf32(W), lo = W - hi (same layout)
-__global__ void k_split_tf32(const float* __restrict__ W, float* __restrict__ hi,
+static __global__ void k_split_tf32(const float* __restrict__ W, float* __restrict__ hi,
                              float* __restrict__ lo, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -601,7 +601,7 @@ inline int sm_count() {
 }
 
 template <int BN, bool SPLIT, int EPI>
-int launch_gemm_t(cudaStream_t s, const float* A, int64_t lda, int64_t M, int K, const float* Bh,
+inline int launch_gemm_t(cudaStream_t s, const float* A, int64_t lda, int64_t M, int K, const float* Bh,
                   const float* Bl, int64_t ldb, int N, float* C, int64_t ldc, const float* G,
                   int64_t ldg) {
   using Cfg = GemmCfg<BN, SPLIT>;
@@ -624,7 +624,7 @@ int launch_gemm_t(cudaStream_t s, const float* A, int64_t lda, int64_t M, int K,
 // C = epi(A[M x K] . B^T) with B = Bh (+ Bl) given K-major (N rows x K,
 // row stride ldb); split = 3xTF32 (Bl required).
 template <int EPI>
-int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t M, int K,
+inline int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t M, int K,
          const float* Bh, const float* Bl, int64_t ldb, int N, float* C, int64_t ldc,
          const float* G, int64_t ldg) {
   if (M <= 0 || N <= 0) return HT_OK;
@@ -642,7 +642,7 @@ int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t M, int
 }
 
 template <int KT, int BN>
-int launch_wgrad_t(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
+inline int launch_wgrad_t(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
                    int N, int64_t M, int splits, int64_t rps, float* P) {
   using Cfg = WgradCfg<KT, BN>;
   CUtensorMap ta, tg;
@@ -659,7 +659,7 @@ int launch_wgrad_t(cudaStream_t s, const float* A, int64_t lda, int K, const flo
 }
 
 template <int KT>
-int wgrad_kt(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
+inline int wgrad_kt(cudaStream_t s, const float* A, int64_t lda, int K, const float* G, int64_t ldg,
              int N, int64_t M, int splits, int64_t rps, float* P) {
   if (N <= 32) return launch_wgrad_t<KT, 32>(s, A, lda, K, G, ldg, N, M, splits, rps, P);
   if (N <= 64) return launch_wgrad_t<KT, 64>(s, A, lda, K, G, ldg, N, M, splits, rps, P);

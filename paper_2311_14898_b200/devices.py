@@ -151,8 +151,15 @@ class _Checkpoints(dict):
     def _materialize(self, layer):
         fleet = self.pending.pop(layer, None)
         if fleet is not None:
-            N.call("ht_fleet_checkpoint_read", fleet._handle, int(layer),
-                   N.ptr(dict.__getitem__(self, layer)), kind=DeviceError)
+            dst = dict.__getitem__(self, layer)
+            # the fleet's mirrors must still hold this store's epoch: a fleet
+            # materializes every other store's pending checkpoints before it
+            # starts a new epoch (DeviceFleet.flush_checkpoints)
+            if fleet._ckpt_shapes.get((id(self), layer)) != tuple(dst.shape):
+                raise SimulationError(f"checkpoint of layer {layer} does not match the "
+                                      f"fleet's mirrors")
+            N.call("ht_fleet_checkpoint_read", fleet._handle, int(layer), N.ptr(dst),
+                   kind=DeviceError)
 
     def materialize_all(self):
         for layer in list(self.pending):
@@ -318,6 +325,7 @@ class DeviceFleet:
         # always writes them through (devices.py:391-404)
         self.checkpoints = checkpoints
         self._ckpt_hosts = weakref.WeakSet()
+        self._ckpt_shapes = {}  # (id(host.agg), layer) -> shape the mirrors hold
         # lean epochs (opt-in): no grad_h^0, and no host copies of h^L /
         # grad_h^L with the owner cache; the transfer
         # meters stay the reference's
@@ -430,14 +438,25 @@ class DeviceFleet:
         N.call("ht_fleet_capacity", self._handle, i, C.byref(c))
         return int(c.value)
 
+    def flush_checkpoints(self, keep=None) -> None:
+        """Copy every HBM-held checkpoint this fleet owes a host store into
+        that store's agg arrays (all stores but `keep`, whose epoch is about
+        to be replaced anyway).  Called before the fleet's mirrors change: at
+        the start of every epoch and at close (the reference keeps agg per
+        store, so a store's reads must never see another store's epoch)."""
+        for host in list(self._ckpt_hosts):
+            if host is keep:
+                continue
+            for layer, fl in list(host.agg.pending.items()):
+                if fl is self:
+                    host.agg._materialize(layer)
+            self._ckpt_hosts.discard(host)
+
     def close(self) -> None:
         """Release the fleet's device buffers now (otherwise at garbage
         collection)."""
         if self._handle is not None and self._finalizer.alive:
-            for host in list(self._ckpt_hosts):  # HBM-held checkpoints -> host first
-                for layer, fl in list(host.agg.pending.items()):
-                    if fl is self:
-                        host.agg._materialize(layer)
+            self.flush_checkpoints()  # HBM-held checkpoints -> host first
             self._finalizer()
 
     # -- meters ---------------------------------------------------------------

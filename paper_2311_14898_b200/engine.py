@@ -150,12 +150,30 @@ def _epoch_reset(host: HostStore, fleet: DeviceFleet, kind: str = "gcn",
 
 
 def _loss(h_, host: HostStore, dims: list, labels, mask) -> None:
+    """Validate labels/mask the way the reference's indexing does
+    (engine.py:308-315: ``h_last[mask]`` and ``p[arange, y]`` raise
+    IndexError; negative labels index from the end), then enqueue the
+    device loss."""
     mask_b = np.ascontiguousarray(np.asarray(mask, dtype=bool))
     labels_i = np.ascontiguousarray(np.asarray(labels, dtype=np.int64))
+    V = int(host.num_vertices)
+    L = len(dims) - 1
+    if mask_b.ndim != 1 or mask_b.shape[0] != V:
+        raise IndexError(f"boolean index did not match: mask has shape {mask_b.shape}, "
+                         f"expected ({V},)")
+    if labels_i.ndim != 1 or labels_i.shape[0] != V:
+        raise IndexError(f"labels have shape {labels_i.shape}, expected ({V},)")
     count = int(mask_b.sum())
     if count == 0:
         warnings.warn("training mask is empty; loss is 0", stacklevel=3)
-    L = len(dims) - 1
+    else:
+        y = labels_i[mask_b]
+        lo, hi = int(y.min()), int(y.max())
+        if lo < -dims[L] or hi >= dims[L]:
+            bad = lo if lo < -dims[L] else hi
+            raise IndexError(f"index {bad} is out of bounds for axis 1 with size {dims[L]}")
+        if lo < 0:  # numpy fancy indexing wraps negative labels
+            labels_i = np.where(labels_i < 0, labels_i + dims[L], labels_i)
     N.call("ht_loss", h_, dims[L], N.ptr(labels_i), N.ptr(mask_b.view(np.uint8)),
            int(host.num_vertices), count, N.ptr(host.grad_h[L]), None)  # value read after SGD
 
@@ -205,6 +223,7 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     A = _f32_params(model.attn, [(2 * dims[l + 1],) for l in range(L)]) if gat else None
     prec = PRECISIONS[fleet.precision]
     fleet.attach_partition(p)
+    fleet.flush_checkpoints(keep=host)  # other stores' HBM-held checkpoints, before reuse
     h_ = fleet._handle
     item = host.dtype.itemsize
     dims_c = (C.c_int * (L + 1))(*dims)
@@ -271,6 +290,7 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
             if ckpt_hbm:
                 host.agg.pending[l] = fleet
                 fleet._ckpt_hosts.add(host)
+                fleet._ckpt_shapes[(id(host.agg), l)] = tuple(agg.shape)
             for j in range(n):
                 fleet._meter_fwd(j, dims[l] * item)
                 for i in range(m):

@@ -246,3 +246,82 @@ def test_project_first_layers(monkeypatch):
     # which the two paths produce with different roundings
     np.testing.assert_array_equal(a[4][0], b[4][0])
     assert np.abs(a[4][1] - b[4][1]).max() <= 1e-4 * np.abs(b[4][1]).max()
+
+
+@pytest.mark.parametrize("wider", [False, True])
+def test_checkpoints_of_two_stores_on_one_fleet(wider):
+    """Store A trains, then store B (other features, possibly a wider model)
+    trains on the same fleet: A's HBM-held checkpoints are copied out before
+    B's epoch overwrites the mirrors, so A.agg reads A's own epoch (the
+    reference keeps agg per store, devices.py:391-404) - checked against A
+    run alone with the checkpoints written through."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=2000, avg_degree=8.0, seed=6), 16, 8)
+    p = H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 1, seed=6), 1)
+    plan = H.plan_for_partition(p)
+    dims_a = [16, 24, 8]
+    dims_b = [16, 40, 8] if wider else dims_a
+
+    def store(dims, X):
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+        host.set_features(X)
+        return host
+
+    # A alone, written-through checkpoints
+    ref = store(dims_a, ds.features)
+    f0 = H.DeviceFleet(plan, mode="full", dtype=np.float32, cache="on", checkpoints="host")
+    H.train_epoch(p, f0, H.init_model("gcn", dims_a, seed=3, dtype=np.float32), ref,
+                  ds.labels, ds.mask)
+    want = [np.array(ref.agg[l]) for l in range(2)]
+    f0.close()
+    # A then B on one fleet with HBM-held checkpoints
+    fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, cache="on")
+    host_a = store(dims_a, ds.features)
+    H.train_epoch(p, fleet, H.init_model("gcn", dims_a, seed=3, dtype=np.float32), host_a,
+                  ds.labels, ds.mask)
+    assert host_a.agg.pending
+    host_b = store(dims_b, np.asarray(ds.features) * 2.0 + 1.0)
+    H.train_epoch(p, fleet, H.init_model("gcn", dims_b, seed=4, dtype=np.float32), host_b,
+                  ds.labels, ds.mask)
+    assert not host_a.agg.pending
+    for l in range(2):
+        np.testing.assert_array_equal(np.array(host_a.agg[l]), want[l])
+    fleet.close()
+
+
+def test_loss_label_and_mask_validation():
+    """Labels / mask follow the reference's numpy indexing (engine.py:308-315):
+    wrong lengths and masked labels outside [-d, d) raise IndexError;
+    negative labels index from the end."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=1500, avg_degree=6.0, seed=2), 16, 4)
+    p = H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 1, seed=2), 1)
+    plan = H.plan_for_partition(p)
+    dims = [16, 12, 4]
+    V = ds.graph.num_vertices
+
+    def run(labels, mask):
+        host = H.HostStore(V, dims, dtype=np.float32)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32)
+        try:
+            return H.train_epoch(p, fleet, H.init_model("gcn", dims, seed=1, dtype=np.float32),
+                                 host, labels, mask).loss
+        finally:
+            fleet.close()
+
+    y = np.asarray(ds.labels).copy()
+    mask = np.asarray(ds.mask)
+    with pytest.raises(IndexError):
+        run(y[:-1], mask)
+    with pytest.raises(IndexError):
+        run(y, mask[:-1])
+    bad = y.copy()
+    bad[np.flatnonzero(mask)[0]] = dims[-1]
+    with pytest.raises(IndexError):
+        run(bad, mask)
+    bad[np.flatnonzero(mask)[0]] = -dims[-1] - 1
+    with pytest.raises(IndexError):
+        run(bad, mask)
+    ok = y.copy()
+    ok[~mask] = 99  # unmasked labels are never read
+    neg = y - dims[-1]  # every label as its negative alias
+    assert run(ok, mask) == run(y, mask) == run(neg, mask)

@@ -10,13 +10,21 @@ do not need a full CPU epoch:
 * the last layer's dW = agg^{L-1}^T (grad_h^L * 1[h^L > 0]) over all 2.4M
   rows against float64 (1xTF32: the north star's 1e-3);
 * W_new = W - lr * dW bitwise (src/engine.py:328-344);
-* the HBM store and the pinned host store give bitwise the same epoch.
+* the HBM store and the pinned host store give bitwise the same epoch;
+* layer by layer against the fp64 oracle fed with the GPU's own layer
+  inputs h^l and output gradients grad_h^{l+1} (so each layer is checked
+  alone, at the north star's 1e-3): every layer's h^{l+1} and dW, grad_h^l
+  on sampled rows plus the 20 highest out-degree sources (the hub pieces of
+  the transposed aggregation), the loss and grad_h^L - for the GCN (whose
+  narrow last layer runs project-first, z = A.(h.W), against the oracle's
+  (A.h).W) and for the bench's GAT (256-128-128-64, dW, da, grad_h).
 """
 
 import numpy as np
 import pytest
 
 import paper_2311_14898_b200 as H
+from oracle import hongtu_oracle as O
 
 pytestmark = pytest.mark.gpu
 
@@ -97,3 +105,79 @@ def test_fullsize_host_store_equals_hbm_store(full):
     for a, b in zip(hd, host_h.h[1:]):
         np.testing.assert_array_equal(a, b)
     f_h.close()
+
+
+def _graph_dict(g):
+    return {"num_vertices": g.num_vertices, "csc_offsets": g.csc_offsets,
+            "csc_sources": g.csc_sources, "edge_weights": g.edge_weights}
+
+
+def _check_rows(l, got, ref, rows, hubs, what):
+    err = O.rel_err(got[rows], ref[rows])
+    assert err < 1e-3, (what, l, "sampled rows", err)
+    err = O.rel_err(got[hubs], ref[hubs])
+    assert err < 1e-3, (what, l, "hub rows", err)
+
+
+def _loss_check(res, h_last, g_last, labels, mask):
+    loss_ref, grad_ref = O.masked_xent_fp64(h_last, labels, mask)
+    assert abs(res.loss - loss_ref) <= 1e-5 * abs(loss_ref), (res.loss, loss_ref)
+    assert O.rel_err(g_last, grad_ref) < 1e-5
+
+
+def test_fullsize_gcn_layerwise_vs_fp64_oracle(full):
+    ds, p, plan = full
+    g = ds.graph
+    res, model, w0, host, fleet = _epoch(full, "device")
+    L = len(DIMS) - 1
+    h = [np.asarray(x) for x in host.h]
+    gh = [np.asarray(x) for x in host.grad_h]
+    fleet.close()
+    _loss_check(res, h[L], gh[L], ds.labels, ds.mask)
+    hubs = np.argsort(np.diff(g.csr_offsets), kind="stable")[-20:]
+    assert np.diff(g.csr_offsets)[hubs].min() > 1024  # they run through the pieces path
+    rows = np.random.default_rng(11).choice(V, 2000, replace=False)
+    A = O.adjacency_fp64(_graph_dict(g))
+    for l in reversed(range(L)):
+        r = O.gcn_layer_fp64(A, h[l], w0[l], gh[l + 1])
+        err = O.rel_err(h[l + 1], r["h_out"])
+        assert err < 1e-3, ("h", l + 1, err)
+        err = O.rel_err(res.grads[l], r["grad_W"])
+        assert err < 1e-3, ("dW", l, err)
+        _check_rows(l, gh[l], r["grad_h"], rows, hubs, "grad_h")
+        del r
+
+
+GAT_DIMS = [256, 128, 128, 64]  # bench.py's GAT line (config 5's widths)
+
+
+def test_fullsize_gat_layerwise_vs_fp64_oracle(full):
+    ds, p, plan = full
+    g = ds.graph
+    X = np.random.default_rng(SEED).standard_normal((V, GAT_DIMS[0]), dtype=np.float32)
+    y = (np.asarray(ds.labels) % GAT_DIMS[-1]).astype(np.int64)
+    model = H.init_model("gat", GAT_DIMS, seed=SEED, lr=0.1, dtype=np.float32)
+    w0 = [w.copy() for w in model.weights]
+    a0 = [a.copy() for a in model.attn]
+    host = H.HostStore(V, GAT_DIMS, dtype=np.float32, placement="device")
+    host.set_features(X)
+    fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision="tf32")
+    res = H.train_epoch(p, fleet, model, host, y, ds.mask)
+    L = len(GAT_DIMS) - 1
+    h = [np.asarray(x) for x in host.h]
+    gh = [np.asarray(x) for x in host.grad_h]
+    fleet.close()
+    _loss_check(res, h[L], gh[L], y, ds.mask)
+    hubs = np.argsort(np.diff(g.csr_offsets), kind="stable")[-20:]
+    rows = np.random.default_rng(12).choice(V, 2000, replace=False)
+    gd = _graph_dict(g)
+    for l in reversed(range(L)):
+        r = O.gat_layer_fp64(gd, h[l], w0[l], a0[l], slope=model.leaky_slope, grad_out=gh[l + 1])
+        err = O.rel_err(h[l + 1], r["h_out"])
+        assert err < 1e-3, ("h", l + 1, err)
+        err = O.rel_err(res.grads[l], r["grad_W"])
+        assert err < 1e-3, ("dW", l, err)
+        err = O.rel_err(res.attn_grads[l], r["grad_a"])
+        assert err < 1e-3, ("da", l, err)
+        _check_rows(l, gh[l], r["grad_h"], rows, hubs, "grad_h")
+        del r
