@@ -167,7 +167,8 @@ def dedup_report():
             "volumes": {"v_ori": v.v_ori, "v_p2p": v.v_p2p, "v_ru": v.v_ru}}
 
 
-def virtual_fleet_epochs(ds, dims, m=8, steps=2, warmup=1, precision="tf32", seed=0, device=0):
+def virtual_fleet_epochs(ds, dims, m=8, steps=2, warmup=1, precision="tf32", seed=0, device=0,
+                         profile=False):
     """The reference-faithful HongTu path at the bench's scale: m virtual
     devices (the 8-GPU partition layout) on this one GPU, the deduplicated
     plan, host-resident vertex data and no HBM owner cache - every batch's
@@ -179,7 +180,8 @@ def virtual_fleet_epochs(ds, dims, m=8, steps=2, warmup=1, precision="tf32", see
     g = ds.graph
     p = H.split_chunks(g, H.partition_vertices(g, m, seed=seed), 1)
     plan = H.plan_for_partition(p, device=device)
-    r = run_epochs(p, plan, ds, dims, "host", steps, warmup, precision, False, seed, cache="off")
+    r = run_epochs(p, plan, ds, dims, "host", steps, warmup, precision, False, seed, cache="off",
+                   profile=profile)
     tot = r["report"]["totals"]
     host = tot["h2d_bytes"] + tot["d2h_bytes"] + tot["dest_bytes"] + tot["chkpt_bytes"]
     L = len(dims) - 1
@@ -191,6 +193,33 @@ def virtual_fleet_epochs(ds, dims, m=8, steps=2, warmup=1, precision="tf32", see
             "planned_host_gb_per_step": pred / 1e9,
             "metered_peer_gb_per_step": tot["d2d_bytes"] / steps / 1e9,
             "loss": r["losses"][-1]}
+
+
+def profile_epoch(args, cfg, ds, p, plan):
+    """bench.py --profile-epoch MODE: W warm-up epochs, then K epochs inside a
+    profiler range, for ncu --replay-mode app-range --profile-from-start off
+    (pcie__read_bytes / pcie__write_bytes / dram bytes of exactly those
+    epochs, copy engines included).  Prints the plan's bytes for the same
+    epochs; never a bench line (a number taken under a profiler is not one)."""
+    dims = cfg["dims"]
+    mode = args.profile_epoch
+    if mode == "virt":
+        r = virtual_fleet_epochs(ds, dims, steps=args.steps, warmup=args.warmup,
+                                 precision=args.precision, seed=cfg["seed"], profile=True)
+        out = {"mode": mode, "planned_host_gb_per_step": r["planned_host_gb_per_step"],
+               "metered_host_gb_per_step": r["metered_host_gb_per_step"],
+               "metered_peer_gb_per_step": r["metered_peer_gb_per_step"]}
+    else:
+        placement = "device" if mode == "value" else "host"
+        r = run_epochs(p, plan, ds, dims, placement, args.steps, args.warmup, args.precision,
+                       False, cfg["seed"], profile=True)
+        h2d, d2h = host_bytes_per_epoch(plan, dims, cached=r["cache"], ckpt_hbm=r["ckpt_hbm"])
+        out = {"mode": mode, "hbm_owner_cache": bool(r["cache"]), "ckpt_hbm": bool(r["ckpt_hbm"])}
+        if placement == "host":
+            out.update({"planned_h2d_gb_per_step": h2d / 1e9, "planned_d2h_gb_per_step": d2h / 1e9})
+    out.update({"config_id": args.config, "steps": args.steps, "warmup": args.warmup,
+                "ms_total_under_profiler": r.get("ms_total")})
+    print(json.dumps(out), flush=True)
 
 
 def dedup_at_scale(ds, dims, m=8, n=1, seed=0, device=None):
@@ -408,7 +437,7 @@ def reference_cpu_baseline(graph, labels, mask, dims, steps=3, warmup=1):
 # ---------------------------------------------------------------------------
 def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed, rank=None,
                kind="gcn", features=None, labels=None, lean=False, checkpoints="auto",
-               cache="auto"):
+               cache="auto", profile=False):
     import paper_2311_14898_b200 as H
     from paper_2311_14898_b200 import _native as N
     dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count()) if rank is not None else 0
@@ -424,13 +453,14 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
                           checkpoints=checkpoints, cache=cache)
     try:
         return _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind,
-                             labels)
+                             labels, profile)
     finally:
         host.agg.pending.clear()  # nobody reads these checkpoints: nothing to materialize
         fleet.close()  # device memory back before the next measurement (also on failure)
 
 
-def _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind, labels):
+def _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind, labels,
+                  profile=False):
     model = H.init_model(kind, dims, seed=seed, lr=0.1, dtype=np.float32)
     losses = []
     for _ in range(warmup):
@@ -440,11 +470,15 @@ def _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, k
         for k, v in d.counter_dict().items():
             setattr(d, k, 0)
     l0 = N.lib().ht_launches()
+    if profile:  # counters of exactly the timed epochs (ncu app-range replay)
+        N.call("ht_profile_range", 1)
     N.call("ht_fleet_mark", fleet._handle, 0)
     t0 = time.perf_counter()
     for _ in range(steps):
         losses.append(H.train_epoch(p, fleet, model, host, labels, ds.mask).loss)
     N.call("ht_fleet_mark", fleet._handle, 1)
+    if profile:
+        N.call("ht_profile_range", 0)
     ms = C.c_double(0)
     N.call("ht_fleet_elapsed", fleet._handle, C.byref(ms))
     wall = time.perf_counter() - t0
@@ -555,6 +589,8 @@ def main():
     ap.add_argument("--no-gat", action="store_true", help="skip the GAT (config 5 model) line")
     ap.add_argument("--kind", default="gcn", choices=["gcn", "gat"],
                     help="profiling: model of the --only-value run")
+    ap.add_argument("--profile-epoch", default=None, choices=["value", "e2e", "virt"],
+                    help="profiling: K epochs inside a cudaProfilerStart/Stop range (ncu app-range)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -595,6 +631,9 @@ def main():
             return hd.allreduce_max(ms)
         return ms
 
+    if args.profile_epoch:  # profiling aid: counters of whole epochs
+        profile_epoch(args, cfg, ds, p, plan)
+        return
     if args.only_value and args.kind == "gat":  # profiling aid
         r = gat_measure(p, plan, ds, args.steps, args.warmup, args.precision, cfg["seed"], rk,
                         slowest)

@@ -211,6 +211,19 @@ int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t n);
  * the owner cache, the host copies of h^L and grad_h^L.  Weights, attention
  * vectors, loss and every other host array are unchanged. */
 int ht_fleet_set_lean(ht_fleet* f, int lean);
+/* Recompute-cache hybrid under an HBM budget (the paper's cache-vs-
+ * recompute policy; the reference keeps every checkpoint,
+ * devices.py:391-425): `bytes` caps what the owner cache may allocate per
+ * device (0 = free HBM less 4 GB).  At each ht_epoch_begin the h^l and
+ * grad_h^l mirrors must fit; agg^l mirrors are kept from the narrowest
+ * layer up, and the layers that do not fit share one scratch buffer - their
+ * agg^l is re-aggregated in the backward from the h^l mirror (the forward's
+ * gather: bitwise the same rows, so epochs equal the all-cached ones).
+ * Recompute needs one device with the identity mirror; otherwise the cache
+ * is all or nothing.  ht_fleet_recompute_state: bit l set = agg^l recomputed
+ * in the current epoch. */
+int ht_fleet_set_budget(ht_fleet* f, int64_t bytes);
+int ht_fleet_recompute_state(ht_fleet* f, int64_t* mask);
 /* Checkpoint tier of the recompute-cache hybrid (replaces the host-side
  * cache of store_checkpoint / load_recomp_chkpt, devices.py:391-425): with
  * hbm = 1 and the owner cache active, a GCN forward keeps the agg
@@ -314,6 +327,18 @@ int ht_pcie_probe(int device, int64_t bytes, double* out);
  * precision HT_PREC_FP32 (SIMT) or HT_PREC_TF32 (tcgen05). */
 int ht_gemm_test(int op, int precision, const float* A, const float* W, const float* G,
                  float* C, int64_t M, int K, int N);
+
+/* GEMM rate (measurement, no reference counterpart): `iters` back-to-back
+ * launches of the layer drivers' GEMM launcher `op` (0, 2, 3 as above) on
+ * device-resident M-row operands.  out[0] ms per launch, out[1] TFLOP/s of
+ * the useful 2*M*K*N flops, out[2] GB/s of the operand rows read once. */
+int ht_gemm_rate(int op, int precision, int64_t M, int K, int N, int iters, double* out);
+
+/* Profiler range (measurement): start != 0 -> cudaProfilerStart, else
+ * cudaProfilerStop.  bench.py --profile-epoch brackets one epoch with it so
+ * `ncu --replay-mode app-range --profile-from-start off` reads the PCIe /
+ * NVLink / DRAM counters of exactly that epoch (kernels and copy engines). */
+int ht_profile_range(int start);
 
 #ifdef __cplusplus
 }

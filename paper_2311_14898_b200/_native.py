@@ -84,6 +84,8 @@ _SIGS = {
     "ht_fleet_set_cache": (i32, [vp, i32]),
     "ht_fleet_set_host_rows": (i32, [vp, vp, i64]),
     "ht_fleet_set_lean": (i32, [vp, i32]),
+    "ht_fleet_set_budget": (i32, [vp, i64]),
+    "ht_fleet_recompute_state": (i32, [vp, C.POINTER(i64)]),
     "ht_fleet_set_checkpoints": (i32, [vp, i32]),
     "ht_fleet_checkpoint_read": (i32, [vp, i32, vp]),
     "ht_fleet_alias_store": (i32, [vp, i32, vp, vp, vp]),
@@ -99,6 +101,8 @@ _SIGS = {
     "ht_launches": (i64, []),
     "ht_gemm_test": (i32, [i32, i32, vp, vp, vp, vp, i64, i32, i32]),
     "ht_pcie_probe": (i32, [i32, i64, vp]),
+    "ht_gemm_rate": (i32, [i32, i32, i64, i32, i32, i32, vp]),
+    "ht_profile_range": (i32, [i32]),
 }
 
 _lib = None

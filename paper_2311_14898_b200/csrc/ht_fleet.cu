@@ -190,17 +190,16 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
   timers_collect(f);
   for (auto& d : f->dev) {
     cudaSetDevice(d.ordinal);
-    for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.gemm_ws,
-                    &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo, &d.hL,
+    for (auto* b : {&d.value, &d.grad, &d.sa, &d.sb, &d.sc, &d.sd, &d.se, &d.partial, &d.work,
+                    &d.gemm_ws, &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo, &d.hL,
                     &d.labels, &d.mask, &d.loss_part, &d.gWall, &d.flags})
       b->release();
     for (auto& c : d.chunks) {
       for (auto* b : {&c.nbr_slot, &c.dest_rows, &c.csc_off, &c.csc_slot, &c.csc_w, &c.csr_off,
-                      &c.csr_dst, &c.csr_w, &c.fw_lo, &c.fw_hi, &c.fw_seg, &c.fw_first, &c.fw_cnt,
-                      &c.bw_lo, &c.bw_hi, &c.bw_seg, &c.bw_first, &c.bw_cnt, &c.bx_off, &c.bx_lo,
-                      &c.bx_hi, &c.bx_seg, &c.bx_first, &c.bx_cnt, &c.csc_loc,
-                      &c.csr_perm, &c.h2d_m, &c.flush_m})
+                      &c.csr_dst, &c.csr_w, &c.bx_off, &c.csc_loc, &c.csr_perm, &c.h2d_m,
+                      &c.flush_m})
         b->release();
+      for (Pieces* pc : {&c.fw, &c.bw, &c.bx}) pc->release();
       for (CopyList* cl : {&c.h2d, &c.flush, &c.base_bwd})
         cl->src.release(), cl->dst.release(), cl->flag.release();
       for (auto& cl : c.d2d) cl.src.release(), cl.dst.release();
@@ -389,18 +388,8 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         HT_TRY(upload(c.csr_dst, dst32, s));
         HT_TRY(upload(c.csr_w, wcsr, s));
         c.ne = h.ne;
-        std::vector<int64_t> lo, hi, sg, fi, cn;
-        make_pieces(h.csc_off, lo, hi, sg, fi, cn);
-        c.fw_np = (int64_t)lo.size();
-        c.fw_nf = (int64_t)sg.size();
-        HT_TRY(upload(c.fw_lo, lo, s)); HT_TRY(upload(c.fw_hi, hi, s));
-        HT_TRY(upload(c.fw_seg, sg, s)); HT_TRY(upload(c.fw_first, fi, s)); HT_TRY(upload(c.fw_cnt, cn, s));
-        lo.clear(); hi.clear(); sg.clear(); fi.clear(); cn.clear();
-        make_pieces(h.csr_off, lo, hi, sg, fi, cn);
-        c.bw_np = (int64_t)lo.size();
-        c.bw_nf = (int64_t)sg.size();
-        HT_TRY(upload(c.bw_lo, lo, s)); HT_TRY(upload(c.bw_hi, hi, s));
-        HT_TRY(upload(c.bw_seg, sg, s)); HT_TRY(upload(c.bw_first, fi, s)); HT_TRY(upload(c.bw_cnt, cn, s));
+        HT_TRY(make_pieces(h.csc_off, c.fw, s));
+        HT_TRY(make_pieces(h.csr_off, c.bw, s));
         c.bx_rows = -1;
         if (m == 1 && n == 1 && f->nrows < ((int64_t)1 << 31)) {
           std::vector<int64_t> offx(f->nrows + 1);
@@ -409,13 +398,8 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
             while (q < h.nn && h.nbr[q] < g) ++q;
             offx[g] = h.csr_off[q];
           }
-          lo.clear(); hi.clear(); sg.clear(); fi.clear(); cn.clear();
-          make_pieces(offx, lo, hi, sg, fi, cn);
-          c.bx_np = (int64_t)lo.size();
-          c.bx_nf = (int64_t)sg.size();
+          HT_TRY(make_pieces(offx, c.bx, s));
           HT_TRY(upload(c.bx_off, offx, s));
-          HT_TRY(upload(c.bx_lo, lo, s)); HT_TRY(upload(c.bx_hi, hi, s));
-          HT_TRY(upload(c.bx_seg, sg, s)); HT_TRY(upload(c.bx_first, fi, s)); HT_TRY(upload(c.bx_cnt, cn, s));
           c.bx_rows = f->nrows;
         }
       }
@@ -678,6 +662,19 @@ extern "C" int ht_fleet_alias_store(ht_fleet* f, int L, void* const* h, void* co
   return HT_OK;
 }
 
+extern "C" int ht_fleet_set_budget(ht_fleet* f, int64_t bytes) {
+  if (bytes < 0) return fail(HT_EINVAL, "HBM budget must be >= 0 bytes");
+  f->hbm_budget = bytes;
+  return HT_OK;
+}
+
+extern "C" int ht_fleet_recompute_state(ht_fleet* f, int64_t* mask) {
+  *mask = 0;
+  for (size_t l = 0; l < f->agg_recompute.size() && l < 63; ++l)
+    if (f->agg_recompute[l]) *mask |= (int64_t)1 << l;
+  return HT_OK;
+}
+
 extern "C" int ht_fleet_set_lean(ht_fleet* f, int lean) {
   f->lean = lean != 0;
   return HT_OK;
@@ -694,18 +691,19 @@ extern "C" int ht_fleet_checkpoint_read(ht_fleet* f, int layer, void* host_agg) 
   HT_TRY(dev_ptr(host_agg, &hp));
   const int64_t rb = (int64_t)f->dims[layer] * 4;
   const bool deferred = layer < (int)f->agg_deferred.size() && f->agg_deferred[layer];
+  // recomputed layers share one scratch buffer: always re-aggregate on read
+  const bool recomputed = layer < (int)f->agg_recompute.size() && f->agg_recompute[layer];
   for (auto& d : f->dev) {
     if (!d.local) continue;
     if (!d.cache || (int)d.ma.size() <= layer || !d.ma[layer].p)
       return fail(HT_ESTATE, "checkpoints are not held in HBM mirrors");
     HT_TRY(set_dev(d));
-    if (deferred) {  // project-first layer: agg^l = A.h^l now, the forward's gather
-      const DevChunk& c = d.chunks[0];
+    if (deferred || recomputed) {  // agg^l = A.h^l now, the forward's gather
       const int din = f->dims[layer];
-      HT_TRY(launch_seg(d.stream, d.ma[layer].as<float>(), d.mh[layer].as<float>(), din, din,
-                        c.csc_off.as<int64_t>(), c.csc_gid.as<int32_t>(), c.csc_w.as<float>(), c.nv,
-                        c.fw_np, c.fw_lo, c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt,
-                        d.partial.as<float>()));
+      for (auto& c : d.chunks)
+        HT_TRY(launch_seg(d.stream, d, d.ma[layer].as<float>() + c.dest_m0 * din,
+                          d.mh[layer].as<float>(), din, din, c.csc_off.as<int64_t>(),
+                          c.csc_gid.as<int32_t>(), c.csc_w.as<float>(), c.nv, c.fw));
     }
     HT_TRY(cache_writeback(f, d, hp, d.ma[layer].as<float>(), rb));
   }

@@ -121,6 +121,19 @@ struct HostSets {
   std::vector<double> w;
 };
 
+// Pieces of the long (> kSplit edges) segments of one offsets array: piece
+// q covers edges [lo[q], hi[q]) of segment seg[pf[q]]; fixup f sums pieces
+// first[f] .. first[f] + cnt[f] - 1 in piece order into segment seg[f].
+struct Pieces {
+  int64_t np = 0, nf = 0;
+  DBuf lo, hi, seg, first, cnt;  // int64
+  DBuf pf;                       // int32 [np]: fixup of each piece
+  void release() {
+    for (DBuf* b : {&lo, &hi, &seg, &first, &cnt, &pf}) b->release();
+    np = nf = 0;
+  }
+};
+
 struct DevChunk {
   int64_t nv = 0, nn = 0, ne = 0, nlive = 0;
   DBuf nbr_slot;   // int64 [nn]
@@ -135,14 +148,13 @@ struct DevChunk {
   // graph
   DBuf csc_off, csc_slot, csc_w;     // int64 [nv+1], int32 [ne], float [ne]
   DBuf csr_off, csr_dst, csr_w;      // int64 [nn+1], int32 [ne], float [ne]
-  int64_t fw_np = 0, fw_nf = 0, bw_np = 0, bw_nf = 0;
-  DBuf fw_lo, fw_hi, fw_seg, fw_first, fw_cnt;  // long-segment pieces (forward)
-  DBuf bw_lo, bw_hi, bw_seg, bw_first, bw_cnt;  // (backward)
+  Pieces fw, bw;                     // long-segment pieces (forward CSC, backward CSR)
   // one device, one batch: the CSR offsets expanded to every host row
   // (empty segments for rows without out-edges) so the transposed
   // aggregation writes the dense grad mirror directly; pieces re-indexed
-  DBuf bx_off, bx_lo, bx_hi, bx_seg, bx_first, bx_cnt;
-  int64_t bx_np = 0, bx_nf = 0, bx_rows = -1;
+  DBuf bx_off;
+  Pieces bx;
+  int64_t bx_rows = -1;
   // GAT: chunk-local CSC sources (rows of q) and the CSC edge id of each
   // CSR edge; uploaded by the first GAT epoch
   DBuf csc_loc, csr_perm;            // int32 [ne], int32 [ne]
@@ -179,6 +191,7 @@ struct Device {
   int64_t cap = 0;
   DBuf value, grad;                    // cap x dim slot buffers
   DBuf sa, sb, sc, sd, se, partial;    // staging
+  DBuf work;                           // work-list counter + fixup tickets of launch_seg
   DBuf tT;                             // A^T gz in d_out space (narrow-side backward)
   DBuf pf_p, pf_z;                     // project-first layers: h.W and A.(h.W), pad4(d_out) wide
   DBuf gemm_ws;
@@ -238,6 +251,10 @@ struct Device {
   DBuf mrows_d;                        // same, on the device
   CopyList own;                        // runs of (host row, mirror position)
   std::vector<DBuf> mh, ma, mg;
+  // recompute-cache hybrid: one scratch buffer serves every layer whose agg
+  // mirror did not fit the HBM budget (ma[l] aliases it; the backward
+  // re-aggregates agg^l from the h^l mirror)
+  DBuf agg_scr;
   cudaEvent_t e_up = nullptr, e_mg = nullptr;
 };
 
@@ -284,6 +301,11 @@ struct ht_fleet {
   // HBM checkpoints): agg^l was never formed; ht_fleet_checkpoint_read
   // aggregates it on demand
   std::vector<char> agg_deferred;
+  // recompute-cache hybrid (the paper's policy): HBM budget
+  // of the owner cache in bytes (0: free HBM less 4 GB of headroom) and the
+  // layers whose agg^l is recomputed in the backward instead of kept
+  int64_t hbm_budget = 0;
+  std::vector<char> agg_recompute;
   // HBM store (placement "device") on a single device: its arrays serve as
   // the owner-cache mirrors directly (h[0..L], agg[0..L-1], grad[0..L])
   std::vector<void*> alias_h, alias_a, alias_g;
@@ -390,15 +412,17 @@ void timer_end(ht_fleet* f, Device& d, TimerRec& r, int which, double bytes,
 
 void timers_collect(ht_fleet* f);
 
-int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, const int64_t* off,
-               const int32_t* idx, const float* w, int64_t nseg, int64_t np, const DBuf& lo,
-               const DBuf& hi, int64_t nf, const DBuf& seg, const DBuf& first, const DBuf& cnt,
-               float* partial);
+// Segment gather-sum over a chunk's CSC (forward) or CSR (backward) view:
+// out[sg] = sum over edges e of segment sg of w[e] * X[idx[e]], sequential in
+// e, long segments through their pieces (`pc`); d's partial / work buffers.
+int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
+               const int64_t* off, const int32_t* idx, const float* w, int64_t nseg,
+               const Pieces& pc);
 
 int upload_weights(Device& d, const float* W, int d_in, int d_out);
 
-void make_pieces(const std::vector<int64_t>& off, std::vector<int64_t>& lo, std::vector<int64_t>& hi,
-                 std::vector<int64_t>& seg, std::vector<int64_t>& first, std::vector<int64_t>& cnt);
+// pieces of the long segments of an offsets array, uploaded on stream s
+int make_pieces(const std::vector<int64_t>& off, Pieces& pc, cudaStream_t s);
 
 int lookup_slots(const HostSets& hs, const std::vector<int64_t>& rows, std::vector<int64_t>& out,
                  int i, int j);

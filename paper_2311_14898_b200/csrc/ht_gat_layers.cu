@@ -77,8 +77,9 @@ int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const flo
                    const float* a_dst = nullptr) {
   // expanded: segments over every host row (gat_direct), outputs in row order
   const int64_t nseg = expanded ? c.bx_rows : c.nn;
-  const int64_t np = expanded ? c.bx_np : c.bw_np, nf = expanded ? c.bx_nf : c.bw_nf;
-  const DBuf &lo = expanded ? c.bx_lo : c.bw_lo, &hi = expanded ? c.bx_hi : c.bw_hi;
+  const Pieces& pc = expanded ? c.bx : c.bw;
+  const int64_t np = pc.np, nf = pc.nf;
+  const DBuf &lo = pc.lo, &hi = pc.hi;
   if (nseg <= 0) return HT_OK;
   const int g = grid_for(nseg);
   const int64_t* off = expanded ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>();
@@ -100,8 +101,7 @@ int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const flo
 #undef GATS
   CU(cudaGetLastError());
   if (nf) {
-    const DBuf &sg = expanded ? c.bx_seg : c.bw_seg, &fi = expanded ? c.bx_first : c.bw_first,
-               &cn = expanded ? c.bx_cnt : c.bw_cnt;
+    const DBuf &sg = pc.seg, &fi = pc.first, &cn = pc.cnt;
     ht::gat::k_gat_src_fixup<<<grid_for(nf), kThreads, 0, s>>>(
         GQ, GTS, part, pgts, d, sg.as<int64_t>(), fi.as<int64_t>(), cn.as<int64_t>(), nf, sgt_add,
         a_dst);
@@ -350,7 +350,7 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
     HT_TRY(d.g_ghd.ensure(mv * dmax * 4));
     HT_TRY(d.g_cpart.ensure((int64_t)kColBlocks * dmax * 4));
     int64_t np = 1;
-    for (int j = 0; j < f->n; ++j) np = std::max(np, d.chunks[j].bw_np);
+    for (int j = 0; j < f->n; ++j) np = std::max({np, d.chunks[j].bw.np, d.chunks[j].bx.np});
     HT_TRY(d.g_pgts.ensure(np * 4));
     if (!d.cache)  // with the owner cache these rows are read in place
       for (int s = 0; s < 2; ++s) {

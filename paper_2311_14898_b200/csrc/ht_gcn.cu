@@ -121,10 +121,9 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
         timer_end(f, d, tg, 2, 2.0 * rows * d_in * d_out, d.stream);
         TimerRec tr;
         timer_begin(f, d, tr, d.stream);
-        HT_TRY(launch_seg(d.stream, d.pf_z.as<float>(), d.pf_p.as<float>(), ldp, ldp,
+        HT_TRY(launch_seg(d.stream, d, d.pf_z.as<float>(), d.pf_p.as<float>(), ldp, ldp,
                           c.csc_off.as<int64_t>(), c.csc_gid.as<int32_t>(), c.csc_w.as<float>(),
-                          c.nv, c.fw_np, c.fw_lo, c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt,
-                          d.partial.as<float>()));
+                          c.nv, c.fw));
         timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * ldp) + (double)c.nv * (4.0 * ldp + 4.0),
                   d.stream);
         HT_TRY(ev_rec(d.e_agg, d.stream));
@@ -149,14 +148,19 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       }
       // cache: the aggregation and h rows land in their mirrors directly
       float* agg = d.cache ? d.ma[layer].as<float>() + c.dest_m0 * d_in : d.fa[s].as<float>();
+      if (d.cache && f->agg_recompute[layer] && !f->ckpt_hbm) {
+        // the recompute scratch is shared by layers: wait for the
+        // write-through of the previous layer's checkpoint rows out of it
+        HT_TRY(ev_wait(d.stream, d.e_out[0]));
+        HT_TRY(ev_wait(d.stream, d.e_out[1]));
+      }
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
       const float* Xd = hbm_inputs(f, d, layer, hin);
-      HT_TRY(launch_seg(d.stream, agg, Xd ? Xd : d.value.as<float>(), d_in, d_in,
+      HT_TRY(launch_seg(d.stream, d, agg, Xd ? Xd : d.value.as<float>(), d_in, d_in,
                         c.csc_off.as<int64_t>(),
                         Xd ? c.csc_gid.as<int32_t>() : c.csc_slot.as<int32_t>(), c.csc_w.as<float>(),
-                        c.nv, c.fw_np, c.fw_lo,
-                        c.fw_hi, c.fw_nf, c.fw_seg, c.fw_first, c.fw_cnt, d.partial.as<float>()));
+                        c.nv, c.fw));
       timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nv * (4.0 * d_in + 4.0),
                 d.stream);
       HT_TRY(ev_rec(d.e_agg, d.stream));
@@ -166,8 +170,9 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
       LayerW& w = d.lw[layer];
       const int64_t* rows = c.dest_rows.as<int64_t>();
       // K4 in host-row chunks when the destination rows are copy-engine
-      // runs: chunk g's h rows go to the host (K5) while chunk g+1 computes
-      const int nck = c.dest_pos.empty() ? 1 : kChunks;
+      // runs to host memory: chunk g's h rows go to the host (K5) while
+      // chunk g+1 computes; one launch when h^{l+1} is HBM (nothing streams)
+      const int nck = c.dest_pos.empty() || f->hdev[layer + 1] ? 1 : kChunks;
       for (int g = 0; g < nck; ++g) {
         const int64_t r0 = nck > 1 ? c.dest_pos[g] : 0, r1 = nck > 1 ? c.dest_pos[g + 1] : c.nv;
         if (r1 > r0) {
@@ -311,6 +316,25 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       if (d.cache) {  // checkpoint and gradient rows straight from the mirrors
         A = d.ma[layer].as<float>() + c.dest_m0 * d_in;
         G = d.mg[layer + 1].as<float>() + c.dest_m0 * d_out;
+        const bool pf = layer < (int)f->agg_deferred.size() && f->agg_deferred[layer] &&
+                        precision == HT_PREC_TF32;
+        if (f->agg_recompute[layer] && !pf) {
+          // recompute-cache hybrid: agg^l was not kept - re-aggregate it from
+          // the h^l mirror (the forward's gather, bitwise the same rows)
+          const float* Xd = hbm_inputs(f, d, layer, nullptr);
+          if (!Xd) return fail(HT_ESTATE, "layer %d: agg recompute needs the in-place h mirror", layer);
+          if (!f->ckpt_hbm) {  // the forward's write-through may still read the scratch
+            HT_TRY(ev_wait(d.stream, d.e_out[0]));
+            HT_TRY(ev_wait(d.stream, d.e_out[1]));
+          }
+          TimerRec tr;
+          timer_begin(f, d, tr, d.stream);
+          HT_TRY(launch_seg(d.stream, d, const_cast<float*>(A), Xd, d_in, d_in,
+                            c.csc_off.as<int64_t>(), c.csc_gid.as<int32_t>(), c.csc_w.as<float>(),
+                            c.nv, c.fw));
+          timer_end(f, d, tr, 0, (double)c.ne * (8.0 + 4.0 * d_in) + (double)c.nv * (4.0 * d_in + 4.0),
+                    d.stream);
+        }
       } else {
       // K6 on tin: checkpoint rows (ready since the forward), then the
       // destination gradients (ready once the layer above has flushed)
@@ -434,15 +458,11 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
         return fail(HT_ESTATE, "project-first layer %d needs the one-device narrow backward", layer);
       const int64_t nseg = dx ? c.bx_rows : c.nn;
       float* views = dx ? d.mg[layer].as<float>() : d.se.as<float>();
-      HT_TRY(launch_seg(d.stream, (narrow || pfl) ? d.tT.as<float>() : views,
+      HT_TRY(launch_seg(d.stream, d, (narrow || pfl) ? d.tT.as<float>() : views,
                         (narrow || pfl) ? GZ : GA, (narrow || pfl) ? ldz : kw,
                         (narrow || pfl) ? ldz : kw,
                         dx ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>(),
-                        c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), nseg,
-                        dx ? c.bx_np : c.bw_np, dx ? c.bx_lo : c.bw_lo, dx ? c.bx_hi : c.bw_hi,
-                        dx ? c.bx_nf : c.bw_nf, dx ? c.bx_seg : c.bw_seg,
-                        dx ? c.bx_first : c.bw_first, dx ? c.bx_cnt : c.bw_cnt,
-                        d.partial.as<float>()));
+                        c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), nseg, dx ? c.bx : c.bw));
       timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * kw) + (double)c.nn * (4.0 * kw + 4.0),
                 d.stream);
       if (pfl && nseg > 0) {  // dW = h^T (A^T gz), rows in row order

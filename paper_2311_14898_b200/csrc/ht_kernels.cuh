@@ -424,6 +424,157 @@ __global__ void __launch_bounds__(256) k_seg_pieces_s(float* __restrict__ partia
   }
 }
 
+// ---------------------------------------------------------------------------
+// Work-list segment reduction: one launch per aggregation.  Work units
+// [0, npu) are the pieces of the long segments (the heaviest items first),
+// then batches of short segments; a warp takes the next unit from a device
+// counter when it is free, so the pieces no longer form a serial tail
+// launch.  A piece writes its partial row, and the piece of a long segment
+// that finishes last (atomic ticket) sums the segment's partials in piece
+// order - the fixed order of k_seg_fixup, so the results are bitwise those
+// of the three-launch sequence.
+// ---------------------------------------------------------------------------
+struct SegWork {
+  const int64_t* off;
+  const int32_t* idx;
+  const float* w;
+  int64_t nseg, split;
+  const int64_t *lo, *hi;  // pieces
+  const int32_t* pf;       // fixup of each piece
+  int64_t np;
+  const int64_t *fseg, *ffirst, *fcnt;  // fixups
+  unsigned* counter;                    // zeroed before the launch
+  int* tickets;                         // [nf], zeroed before the launch
+  float* partial;
+};
+
+// partials first .. first + cnt - 1 of one fixup, summed in piece order
+// (L2 reads: they were written by other SMs), float4 column c
+__device__ __forceinline__ float4 sum_partials(const float* __restrict__ partial, int64_t first,
+                                               int64_t cnt, int d, int c) {
+  const float4* p = reinterpret_cast<const float4*>(partial + first * (int64_t)d) + c;
+  const int64_t d4 = d >> 2;
+  float4 s = __ldcg(p);
+  for (int64_t q = 1; q < cnt; ++q) {
+    const float4 v = __ldcg(p + q * d4);
+    s.x = __fadd_rn(s.x, v.x);
+    s.y = __fadd_rn(s.y, v.y);
+    s.z = __fadd_rn(s.z, v.z);
+    s.w = __fadd_rn(s.w, v.w);
+  }
+  return s;
+}
+
+template <int NV, int US, int UP, int B, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_seg_work_v4(float* __restrict__ out,
+                                                           const float* __restrict__ X,
+                                                           int64_t ldx, int d, SegWork wk) {
+  const int lane = lane_id();
+  const int d4 = d >> 2;
+  const int64_t nunits = wk.np + (wk.nseg + B - 1) / B;
+  for (;;) {
+    unsigned u = 0;
+    if (lane == 0) u = atomicAdd(wk.counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if ((int64_t)u >= nunits) break;
+    float4 acc[NV];
+    if ((int64_t)u < wk.np) {  // a piece of a long segment
+#pragma unroll
+      for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      seg_sum_v4<NV, UP>(acc, X, ldx, d4, wk.idx, wk.w, wk.lo[u], wk.hi[u], lane);
+      float4* prow = reinterpret_cast<float4*>(wk.partial + (int64_t)u * d);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const int c = lane + t * kWarp;
+        if (c < d4) prow[c] = acc[t];
+      }
+      __threadfence();  // this lane's partial stores, then the warp's ticket
+      __syncwarp();
+      const int f = wk.pf[u];
+      int last = 0;
+      if (lane == 0) last = atomicAdd(wk.tickets + f, 1) == (int)wk.fcnt[f] - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {  // every piece of the segment is written: fixed-order sum
+        __threadfence();
+        float4* o = reinterpret_cast<float4*>(out + wk.fseg[f] * (int64_t)d);
+        for (int c = lane; c < d4; c += kWarp) o[c] = sum_partials(wk.partial, wk.ffirst[f], wk.fcnt[f], d, c);
+      }
+      continue;
+    }
+    const int64_t s0 = ((int64_t)u - wk.np) * B;
+    const int64_t s1 = s0 + B < wk.nseg ? s0 + B : wk.nseg;
+    for (int64_t sg = s0; sg < s1; ++sg) {
+      const int64_t e0 = wk.off[sg], e1 = wk.off[sg + 1];
+      if (e1 - e0 > wk.split) continue;  // a long segment: its pieces
+#pragma unroll
+      for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      seg_sum_v4<NV, US>(acc, X, ldx, d4, wk.idx, wk.w, e0, e1, lane);
+      float4* o = reinterpret_cast<float4*>(out + sg * (int64_t)d);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const int c = lane + t * kWarp;
+        if (c < d4) o[c] = acc[t];
+      }
+    }
+  }
+}
+
+// narrow rows (d4 <= G): 32/G sub-groups per warp, each its own piece or
+// segment, summed sequentially in edge order (seg_sum_sub)
+template <int G, int U, int B, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_seg_work_sub(float* __restrict__ out,
+                                                            const float* __restrict__ X,
+                                                            int64_t ldx, int d, SegWork wk) {
+  constexpr int S = 32 / G;
+  const int lane = lane_id(), sl = lane % G, sub = lane / G;
+  const int d4 = d >> 2;
+  const int64_t npu = (wk.np + S - 1) / S;
+  const int64_t nunits = npu + (wk.nseg + S * B - 1) / (S * B);
+  for (;;) {
+    unsigned u = 0;
+    if (lane == 0) u = atomicAdd(wk.counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if ((int64_t)u >= nunits) break;
+    if ((int64_t)u < npu) {  // S pieces, one per sub-group
+      const int64_t p = (int64_t)u * S + sub;
+      const bool mine = p < wk.np;
+      const int64_t e0 = mine ? wk.lo[p] : 0, e1 = mine ? wk.hi[p] : 0;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      seg_sum_sub<G, U>(acc, X, ldx, d4, wk.idx, wk.w, e0, e1, sl);
+      if (mine && sl < d4) reinterpret_cast<float4*>(wk.partial + p * (int64_t)d)[sl] = acc;
+      __threadfence();  // this lane's partial stores, then the warp's ticket
+      __syncwarp();
+      const int f = mine ? wk.pf[p] : 0;
+      int last = 0;
+      if (mine && sl == 0) last = atomicAdd(wk.tickets + f, 1) == (int)wk.fcnt[f] - 1;
+      last = __shfl_sync(0xffffffffu, last, sub * G);
+      if (mine && last) {
+        __threadfence();
+        if (sl < d4)
+          reinterpret_cast<float4*>(out + wk.fseg[f] * (int64_t)d)[sl] =
+              sum_partials(wk.partial, wk.ffirst[f], wk.fcnt[f], d, sl);
+      }
+      continue;
+    }
+    const int64_t s0 = ((int64_t)u - npu) * (S * B);
+    for (int b = 0; b < B; ++b) {
+      const int64_t sg = s0 + (int64_t)b * S + sub;
+      if (s0 + (int64_t)b * S >= wk.nseg) break;  // warp-uniform
+      int64_t e0 = 0, e1 = 0;
+      const bool inr = sg < wk.nseg;
+      if (inr) {
+        e0 = wk.off[sg];
+        e1 = wk.off[sg + 1];
+      }
+      const bool skip = !inr || e1 - e0 > wk.split;  // long: its pieces
+      if (skip) e1 = e0;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      seg_sum_sub<G, U>(acc, X, ldx, d4, wk.idx, wk.w, e0, e1, sl);
+      if (!skip && sl < d4) reinterpret_cast<float4*>(out + sg * (int64_t)d)[sl] = acc;
+    }
+  }
+}
+
 // out[seg[f]] = ((partial[first] + partial[first+1]) + ...) in piece order.
 static __global__ void __launch_bounds__(256) k_seg_fixup(float* __restrict__ out,
                                                    const float* __restrict__ partial, int d,
@@ -688,6 +839,18 @@ static __global__ void k_xbarrier(uint32_t* self, uint32_t* const* peers, int m,
   }
   __syncwarp();
   __threadfence_system();
+}
+
+// deterministic operand pattern in [-1, 1) for the measurement entries
+static __global__ void k_fill_pattern(float* __restrict__ x, int64_t n, uint32_t seed) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)e * 2654435761u ^ (seed * 0x9E3779B9u);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    x[e] = (float)(h & 0xFFFFFF) * (2.0f / 16777216.0f) - 1.0f;
+  }
 }
 
 // K12: total = ((0 + g_0) + g_1) + ...; W = W - lr * total (separate roundings)

@@ -1,5 +1,7 @@
 // Measurement and unit-test entry points: PCIe probe, GEMM unit entry.
 
+#include <cuda_profiler_api.h>
+
 #include "ht_fleet_internal.h"
 
 using ht::fail;
@@ -139,3 +141,92 @@ extern "C" int ht_gemm_test(int op, int precision, const float* A, const float* 
   return rc;
 }
 
+
+// ---------------------------------------------------------------------------
+// Profiler range (ncu --replay-mode app-range --profile-from-start off):
+// bench.py brackets one epoch with it so the PCIe / NVLink / DRAM counters
+// cover every kernel and copy-engine transfer of exactly that epoch.
+// ---------------------------------------------------------------------------
+extern "C" int ht_profile_range(int start) {
+  CU(start ? cudaProfilerStart() : cudaProfilerStop());
+  return HT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM rate (measurement): the layer drivers' launchers on device-resident
+// random operands, `iters` back-to-back launches timed with CUDA events.
+// op as ht_gemm_test (0: relu(A W) 3xTF32, 2: A W^T 1xTF32, 3: A^T G).
+// out[0] ms per launch, out[1] TFLOP/s of the useful 2 M K N flops,
+// out[2] GB/s of the compulsory operand bytes (A, G/C rows once).
+// ---------------------------------------------------------------------------
+extern "C" int ht_gemm_rate(int op, int precision, int64_t M, int K, int N, int iters,
+                            double* out) {
+  CU(cudaSetDevice(0));
+  if (op != 0 && op != 2 && op != 3) return fail(HT_EINVAL, "gemm rate: op %d not timed", op);
+  if (iters <= 0) return fail(HT_EINVAL, "gemm rate: iters %d", iters);
+  cudaStream_t s = nullptr;
+  CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const int ka = op == 2 ? N : K, lda = pad4(ka), ldn = pad4(N);
+  const int64_t c_rows = op == 3 ? K : M, c_cols = op == 2 ? K : N;
+  Device d;
+  d.stream = s;
+  DBuf dA, dG, dC, ws;
+  HT_TRY(dA.ensure(std::max<int64_t>(1, M * lda) * 4));
+  HT_TRY(dG.ensure(std::max<int64_t>(1, M * ldn) * 4));
+  HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * c_cols) * 4));
+  HT_TRY(ws.ensure((int64_t)148 * K * N * 4 + 4));
+  // operands: a fixed bit pattern in [-1, 1) (values do not affect timing)
+  count_launch(2);
+  ht::k_fill_pattern<<<1184, 256, 0, s>>>(dA.as<float>(), M * lda, 1u);
+  ht::k_fill_pattern<<<1184, 256, 0, s>>>(dG.as<float>(), M * ldn, 2u);
+  std::vector<float> W((size_t)K * N);
+  for (size_t e = 0; e < W.size(); ++e) W[e] = (float)((e * 2654435761u) % 2001) / 1000.f - 1.f;
+  HT_TRY(upload_weights(d, W.data(), K, N));
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  int rc = HT_OK;
+  auto launch = [&]() -> int {
+    const bool tc = precision == HT_PREC_TF32;
+    if (op == 0)
+      return tc ? ht::tc::rows<ht::tc::TC_RELU>(s, true, dA.as<float>(), lda, M, K,
+                                                d.Wt_hi.as<float>(), d.Wt_lo.as<float>(), K, N,
+                                                dC.as<float>(), N, nullptr, 0)
+                : gemm<false, false, ht::EPI_RELU>(s, dA.as<float>(), lda, d.W.as<float>(), N,
+                                                   dC.as<float>(), N, nullptr, 0, M, N, K, 1, K);
+    if (op == 2)
+      return tc ? ht::tc::rows<ht::tc::TC_STORE>(s, false, dA.as<float>(), lda, M, N,
+                                                 d.Wp_hi.as<float>(), nullptr, pad4(N), K,
+                                                 dC.as<float>(), K, nullptr, 0)
+                : gemm<false, true, ht::EPI_STORE>(s, dA.as<float>(), lda, d.W.as<float>(), N,
+                                                   dC.as<float>(), K, nullptr, 0, M, K, N, 1, N);
+    int used = 1;
+    if (!tc) return fail(HT_EINVAL, "gemm rate: op 3 is timed on the tf32 path only");
+    return ht::tc::wgrad(s, dA.as<float>(), lda, K, dG.as<float>(), ldn, N, M, 148,
+                         ws.as<float>(), &used);
+  };
+  rc = launch();  // warm-up (tensor maps, first-touch)
+  if (rc == HT_OK) {
+    CU(cudaEventRecord(a, s));
+    for (int t = 0; t < iters && rc == HT_OK; ++t) rc = launch();
+    CU(cudaEventRecord(b, s));
+  }
+  if (rc == HT_OK) {
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, a, b));
+    const double per = ms / iters;
+    const double flops = 2.0 * (double)M * K * N;
+    const double bytes = op == 0 ? 4.0 * M * (K + N) : op == 2 ? 4.0 * M * (N + K)
+                                                               : 4.0 * M * (K + N);
+    out[0] = per;
+    out[1] = flops / (per * 1e-3) / 1e12;
+    out[2] = bytes / (per * 1e-3) / 1e9;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  for (DBuf* bb : {&dA, &dG, &dC, &ws, &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo})
+    bb->release();
+  cudaStreamDestroy(s);
+  return rc;
+}

@@ -229,37 +229,79 @@ void timers_collect(ht_fleet* f) {
 }
 
 // Segment gather-sum over a chunk's CSC (forward) or CSR (backward) view.
-int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, const int64_t* off,
-               const int32_t* idx, const float* w, int64_t nseg, int64_t np, const DBuf& lo,
-               const DBuf& hi, int64_t nf, const DBuf& seg, const DBuf& first, const DBuf& cnt,
-               float* partial) {
+// float4 rows (d % 4 == 0, the tf32 path's pad4 widths): ONE work-list
+// launch - the pieces of the long segments first, then batches of short
+// segments, taken from a device counter by whichever warp is free; the
+// last piece of a long segment to finish sums its partials in piece order
+// (k_seg_work_*).  Other widths (the fp32 validation path's odd widths):
+// the per-segment kernel, the pieces kernel and the fixup in turn.
+namespace {
+template <class K>
+int resident_grid(K kernel, int64_t warps_needed) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0) != cudaSuccess ||
+      per_sm <= 0)
+    per_sm = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (warps_needed * 32 + kThreads - 1) / kThreads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sms));
+}
+}  // namespace
+
+int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
+               const int64_t* off, const int32_t* idx, const float* w, int64_t nseg,
+               const Pieces& pc) {
   if (nseg <= 0) return HT_OK;
-  const int g = grid_for(nseg);
-  count_launch(1 + (np ? 1 : 0) + (nf ? 1 : 0));
+  const int64_t np = pc.np, nf = pc.nf;
   static const bool sub_ok = [] {  // HT_NO_SUBWARP=1: narrow rows on the warp kernels
     const char* e = getenv("HT_NO_SUBWARP");
     return !(e && atoi(e));
   }();
-  if (d % 4 == 0 && d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
-    static const int sv = [] {
-      const char* e = getenv("HT_SUB_VARIANT");
-      return e ? atoi(e) : 0;
-    }();
+  static const bool worklist = [] {  // HT_SEG_SPLIT_LAUNCH=1: r1's three-launch sequence
+    const char* e = getenv("HT_SEG_SPLIT_LAUNCH");
+    return !(e && atoi(e));
+  }();
+  float* partial = dv.partial.as<float>();
+  if (d % 4 == 0 && d <= 512 && worklist) {
+    ht::SegWork wk{off, idx, w, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(),
+                   pc.pf.as<int32_t>(), np, pc.seg.as<int64_t>(), pc.first.as<int64_t>(),
+                   pc.cnt.as<int64_t>(), dv.work.as<unsigned>(), dv.work.as<int>() + 1, partial};
+    if (dv.work.bytes < (nf + 2) * 4) return fail(HT_ESTATE, "work-list buffer not sized");
+    CU(cudaMemsetAsync(dv.work.p, 0, (nf + 2) * 4, s));  // counter + fixup tickets
+    count_launch();
+    if (d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
+      if (d <= 32) {
+        auto k = ht::k_seg_work_sub<8, 8, 4, 4>;
+        k<<<resident_grid(k, (nseg + 3) / 4), kThreads, 0, s>>>(out, X, ldx, d, wk);
+      } else {
+        auto k = ht::k_seg_work_sub<16, 8, 4, 4>;
+        k<<<resident_grid(k, (nseg + 1) / 2), kThreads, 0, s>>>(out, X, ldx, d, wk);
+      }
+    } else {
+      switch ((d / 4 + 31) / 32) {
+        case 1: { auto k = ht::k_seg_work_v4<1, 8, 8, 16, 4>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+        case 2: { auto k = ht::k_seg_work_v4<2, 2, 8, 16, 4>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+        case 3: { auto k = ht::k_seg_work_v4<3, 2, 4, 16, 2>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+        default: { auto k = ht::k_seg_work_v4<4, 2, 4, 16, 2>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+      }
+    }
+    CU(cudaGetLastError());
+    return HT_OK;
+  }
+  const int g = grid_for(nseg);
+  count_launch(1 + (np ? 1 : 0) + (nf ? 1 : 0));
+  const DBuf &lo = pc.lo, &hi = pc.hi;
+  if (d % 4 == 0 && d <= 64 && sub_ok) {
     if (d <= 32) {
       ht::k_seg_gather_sub<8><<<grid_for((nseg + 3) / 4), kThreads, 0, s>>>(out, X, ldx, d, off, idx,
                                                                            w, nseg, kSplit);
       if (np) ht::k_seg_pieces_sub<8><<<grid_for((np + 3) / 4), kThreads, 0, s>>>(
           partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
     } else {
-      const int g2 = grid_for((nseg + 1) / 2);
-      if (sv == 1)
-        ht::k_seg_gather_sub<16, 4, 4><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
-      else if (sv == 2)
-        ht::k_seg_gather_sub<16, 8, 3><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
-      else if (sv == 3)
-        ht::k_seg_gather_sub<16, 16, 2><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
-      else
-        ht::k_seg_gather_sub<16, 8, 4><<<g2, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit);
+      ht::k_seg_gather_sub<16, 8, 4><<<grid_for((nseg + 1) / 2), kThreads, 0, s>>>(
+          out, X, ldx, d, off, idx, w, nseg, kSplit);
       if (np) ht::k_seg_pieces_sub<16><<<grid_for((np + 1) / 2), kThreads, 0, s>>>(
           partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
     }
@@ -292,8 +334,8 @@ int launch_seg(cudaStream_t s, float* out, const float* X, int64_t ldx, int d, c
   }
   CU(cudaGetLastError());
   if (nf) {
-    ht::k_seg_fixup<<<grid_for(nf), kThreads, 0, s>>>(out, partial, d, seg.as<int64_t>(),
-                                                       first.as<int64_t>(), cnt.as<int64_t>(), nf);
+    ht::k_seg_fixup<<<grid_for(nf), kThreads, 0, s>>>(out, partial, d, pc.seg.as<int64_t>(),
+                                                       pc.first.as<int64_t>(), pc.cnt.as<int64_t>(), nf);
     CU(cudaGetLastError());
   }
   return HT_OK;
@@ -329,8 +371,9 @@ int upload_weights(Device& d, const float* W, int d_in, int d_out) {
 }
 
 // long-segment pieces of an offsets array
-void make_pieces(const std::vector<int64_t>& off, std::vector<int64_t>& lo, std::vector<int64_t>& hi,
-                 std::vector<int64_t>& seg, std::vector<int64_t>& first, std::vector<int64_t>& cnt) {
+int make_pieces(const std::vector<int64_t>& off, Pieces& pc, cudaStream_t s) {
+  std::vector<int64_t> lo, hi, seg, first, cnt;
+  std::vector<int32_t> pf;
   for (size_t sg = 0; sg + 1 < off.size(); ++sg) {
     const int64_t a = off[sg], b = off[sg + 1];
     if (b - a <= kSplit) continue;
@@ -340,9 +383,19 @@ void make_pieces(const std::vector<int64_t>& off, std::vector<int64_t>& lo, std:
     for (int64_t x = a; x < b; x += kSplit, ++c) {
       lo.push_back(x);
       hi.push_back(std::min(b, x + kSplit));
+      pf.push_back((int32_t)(seg.size() - 1));
     }
     cnt.push_back(c);
   }
+  pc.np = (int64_t)lo.size();
+  pc.nf = (int64_t)seg.size();
+  HT_TRY(upload(pc.lo, lo, s));
+  HT_TRY(upload(pc.hi, hi, s));
+  HT_TRY(upload(pc.seg, seg, s));
+  HT_TRY(upload(pc.first, first, s));
+  HT_TRY(upload(pc.cnt, cnt, s));
+  HT_TRY(upload(pc.pf, pf, s));
+  return HT_OK;
 }
 
 int lookup_slots(const HostSets& hs, const std::vector<int64_t>& rows, std::vector<int64_t>& out,
@@ -681,6 +734,73 @@ int prefetch_checkpoints(ht_fleet* f, Device& d, int layer, void* aout, int64_t 
 
 // extra_grad: floats of further parameter gradients kept behind the weight
 // gradients in the (IPC-shared) accumulator (GAT attention vectors)
+// Owner-cache decision of one device under the HBM budget (the recompute-
+// cache hybrid).  The h^l and grad_h^l mirrors (and the
+// one-device buffers of project-first layers / GAT kept projections) must
+// fit; agg^l mirrors are kept greedily from the narrowest layer up, and a
+// single scratch buffer of the widest remaining layer serves the others -
+// their agg^l is re-aggregated in the backward from the h^l mirror (the
+// forward's gather: bitwise the same rows).  Recompute needs the gathers to
+// read the mirror in place (one device, identity mirror); elsewhere the
+// cache is all or nothing.
+int plan_cache(ht_fleet* f, Device& d, int L, const int* dims, bool gat, int64_t mv, int64_t mn,
+               int dmax) {
+  const int64_t R = std::max<int64_t>(1, d.mcount);
+  int64_t base = 0;
+  for (int l = 0; l < L; ++l) base += R * dims[l] * 4;   // h mirrors
+  for (int l = 0; l <= L; ++l) base += R * dims[l] * 4;  // grad mirrors
+  const bool one = f->m == 1 && d.mcount == f->nrows && d.chunks[0].csc_gid.p &&
+                   (d.mrows.empty() || d.mrows.back() == d.mcount - 1);
+  if (gat) {  // GAT staging allocated after this decision (ht_gat_epoch_begin)
+    int64_t me = 1;
+    for (int j = 0; j < f->n; ++j) me = std::max(me, d.chunks[j].ne);
+    base += (3 * mn + 4 * mv) * (int64_t)dmax * 4 + 4 * me * 4;
+    if (one && f->n == 1)  // gat_direct: each layer's projection and el_src kept
+      for (int l = 0; l < L; ++l) base += R * (pad4(dims[l + 1]) + 1) * 4;
+  } else if (one && f->n == 1) {  // project-first buffers (pf_p, pf_z)
+    int pw = 0;
+    for (int l = 0; l < L; ++l)
+      if (dims[l + 1] < dims[l]) pw = std::max(pw, pad4(dims[l + 1]));
+    base += 2 * R * pw * 4;
+  }
+  size_t fr = 0, tot = 0;
+  CU(cudaMemGetInfo(&fr, &tot));
+  int64_t avail = (int64_t)fr - ((int64_t)4 << 30);
+  if (f->hbm_budget > 0) avail = std::min(avail, f->hbm_budget);
+  int64_t agg_all = 0;
+  if (!gat)
+    for (int l = 0; l < L; ++l) agg_all += R * dims[l] * 4;
+  if (base + agg_all <= avail) {
+    d.cache = true;
+    return HT_OK;
+  }
+  const bool recompute_ok = !gat && one && !getenv("HT_NO_RECOMPUTE");
+  if (recompute_ok) {
+    std::vector<int> order(L);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return dims[a] < dims[b]; });
+    for (int keep = L - 1; keep >= 0; --keep) {  // keep the `keep` narrowest agg mirrors
+      int64_t need = base;
+      int scr = 0;
+      for (int q = 0; q < L; ++q) {
+        if (q < keep) need += R * dims[order[q]] * 4;
+        else scr = std::max(scr, dims[order[q]]);
+      }
+      need += R * scr * 4;
+      if (need <= avail) {
+        for (int q = keep; q < L; ++q) f->agg_recompute[order[q]] = 1;
+        d.cache = true;
+        return HT_OK;
+      }
+    }
+  }
+  if (f->cache_req == 1)
+    return fail(HT_ENOMEM, "HBM owner cache needs %lld bytes (%lld with recompute), %lld available",
+                (long long)(base + agg_all), (long long)base, (long long)avail);
+  d.cache = false;
+  return HT_OK;
+}
+
 int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bool gat) {
   if (!f->finalized) return fail(HT_ESTATE, "fleet not finalized");
   HT_TRY(check_chunks(f));
@@ -690,6 +810,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
   f->hptr.assign(L + 1, nullptr);
   f->hdev.assign(L + 1, 0);
   f->agg_deferred.assign(L, 0);
+  f->agg_recompute.assign(L, 0);
   int dmax = 0;
   for (int l = 0; l <= L; ++l) dmax = std::max(dmax, pad4(dims[l]));
   for (auto& d : f->dev) {
@@ -705,12 +826,13 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     }
     // every buffer of the epoch is sized here, once: no allocation (and no
     // implicit device synchronization) inside the layer calls
-    int64_t mv = 1, mn = 1, np = 1;
+    int64_t mv = 1, mn = 1, np = 1, nf = 0;
     d.hL_off.assign(f->n + 1, 0);
     for (int j = 0; j < f->n; ++j) {
       mv = std::max(mv, d.chunks[j].nv);
       mn = std::max(mn, d.chunks[j].nn);
-      np = std::max({np, d.chunks[j].fw_np, d.chunks[j].bw_np});
+      np = std::max({np, d.chunks[j].fw.np, d.chunks[j].bw.np, d.chunks[j].bx.np});
+      nf = std::max({nf, d.chunks[j].fw.nf, d.chunks[j].bw.nf, d.chunks[j].bx.nf});
       d.hL_off[j + 1] = d.hL_off[j] + d.chunks[j].nv;
     }
     // sized for 180 GB of HBM: the buffers every path needs first, then
@@ -725,6 +847,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     if (narrow_w)  // (the expanded CSR of one device / one batch has a row per host row)
       HT_TRY(d.tT.ensure(std::max<int64_t>(mn, f->m == 1 && f->n == 1 ? f->nrows : 0) * narrow_w * 4));
     HT_TRY(d.partial.ensure(np * dmax * 4));
+    HT_TRY(d.work.ensure((nf + 2) * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
     // HBM owner cache: decided per epoch (requested mode, plan, free HBM).
@@ -747,22 +870,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
           return fail(HT_EINVAL, "HBM owner cache needs mode p2p/full and destination sets that "
                                  "are contiguous ranges of each device's owned rows");
       } else {
-        int64_t per_row = 0;
-        for (int l = 0; l < L; ++l) per_row += dims[l] * (gat ? 1 : 2);  // h (+ agg)
-        for (int l = 0; l <= L; ++l) per_row += dims[l];                // grad
-        int64_t need = d.mcount * per_row * 4;
-        if (gat) {  // GAT staging allocated after this decision (ht_gat_epoch_begin)
-          int64_t me = 1;
-          for (int j = 0; j < f->n; ++j) me = std::max(me, d.chunks[j].ne);
-          need += (3 * mn + 4 * mv) * (int64_t)dmax * 4 + 2 * me * 4 + 2 * me * 4;
-        }
-        size_t fr = 0, tot = 0;
-        CU(cudaMemGetInfo(&fr, &tot));
-        const bool fits = need + ((int64_t)4 << 30) <= (int64_t)fr;
-        if (!fits && f->cache_req == 1)
-          return fail(HT_ENOMEM, "HBM owner cache needs %lld bytes, %lld free", (long long)need,
-                      (long long)fr);
-        d.cache = fits;
+        HT_TRY(plan_cache(f, d, L, dims, gat, mv, mn, dmax));
       }
     }
     // the slot value buffer: not needed when a single device's gathers read
@@ -785,8 +893,29 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
       d.ma.resize(gat ? 0 : L);
       d.mg.resize(L + 1);
       for (int l = 0; l < L; ++l) HT_TRY(d.mh[l].ensure(std::max<int64_t>(1, d.mcount) * dims[l] * 4));
+      int scr = 0;  // widest recomputed layer
       for (int l = 0; l < (gat ? 0 : L); ++l)
-        HT_TRY(d.ma[l].ensure(std::max<int64_t>(1, d.mcount) * dims[l] * 4));
+        if (f->agg_recompute[l]) scr = std::max(scr, dims[l]);
+      if (scr) {
+        HT_TRY(d.agg_scr.ensure(std::max<int64_t>(1, d.mcount) * scr * 4));
+      } else {
+        d.agg_scr.release();
+      }
+      for (int l = 0; l < (gat ? 0 : L); ++l) {
+        if (f->agg_recompute[l])
+          d.ma[l].set_alias(d.agg_scr.p);
+        else
+          HT_TRY(d.ma[l].ensure(std::max<int64_t>(1, d.mcount) * dims[l] * 4));
+      }
+      if (!gat && f->m == 1 && f->n == 1) {  // project-first buffers, sized once (no
+        int pw = 0;                          // allocation inside a layer call)
+        for (int l = 0; l < L; ++l)
+          if (dims[l + 1] < dims[l]) pw = std::max(pw, pad4(dims[l + 1]));
+        if (pw) {
+          HT_TRY(d.pf_p.ensure(std::max<int64_t>(1, d.mcount) * pw * 4));
+          HT_TRY(d.pf_z.ensure(std::max<int64_t>(1, d.mcount) * pw * 4));
+        }
+      }
       for (int l = 0; l <= L; ++l) HT_TRY(d.mg[l].ensure(std::max<int64_t>(1, d.mcount) * dims[l] * 4));
     }
     if (f->prefetch && !d.cache) {

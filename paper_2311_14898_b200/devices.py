@@ -305,7 +305,8 @@ class DeviceFleet:
 
     def __init__(self, plan: DedupPlan, mode: str = "full", flush_policy: str = "on_eviction",
                  dtype=np.float64, devices=None, precision: str = "tf32", rank: int | None = None,
-                 cache: str = "auto", lean: bool = False, checkpoints: str = "auto"):
+                 cache: str = "auto", lean: bool = False, checkpoints: str = "auto",
+                 hbm_budget_gb: float | None = None):
         if mode not in _MODES:
             raise SimulationError(f"unknown mode {mode!r}")
         if flush_policy not in _FLUSH_POLICIES:
@@ -324,6 +325,13 @@ class DeviceFleet:
         # mirrors when it is active (host.agg filled on first read), "host"
         # always writes them through (devices.py:391-404)
         self.checkpoints = checkpoints
+        # recompute-cache hybrid: cap on the owner cache's
+        # HBM per device; agg^l mirrors that do not fit are recomputed in the
+        # backward (one device) - see recompute_layers
+        if hbm_budget_gb is not None and not hbm_budget_gb > 0:
+            raise SimulationError(f"hbm_budget_gb must be positive, got {hbm_budget_gb!r}")
+        self.hbm_budget_gb = hbm_budget_gb
+        self.recompute_layers: list = []  # set per epoch by train_epoch
         self._ckpt_hosts = weakref.WeakSet()
         self._ckpt_shapes = {}  # (id(host.agg), layer) -> shape the mirrors hold
         # lean epochs (opt-in): no grad_h^0, and no host copies of h^L /

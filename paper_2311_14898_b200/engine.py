@@ -252,11 +252,16 @@ def train_epoch(p: TwoLevelPartition, fleet: DeviceFleet, model: ModelConfig, ho
     else:
         N.call("ht_fleet_alias_store", h_, L, None, None, None)
     N.call("ht_fleet_set_cache", h_, want)
+    N.call("ht_fleet_set_budget", h_,
+           0 if fleet.hbm_budget_gb is None else int(fleet.hbm_budget_gb * (1 << 30)))
     N.call("ht_fleet_set_lean", h_, int(fleet.lean))
     N.call("ht_gat_epoch_begin" if gat else "ht_epoch_begin", h_, L, dims_c)
     on = C.c_int(0)
     N.call("ht_fleet_cache_state", h_, C.byref(on))
     fleet.cache_active = bool(on.value)
+    rmask = C.c_int64(0)
+    N.call("ht_fleet_recompute_state", h_, C.byref(rmask))
+    fleet.recompute_layers = [l for l in range(L) if (rmask.value >> l) & 1]
     # checkpoint tier: with the owner cache the agg checkpoints stay in HBM
     # (the hybrid sized to 180 GB); host.agg is filled from there on read
     ckpt_hbm = fleet.cache_active and fleet.checkpoints == "auto" and not gat

@@ -325,3 +325,80 @@ def test_loss_label_and_mask_validation():
     ok[~mask] = 99  # unmasked labels are never read
     neg = y - dims[-1]  # every label as its negative alias
     assert run(ok, mask) == run(y, mask) == run(neg, mask)
+
+
+@pytest.mark.parametrize("n", [1, 3])
+@pytest.mark.parametrize("ck", ["auto", "host"])
+def test_recompute_hybrid_under_budget(n, ck, monkeypatch):
+    """Recompute-cache hybrid: under an HBM budget that
+    holds the h / grad mirrors but not every agg mirror, the agg^l that do
+    not fit are re-aggregated in the backward from the h^l mirror.  The
+    forward gather is deterministic, so the epochs equal the all-cached
+    epoch and the cache-off (host staging) epoch bitwise - weights, loss,
+    every host array including host.agg (re-aggregated when read)."""
+    monkeypatch.setenv("HT_NO_NARROW_BWD", "1")     # compare like with like with
+    monkeypatch.setenv("HT_NO_PROJECT_FIRST", "1")  # the host-staging path
+    V = 3000
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=V, avg_degree=8.0, seed=9), 64, 8)
+    p = H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 1, seed=9), n)
+    dims = [64, 32, 128, 8]
+    mirrors = 4 * V * (sum(dims[:-1]) + sum(dims))  # h + grad mirrors
+    if n == 1:
+        mirrors += 2 * 4 * V * 32  # the project-first buffers are reserved for one batch
+    slack = 64 * 1024  # < 4 V (the next width step) bytes
+    budgets = {"all": None,
+               "one": (mirrors + 4 * V * (32 + 128) + slack) / 2 ** 30,  # keep agg^1, scratch 128
+               "none": (mirrors + 4 * V * 128 + slack) / 2 ** 30,        # scratch only
+               "off": None}
+    res = {}
+    for key, b in budgets.items():
+        res[key] = _epochs_budget(p, ds, dims, "off" if key == "off" else "on", b, ck)
+    assert res["all"][3] == [] and res["off"][2] is False
+    assert res["one"][3] == [0, 2], res["one"][3]
+    assert res["none"][3] == [0, 1, 2], res["none"][3]
+    for key in ("all", "one", "none"):
+        a, b = res["off"][0], res[key][0]
+        assert a["loss"] == b["loss"], key
+        for name in ("W", "h", "gh"):
+            for x, y in zip(a[name], b[name]):
+                np.testing.assert_array_equal(x, y, err_msg=f"{key} {name}")
+        for l in a["agg"]:
+            np.testing.assert_array_equal(a["agg"][l], b["agg"][l], err_msg=f"{key} agg{l}")
+
+
+def _epochs_budget(p, ds, dims, cache, budget, ck, epochs=2):
+    plan = H.plan_for_partition(p)
+    model = H.init_model("gcn", dims, seed=3, lr=0.1, dtype=np.float32)
+    host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+    host.set_features(ds.features)
+    fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, cache=cache, hbm_budget_gb=budget,
+                          checkpoints=ck)
+    for _ in range(epochs):
+        r = H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+    snap = {"loss": r.loss, "W": [w.copy() for w in model.weights],
+            "h": [np.array(x) for x in host.h], "gh": [np.array(x) for x in host.grad_h],
+            "agg": {l: np.array(host.agg[l]) for l in range(len(dims) - 1)}}
+    out = (snap, fleet.recompute_layers, fleet.cache_active, list(fleet.recompute_layers))
+    fleet.close()
+    return out
+
+
+def test_budget_too_small_for_the_mirrors():
+    """A budget below the h / grad mirrors: "auto" falls back to host
+    staging, "on" refuses."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=2000, avg_degree=8.0, seed=9), 16, 8)
+    p = H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 1, seed=9), 1)
+    plan = H.plan_for_partition(p)
+    dims = [16, 24, 8]
+    for cache in ("auto", "on"):
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, dtype=np.float32, cache=cache, hbm_budget_gb=1e-6)
+        model = H.init_model("gcn", dims, seed=3, dtype=np.float32)
+        if cache == "auto":
+            H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+            assert not fleet.cache_active and fleet.recompute_layers == []
+        else:
+            with pytest.raises(H.ChunktrainError, match="recompute"):
+                H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+        fleet.close()
