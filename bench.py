@@ -47,8 +47,25 @@ CONFIGS = {
     "cfg3s": dict(V=8_200_000, avg_degree=28.5, dims=[256, 128, 128, 64], n=1, seed=0,
                   name="3-layer GCN 256-128-128-64, per-GPU share of the friendster-shape config 3 "
                        "(8.2M V / ~227M E synthetic)"),
+    # one GPU's share of BASELINE config 4 (ogbn-papers100M-shape 111M V /
+    # 1.6B E over 8 GPUs): 13.9M V / ~200M E, 200-128-128-172, host-resident
+    # data through the recompute-cache hybrid
+    "cfg4s": dict(V=13_900_000, avg_degree=14.4, dims=[200, 128, 128, 172], n=1, seed=0,
+                  name="3-layer GCN 200-128-128-172, per-GPU share of the ogbn-papers100M-shape "
+                       "config 4 (13.9M V / ~200M E synthetic)"),
+    # one GPU's share of BASELINE config 5 (it-2004-shape 41M V / 1.15B E
+    # over 8 GPUs): 5.15M V / ~144M E, 3-layer GAT 256-128-128-64
+    "cfg5s": dict(V=5_150_000, avg_degree=28.0, dims=[256, 128, 128, 64], n=1, seed=0,
+                  model="gat",
+                  name="3-layer GAT 256-128-128-64, per-GPU share of the it-2004-shape config 5 "
+                       "(5.15M V / ~144M E synthetic)"),
 }
 METRIC = "full-graph GCN epoch GTEPS (L*|E|/epoch_s)"
+GAT_METRIC = METRIC.replace("GCN", "GAT")
+
+
+def model_of(cfg):
+    return cfg.get("model", "gcn")
 
 
 def log(*a):
@@ -306,8 +323,14 @@ def reference_impl():
         def nedges(ch):
             return int(ch.num_edges)
 
-        return "reference", dict(chunk=chunk, fwd=fwd, bwd=bwd, loss=E.downstream_loss,
-                                 sources=src_of, edges=nedges,
+        def gfwd(ch, h_nbr, h_dst, W, a):
+            return E.gat_layer_forward(ch, h_nbr, h_dst, W, a)
+
+        def gbwd(ch, h_nbr, h_dst, gout, W, a):
+            return E.gat_layer_backward_recompute(ch, h_nbr, h_dst, gout, W, a)
+
+        return "reference", dict(chunk=chunk, fwd=fwd, bwd=bwd, gfwd=gfwd, gbwd=gbwd,
+                                 loss=E.downstream_loss, sources=src_of, edges=nedges,
                                  what="chunktrain (unmodified reference, baseline/_ref)")
     except ImportError:
         from oracle import hongtu_oracle as O
@@ -318,6 +341,7 @@ def reference_impl():
             return O.chunk_of(gd, verts)
 
         return "port", dict(chunk=chunk, fwd=O.gcn_chunk_forward, bwd=O.gcn_chunk_backward,
+                            gfwd=O.gat_chunk_forward, gbwd=O.gat_chunk_backward,
                             loss=O.softmax_xent, sources=lambda ch: ch["sources"],
                             edges=lambda ch: int(ch["csc_local_src"].size),
                             what="oracle port (oracle/hongtu_oracle.py, numpy)")
@@ -363,9 +387,11 @@ class ReferenceSampler:
     edges actually traversed (each edge once per layer, as GTEPS counts
     them) over the step's wall time."""
 
-    def __init__(self, graph, labels, mask, dims, budget_edges=250_000, windows=16, seed=0):
+    def __init__(self, graph, labels, mask, dims, budget_edges=250_000, windows=16, seed=0,
+                 model="gcn"):
         self.kind, self.api = reference_impl()
         self.dims = dims
+        self.model = model
         V = int(graph.num_vertices)
         off = np.asarray(graph.csc_offsets)
         self.chunks = []
@@ -384,6 +410,7 @@ class ReferenceSampler:
                    np.sqrt(2.0 / (dims[l] + dims[l + 1]))).astype(np.float32) for l in range(L)]
         self.gup = [rng.standard_normal((budget_edges, dims[l + 1]), dtype=np.float32) * 1e-3
                     for l in range(L)]
+        self.A = [(rng.standard_normal(2 * dims[l + 1]) * 0.1).astype(np.float32) for l in range(L)]
         self.labels, self.mask = np.asarray(labels), np.asarray(mask)
         self.step_i = 0
 
@@ -395,6 +422,17 @@ class ReferenceSampler:
         src = api["sources"](ch)
         nv = verts.size
         t0 = time.perf_counter()
+        if self.model == "gat":  # engine.py:418-423, 455-470: no checkpoints, recompute
+            for l in range(L):
+                h_out, _ = api["gfwd"](ch, self.h[l][src], self.h[l][verts], self.W[l], self.A[l])
+            _, grad = api["loss"](h_out, self.labels[verts], self.mask[verts])
+            for l in reversed(range(L)):
+                gout = grad if l == L - 1 else self.gup[l][:nv]
+                out = api["gbwd"](ch, self.h[l][src], self.h[l][verts], gout, self.W[l], self.A[l])
+                self.g[l][verts] += out[1]
+                self.g[l][src] += out[0]
+            dt = time.perf_counter() - t0
+            return dt, L * api["edges"](ch)
         aggs = []
         for l in range(L):
             h_out, agg, _ = api["fwd"](ch, self.h[l][src], self.W[l])
@@ -409,17 +447,19 @@ class ReferenceSampler:
 
     def describe(self):
         e = [self.api["edges"](c) for _, c in self.chunks]
+        fw, bw = (("gat_layer_forward", "gat_layer_backward_recompute") if self.model == "gat"
+                  else ("gcn_layer_forward", "gcn_layer_backward_hybrid"))
         return (f"{self.api['what']}: per step, one window of consecutive destinations "
                 f"(~{int(np.mean(e))} in-edges; {len(e)} windows spread over the vertex range, "
                 f"one per step in turn) through every layer: gather h^l[N] from the full "
-                f"(V, d_l) host array, gcn_layer_forward, downstream_loss, "
-                f"gcn_layer_backward_hybrid, flush into the (V, d_l) gradient array; "
+                f"(V, d_l) host array, {fw}, downstream_loss, "
+                f"{bw}, flush into the (V, d_l) gradient array; "
                 f"GTEPS = edges traversed (once per layer) / step wall time, not extrapolated")
 
 
-def reference_cpu_baseline(graph, labels, mask, dims, steps=3, warmup=1):
+def reference_cpu_baseline(graph, labels, mask, dims, steps=3, warmup=1, model="gcn"):
     """cpu_baseline of the ours-arm line: a few ReferenceSampler steps."""
-    rs = ReferenceSampler(graph, labels, mask, dims)
+    rs = ReferenceSampler(graph, labels, mask, dims, model=model)
     for _ in range(warmup):
         rs.step()
     t = e = 0.0
@@ -494,45 +534,89 @@ def _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, k
 GAT_DIMS = [256, 128, 128, 64]  # it-2004 / config 5 widths
 
 
-def gat_measure(p, plan, ds, steps, warmup, precision, seed, rank, slowest):
-    """BASELINE config 5's model (3-layer GAT 256-128-128-64) on the bench
-    graph: config 5's 41M-vertex graph needs ~190 GB of pinned host rows,
-    beyond one box's host memory, so the GAT path is measured on the same
-    2.4M-vertex graph (synthetic 256-wide features, 64 classes)."""
+def gat_measure(p, plan, ds, steps, warmup, precision, seed, rank, slowest, dims=None,
+                native_data=False):
+    """A 3-layer GAT epoch (value: HBM store; e2e: pinned host store).  By
+    default BASELINE config 5's model (256-128-128-64) on the bench graph:
+    config 5's 41M-vertex graph needs ~190 GB of pinned host rows, beyond one
+    box's host memory, so the GAT path is measured on the same graph with
+    synthetic 256-wide features and 64 classes; native_data: the dataset's
+    own features / labels (the cfg5s per-GPU share)."""
+    dims = GAT_DIMS if dims is None else dims
     V = ds.graph.num_vertices
-    rng = np.random.default_rng(seed)
-    X = rng.standard_normal((V, GAT_DIMS[0]), dtype=np.float32)
-    y = (np.asarray(ds.labels) % GAT_DIMS[-1]).astype(np.int64)
-    L = len(GAT_DIMS) - 1
+    if native_data:
+        X, y = ds.features, ds.labels
+    else:
+        rng = np.random.default_rng(seed)
+        X = rng.standard_normal((V, dims[0]), dtype=np.float32)
+        y = (np.asarray(ds.labels) % dims[-1]).astype(np.int64)
+    L = len(dims) - 1
     E = ds.graph.num_edges
-    out = {"workload": f"3-layer GAT {'-'.join(map(str, GAT_DIMS))} on the bench graph "
+    out = {"workload": f"3-layer GAT {'-'.join(map(str, dims))} on the bench graph "
                        f"({V} V / {E} E), m=n=1, mode full",
-           "metric": METRIC.replace("GCN", "GAT"), "unit": "GTEPS"}
-    val = run_epochs(p, plan, ds, GAT_DIMS, "device", steps, warmup, precision, True, seed,
+           "metric": GAT_METRIC, "unit": "GTEPS"}
+    val = run_epochs(p, plan, ds, dims, "device", steps, warmup, precision, True, seed,
                      rank=rank, kind="gat", features=X, labels=y)
     ms_v = slowest(val["ms_total"]) / steps
-    e2e = run_epochs(p, plan, ds, GAT_DIMS, "host", steps, warmup, precision, True, seed,
+    e2e = run_epochs(p, plan, ds, dims, "host", steps, warmup, precision, True, seed,
                      rank=rank, kind="gat", features=X, labels=y)
     ms_e = slowest(e2e["ms_total"]) / steps
     lf, msf, bf = val["stats"][0]
     lb, msb, bb = val["stats"][1]
     lg, msg, flops = val["stats"][2]
+    hb = host_bytes_per_epoch(plan, dims, cached=e2e["cache"], kind="gat") if e2e["cache"] else None
     out.update({
         "value": L * E / (ms_v / 1e3) / 1e9, "ms_per_step": ms_v,
-        "e2e": {"value": L * E / (ms_e / 1e3) / 1e9, "ms_per_step": ms_e,
+        "e2e": {"value": L * E / (ms_e / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": ms_e,
+                "wall_ms_per_step": e2e["wall_s"] / steps * 1e3,
                 "hbm_owner_cache": bool(e2e["cache"]),
-                "h2d_bytes_per_step": host_bytes_per_epoch(plan, GAT_DIMS, cached=e2e["cache"],
-                                                           kind="gat")[0] if e2e["cache"] else None,
-                "d2h_bytes_per_step": host_bytes_per_epoch(plan, GAT_DIMS, cached=e2e["cache"],
-                                                           kind="gat")[1] if e2e["cache"] else None},
+                "h2d_bytes_per_step": hb[0] if hb else None,
+                "d2h_bytes_per_step": hb[1] if hb else None},
         "edge_kernels": {"fwd_ms_per_step": msf / steps, "bwd_ms_per_step": msb / steps,
                          "fwd_gbs": bf / (msf / 1e3) / 1e9 if msf else None,
                          "bwd_gbs": bb / (msb / 1e3) / 1e9 if msb else None,
+                         "bytes_per_step": (bf + bb) / steps,
+                         "launches_per_step": (lf + lb) / steps,
                          "share_of_step": (msf + msb) / val["ms_total"] if val["ms_total"] else None},
         "gemm": {"ms_per_step": msg / steps, "tflops": flops / (msg / 1e3) / 1e12 if msg else None},
         "gpu_launches": int(val["launches"]),
+        "gpu_launches_e2e": int(e2e["launches"]),
         "losses": {"value": val["losses"][-1], "e2e": e2e["losses"][-1]},
     })
+    return out
+
+
+def gat_config_line(args, cfg, config, p, plan, ds, rk, slowest, hbm_peak, hbm_src):
+    """The contract line of a GAT workload (cfg5s): value / e2e / roofline of
+    the edge kernels / cpu_baseline, like the GCN line."""
+    with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk:
+        r = gat_measure(p, plan, ds, args.steps, args.warmup, args.precision, cfg["seed"], rk,
+                        slowest, dims=cfg["dims"], native_data=True)
+    ek = r["edge_kernels"]
+    ms_ek = ek["fwd_ms_per_step"] + ek["bwd_ms_per_step"]
+    achieved = ek["bytes_per_step"] / (ms_ek / 1e3) / 1e9 if ms_ek else 0.0
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = reference_cpu_baseline(ds.graph, ds.labels, ds.mask, cfg["dims"], model="gat")
+    n_gpus = int(os.environ.get("WORLD_SIZE", "1"))
+    out = {"metric": GAT_METRIC, "value": r["value"], "unit": "GTEPS",
+           "n_gpus": n_gpus if n_gpus > 1 else args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": ("f32 edge softmax / aggregation, tf32 tcgen05 GEMMs (3xTF32 projections)"
+                     if args.precision == "tf32" else "f32"),
+           "data": "synthetic (seeded clustered power-law graph, random-init weights)",
+           "config": config, "e2e": r["e2e"],
+           "roofline": {"bound": "hbm", "kernel": "k_gat_dst / k_gat_src (edge softmax "
+                        "aggregation, forward + backward)", "achieved": achieved,
+                        "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
+                        "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                        "algorithmic_bytes_per_launch": ek["bytes_per_step"] / ek["launches_per_step"]
+                        if ek["launches_per_step"] else None,
+                        "share_of_step": ek["share_of_step"]},
+           "gemm": r["gemm"], "gpu_launches": r["gpu_launches"],
+           "gpu_launches_e2e": r["gpu_launches_e2e"], "cpu_baseline": cpu,
+           "clocks": clk.summary(), "losses": r["losses"]}
     return out
 
 
@@ -552,7 +636,7 @@ def reference_arm(args, cfg, n_gpus):
     t0 = time.time()
     graph, labels, mask = reference_graph(cfg)
     log(f"[bench-ref] graph {time.time() - t0:.1f}s |E|={graph.num_edges}")
-    rs = ReferenceSampler(graph, labels, mask, dims, seed=cfg["seed"])
+    rs = ReferenceSampler(graph, labels, mask, dims, seed=cfg["seed"], model=model_of(cfg))
     # numpy has nothing to warm beyond the first touch of the host arrays:
     # one warm-up sample (reported as executed) keeps the run to minutes
     warm = min(args.warmup, 1)
@@ -563,7 +647,8 @@ def reference_arm(args, cfg, n_gpus):
         dt, ne = rs.step()
         t, e = t + dt, e + ne
     v = e / t / 1e9
-    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GTEPS",
+    metric = GAT_METRIC if model_of(cfg) == "gat" else METRIC
+    out = {"impl": "reference", "metric": metric, "value": v, "unit": "GTEPS",
            "n_gpus": n_gpus, "steps": args.steps, "warmup": warm,
            "warmup_requested": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -633,6 +718,15 @@ def main():
 
     if args.profile_epoch:  # profiling aid: counters of whole epochs
         profile_epoch(args, cfg, ds, p, plan)
+        return
+    if model_of(cfg) == "gat":  # a GAT workload (cfg5s): its own contract line
+        out = gat_config_line(args, cfg, config, p, plan, ds, rk, slowest, hbm_peak, hbm_src)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
         return
     if args.only_value and args.kind == "gat":  # profiling aid
         r = gat_measure(p, plan, ds, args.steps, args.warmup, args.precision, cfg["seed"], rk,

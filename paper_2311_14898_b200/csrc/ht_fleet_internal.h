@@ -267,8 +267,26 @@ const float* hbm_inputs(ht_fleet* f, Device& d, int layer, const void* hin);
 
 using namespace htf;
 
+// Validation switches: each turns one optimisation off
+// to compare against the reference's association; read from the
+// environment once per epoch (ht_epoch_begin), never inside the layer loops
+struct Switches {
+  bool no_project_first = false, no_narrow_bwd = false, no_gat_direct = false;
+  bool no_direct_bwd = false, no_direct_read = false, no_recompute = false;
+  void read() {
+    auto on = [](const char* k) { const char* e = getenv(k); return e && *e && atoi(e) != 0; };
+    no_project_first = on("HT_NO_PROJECT_FIRST");
+    no_narrow_bwd = on("HT_NO_NARROW_BWD");
+    no_gat_direct = on("HT_NO_GAT_DIRECT");
+    no_direct_bwd = on("HT_NO_DIRECT_BWD");
+    no_direct_read = on("HT_NO_DIRECT_READ");
+    no_recompute = on("HT_NO_RECOMPUTE");
+  }
+};
+
 struct ht_fleet {
   int m = 0, n = 0, mode = HT_MODE_FULL, flush = HT_FLUSH_ON_EVICTION;
+  Switches sw;
   std::vector<Device> dev;
   std::vector<std::vector<HostSets>> sets;  // [i][j]
   bool finalized = false;
@@ -323,44 +341,6 @@ namespace htf {
 
 
 inline int64_t chunk_bound(int64_t V, int g) { return V * g / kChunks; }
-
-// Aggregation kernel variant: edges in flight per warp (U) and the
-// register cap (MINB resident CTAs per SM); HT_SEG_VARIANT selects one for
-// tuning runs, the default is the measured best.
-template <int NV>
-void seg_variant(int g, cudaStream_t s, float* out, const float* X, int64_t ldx, int d,
-                 const int64_t* off, const int32_t* idx, const float* w, int64_t nseg) {
-  static int v = [] {
-    const char* e = getenv("HT_SEG_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  static int v1 = [] {  // narrow rows (<= 128 floats): separate tuning knob
-    const char* e = getenv("HT_SEG_VARIANT1");
-    return e ? atoi(e) : 0;
-  }();
-  if (NV == 1) {
-    switch (v1) {
-      case 1: ht::k_seg_gather_v4<NV, 4, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
-      case 2: ht::k_seg_gather_v4<NV, 8, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
-      case 3: ht::k_seg_gather_v4<NV, 8, 6><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
-      case 4: ht::k_seg_gather_v4<NV, 16, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
-      case 5: ht::k_seg_gather_v4<NV, 4, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
-      case 6: ht::k_seg_gather_v4<NV, 8, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
-      case 7: ht::k_seg_gather_v4<NV, 2, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;
-      default: ht::k_seg_gather_v4<NV, 8, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); return;  // measured best (sweep, r1)
-    }
-  }
-  switch (v) {
-    case 1: ht::k_seg_gather_v4<NV, 4, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    case 2: ht::k_seg_gather_v4<NV, 8, 2><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    case 3: ht::k_seg_gather_v4<NV, 8, 3><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    case 4: ht::k_seg_gather_v4<NV, 4, 1><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    case 5: ht::k_seg_gather_v4<NV, 2, 6><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    case 6: ht::k_seg_gather_v4<NV, 1, 8><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    case 7: ht::k_seg_gather_v4<NV, 4, 5><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-    default: ht::k_seg_gather_v4<NV, 2, 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, w, nseg, kSplit); break;
-  }
-}
 
 template <bool TA, bool TB, int EPI>
 int gemm(cudaStream_t s, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,

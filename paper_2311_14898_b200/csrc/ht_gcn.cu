@@ -393,7 +393,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // d_out < d_in (K8 gathers d_out-wide rows instead of d_in-wide ones;
       // same product, reassociated).  Needs gz with zeroed pad columns.
       const bool no_in = f->lean && layer == 0;  // lean: grad_h^0 is not produced
-      const bool narrow = !no_in && HO && d_out < d_in && !getenv("HT_NO_NARROW_BWD");
+      const bool narrow = !no_in && HO && d_out < d_in && !f->sw.no_narrow_bwd;
       // project-first forward (agg^l never formed): the narrow-side rows
       // A^T gz give dW = h^T (A^T gz); needs them in row order (expanded CSR)
       const bool pfl = layer < (int)f->agg_deferred.size() && f->agg_deferred[layer] &&

@@ -308,7 +308,8 @@ int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t l
   } else if (d % 4 == 0 && d <= 512) {
     const int nv = (d / 4 + 31) / 32;
 #define SEGV(NV)                                                                               \
-  seg_variant<NV>(g, s, out, X, ldx, d, off, idx, w, nseg);                                \
+  ht::k_seg_gather_v4<NV, (NV == 1 ? 8 : 2), 4><<<g, kThreads, 0, s>>>(out, X, ldx, d, off, idx, \
+                                                                       w, nseg, kSplit);       \
   if (np) ht::k_seg_pieces_v4<NV><<<grid_for(np), kThreads, 0, s>>>(                           \
       partial, X, ldx, d, lo.as<int64_t>(), hi.as<int64_t>(), idx, w, np);
     switch (nv) {
@@ -599,7 +600,7 @@ const float* hbm_outputs(ht_fleet* f, Device& d, int j, int layer, int d_out,
 // owner-cache mirror when it is the identity map, or an HBM host store),
 // or nullptr.  The gathers then read it in place: no slot loads.
 const float* hbm_inputs(ht_fleet* f, Device& d, int layer, const void* hin) {
-  if (f->m != 1 || !d.chunks[0].csc_gid.p || getenv("HT_NO_DIRECT_READ")) return nullptr;
+  if (f->m != 1 || !d.chunks[0].csc_gid.p || f->sw.no_direct_read) return nullptr;
   if (d.cache && d.mcount == f->nrows && (d.mrows.empty() || d.mrows.back() == d.mcount - 1))
     return d.mh[layer].as<float>();
   if (is_dev_mem(hin)) return static_cast<const float*>(hin);
@@ -613,7 +614,7 @@ const float* hbm_inputs(ht_fleet* f, Device& d, int layer, const void* hin) {
 // is a store (GCN), or follows the destination-gradient add (GAT).
 bool direct_bwd(ht_fleet* f, Device& d) {
   return f->m == 1 && f->n == 1 && d.cache && d.chunks[0].nbr_gid.p && d.mcount == f->nrows &&
-         (d.mrows.empty() || d.mrows.back() == d.mcount - 1) && !getenv("HT_NO_DIRECT_BWD");
+         (d.mrows.empty() || d.mrows.back() == d.mcount - 1) && !f->sw.no_direct_bwd;
 }
 
 // GAT with one device, one batch and the identity-mapped mirror: N_ij is a
@@ -626,7 +627,7 @@ bool direct_bwd(ht_fleet* f, Device& d) {
 // the same sums in a different association than the staged path.
 bool gat_direct(ht_fleet* f, Device& d) {
   const DevChunk& c = d.chunks[0];
-  return !getenv("HT_NO_GAT_DIRECT") && direct_bwd(f, d) && c.bx_rows == d.mcount && c.nv == d.mcount && c.dest_m0 == 0;
+  return !f->sw.no_gat_direct && direct_bwd(f, d) && c.bx_rows == d.mcount && c.nv == d.mcount && c.dest_m0 == 0;
 }
 
 // Project-first GCN layer (d_out < d_in, one device, one batch, identity
@@ -639,7 +640,7 @@ bool project_first(ht_fleet* f, Device& d, int d_in, int d_out, int precision) {
   const DevChunk& c = d.chunks[0];
   return precision == HT_PREC_TF32 && d_out < d_in && f->ckpt_hbm && !f->gat &&
          direct_bwd(f, d) && c.bx_rows == d.mcount && c.nv == d.mcount && c.dest_m0 == 0 &&
-         !getenv("HT_NO_PROJECT_FIRST");
+         !f->sw.no_project_first;
 }
 
 // HBM owner cache: owned rows of a host array -> mirror (on `s`)
@@ -774,7 +775,7 @@ int plan_cache(ht_fleet* f, Device& d, int L, const int* dims, bool gat, int64_t
     d.cache = true;
     return HT_OK;
   }
-  const bool recompute_ok = !gat && one && !getenv("HT_NO_RECOMPUTE");
+  const bool recompute_ok = !gat && one && !f->sw.no_recompute;
   if (recompute_ok) {
     std::vector<int> order(L);
     std::iota(order.begin(), order.end(), 0);
@@ -805,6 +806,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
   if (!f->finalized) return fail(HT_ESTATE, "fleet not finalized");
   HT_TRY(check_chunks(f));
   HT_TRY(sync_all(f));
+  f->sw.read();
   f->L = L;
   f->dims.assign(dims, dims + L + 1);
   f->hptr.assign(L + 1, nullptr);
@@ -876,7 +878,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     // the slot value buffer: not needed when a single device's gathers read
     // the identity-mapped mirror in place (hbm_inputs)
     const bool direct = d.cache && f->m == 1 && d.chunks[0].csc_gid.p &&
-                        d.mcount == f->nrows && !getenv("HT_NO_DIRECT_READ");
+                        d.mcount == f->nrows && !f->sw.no_direct_read;
     if (!direct) HT_TRY(d.value.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
     if (!d.cache)
       for (int s = 0; s < 2; ++s) {

@@ -121,6 +121,24 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// shared -> global tensor store (TMA), bulk-group completion
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+      "r"(smem_u32(src)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -204,15 +222,18 @@ struct GemmCfg {
   static constexpr int STAGE = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
   static constexpr int STAGES = (200 * 1024 / STAGE) < 4 ? (200 * 1024 / STAGE) : 4;
   static constexpr int TX = A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;  // TMA bytes per stage
-  static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;  // per-warp 32x32 transpose tiles
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 256 + EPI_BYTES;
+  // epilogue staging: per warp two 32 x 32 swizzled tiles for the TMA
+  // stores (or one padded 32 x 33 transpose tile on the scalar-store path)
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + EPI_BYTES + 256;
 };
 
 template <int BN, bool SPLIT, int EPI>
 __global__ void __launch_bounds__(256, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
-              const __grid_constant__ CUtensorMap tmBl, int64_t M, int K, int N,
-              float* __restrict__ C, int64_t ldc, const float* __restrict__ G, int64_t ldg) {
+              const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmC,
+              int tma_store, int64_t M, int K, int N, float* __restrict__ C, int64_t ldc,
+              const float* __restrict__ G, int64_t ldg) {
   using Cfg = GemmCfg<BN, SPLIT>;
   constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -222,7 +243,8 @@ __global__ void __launch_bounds__(256, 1)
   auto sAlo = [&](int s) { return sA(s) + Cfg::A_BYTES; };
   auto sBh = [&](int s) { return sA(s) + (SPLIT ? 2 : 1) * Cfg::A_BYTES; };
   auto sBl = [&](int s) { return sBh(s) + Cfg::B_BYTES; };
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)ST * Cfg::STAGE);
+  uint8_t* epi = smem + (size_t)ST * Cfg::STAGE;  // 1024-aligned
+  uint64_t* bar = reinterpret_cast<uint64_t*>(epi + Cfg::EPI_BYTES);
   uint64_t* full = bar;            // [ST] TMA landed
   uint64_t* conv = bar + ST;       // [ST] converters done
   uint64_t* empty = bar + 2 * ST;  // [ST] MMAs done reading
@@ -313,11 +335,77 @@ __global__ void __launch_bounds__(256, 1)
         fence_proxy_async();
         mbar_arrive(&conv[s]);
       }
-  } else {  // ---------------- epilogue (warps 4-7) ----------------
-    // TMEM gives a thread one row; a padded 32x32 smem transpose turns that
-    // into row-contiguous 128-byte stores (and G loads) per warp instruction
+  } else if (tma_store) {  // ---------------- epilogue (warps 4-7), TMA stores ----------------
+    // TMEM gives a thread one row; each 32-column block goes to a 32 x 32
+    // SWIZZLE_128B smem tile (16-byte chunk j of row r at j ^ (r & 7):
+    // conflict-free float4 writes) and leaves with one TMA tensor store per
+    // warp; two tiles per warp so the next block is written while the
+    // previous store drains.  Rows >= M and columns >= N are clipped by TMA.
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
-    float* tile = reinterpret_cast<float*>(smem + (size_t)ST * Cfg::STAGE + 256) + q4 * 32 * 33;
+    float* tiles = reinterpret_cast<float*>(epi) + q4 * 2 * 32 * 32;
+    const bool g4 = (ldg & 3) == 0 && ((uintptr_t)G & 15) == 0;
+    int acc = 0, buf = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
+      const int a = acc & 1;
+      mbar_wait(&tfull[a], (acc >> 1) & 1);
+      tc_fence_after();
+      const int64_t r0 = t * 128 + q4 * 32;
+      const uint32_t base = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(a * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        if (c0 >= N) break;
+        float g[32];
+        if (EPI == TC_MASK) {  // this thread's row of the incoming gradient
+          const int64_t m = r0 + lane;
+#pragma unroll
+          for (int q = 0; q < 32; q += 4) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (m < M) {
+              if (c0 + q + 3 < N && g4) {
+                v = __ldg(reinterpret_cast<const float4*>(G + m * ldg + c0 + q));
+              } else {
+                v.x = c0 + q < N ? __ldg(G + m * ldg + c0 + q) : 0.f;
+                v.y = c0 + q + 1 < N ? __ldg(G + m * ldg + c0 + q + 1) : 0.f;
+                v.z = c0 + q + 2 < N ? __ldg(G + m * ldg + c0 + q + 2) : 0.f;
+                v.w = c0 + q + 3 < N ? __ldg(G + m * ldg + c0 + q + 3) : 0.f;
+              }
+            }
+            g[q] = v.x; g[q + 1] = v.y; g[q + 2] = v.z; g[q + 3] = v.w;
+          }
+        }
+        float v[32];
+        tmem_ld32(base + (uint32_t)c0, v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          if (EPI == TC_RELU) v[q] = v[q] > 0.f ? v[q] : 0.f;
+          if (EPI == TC_MASK) v[q] = v[q] > 0.f ? g[q] : 0.f;
+        }
+        if (lane == 0) bulk_wait_read<1>();  // the store that used this tile has read it
+        __syncwarp();
+        float* tile = tiles + buf * 32 * 32;
+        uint8_t* row = reinterpret_cast<uint8_t*>(tile) + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(row + ((j ^ (lane & 7)) << 4)) =
+              make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, tile, c0, (int)r0);
+          bulk_commit();
+        }
+        buf ^= 1;
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[a]);
+    }
+    if (lane == 0) bulk_wait_all();
+  } else {  // ---------------- epilogue (warps 4-7), scalar stores ----------------
+    // (C rows not 16-byte aligned, e.g. a 47-wide last layer) a padded 32x32
+    // smem transpose turns a thread's row into row-contiguous 128-byte
+    // stores (and G loads) per warp instruction
+    const int q4 = warp & 3;  // TMEM lane quarter this warp may access
+    float* tile = reinterpret_cast<float*>(epi) + q4 * 32 * 33;
     int acc = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
       const int a = acc & 1;
@@ -605,17 +693,25 @@ inline int launch_gemm_t(cudaStream_t s, const float* A, int64_t lda, int64_t M,
                   const float* Bl, int64_t ldb, int N, float* C, int64_t ldc, const float* G,
                   int64_t ldg) {
   using Cfg = GemmCfg<BN, SPLIT>;
-  CUtensorMap ta, tbh, tbl;
+  CUtensorMap ta, tbh, tbl, tc_;
   HT_TRY(tmap(&ta, A, M, K, lda, 32, 128, true));
   HT_TRY(tmap(&tbh, Bh, N, K, ldb, 32, BN, true));
   HT_TRY(tmap(&tbl, SPLIT ? Bl : Bh, N, K, ldb, 32, BN, true));
+  // TMA stores of the output when its rows are 16-byte aligned
+  static const bool no_tma_store = [] {
+    const char* e = getenv("HT_NO_TMA_STORE");
+    return e && atoi(e);
+  }();
+  const int use_tma = !no_tma_store && ((uintptr_t)C & 15) == 0 && (ldc & 3) == 0;
+  if (use_tma) HT_TRY(tmap(&tc_, C, M, N, ldc, 32, 32, true));
+  else tc_ = ta;  // (unused)
   auto kern = k_tc_gemm<BN, SPLIT, EPI>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
   if (e != cudaSuccess) return fail(HT_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
   const int64_t ntiles = (M + 127) / 128;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count()));
-  kern<<<grid, 256, Cfg::SMEM, s>>>(ta, tbh, tbl, M, K, N, C, ldc, G, ldg);
+  kern<<<grid, 256, Cfg::SMEM, s>>>(ta, tbh, tbl, tc_, use_tma, M, K, N, C, ldc, G, ldg);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HT_ECUDA, "k_tc_gemm launch: %s", cudaGetErrorString(e));
   return HT_OK;
