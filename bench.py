@@ -788,6 +788,26 @@ def main():
             log(f"[bench] dedup at scale (host planner) failed: {exc2}")
     pcie = pcie_peaks()
     pcie_bidir = pcie[2] if pcie else None
+    # PCIe bytes of one epoch from hardware counters (ncu app-range capture of
+    # this workload, profiles/r2_pcie_counters.json), the plan's bytes beside
+    pc_src = os.path.join("profiles", "r2_pcie_counters.json")
+    pc_e2e = pc_virt = None
+    try:
+        with open(os.path.join(ROOT, pc_src)) as fh:
+            pcj = json.load(fh)
+        if pcj.get("e2e", {}).get("config_id") == args.config and m == 1 and cached:
+            pc_e2e = pcj["e2e"]
+        if pcj.get("virt", {}).get("config_id") == args.config:
+            pc_virt = pcj["virt"]
+    except (OSError, ValueError):
+        pass
+    pcie_bytes = pc_e2e["pcie_bytes"] if pc_e2e else h2d + d2h
+    if virt and pc_virt:
+        vs = virt["ms_per_step"] / 1e3
+        virt["pcie_counter_bytes_per_step"] = pc_virt["pcie_bytes"]
+        virt["pcie_counter_gbs"] = pc_virt["pcie_bytes"] / vs / 1e9
+        virt["pcie_frac_of_bidir_peak"] = pc_virt["pcie_bytes"] / vs / 1e9 / pcie_bidir if pcie_bidir else None
+        virt["pcie_counter_file"] = pc_src
 
     # dominant kernel of the value run: the aggregation kernels (fwd CSC + bwd CSR)
     lf, msf, bf = val["stats"][0]
@@ -861,10 +881,15 @@ def main():
         "cpu_baseline": cpu,
         "roofline_pcie": {
             "bound": "pcie", "what": "all host<->GPU bytes of the e2e epoch / epoch time",
+            "source": "ncu" if pc_e2e else "plan",
+            "counter_bytes_per_step": pc_e2e["pcie_bytes"] if pc_e2e else None,
+            "counter_file": pc_src if pc_e2e else None,
+            "plan_bytes_per_step": h2d + d2h,
+            "plan_gbs": (h2d + d2h) / (ms_e / 1e3) / 1e9,
             "d2h_bound_frac": (d2h / (ms_e / 1e3) / 1e9) / pcie[1] if pcie else None,
-            "achieved": (h2d + d2h) / (ms_e / 1e3) / 1e9, "unit": "GB/s",
+            "achieved": pcie_bytes / (ms_e / 1e3) / 1e9, "unit": "GB/s",
             "peak": pcie_bidir, "peak_source": "measured (copy engines, both directions at once)",
-            "frac": ((h2d + d2h) / (ms_e / 1e3) / 1e9) / pcie_bidir if pcie_bidir else None,
+            "frac": (pcie_bytes / (ms_e / 1e3) / 1e9) / pcie_bidir if pcie_bidir else None,
             "peaks_gbs": {"h2d": pcie[0], "d2h": pcie[1], "bidir": pcie[2],
                           "zero_copy_read": pcie[3], "zero_copy_write": pcie[4]} if pcie else None},
         "dedup": dedup,
