@@ -477,7 +477,7 @@ def reference_cpu_baseline(graph, labels, mask, dims, steps=3, warmup=1, model="
 # ---------------------------------------------------------------------------
 def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, seed, rank=None,
                kind="gcn", features=None, labels=None, lean=False, checkpoints="auto",
-               cache="auto", profile=False):
+               cache="auto", profile=False, hbm_budget_gb=None):
     import paper_2311_14898_b200 as H
     from paper_2311_14898_b200 import _native as N
     dev = int(os.environ.get("LOCAL_RANK", "0")) % max(1, N.device_count()) if rank is not None else 0
@@ -490,7 +490,7 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     labels = ds.labels if labels is None else labels
     fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, precision=precision, rank=rank,
                           devices=[dev] if rank is not None else None, lean=lean,
-                          checkpoints=checkpoints, cache=cache)
+                          checkpoints=checkpoints, cache=cache, hbm_budget_gb=hbm_budget_gb)
     try:
         return _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind,
                              labels, profile)
@@ -528,7 +528,20 @@ def _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, k
     cache = fleet.cache_active
     ckpt_hbm = bool(host.agg.pending)
     return {"ms_total": ms.value, "wall_s": wall, "losses": losses, "launches": launches,
-            "stats": stats, "report": rep, "cache": cache, "ckpt_hbm": ckpt_hbm}
+            "stats": stats, "report": rep, "cache": cache, "ckpt_hbm": ckpt_hbm,
+            "recompute_layers": list(fleet.recompute_layers)}
+
+
+def hybrid_budget_gb(V, dims):
+    """An HBM budget (GB) for the recompute-cache hybrid on one device, one
+    batch: the h + grad mirrors, the project-first buffers, the narrowest agg
+    mirror and one scratch of the widest - the other agg mirrors do not fit
+    and share the scratch (their agg^l re-aggregated in the backward)."""
+    L = len(dims) - 1
+    base = 4 * V * (sum(dims[:L]) + sum(dims))
+    pw = max([(dims[l + 1] + 3) // 4 * 4 for l in range(L) if dims[l + 1] < dims[l]] or [0])
+    base += 2 * 4 * V * pw
+    return (base + 4 * V * (min(dims[:L]) + max(dims[:L])) + (1 << 20)) / 2 ** 30
 
 
 GAT_DIMS = [256, 128, 128, 64]  # it-2004 / config 5 widths (PAPER.md:79)
@@ -754,6 +767,13 @@ def main():
     e2e_hc = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,
                         False, cfg["seed"], rank=rk, checkpoints="host")
     ms_hc = slowest(e2e_hc["ms_total"]) / args.steps
+    # the recompute-cache hybrid under an HBM budget: the widest agg mirror
+    # does not fit, its agg^l is re-aggregated in the backward
+    bud = hybrid_budget_gb(ds.graph.num_vertices, dims)
+    e2e_b = None
+    if world == 1 and cfg["n"] == 1:
+        e2e_b = run_epochs(p, plan, ds, dims, "host", args.steps, args.warmup, args.precision,
+                           False, cfg["seed"], rank=rk, hbm_budget_gb=bud)
     gat = None
     if not args.no_gat:
         with Clocks(int(os.environ.get("LOCAL_RANK", "0"))) as clk_g:
@@ -868,6 +888,15 @@ def main():
             "h2d_bytes_per_step": hc_h2d, "d2h_bytes_per_step": hc_d2h,
             "what": "DeviceFleet(checkpoints='host'): agg checkpoints written through to "
                     "host.agg every epoch (the reference's host-side checkpoint cache)"},
+        "e2e_hbm_budget": {
+            "value": L * E / (e2e_b["ms_total"] / args.steps / 1e3) / 1e9, "unit": "GTEPS",
+            "ms_per_step": e2e_b["ms_total"] / args.steps, "hbm_budget_gb": bud,
+            "cache": bool(e2e_b["cache"]), "recompute_layers": e2e_b["recompute_layers"],
+            "what": "DeviceFleet(hbm_budget_gb=...): the owner cache under a budget that holds "
+                    "the h / grad mirrors, the narrowest agg mirror and one scratch - the other "
+                    "layers' agg^l re-aggregated in the backward from the h^l mirror (the "
+                    "recompute-cache hybrid; a project-first layer needs no agg^l)"}
+        if e2e_b else None,
         "epoch_s": {"hbm_resident": ms_v / 1e3, "host_resident": ms_e / 1e3},
         "host_gb_per_epoch": {"measured_path": (h2d + d2h) / 1e9,
                               "hbm_owner_cache": bool(cached),

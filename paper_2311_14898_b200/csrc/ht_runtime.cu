@@ -268,26 +268,10 @@ int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t l
     ht::SegWork wk{off, idx, w, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(),
                    pc.pf.as<int32_t>(), np, pc.seg.as<int64_t>(), pc.first.as<int64_t>(),
                    pc.cnt.as<int64_t>(), dv.work.as<unsigned>(), dv.work.as<int>() + 1, partial};
-    // wide rows: column slices of col_slice floats (HT_COL_SLICE; 0 = whole rows)
-    static const int col_slice = [] {
-      const char* e = getenv("HT_COL_SLICE");
-      const int v = e ? atoi(e) : 32;
-      return v == 32 || v == 64 ? v : 0;
-    }();
-    const int nsl = col_slice && d > 64 ? (d + col_slice - 1) / col_slice : 1;
-    const int64_t wbytes = ((int64_t)nsl * nf + 2) * 4;
-    if (dv.work.bytes < wbytes) return fail(HT_ESTATE, "work-list buffer not sized");
-    CU(cudaMemsetAsync(dv.work.p, 0, wbytes, s));  // counter + fixup tickets
+    if (dv.work.bytes < (nf + 2) * 4) return fail(HT_ESTATE, "work-list buffer not sized");
+    CU(cudaMemsetAsync(dv.work.p, 0, (nf + 2) * 4, s));  // counter + fixup tickets
     count_launch();
-    if (nsl > 1) {
-      if (col_slice == 32) {
-        auto k = ht::k_seg_work_cols<8, 8, 4, 4>;
-        k<<<resident_grid(k, (nseg + 3) / 4), kThreads, 0, s>>>(out, d, X, ldx, d, (int)nf, wk);
-      } else {
-        auto k = ht::k_seg_work_cols<16, 8, 4, 4>;
-        k<<<resident_grid(k, (nseg + 1) / 2), kThreads, 0, s>>>(out, d, X, ldx, d, (int)nf, wk);
-      }
-    } else if (d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
+    if (d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
       if (d <= 32) {
         auto k = ht::k_seg_work_sub<8, 8, 4, 4>;
         k<<<resident_grid(k, (nseg + 3) / 4), kThreads, 0, s>>>(out, X, ldx, d, wk);
@@ -865,7 +849,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     if (narrow_w)  // (the expanded CSR of one device / one batch has a row per host row)
       HT_TRY(d.tT.ensure(std::max<int64_t>(mn, f->m == 1 && f->n == 1 ? f->nrows : 0) * narrow_w * 4));
     HT_TRY(d.partial.ensure(np * dmax * 4));
-    HT_TRY(d.work.ensure((nf * ((dmax + 31) / 32) + 2) * 4));  // tickets per column slice
+    HT_TRY(d.work.ensure((nf + 2) * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
     // HBM owner cache: decided per epoch (requested mode, plan, free HBM).

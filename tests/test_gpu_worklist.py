@@ -1,4 +1,4 @@
-"""The one-launch work-list aggregation (whole rows or column slices) (k_seg_work_*: pieces of long
+"""The one-launch work-list aggregation (k_seg_work_*: pieces of long
 segments and short segments from one device counter, the last piece of a
 segment summing the partials in piece order) against r1's three-launch
 sequence (segment kernel, pieces kernel, fixup; HT_SEG_SPLIT_LAUNCH=1):
@@ -82,10 +82,8 @@ def _run(tmp_path, tag, env_extra, m, n, dims, prec):
                                            (2, 2, [64, 192, 40], "tf32"),
                                            (1, 1, [64, 384, 500, 40], "fp32")])
 def test_worklist_equals_split_launch(tmp_path, m, n, dims, prec):
+    a = _run(tmp_path, "work", {}, m, n, dims, prec)
     b = _run(tmp_path, "split", {"HT_SEG_SPLIT_LAUNCH": "1"}, m, n, dims, prec)
-    # whole rows, and wide rows (> 64 floats) in 32- / 64-float column slices
-    for cs in ("0", "32", "64"):
-        a = _run(tmp_path, f"work{cs}", {"HT_COL_SLICE": cs}, m, n, dims, prec)
-        assert sorted(a.files) == sorted(b.files)
-        for k in a.files:
-            np.testing.assert_array_equal(a[k], b[k], err_msg=f"slice {cs}: {k}")
+    assert sorted(a.files) == sorted(b.files)
+    for k in a.files:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
