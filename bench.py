@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes as C
+import gc
 import json
 import os
 import statistics
@@ -497,6 +498,8 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     finally:
         host.agg.pending.clear()  # nobody reads these checkpoints: nothing to materialize
         fleet.close()  # device memory back before the next measurement (also on failure)
+        del host, fleet  # an HBM store's arrays too (cfg4s needs the whole HBM per run)
+        gc.collect()
 
 
 def _timed_epochs(H, N, p, fleet, host, ds, dims, steps, warmup, timing, seed, kind, labels,

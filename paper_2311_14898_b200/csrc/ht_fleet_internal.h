@@ -232,7 +232,7 @@ struct Device {
   int64_t sgd_pin_cap = 0;
   // GAT staging (sized by ht_gat_epoch_begin): neighbour / destination
   // inputs, projections q / p, scores, backward rows and per-edge values
-  DBuf g_hn, g_hd[2], g_q, g_p, g_els, g_gs, g_gp, g_al, g_gt, g_sgt, g_gq, g_gts, g_ghd, g_gin[2];
+  DBuf g_hn, g_hd[2], g_q, g_p, g_els, g_gs, g_gp, g_al, g_sgt, g_gq, g_gts, g_ghd, g_gin[2];
   // gat_direct: each layer's projection p = h.W and el_src = p.a_src kept
   // from the forward for the backward (the recompute-cache hybrid sized to
   // HBM: the backward skips the recompute GEMM, bitwise the same values)

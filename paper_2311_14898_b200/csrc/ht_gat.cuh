@@ -14,6 +14,8 @@
 //                 g_t = alpha (g_alpha - sum alpha g_alpha) * LeakyReLU'(t),
 //                 writes gs rows, alpha / g_t per edge (CSC order), the
 //                 segment sum of g_t and the rank-1 gp_v = seg_gt_v * a_dst.
+//                 alpha / g_t are stored interleaved per edge ({alpha, g_t}
+//                 8-byte records in CSC order: AL = record base, GT = AL + 1).
 //   k_gat_src     BWD, one warp per source u over its CSR out-edges:
 //                 gq_u = sum_e (alpha_e gs_{dst e} + g_t_e a_src) in edge
 //                 order (the np.add.at of src/engine.py:275/280), and
@@ -164,9 +166,9 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (BWD && HO) {
       load4<NV>(acc, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
-      if (in0) AL[e0 + lane] = a0;
+      if (in0) AL[2 * (e0 + lane)] = a0;
       for (int64_t e = e0 + kW + lane; e < e1; e += kW)
-        AL[e] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
+        AL[2 * (e)] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
     }
     for (int64_t base = e0; base < ((BWD && HO) ? e0 : e1); base += kW) {
       const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
@@ -176,7 +178,7 @@ __global__ void __launch_bounds__(256) k_gat_dst(
         my_i = __ldg(idx + base + lane);
         my_a = expf(leaky(el_d + __ldg(el_src + my_i), slope) - mx) / den;
       }
-      if (BWD && lane < cnt) AL[base + lane] = my_a;
+      if (BWD && lane < cnt) AL[2 * (base + lane)] = my_a;
       int k = 0;
       if (!BWD && NV == 1 && d4 <= 16) {
         // rows of <= 64 floats: each half-warp loads one row, so one
@@ -288,8 +290,8 @@ __global__ void __launch_bounds__(256) k_gat_dst(
           g0 = my_g;
           sdot += a0 * my_g;
         } else {
-          GT[base + lane] = my_g;
-          sdot += AL[base + lane] * my_g;
+          GT[2 * (base + lane)] = my_g;
+          sdot += AL[2 * (base + lane)] * my_g;
         }
       }
     }
@@ -297,13 +299,13 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     float sgt = 0.f;
     if (in0) {
       const float gt = a0 * (g0 - sdot) * (t0 > 0.f ? 1.f : slope);
-      GT[e0 + lane] = gt;
+      GT[2 * (e0 + lane)] = gt;
       sgt = gt;
     }
     for (int64_t e = e0 + kW + lane; e < e1; e += kW) {
       const float t = el_d + __ldg(el_src + __ldg(idx + e));
-      const float gt = AL[e] * (GT[e] - sdot) * (t > 0.f ? 1.f : slope);
-      GT[e] = gt;
+      const float gt = AL[2 * (e)] * (GT[2 * (e)] - sdot) * (t > 0.f ? 1.f : slope);
+      GT[2 * (e)] = gt;
       sgt += gt;
     }
     sgt = warp_sum(sgt);
@@ -336,11 +338,12 @@ __device__ __forceinline__ void src_sum(float4 (&acc)[NV], float& gts, int64_t e
     const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
     int my_d = 0;
     float my_a = 0.f, my_t = 0.f;
-    if (lane < cnt) {
+    if (lane < cnt) {  // alpha and g_t of the edge: one 8-byte record (CSC order)
       my_d = __ldg(dst + base + lane);
       const int32_t pe = __ldg(perm + base + lane);
-      my_a = __ldg(AL + pe);
-      my_t = __ldg(GT + pe);
+      const float2 at = __ldg(reinterpret_cast<const float2*>(AL) + pe);
+      my_a = at.x;
+      my_t = at.y;
       gts += my_t;
     }
     int k = 0;

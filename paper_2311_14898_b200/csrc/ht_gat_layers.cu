@@ -342,8 +342,7 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
     HT_TRY(d.g_els.ensure(mn * 4));
     HT_TRY(d.g_gs.ensure(mv * dmax * 4));
     HT_TRY(d.g_gp.ensure(mv * dmax * 4));
-    HT_TRY(d.g_al.ensure(me * 4));
-    HT_TRY(d.g_gt.ensure(me * 4));
+    HT_TRY(d.g_al.ensure(me * 8));  // {alpha, g_t} records per edge
     HT_TRY(d.g_sgt.ensure(mv * 4));
     HT_TRY(d.g_gq.ensure(mn * dmax * 4));
     HT_TRY(d.g_gts.ensure(mn * 4));
@@ -456,7 +455,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
     HT_TRY(set_dev(d));
     if (!d.lw[layer].valid) HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
     HT_TRY(upload_attn(d, layer, A, d_out));
-    if (f->mode != HT_MODE_BASELINE)  // begin_backward_layer: zeroed gradient slots
+    if (f->mode != HT_MODE_BASELINE && !gat_direct(f, d))  // zeroed gradient slots
       CU(cudaMemsetAsync(d.grad.p, 0, d.cap * (int64_t)d_in * 4, d.stream));
     if (d.cache) CU(cudaMemsetAsync(d.mg[layer].p, 0, d.mcount * (int64_t)d_in * 4, d.stream));
   }
@@ -485,7 +484,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       float *P = dir ? d.g_pl[layer].as<float>() : d.g_p.as<float>(), *Q = dir ? P : d.g_q.as<float>();
       float* els = dir ? d.g_elsl[layer].as<float>() : d.g_els.as<float>();
       float *GS = d.g_gs.as<float>(), *GP = d.g_gp.as<float>(), *GQ = d.g_gq.as<float>();
-      float *AL = d.g_al.as<float>(), *GT = d.g_gt.as<float>();
+      float *AL = d.g_al.as<float>(), *GT = AL + 1;  // interleaved {alpha, g_t}
       TimerRec tg;
       timer_begin(f, d, tg, d.stream);
       if (!dir) HT_TRY(gat_proj(d, precision, HN, c.nn, d_in, d_out, Q, w));

@@ -839,10 +839,8 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     }
     // sized for 180 GB of HBM: the buffers every path needs first, then
     // either the owner-cache mirrors or the host-path staging sets
-    HT_TRY(d.grad.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
     HT_TRY(d.sc.ensure(mv * dmax * 4));
     HT_TRY(d.sd.ensure(mv * dmax * 4));
-    HT_TRY(d.se.ensure(mn * dmax * 4));
     int narrow_w = 0;  // widest d_out of the layers whose backward runs narrow-side
     for (int l = 0; l < L; ++l)
       if (dims[l + 1] < dims[l]) narrow_w = std::max(narrow_w, pad4(dims[l + 1]));
@@ -880,6 +878,12 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     const bool direct = d.cache && f->m == 1 && d.chunks[0].csc_gid.p &&
                         d.mcount == f->nrows && !f->sw.no_direct_read;
     if (!direct) HT_TRY(d.value.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
+    // slot gradients and neighbour-gradient views: not needed when one
+    // device's backward writes the grad mirror in place (cfg 4's share: 22 GB)
+    const bool dbwd = gat ? gat_direct(f, d) : direct_bwd(f, d);
+    const bool dviews = gat ? gat_direct(f, d) : direct_bwd(f, d) && d.chunks[0].bx_rows == d.mcount;
+    if (!dbwd) HT_TRY(d.grad.ensure(std::max<int64_t>(1, d.cap) * dmax * 4));
+    if (!dviews) HT_TRY(d.se.ensure(mn * dmax * 4));
     if (!d.cache)
       for (int s = 0; s < 2; ++s) {
         HT_TRY(d.fa[s].ensure(mv * dmax * 4));
