@@ -485,6 +485,8 @@ def run_epochs(p, plan, ds, dims, placement, steps, warmup, precision, timing, s
     # one process per GPU: a compact host store with only the rank's owned
     # rows (host memory per process ~ V/N; every host copy contiguous)
     rows = np.flatnonzero(plan.owner == rank) if rank is not None and placement == "host" else None
+    fr, tot = N.mem_info(dev)
+    log(f"[bench] {placement} store, {kind}: {fr / 2**30:.1f} of {tot / 2**30:.1f} GiB HBM free")
     host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement,
                        device=dev, rows=rows)
     host.set_features(ds.features if features is None else features)
@@ -841,13 +843,14 @@ def main():
     lt, mst, tb = e2e["stats"][3]
     traffic, traffic_src = None, None
     try:  # DRAM bytes per bracket from the committed ncu launch list of this workload
-        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as fh:
             tj = json.load(fh)
         if tj.get("config_id") == args.config and tj.get("m") == m:
             traffic, traffic_src = tj["dram_bytes_per_launch"], tj["source"]
     except (OSError, ValueError, KeyError):
         pass
-    roofline = {"bound": "hbm", "kernel": "k_seg_gather (CSC forward + CSR backward aggregation)",
+    roofline = {"bound": "hbm", "kernel": "k_seg_work_* (CSC forward + CSR backward aggregation "
+                "work lists)",
                 "achieved": achieved, "peak": hbm_peak, "peak_source": hbm_src, "unit": "GB/s",
                 "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
                 "traffic_source": traffic_src,
@@ -859,6 +862,12 @@ def main():
                 if traffic and lf + lb and hbm_peak else None,
                 "launches_per_step": (lf + lb) / args.steps,
                 "share_of_step": agg_ms / val["ms_total"] if val["ms_total"] else None}
+    tf32_peak = None
+    try:  # measured TF32 tensor-core ceiling (cuBLAS, profiles/tools/tf32_peak.py)
+        with open(os.path.join(ROOT, "profiles", "r2_tf32_rates_tma_epilogue.json")) as fh:
+            tf32_peak = float(json.load(fh)["cublas_tf32_tflops_8192"])
+    except (OSError, ValueError, KeyError):
+        pass
     cpu = None
     if not args.no_cpu_baseline:
         cpu = reference_cpu_baseline(ds.graph, ds.labels, ds.mask, dims)
@@ -909,7 +918,12 @@ def main():
         "gpu_launches_e2e": int(e2e["launches"]),
         "roofline": roofline,
         "gemm": {"ms_per_step": msg / args.steps, "tflops": flops / (msg / 1e3) / 1e12 if msg else None,
-                 "precision": args.precision},
+                 "precision": args.precision, "tf32_peak_tflops": tf32_peak,
+                 "tf32_peak_source": "cuBLAS TF32 8192^3 on this B200 (profiles/r2_tf32_rates_tma_epilogue.json)"
+                 if tf32_peak else None,
+                 "frac_of_tf32_peak": (flops / (msg / 1e3) / 1e12) / tf32_peak if msg and tf32_peak else None,
+                 "note": "useful 2*M*K*N flops (3xTF32 forward projections issue 3x the MMAs); "
+                         "the backward GEMMs are HBM-bound at these shapes"},
         "cpu_baseline": cpu,
         "roofline_pcie": {
             "bound": "pcie", "what": "all host<->GPU bytes of the e2e epoch / epoch time",

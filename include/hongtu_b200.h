@@ -340,6 +340,10 @@ int ht_gemm_rate(int op, int precision, int64_t M, int K, int N, int iters, doub
  * NVLink / DRAM counters of exactly that epoch (kernels and copy engines). */
 int ht_profile_range(int start);
 
+/* Free and total HBM of `device` in bytes (cudaMemGetInfo): sizing an
+ * hbm_budget for DeviceFleet, bench diagnostics. */
+int ht_mem_info(int device, int64_t* free_bytes, int64_t* total_bytes);
+
 #ifdef __cplusplus
 }
 #endif

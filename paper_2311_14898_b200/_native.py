@@ -103,6 +103,7 @@ _SIGS = {
     "ht_pcie_probe": (i32, [i32, i64, vp]),
     "ht_gemm_rate": (i32, [i32, i32, i64, i32, i32, i32, vp]),
     "ht_profile_range": (i32, [i32]),
+    "ht_mem_info": (i32, [i32, P_I64, P_I64]),
 }
 
 _lib = None
@@ -224,3 +225,10 @@ def staged(a: np.ndarray, dtype=None) -> np.ndarray:
     out = pinned_empty(a.shape, dtype)
     out[...] = a
     return out
+
+
+def mem_info(device: int = 0):
+    """(free, total) HBM bytes of a device."""
+    fr, tot = C.c_int64(0), C.c_int64(0)
+    call("ht_mem_info", device, C.byref(fr), C.byref(tot))
+    return int(fr.value), int(tot.value)

@@ -82,5 +82,38 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+def build_variant(name: str, defines: list) -> str:
+    """A same-box A/B build: every source compiled with extra ``-D`` flags
+    into ``build/<name>/`` and linked to ``lib/variants/<name>/`` (load it
+    with ``HT_LIB=<path>``).  Not part of the product build."""
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    odir = os.path.join(OBJ, name)
+    out = os.path.join(HERE, "lib", "variants", name, "libhongtu_b200.so")
+    os.makedirs(odir, exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    flags = [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        o = os.path.join(odir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc, *COMPILE_FLAGS, *flags, "-c", "-o", o, os.path.join(CSRC, src)]
+        return o, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for o, r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"variant {name}: nvcc failed on {o}")
+    res = subprocess.run([nvcc, *LINK_FLAGS, "-o", out, *[o for o, _ in results]],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"variant {name}: link failed")
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if len(sys.argv) > 2 and sys.argv[1] == "--variant":
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

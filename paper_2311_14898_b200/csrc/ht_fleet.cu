@@ -197,13 +197,13 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (auto& c : d.chunks) {
       for (auto* b : {&c.nbr_slot, &c.dest_rows, &c.csc_off, &c.csc_slot, &c.csc_w, &c.csr_off,
                       &c.csr_dst, &c.csr_w, &c.bx_off, &c.csc_loc, &c.csr_perm, &c.h2d_m,
-                      &c.flush_m})
+                      &c.flush_m, &c.csc_gid, &c.nbr_gid})
         b->release();
       for (Pieces* pc : {&c.fw, &c.bw, &c.bx}) pc->release();
-      for (CopyList* cl : {&c.h2d, &c.flush, &c.base_bwd})
+      for (CopyList* cl : {&c.h2d, &c.flush, &c.base_bwd, &c.dest})
         cl->src.release(), cl->dst.release(), cl->flag.release();
-      for (auto& cl : c.d2d) cl.src.release(), cl.dst.release();
-      for (auto& cl : c.push) cl.src.release(), cl.dst.release();
+      for (auto& cl : c.d2d) cl.src.release(), cl.dst.release(), cl.flag.release();
+      for (auto& cl : c.push) cl.src.release(), cl.dst.release(), cl.flag.release();
     }
     if (d.ev) cudaEventDestroy(d.ev);
     for (auto& e : d.mark)
@@ -231,7 +231,8 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (auto* v : {&d.mh, &d.ma, &d.mg})
       for (auto& b : *v) b.release();
     d.mrows_d.release();
-    for (DBuf* b : {&d.sgd_p, &d.sgd_w, &d.sgd_t, &d.pf_p, &d.pf_z}) b->release();
+    d.own.src.release(), d.own.dst.release(), d.own.flag.release();
+    for (DBuf* b : {&d.sgd_p, &d.sgd_w, &d.sgd_t, &d.pf_p, &d.pf_z, &d.tT, &d.agg_scr}) b->release();
     if (d.wpin) cudaFreeHost(d.wpin);
     if (d.lpin) cudaFreeHost(d.lpin);
     if (d.sgd_pin) cudaFreeHost(d.sgd_pin);
@@ -243,6 +244,7 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (cudaEvent_t e : d.e_ck)
       if (e) cudaEventDestroy(e);
   }
+  f->flag_ptrs.release();
   delete f;
   return HT_OK;
 }

@@ -123,6 +123,11 @@ __global__ void __launch_bounds__(256) k_rowdot(float* __restrict__ out, const f
 
 // One warp per destination segment of a chunk's CSC view.  `idx` are
 // chunk-local source ids (rows of Q / el_src), rows are d floats wide.
+// DU source rows in flight per warp in the row passes.
+#ifndef HT_GAT_DU
+#define HT_GAT_DU 4
+#endif
+constexpr int DU = HT_GAT_DU;
 template <int NV, bool BWD>
 __global__ void __launch_bounds__(256) k_gat_dst(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
@@ -207,17 +212,17 @@ __global__ void __launch_bounds__(256) k_gat_dst(
           }
         }
       }
-      for (; k + 4 <= cnt; k += 4) {  // four rows in flight
-        float4 x[4][NV];
-        float a[4];
+      for (; k + DU <= cnt; k += DU) {  // DU rows in flight
+        float4 x[DU][NV];
+        float a[DU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < DU; ++u) {
           const int s = __shfl_sync(0xffffffffu, my_i, k + u);
           a[u] = __shfl_sync(0xffffffffu, my_a, k + u);
           load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < DU; ++u)
 #pragma unroll
           for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a[u], x[u][t]);
       }
@@ -260,22 +265,22 @@ __global__ void __launch_bounds__(256) k_gat_dst(
       const int my_i = base == e0 ? i0 : (lane < cnt ? __ldg(idx + base + lane) : 0);
       float my_g = 0.f;
       int k = 0;
-      for (; k + 4 <= cnt; k += 4) {  // four rows in flight, four interleaved reductions
-        float4 x[4][NV];
+      for (; k + DU <= cnt; k += DU) {  // DU rows in flight, DU interleaved reductions
+        float4 x[DU][NV];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < DU; ++u) {
           const int s = __shfl_sync(0xffffffffu, my_i, k + u);
           load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
         }
-        float g[4];
+        float g[DU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) g[u] = dot4<NV>(gs, x[u]);
+        for (int u = 0; u < DU; ++u) g[u] = dot4<NV>(gs, x[u]);
 #pragma unroll
         for (int o = 16; o; o >>= 1)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) g[u] += __shfl_xor_sync(0xffffffffu, g[u], o);
+          for (int u = 0; u < DU; ++u) g[u] += __shfl_xor_sync(0xffffffffu, g[u], o);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < DU; ++u)
           if (lane == k + u) my_g = g[u];
       }
       for (; k < cnt; ++k) {

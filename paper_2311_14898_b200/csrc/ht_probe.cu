@@ -230,3 +230,15 @@ extern "C" int ht_gemm_rate(int op, int precision, int64_t M, int K, int N, int 
   cudaStreamDestroy(s);
   return rc;
 }
+
+// ---------------------------------------------------------------------------
+// Free / total HBM of a device (sizing an HBM budget; bench diagnostics)
+// ---------------------------------------------------------------------------
+extern "C" int ht_mem_info(int device, int64_t* free_bytes, int64_t* total_bytes) {
+  CU(cudaSetDevice(device));
+  size_t fr = 0, tot = 0;
+  CU(cudaMemGetInfo(&fr, &tot));
+  *free_bytes = (int64_t)fr;
+  *total_bytes = (int64_t)tot;
+  return HT_OK;
+}

@@ -1,13 +1,14 @@
 """DRAM traffic of the bench's dominant kernel class from an ncu launch list.
 
-    python profiles/make_traffic.py profiles/r1_value_epoch_launches.csv EPOCHS > profiles/r1_traffic.json
+    python profiles/make_traffic.py LAUNCHES.csv EPOCHS > profiles/r2_traffic.json
 
-The launch list is `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
-dram__bytes_write.sum,... --clock-control none --csv` of
-`bench.py --only-value --steps 1 --warmup 3` (EPOCHS = 4 value epochs).  The
-aggregation class (bench.py `roofline`) is the forward CSC + backward CSR
-segment gathers incl. their piece / fixup kernels; bench.py times it as L
-forward + L backward brackets per epoch, so the traffic per bracket is
+The launch list is `ncu --profile-from-start off --metrics gpu__time_duration.sum,
+dram__bytes_read.sum,dram__bytes_write.sum,... --clock-control none --csv` of
+`bench.py --profile-epoch value --steps 1 --warmup 2` (EPOCHS = 1: only the
+epoch inside the profiler range is captured).  The aggregation class
+(bench.py `roofline`) is the forward CSC + backward CSR work-list launches
+(r1: the segment gathers with their piece / fixup kernels); bench.py times it
+as L forward + L backward brackets per epoch, so the traffic per bracket is
 (DRAM read + write of those kernels) / (EPOCHS * 2 L).  bench.py reports it
 as `roofline.traffic` for the workload it was captured on.
 """
@@ -17,7 +18,7 @@ import json
 import re
 import sys
 
-AGG = re.compile(r"k_seg_(gather|pieces|fixup)")
+AGG = re.compile(r"k_seg_(work|gather|pieces|fixup)")
 
 
 def main(path, epochs, layers=3):
@@ -46,11 +47,12 @@ def main(path, epochs, layers=3):
             tot += v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)
             n += 1
     brackets = epochs * 2 * layers
-    print(json.dumps({"config_id": "cfg2", "m": 1, "kernel_class": "k_seg_gather/pieces/fixup (CSC fwd + CSR bwd)",
+    print(json.dumps({"config_id": "cfg2", "m": 1, "kernel_class": "k_seg_work_* (CSC fwd + CSR bwd work lists)",
                       "dram_bytes_per_launch": tot / brackets, "brackets": brackets,
                       "kernel_launches": n, "source": path,
-                      "capture": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum "
-                                 "--clock-control none, bench.py --only-value --steps 1 --warmup 3"},
+                      "capture": "ncu --profile-from-start off --metrics dram__bytes_read.sum,"
+                                 "dram__bytes_write.sum --clock-control none, bench.py "
+                                 "--profile-epoch value --steps 1 --warmup 2"},
                      indent=1))
 
 

@@ -87,3 +87,46 @@ def test_worklist_equals_split_launch(tmp_path, m, n, dims, prec):
     assert sorted(a.files) == sorted(b.files)
     for k in a.files:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+def test_forward_hub_pieces_reassociate_only_hub_rows():
+    """Forward CSC aggregation rows are the sequential multiply-then-add of
+    np.add.at (src/engine.py:139) bitwise - except destinations with more
+    than 1024 in-edges, whose pieces are summed separately and then added in
+    piece order: deterministic, within FP32 reassociation error of the
+    sequential sum (the oracle's association)."""
+    import paper_2311_14898_b200 as H
+    from paper_2311_14898_b200 import synth as S
+    from paper_2311_14898_b200.graph import dedup_edges
+    spec = S.SynthSpec(num_vertices=20000, avg_degree=12.0, seed=6)
+    src, dst, cl = S.synth_edges(spec)
+    rng = np.random.default_rng(3)
+    hubs = np.array([5, 777, 19999])
+    hs = np.concatenate([rng.choice(spec.num_vertices, 2500 * (k + 1), replace=False) for k in range(3)])
+    hd = np.repeat(hubs, [2500, 5000, 7500])
+    src, dst = np.concatenate([src, hs]), np.concatenate([dst, hd])
+    keep = dedup_edges(src, dst, spec.num_vertices)
+    g = H.from_edges(src[keep], dst[keep], num_vertices=spec.num_vertices)
+    X, y, mask = S.synth_node_data(spec.num_vertices, 32, 8, 6, cluster_of=cl)
+    p = H.split_chunks(g, H.partition_vertices(g, 1, seed=6), 1)
+    dims = [32, 16, 8]
+    host = H.HostStore(g.num_vertices, dims, dtype=np.float32, placement="device")
+    host.set_features(X)
+    fleet = H.DeviceFleet(H.plan_for_partition(p), dtype=np.float32)
+    H.train_epoch(p, fleet, H.init_model("gcn", dims, seed=2, dtype=np.float32), host, y, mask)
+    agg0 = np.array(host.agg[0])
+    fleet.close()
+    x32 = np.asarray(host.h[0])
+    w32 = np.asarray(g.edge_weights, dtype=np.float32)
+    off, srcs = g.csc_offsets, g.csc_sources
+    deg = np.diff(off)
+    assert (deg[hubs] > 1024).all() and np.sort(deg)[-4] <= 1024
+    sample = np.concatenate([hubs, rng.choice(g.num_vertices, 200, replace=False)])
+    for v in sample:
+        acc = np.zeros(dims[0], np.float32)
+        for e in range(off[v], off[v + 1]):
+            acc = acc + w32[e] * x32[srcs[e]]
+        if deg[v] > 1024:
+            assert np.abs(agg0[v] - acc).max() <= 1e-5 * max(np.abs(acc).max(), 1e-30), v
+        else:
+            np.testing.assert_array_equal(agg0[v], acc, err_msg=f"row {v}")
