@@ -221,7 +221,7 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (auto& w : d.lw)
       for (DBuf* b : {&w.W, &w.Wt, &w.Wp, &w.Wt_hi, &w.Wt_lo, &w.Wp_hi, &w.Wp_lo, &w.A}) b->release();
     for (DBuf* b : {&d.g_hn, &d.g_hd[0], &d.g_hd[1], &d.g_q, &d.g_p, &d.g_els, &d.g_gs, &d.g_gp,
-                    &d.g_al, &d.g_sgt, &d.g_gq, &d.g_gts, &d.g_ghd, &d.g_gin[0],
+                    &d.g_al, &d.g_sgt, &d.g_eld, &d.g_gq, &d.g_gts, &d.g_ghd, &d.g_gin[0],
                     &d.g_gin[1], &d.g_cpart, &d.g_pgts})
       b->release();
     for (auto* v : {&d.g_pl, &d.g_elsl})

@@ -232,7 +232,7 @@ struct Device {
   int64_t sgd_pin_cap = 0;
   // GAT staging (sized by ht_gat_epoch_begin): neighbour / destination
   // inputs, projections q / p, scores, backward rows and per-edge values
-  DBuf g_hn, g_hd[2], g_q, g_p, g_els, g_gs, g_gp, g_al, g_sgt, g_gq, g_gts, g_ghd, g_gin[2];
+  DBuf g_hn, g_hd[2], g_q, g_p, g_els, g_gs, g_gp, g_al, g_sgt, g_eld, g_gq, g_gts, g_ghd, g_gin[2];
   // gat_direct: each layer's projection p = h.W and el_src = p.a_src kept
   // from the forward for the backward (the recompute-cache hybrid sized to
   // HBM: the backward skips the recompute GEMM, bitwise the same values)
@@ -272,7 +272,7 @@ using namespace htf;
 // environment once per epoch (ht_epoch_begin), never inside the layer loops
 struct Switches {
   bool no_project_first = false, no_narrow_bwd = false, no_gat_direct = false;
-  bool no_direct_bwd = false, no_direct_read = false, no_recompute = false;
+  bool no_direct_bwd = false, no_direct_read = false, no_recompute = false, no_gat_split = false;
   void read() {
     auto on = [](const char* k) { const char* e = getenv(k); return e && *e && atoi(e) != 0; };
     no_project_first = on("HT_NO_PROJECT_FIRST");
@@ -281,6 +281,7 @@ struct Switches {
     no_direct_bwd = on("HT_NO_DIRECT_BWD");
     no_direct_read = on("HT_NO_DIRECT_READ");
     no_recompute = on("HT_NO_RECOMPUTE");
+    no_gat_split = on("HT_NO_GAT_SPLIT");
   }
 };
 

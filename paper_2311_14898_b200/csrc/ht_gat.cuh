@@ -471,6 +471,283 @@ static __global__ void __launch_bounds__(256) k_gat_src_fixup(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Split backward (the layer output h = ReLU(s) in HBM, so s's sign is known
+// without re-aggregating): ONE row gather per edge instead of two.
+//   A  (per destination)  alpha_e, gs_v = g_v (s_v > 0), el_d[v]
+//   S1 (per source, CSR)  gathers gs_v rows: g_alpha_e = gs_v . q_u (q_u in
+//                         registers) and A_u = sum_e alpha_e gs_v in edge order
+//   B  (per destination)  sdot_v, g_t_e, seg sum of g_t (scalars only)
+//   S2 (per source)       gts_u = sum_e g_t_e; gq_u = A_u + gts_u a_src
+// g_alpha, alpha, g_t, sdot, gts are the fused kernels' values bitwise; gq
+// is the same sum in a different association (A_u, then the a_src term).
+// Per-edge records {alpha, g_alpha -> g_t} in CSC order.
+// ---------------------------------------------------------------------------
+template <int NV>
+__global__ void __launch_bounds__(256) k_gat_bwd_a(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
+    const float* __restrict__ P, const float* __restrict__ el_src, const float* __restrict__ a_dst,
+    int d, float slope, const float* __restrict__ G, const float* __restrict__ HO,
+    const int64_t* __restrict__ ho_rows, float* __restrict__ GS, float* __restrict__ AL,
+    float* __restrict__ ELD) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  float4 ad[NV];
+  load4<NV>(ad, a_dst, d4, lane);
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nseg; v += nw) {
+    const int64_t e0 = off[v], e1 = off[v + 1];
+    float4 pv[NV], ho[NV], gv[NV];
+    load4<NV>(pv, P + v * (int64_t)d, d4, lane);
+    load4<NV>(ho, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
+    load4<NV>(gv, G + v * (int64_t)d, d4, lane);
+    const float el_d = warp_sum(dot4<NV>(pv, ad));
+    const int c0 = (e1 - e0) < (int64_t)kW ? (int)(e1 - e0) : kW;
+    const bool in0 = lane < c0;
+    const float t0 = in0 ? el_d + __ldg(el_src + __ldg(idx + e0 + lane)) : 0.f;
+    float mx = in0 ? leaky(t0, slope) : -CUDART_INF_F;
+    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+      mx = fmaxf(mx, leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope));
+    mx = warp_max(mx);
+    const float x0 = in0 ? expf(leaky(t0, slope) - mx) : 0.f;
+    float den = x0;
+    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+      den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
+    den = warp_sum(den);
+    if (in0) AL[2 * (e0 + lane)] = x0 / den;
+    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+      AL[2 * e] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {  // gs = g (s > 0), (s > 0) == (h > 0)
+      gv[t].x = ho[t].x > 0.f ? gv[t].x : 0.f;
+      gv[t].y = ho[t].y > 0.f ? gv[t].y : 0.f;
+      gv[t].z = ho[t].z > 0.f ? gv[t].z : 0.f;
+      gv[t].w = ho[t].w > 0.f ? gv[t].w : 0.f;
+    }
+    store4<NV>(GS + v * (int64_t)d, gv, d4, lane);
+    if (lane == 0) ELD[v] = el_d;
+  }
+}
+
+// S1 over CSR edges [e0, e1) of source u (one warp; q_u in registers):
+// A_u += alpha_e gs_v in edge order; g_alpha_e -> record .y
+template <int NV>
+__device__ __forceinline__ void src_rows_a(float4 (&acc)[NV], const float4 (&qu)[NV], int64_t e0,
+                                           int64_t e1, const int32_t* __restrict__ dst,
+                                           const int32_t* __restrict__ perm,
+                                           const float* __restrict__ GS, float* __restrict__ AL,
+                                           int d, int d4, int lane) {
+  for (int64_t base = e0; base < e1; base += kW) {
+    const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
+    int my_d = 0, my_p = 0;
+    float my_a = 0.f;
+    if (lane < cnt) {
+      my_d = __ldg(dst + base + lane);
+      my_p = __ldg(perm + base + lane);
+      my_a = AL[2 * (int64_t)my_p];  // (plain load: the record's .y is written in this kernel)
+    }
+    float my_g = 0.f;
+    int k = 0;
+    for (; k + SU <= cnt; k += SU) {
+      float4 x[SU][NV];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const int r = __shfl_sync(0xffffffffu, my_d, k + u);
+        load4<NV>(x[u], GS + (int64_t)r * d, d4, lane);
+      }
+      float g[SU];
+#pragma unroll
+      for (int u = 0; u < SU; ++u) {
+        const float a = __shfl_sync(0xffffffffu, my_a, k + u);
+#pragma unroll
+        for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a, x[u][t]);
+        g[u] = dot4<NV>(x[u], qu);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < SU; ++u) g[u] += __shfl_xor_sync(0xffffffffu, g[u], o);
+#pragma unroll
+      for (int u = 0; u < SU; ++u)
+        if (lane == k + u) my_g = g[u];
+    }
+    for (; k < cnt; ++k) {
+      const int r = __shfl_sync(0xffffffffu, my_d, k);
+      const float a = __shfl_sync(0xffffffffu, my_a, k);
+      float4 x[NV];
+      load4<NV>(x, GS + (int64_t)r * d, d4, lane);
+#pragma unroll
+      for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a, x[t]);
+      const float g = warp_sum(dot4<NV>(x, qu));
+      if (lane == k) my_g = g;
+    }
+    if (lane < cnt) AL[2 * (int64_t)my_p + 1] = my_g;
+  }
+}
+
+// S1: one warp per source segment (segments > split: k_gat_bwd_s1_pieces)
+template <int NV>
+__global__ void __launch_bounds__(256) k_gat_bwd_s1(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ dst,
+    const int32_t* __restrict__ perm, int64_t nseg, int64_t split, const float* __restrict__ GS,
+    const float* __restrict__ Q, const int32_t* __restrict__ qrow, float* __restrict__ AL, int d,
+    float* __restrict__ GQ) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nseg; u += nw) {
+    const int64_t e0 = off[u], e1 = off[u + 1];
+    if (e1 - e0 > split) continue;
+    float4 acc[NV], qu[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e1 > e0) load4<NV>(qu, Q + (int64_t)(qrow ? qrow[u] : (int32_t)u) * d, d4, lane);
+    src_rows_a<NV>(acc, qu, e0, e1, dst, perm, GS, AL, d, d4, lane);
+    store4<NV>(GQ + u * (int64_t)d, acc, d4, lane);
+  }
+}
+
+// S1 pieces [lo, hi) of long source segments (seg[pf] gives the source)
+template <int NV>
+__global__ void __launch_bounds__(256) k_gat_bwd_s1_pieces(
+    const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, const int32_t* __restrict__ pf,
+    const int64_t* __restrict__ fseg, int64_t np, const int32_t* __restrict__ dst,
+    const int32_t* __restrict__ perm, const float* __restrict__ GS, const float* __restrict__ Q,
+    const int32_t* __restrict__ qrow, float* __restrict__ AL, int d, float* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < np; q += nw) {
+    const int64_t u = fseg[pf[q]];
+    float4 acc[NV], qu[NV];
+#pragma unroll
+    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    load4<NV>(qu, Q + (int64_t)(qrow ? qrow[u] : (int32_t)u) * d, d4, lane);
+    src_rows_a<NV>(acc, qu, lo[q], hi[q], dst, perm, GS, AL, d, d4, lane);
+    store4<NV>(part + q * (int64_t)d, acc, d4, lane);
+  }
+}
+
+// B: per destination, scalars only: sdot_v = sum alpha_e g_alpha_e (lane
+// partial sums, then the warp sum: the fused kernel's association), g_t_e
+// into record .y, sgt_v = seg sum of g_t, optionally gp_v = sgt_v a_dst
+template <int NV>
+__global__ void __launch_bounds__(256) k_gat_bwd_b(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
+    const float* __restrict__ el_src, const float* __restrict__ ELD, float slope,
+    float* __restrict__ AL, float* __restrict__ SGT, float* __restrict__ GP,
+    const float* __restrict__ a_dst, int d) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nseg; v += nw) {
+    const int64_t e0 = off[v], e1 = off[v + 1];
+    const float el_d = ELD[v];
+    float sdot = 0.f;
+    for (int64_t e = e0 + lane; e < e1; e += kW) {
+      const float2 r = *reinterpret_cast<const float2*>(AL + 2 * e);
+      sdot += r.x * r.y;
+    }
+    sdot = warp_sum(sdot);
+    float sgt = 0.f;
+    for (int64_t e = e0 + lane; e < e1; e += kW) {
+      float2 r = *reinterpret_cast<float2*>(AL + 2 * e);
+      const float t = el_d + __ldg(el_src + __ldg(idx + e));
+      const float gt = r.x * (r.y - sdot) * (t > 0.f ? 1.f : slope);
+      AL[2 * e + 1] = gt;
+      sgt += gt;
+    }
+    sgt = warp_sum(sgt);
+    if (lane == 0) SGT[v] = sgt;
+    if (GP) {
+      float4 ad[NV], gp[NV];
+      load4<NV>(ad, a_dst, d4, lane);
+#pragma unroll
+      for (int t = 0; t < NV; ++t)
+        gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
+      store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+    }
+  }
+}
+
+// S2: gts_u = sum of the g_t of u's out-edges (lane partial sums in edge
+// order, then the warp sum - the fused kernel's association); hubs in
+// pieces (partial gts, then summed in piece order by the last piece of
+// the segment: atomic ticket).  gq_u = A_u + gts_u a_src (+ sgt_u a_dst
+// when the destination term is folded in).
+template <int NV>
+__device__ __forceinline__ void s2_finish(float* __restrict__ GQ, float* __restrict__ GTS,
+                                          int64_t u, float gts, const float* __restrict__ a_src,
+                                          const float* __restrict__ sgt_add,
+                                          const float* __restrict__ a_dst, int d, int d4, int lane) {
+  float4 acc[NV], as[NV];
+  load4<NV>(acc, GQ + u * (int64_t)d, d4, lane);
+  load4<NV>(as, a_src, d4, lane);
+  const float g = sgt_add ? __ldg(sgt_add + u) : 0.f;
+#pragma unroll
+  for (int t = 0; t < NV; ++t) {
+    acc[t].x += gts * as[t].x;
+    acc[t].y += gts * as[t].y;
+    acc[t].z += gts * as[t].z;
+    acc[t].w += gts * as[t].w;
+  }
+  if (sgt_add) {
+    float4 ad[NV];
+    load4<NV>(ad, a_dst, d4, lane);
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      acc[t].x += g * ad[t].x;
+      acc[t].y += g * ad[t].y;
+      acc[t].z += g * ad[t].z;
+      acc[t].w += g * ad[t].w;
+    }
+  }
+  store4<NV>(GQ + u * (int64_t)d, acc, d4, lane);
+  if (lane == 0) GTS[u] = gts;
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256) k_gat_bwd_s2(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ perm, int64_t nseg,
+    int64_t split, const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
+    const int32_t* __restrict__ pf, const int64_t* __restrict__ fseg,
+    const int64_t* __restrict__ ffirst, const int64_t* __restrict__ fcnt, int64_t np,
+    int* __restrict__ tickets, float* __restrict__ pgts, const float* __restrict__ AL,
+    const float* __restrict__ a_src, const float* __restrict__ sgt_add,
+    const float* __restrict__ a_dst, int d, float* __restrict__ GQ, float* __restrict__ GTS) {
+  const int lane = threadIdx.x & 31;
+  const int d4 = d >> 2;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < np + nseg; w += nw) {
+    if (w < np) {  // a piece of a hub source
+      float gts = 0.f;
+      for (int64_t e = lo[w] + lane; e < hi[w]; e += kW) gts += __ldg(AL + 2 * (int64_t)__ldg(perm + e) + 1);
+      gts = warp_sum(gts);
+      if (lane == 0) pgts[w] = gts;
+      __threadfence();
+      __syncwarp();
+      const int f = pf[w];
+      int last = 0;
+      if (lane == 0) last = atomicAdd(tickets + f, 1) == (int)fcnt[f] - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        __threadfence();
+        float s = 0.f;
+        for (int64_t q = 0; q < fcnt[f]; ++q) s += __ldcg(pgts + ffirst[f] + q);
+        s2_finish<NV>(GQ, GTS, fseg[f], s, a_src, sgt_add, a_dst, d, d4, lane);
+      }
+      continue;
+    }
+    const int64_t u = w - np;
+    const int64_t e0 = off[u], e1 = off[u + 1];
+    if (e1 - e0 > split) continue;
+    float gts = 0.f;
+    for (int64_t e = e0 + lane; e < e1; e += kW) gts += __ldg(AL + 2 * (int64_t)__ldg(perm + e) + 1);
+    gts = warp_sum(gts);
+    s2_finish<NV>(GQ, GTS, u, gts, a_src, sgt_add, a_dst, d, d4, lane);
+  }
+}
+
 // partial[b][c] = sum over block b's rows r of w[r] * X[r][c]: warps take
 // rows, lanes float4 columns, the block's 8 warp sums combined in shared
 // memory in warp order (deterministic)

@@ -71,6 +71,60 @@ int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const floa
   return HT_OK;
 }
 
+// Split backward (k_gat_bwd_a / s1 / b / s2, ht_gat.cuh) when the layer
+// output is in HBM: one row gather per edge instead of two.  AL: per-edge
+// {alpha, g_alpha -> g_t} records; GQ receives gq; ELD, SGT, GTS scalars.
+int launch_gat_bwd_split(cudaStream_t s, Device& dv, const DevChunk& c, const float* Q,
+                         const float* P, const float* els, const float* a_dst, const float* a_src,
+                         int d, float slope, const float* G, const float* HO,
+                         const int64_t* ho_rows, float* GS, float* GP, float* AL, float* ELD,
+                         float* SGT, float* GQ, float* GTS, float* part, float* pgts,
+                         bool expanded, const float* sgt_add) {
+  const int64_t* coff = c.csc_off.as<int64_t>();
+  const int32_t* cidx = expanded ? c.csc_gid.as<int32_t>() : c.csc_loc.as<int32_t>();
+  const Pieces& pc = expanded ? c.bx : c.bw;
+  const int64_t nseg = expanded ? c.bx_rows : c.nn;
+  const int64_t* roff = expanded ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>();
+  const int32_t* dst = c.csr_dst.as<int32_t>();
+  const int32_t* perm = c.csr_perm.as<int32_t>();
+  const int gv = grid_for(std::max<int64_t>(1, c.nv)), gs = grid_for(std::max<int64_t>(1, nseg));
+  if (dv.work.bytes < (pc.nf + 2) * 4) return fail(HT_ESTATE, "work buffer not sized");
+  CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s));  // S2 tickets
+  count_launch(4 + (pc.np ? 2 : 0));
+#define GATB(NV)                                                                                   \
+  if (c.nv > 0)                                                                                    \
+    ht::gat::k_gat_bwd_a<NV><<<gv, kThreads, 0, s>>>(coff, cidx, c.nv, P, els, a_dst, d, slope, G,  \
+                                                     HO, ho_rows, GS, AL, ELD);                    \
+  if (nseg > 0)                                                                                    \
+    ht::gat::k_gat_bwd_s1<NV><<<gs, kThreads, 0, s>>>(roff, dst, perm, nseg, kSplit, GS, Q,         \
+                                                      nullptr, AL, d, GQ);                          \
+  if (pc.np) {                                                                                     \
+    ht::gat::k_gat_bwd_s1_pieces<NV><<<grid_for(pc.np), kThreads, 0, s>>>(                         \
+        pc.lo.as<int64_t>(), pc.hi.as<int64_t>(), pc.pf.as<int32_t>(), pc.seg.as<int64_t>(),       \
+        pc.np, dst, perm, GS, Q, nullptr, AL, d, part);                                            \
+    ht::k_seg_fixup<<<grid_for(pc.nf), kThreads, 0, s>>>(GQ, part, d, pc.seg.as<int64_t>(),       \
+                                                          pc.first.as<int64_t>(),                  \
+                                                          pc.cnt.as<int64_t>(), pc.nf);            \
+  }                                                                                                \
+  if (c.nv > 0)                                                                                    \
+    ht::gat::k_gat_bwd_b<NV><<<gv, kThreads, 0, s>>>(coff, cidx, c.nv, els, ELD, slope, AL, SGT,    \
+                                                     GP, a_dst, d);                                \
+  if (nseg > 0)                                                                                    \
+    ht::gat::k_gat_bwd_s2<NV><<<grid_for(nseg + pc.np), kThreads, 0, s>>>(                         \
+        roff, perm, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(), pc.pf.as<int32_t>(),   \
+        pc.seg.as<int64_t>(), pc.first.as<int64_t>(), pc.cnt.as<int64_t>(), pc.np,                 \
+        dv.work.as<int>() + 1, pgts, AL, a_src, sgt_add, a_dst, d, GQ, GTS)
+  switch (nv_of(d)) {
+    case 1: GATB(1); break;
+    case 2: GATB(2); break;
+    case 3: GATB(3); break;
+    default: GATB(4); break;
+  }
+#undef GATB
+  CU(cudaGetLastError());
+  return HT_OK;
+}
+
 int launch_gat_src(cudaStream_t s, const DevChunk& c, const float* GS, const float* AL,
                    const float* GT, const float* a_src, int d, float* GQ, float* GTS, float* part,
                    float* pgts, bool expanded = false, const float* sgt_add = nullptr,
@@ -344,6 +398,7 @@ extern "C" int ht_gat_epoch_begin(ht_fleet* f, int L, const int* dims) {
     HT_TRY(d.g_gp.ensure(mv * dmax * 4));
     HT_TRY(d.g_al.ensure(me * 8));  // {alpha, g_t} records per edge
     HT_TRY(d.g_sgt.ensure(mv * 4));
+    HT_TRY(d.g_eld.ensure(mv * 4));
     HT_TRY(d.g_gq.ensure(mn * dmax * 4));
     HT_TRY(d.g_gts.ensure(mn * 4));
     HT_TRY(d.g_ghd.ensure(mv * dmax * 4));
@@ -498,15 +553,32 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
       // direct: gp_v = sgt_v a_dst (rank 1) is added into gq_v by the CSR pass
       // (rows are the same vertices), so dW and the input gradients take one
       // GEMM each over gq + gp instead of two plus an add
-      HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, els, a_dst, d_out, slope,
-                                  nullptr, Gin, GS, dir ? nullptr : GP, AL, GT, d.g_sgt.as<float>(),
-                                  HO, hrows, dir));
-      HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
-                            d.partial.as<float>(), d.g_pgts.as<float>(), dir,
-                            dir ? d.g_sgt.as<float>() : nullptr, a_dst));
+      const bool split = HO && !f->sw.no_gat_split;
+      if (split) {  // one row gather per edge (the h^{l+1} sign is in HBM)
+        HT_TRY(launch_gat_bwd_split(d.stream, d, c, Q, P, els, a_dst, a_src, d_out, slope, Gin, HO,
+                                    hrows, GS, dir ? nullptr : GP, AL, d.g_eld.as<float>(),
+                                    d.g_sgt.as<float>(), GQ, d.g_gts.as<float>(),
+                                    d.partial.as<float>(), d.g_pgts.as<float>(), dir,
+                                    dir ? d.g_sgt.as<float>() : nullptr));
+      } else {
+        HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, els, a_dst, d_out, slope,
+                                    nullptr, Gin, GS, dir ? nullptr : GP, AL, GT, d.g_sgt.as<float>(),
+                                    HO, hrows, dir));
+        HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
+                              d.partial.as<float>(), d.g_pgts.as<float>(), dir,
+                              dir ? d.g_sgt.as<float>() : nullptr, a_dst));
+      }
+      const int64_t nsrc = dir ? c.bx_rows : c.nn;
+      // algorithmic bytes: split - per edge one gs row + 14 index / scalar
+      // words; per destination p, h, g rows in, gs (+ gp) out; per source q
+      // row in, gq out + read-modify-write.  Fused - per edge q and gs rows
+      // (+ the recomputed sum without h in HBM)
       timer_end(f, d, tr, 1,
-                (double)c.ne * (28.0 + 12.0 * d_out) + (double)c.nv * (16.0 * d_out + 16.0) +
-                    (double)c.nn * (4.0 * d_out + 12.0),
+                split ? (double)c.ne * (56.0 + 4.0 * d_out) +
+                            (double)c.nv * ((dir ? 16.0 : 20.0) * d_out + 12.0) +
+                            (double)nsrc * (16.0 * d_out + 8.0)
+                      : (double)c.ne * (28.0 + 12.0 * d_out) + (double)c.nv * (16.0 * d_out + 16.0) +
+                            (double)c.nn * (4.0 * d_out + 12.0),
                 d.stream);
       // attention gradients: a_dst <- sum_v seg_gt_v p_v, a_src <- sum_u gts_u q_u
       float* gA = d.gWall.as<float>() + d.gW_off[f->L] + d.gA_off[layer];

@@ -157,3 +157,39 @@ def test_gat_width_must_be_multiple_of_four(golden_small):
     fleet = H.DeviceFleet(plan, dtype=np.float32, precision="fp32")
     with pytest.raises(H.ChunktrainError, match="multiples of 4"):
         H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 2)])
+def test_gat_split_backward_equals_fused(m, n, monkeypatch):
+    """With h^{l+1} in HBM the backward runs split (one row gather per edge:
+    g_alpha and sum alpha gs_v from the CSR pass, scalars per destination,
+    then gq = A_u + gts_u a_src) instead of the fused two-gather pass
+    (HT_NO_GAT_SPLIT=1).  alpha, g_t, their segment sums - hence the
+    attention gradients and the loss - are bitwise the same; gq and what
+    depends on it (dW, the input gradients) only reassociate."""
+    rng = np.random.default_rng(11)
+    V = 5000
+    src = np.concatenate([np.full(3000, 3, np.int64), rng.integers(0, V, 30000)])
+    dst = np.concatenate([rng.integers(0, V, 3000), rng.integers(0, V, 30000)])
+    g = H.from_edges(src, dst, V)
+    X = rng.standard_normal((V, 16))
+    ds = H.SynthDataset(graph=g, features=X, labels=rng.integers(0, 8, V), mask=rng.random(V) < 0.5)
+    a = H.PartitionAssignment(owner=(np.arange(V) % m).astype(np.int64), m=m)
+    p = H.split_chunks(g, a, n)
+    dims = [16, 24, 8]
+    out = {}
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("HT_NO_GAT_SPLIT", flag)
+        else:
+            monkeypatch.delenv("HT_NO_GAT_SPLIT", raising=False)
+        losses, snaps, fleet, _ = _run(p, ds, dims, epochs=1)
+        assert fleet.cache_active
+        out[flag] = (losses, snaps[0])
+        fleet.close()
+    (la, a_), (lb, b_) = out["1"], out[None]
+    assert la == lb
+    for l in range(2):
+        np.testing.assert_array_equal(a_["attn_grads"][l], b_["attn_grads"][l])
+        assert O.rel_err(b_["grads"][l], a_["grads"][l]) < 1e-6
+    assert O.rel_err(b_["gh0"], a_["gh0"]) < 1e-6
