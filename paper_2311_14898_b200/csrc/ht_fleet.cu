@@ -249,6 +249,10 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
   return HT_OK;
 }
 
+static void release_lists(std::vector<CopyList>& v) {
+  for (auto& cl : v) cl.src.release(), cl.dst.release(), cl.flag.release();
+}
+
 static std::vector<int64_t> vec(const int64_t* p, int64_t n) {
   return n > 0 ? std::vector<int64_t>(p, p + n) : std::vector<int64_t>();
 }
@@ -342,6 +346,7 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         HT_TRY(lookup_slots(h, rows, b, i, j));
         HT_TRY(upload_list(c.h2d, rows, b, s));
         make_runs(c.h2d, rows, b, nullptr);
+        release_lists(c.d2d);  // (a re-finalize: free the previous lists)
         c.d2d.assign(m, CopyList());
         for (int st = 1; st < m; ++st) {
           const int k = (i + st) % m;
@@ -472,6 +477,7 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
         cudaStream_t s = d.stream;
         DevChunk& c = d.chunks[j];
         HostSets& hk = f->sets[k][j];
+        release_lists(c.push);
         c.push.assign(m, CopyList());
         for (int i = 0; i < m; ++i) {
           HostSets& hi = f->sets[i][j];

@@ -62,7 +62,16 @@ struct DBuf {
     p = nullptr;
     bytes = 0;
     if (want <= 0) return HT_OK;
-    CU(cudaMalloc(&p, want));
+    const cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      return fail(e == cudaErrorMemoryAllocation ? HT_ENOMEM : HT_ECUDA,
+                  "cudaMalloc of %lld bytes failed: %s (%lld of %lld bytes free)", (long long)want,
+                  cudaGetErrorString(e), (long long)fr, (long long)tot);
+    }
     bytes = want;
     return HT_OK;
   }

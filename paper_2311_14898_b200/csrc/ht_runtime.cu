@@ -771,6 +771,10 @@ int plan_cache(ht_fleet* f, Device& d, int L, const int* dims, bool gat, int64_t
   int64_t agg_all = 0;
   if (!gat)
     for (int l = 0; l < L; ++l) agg_all += R * dims[l] * 4;
+  if (getenv("HT_TRACE_CACHE"))
+    fprintf(stderr, "[ht] owner cache plan: mirrors+buffers %.2f GB, agg %.2f GB, available %.2f GB "
+                    "(free %.2f GB, budget %.2f GB)\n", base / 1e9, agg_all / 1e9, avail / 1e9,
+            fr / 1e9, f->hbm_budget / 1e9);
   if (base + agg_all <= avail) {
     d.cache = true;
     return HT_OK;
