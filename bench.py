@@ -227,6 +227,15 @@ def profile_epoch(args, cfg, ds, p, plan):
         out = {"mode": mode, "planned_host_gb_per_step": r["planned_host_gb_per_step"],
                "metered_host_gb_per_step": r["metered_host_gb_per_step"],
                "metered_peer_gb_per_step": r["metered_peer_gb_per_step"]}
+    elif args.kind == "gat" or model_of(cfg) == "gat":  # GAT epochs (profiling)
+        gd = cfg["dims"] if model_of(cfg) == "gat" else GAT_DIMS
+        X = ds.features if model_of(cfg) == "gat" else np.random.default_rng(cfg["seed"]).standard_normal(
+            (ds.graph.num_vertices, gd[0]), dtype=np.float32)
+        y = (np.asarray(ds.labels) % gd[-1]).astype(np.int64)
+        r = run_epochs(p, plan, ds, gd, "device" if mode == "value" else "host", args.steps,
+                       args.warmup, args.precision, False, cfg["seed"], kind="gat", features=X,
+                       labels=y, profile=True)
+        out = {"mode": mode, "kind": "gat"}
     else:
         placement = "device" if mode == "value" else "host"
         r = run_epochs(p, plan, ds, dims, placement, args.steps, args.warmup, args.precision,

@@ -766,15 +766,22 @@ int plan_cache(ht_fleet* f, Device& d, int L, const int* dims, bool gat, int64_t
   }
   size_t fr = 0, tot = 0;
   CU(cudaMemGetInfo(&fr, &tot));
-  int64_t avail = (int64_t)fr - ((int64_t)4 << 30);
+  // the previous epoch's mirrors / scratch / project-first buffers are
+  // reused (grow-only): they count as available
+  int64_t held = 0;
+  for (auto* v : {&d.mh, &d.ma, &d.mg})
+    for (auto& b : *v)
+      if (!b.alias) held += b.bytes;
+  for (DBuf* b : {&d.agg_scr, &d.pf_p, &d.pf_z}) held += b->bytes;
+  int64_t avail = (int64_t)fr + held - ((int64_t)4 << 30);
   if (f->hbm_budget > 0) avail = std::min(avail, f->hbm_budget);
   int64_t agg_all = 0;
   if (!gat)
     for (int l = 0; l < L; ++l) agg_all += R * dims[l] * 4;
   if (getenv("HT_TRACE_CACHE"))
     fprintf(stderr, "[ht] owner cache plan: mirrors+buffers %.2f GB, agg %.2f GB, available %.2f GB "
-                    "(free %.2f GB, budget %.2f GB)\n", base / 1e9, agg_all / 1e9, avail / 1e9,
-            fr / 1e9, f->hbm_budget / 1e9);
+                    "(free %.2f GB + held %.2f GB, budget %.2f GB)\n", base / 1e9, agg_all / 1e9,
+            avail / 1e9, fr / 1e9, held / 1e9, f->hbm_budget / 1e9);
   if (base + agg_all <= avail) {
     d.cache = true;
     return HT_OK;
@@ -803,6 +810,9 @@ int plan_cache(ht_fleet* f, Device& d, int L, const int* dims, bool gat, int64_t
     return fail(HT_ENOMEM, "HBM owner cache needs %lld bytes (%lld with recompute), %lld available",
                 (long long)(base + agg_all), (long long)base, (long long)avail);
   d.cache = false;
+  for (auto* v : {&d.mh, &d.ma, &d.mg})  // room for the host-path staging
+    for (auto& b : *v) b.release();
+  d.agg_scr.release();
   return HT_OK;
 }
 
