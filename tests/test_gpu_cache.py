@@ -44,6 +44,8 @@ def test_cache_bitwise_equals_host_path(kind, m, n, mode, monkeypatch):
     # without out-edges add zeros: a different association of the same sums)
     monkeypatch.setenv("HT_NO_GAT_DIRECT", "1")
     monkeypatch.setenv("HT_NO_PROJECT_FIRST", "1")  # (needs HBM checkpoints; reassociates)
+    # the split GAT backward needs h^{l+1} in HBM (cache on) and reassociates gq
+    monkeypatch.setenv("HT_NO_GAT_SPLIT", "1")
     ds = H.synth_dataset(H.SynthSpec(num_vertices=2500, avg_degree=8.0, seed=4), 16, 8)
     a = H.partition_vertices(ds.graph, m, seed=4)
     p = H.split_chunks(ds.graph, a, n)

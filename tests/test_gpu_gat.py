@@ -164,10 +164,8 @@ def test_gat_split_backward_equals_fused(m, n, monkeypatch):
     """With h^{l+1} in HBM the backward runs split (one row gather per edge:
     g_alpha and sum alpha gs_v from the CSR pass, scalars per destination,
     then gq = A_u + gts_u a_src) instead of the fused two-gather pass
-    (HT_NO_GAT_SPLIT=1).  alpha, g_t and their segment sums are bitwise the
-    same for the same inputs (the top layer's attention gradient, the
-    loss); gq and what depends on it (dW, the input gradients, the layers
-    below) only reassociate."""
+    (HT_NO_GAT_SPLIT=1).  The forward (loss) is the same; the backward
+    reassociates (g_alpha's warp sum, gq), within FP32 rounding."""
     rng = np.random.default_rng(11)
     V = 5000
     src = np.concatenate([np.full(3000, 3, np.int64), rng.integers(0, V, 30000)])
@@ -190,10 +188,7 @@ def test_gat_split_backward_equals_fused(m, n, monkeypatch):
         fleet.close()
     (la, a_), (lb, b_) = out["1"], out[None]
     assert la == lb
-    # the top layer's attention gradient sees identical inputs: bitwise; the
-    # layers below see the reassociated input gradient
-    np.testing.assert_array_equal(a_["attn_grads"][1], b_["attn_grads"][1])
-    assert O.rel_err(b_["attn_grads"][0], a_["attn_grads"][0]) < 1e-5
     for l in range(2):
+        assert O.rel_err(b_["attn_grads"][l], a_["attn_grads"][l]) < 1e-5
         assert O.rel_err(b_["grads"][l], a_["grads"][l]) < 1e-5
     assert O.rel_err(b_["gh0"], a_["gh0"]) < 1e-5
