@@ -479,9 +479,10 @@ static __global__ void __launch_bounds__(256) k_gat_src_fixup(
 //                         registers) and A_u = sum_e alpha_e gs_v in edge order
 //   B  (per destination)  sdot_v, g_t_e, seg sum of g_t (scalars only)
 //   S2 (per source)       gts_u = sum_e g_t_e; gq_u = A_u + gts_u a_src
-// alpha is the fused kernels' value bitwise; g_alpha's warp sum (eight
-// edges reduced together: 9 shuffles instead of 40) and gq (A_u, then the
-// a_src term) are the same sums in a different association.
+// alpha, g_alpha, g_t, sdot, gts are the fused kernels' values bitwise; gq
+// is the same sum in a different association (A_u, then the a_src term).
+// (A transposed reduction of eight edges' g_alpha sums in 9 shuffles
+// instead of 40 measured 12 % slower in S1: the pass is memory-bound.)
 // Per-edge records {alpha, g_alpha -> g_t} in CSC order.
 // ---------------------------------------------------------------------------
 template <int NV>
@@ -549,45 +550,28 @@ __device__ __forceinline__ void src_rows_a(float4 (&acc)[NV], const float4 (&qu)
     }
     float my_g = 0.f;
     int k = 0;
-    for (; k + 8 <= cnt; k += 8) {
-      float4 x[8][NV];
+    for (; k + SU <= cnt; k += SU) {
+      float4 x[SU][NV];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < SU; ++u) {
         const int r = __shfl_sync(0xffffffffu, my_d, k + u);
         load4<NV>(x[u], GS + (int64_t)r * d, d4, lane);
       }
-      float g[8];
+      float g[SU];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < SU; ++u) {
         const float a = __shfl_sync(0xffffffffu, my_a, k + u);
 #pragma unroll
         for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a, x[u][t]);
         g[u] = dot4<NV>(x[u], qu);
       }
-      // eight warp sums in 9 shuffles (transposed reduction): halve the
-      // set per step, lanes keep the half their xor partner does not
-      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float keep = b16 ? g[i + 4] : g[i], send = b16 ? g[i] : g[i + 4];
-        g[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-      }
+      for (int o = 16; o; o >>= 1)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const float keep = b8 ? g[i + 2] : g[i], send = b8 ? g[i] : g[i + 2];
-        g[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-      {
-        const float keep = b4 ? g[1] : g[0], send = b4 ? g[0] : g[1];
-        g[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      g[0] += __shfl_xor_sync(0xffffffffu, g[0], 2);
-      g[0] += __shfl_xor_sync(0xffffffffu, g[0], 1);
-      // edge u's sum sits in lanes ((u&4)<<2 | (u&2)<<2 | (u&1)<<2) + 0..3
-      const int u = lane - k;
-      const int srcl = ((u & 4) << 2) | ((u & 2) << 2) | ((u & 1) << 2);
-      const float gu = __shfl_sync(0xffffffffu, g[0], srcl & 31);
-      if (u >= 0 && u < 8) my_g = gu;
+        for (int u = 0; u < SU; ++u) g[u] += __shfl_xor_sync(0xffffffffu, g[u], o);
+#pragma unroll
+      for (int u = 0; u < SU; ++u)
+        if (lane == k + u) my_g = g[u];
     }
     for (; k < cnt; ++k) {
       const int r = __shfl_sync(0xffffffffu, my_d, k);
