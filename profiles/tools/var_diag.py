@@ -4,6 +4,7 @@ native calls of train_epoch."""
 import collections, ctypes as C, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import bench
 import paper_2311_14898_b200 as H
 from paper_2311_14898_b200 import _native as N
