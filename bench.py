@@ -661,6 +661,41 @@ def workload_config(config_id, cfg, E, m, ordering):
                    else "inputs fit in the 126 MB L2 (not flushed between steps)")}
 
 
+def reference_full_epoch_cfg1(seed=0):
+    """BASELINE.md §3's plan for the CPU reference: one whole
+    ``chunktrain.engine.train_epoch`` of config 1 (2-layer GCN 64-128-16,
+    100K V / 1.87M E, m=4, n=4, reorganized, float32) through the unmodified
+    package - setup untimed, the epoch timed end to end (~20 s on the
+    container's cores).  None when the reference is not installed."""
+    if not os.path.isdir(REF_DIR):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from chunktrain import devices as D
+    from chunktrain import engine as E
+    from chunktrain import partition as P
+    from chunktrain import planner as PL
+    from chunktrain import synth as S
+    c = CONFIGS["cfg1"]
+    ds = S.synth_dataset(S.SynthSpec(num_vertices=c["V"], avg_degree=c["avg_degree"], seed=seed),
+                         c["dims"][0], c["dims"][-1])
+    p = P.split_chunks(ds.graph, P.partition_vertices(ds.graph, 4, seed=seed), c["n"])
+    p = PL.reorganize(p).partition
+    plan = PL.plan_for_partition(p)
+    model = E.init_model("gcn", c["dims"], seed=seed, lr=0.1, dtype=np.float32)
+    host = D.HostStore(ds.graph.num_vertices, c["dims"], dtype=np.float32)
+    host.set_features(ds.features)
+    fleet = D.DeviceFleet(plan, mode="full", dtype=np.float32)
+    t0 = time.perf_counter()
+    res = E.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
+    dt = time.perf_counter() - t0
+    L = len(c["dims"]) - 1
+    return {"what": "chunktrain.engine.train_epoch, config 1 (m=4, n=4, reorganized, float32), "
+                    "one whole epoch", "seconds": dt,
+            "gteps": L * ds.graph.num_edges / dt / 1e9, "edges": int(ds.graph.num_edges),
+            "loss": float(res.loss), "cores": host_threads()}
+
+
 def reference_arm(args, cfg, n_gpus):
     """bench.py --impl reference: the reference's own CPU implementation of
     the path (ReferenceSampler), W warm-up + K timed steps, each a bounded
@@ -691,6 +726,10 @@ def reference_arm(args, cfg, n_gpus):
                             "sample": rs.describe(),
                             "note": "np.add.at / np.add.reduceat are single-threaded"},
            "e2e": {"value": v, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:  # the reference's own full epoch at config 1, beside the samples
+        out["full_epoch_cfg1"] = reference_full_epoch_cfg1(cfg["seed"])
+    except Exception as exc:  # noqa: BLE001 - report, do not fail the arm
+        out["full_epoch_cfg1"] = {"error": str(exc)[:200]}
     print(json.dumps(out), flush=True)
 
 
