@@ -211,12 +211,6 @@ int ht_fleet_set_host_rows(ht_fleet* f, const int64_t* rows, int64_t n);
  * the owner cache, the host copies of h^L and grad_h^L.  Weights, attention
  * vectors, loss and every other host array are unchanged. */
 int ht_fleet_set_lean(ht_fleet* f, int lean);
-/* Processing order of the one-device transposed aggregation's segments
- * (every host row; `n` = rows): a permutation, e.g. community-major, so
- * the gathered rows of one community are reused from L2 while its sources
- * are summed.  Values are unchanged (each row is still its own sequential
- * sum).  order == NULL restores ascending order. */
-int ht_fleet_set_bwd_order(ht_fleet* f, const int32_t* order, int64_t n);
 /* Recompute-cache hybrid under an HBM budget (the paper's cache-vs-
  * recompute policy; the reference keeps every checkpoint,
  * devices.py:391-425): `bytes` caps what the owner cache may allocate per

@@ -84,7 +84,6 @@ _SIGS = {
     "ht_fleet_set_cache": (i32, [vp, i32]),
     "ht_fleet_set_host_rows": (i32, [vp, vp, i64]),
     "ht_fleet_set_lean": (i32, [vp, i32]),
-    "ht_fleet_set_bwd_order": (i32, [vp, vp, i64]),
     "ht_fleet_set_budget": (i32, [vp, i64]),
     "ht_fleet_recompute_state": (i32, [vp, C.POINTER(i64)]),
     "ht_fleet_set_checkpoints": (i32, [vp, i32]),

@@ -198,7 +198,7 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     for (auto& c : d.chunks) {
       for (auto* b : {&c.nbr_slot, &c.dest_rows, &c.csc_off, &c.csc_slot, &c.csc_w, &c.csr_off,
                       &c.csr_dst, &c.csr_w, &c.bx_off, &c.csc_loc, &c.csr_perm, &c.h2d_m,
-                      &c.flush_m, &c.csc_gid, &c.nbr_gid, &c.bx_order})
+                      &c.flush_m, &c.csc_gid, &c.nbr_gid})
         b->release();
       for (Pieces* pc : {&c.fw, &c.bw, &c.bx}) pc->release();
       for (CopyList* cl : {&c.h2d, &c.flush, &c.base_bwd, &c.dest})
@@ -684,25 +684,6 @@ extern "C" int ht_fleet_recompute_state(ht_fleet* f, int64_t* mask) {
   *mask = 0;
   for (size_t l = 0; l < f->agg_recompute.size() && l < 63; ++l)
     if (f->agg_recompute[l]) *mask |= (int64_t)1 << l;
-  return HT_OK;
-}
-
-extern "C" int ht_fleet_set_bwd_order(ht_fleet* f, const int32_t* order, int64_t n) {
-  for (auto& d : f->dev) {
-    if (!d.local) continue;
-    HT_TRY(set_dev(d));
-    DevChunk& c = d.chunks[0];
-    if (!order || n <= 0) {
-      c.bx_order.release();
-      continue;
-    }
-    if (f->m != 1 || f->n != 1 || n != c.bx_rows)
-      return fail(HT_EINVAL, "a backward segment order needs one device, one batch and %lld rows",
-                  (long long)c.bx_rows);
-    std::vector<int32_t> o(order, order + n);
-    HT_TRY(upload(c.bx_order, o, d.stream));
-    CU(cudaStreamSynchronize(d.stream));
-  }
   return HT_OK;
 }
 

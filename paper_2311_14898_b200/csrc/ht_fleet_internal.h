@@ -162,7 +162,6 @@ struct DevChunk {
   // (empty segments for rows without out-edges) so the transposed
   // aggregation writes the dense grad mirror directly; pieces re-indexed
   DBuf bx_off;
-  DBuf bx_order;  // int32 [bx_rows]: processing order of the expanded CSR segments (optional)
   Pieces bx;
   int64_t bx_rows = -1;
   // GAT: chunk-local CSC sources (rows of q) and the CSC edge id of each
@@ -413,7 +412,7 @@ void timers_collect(ht_fleet* f);
 // e, long segments through their pieces (`pc`); d's partial / work buffers.
 int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
                const int64_t* off, const int32_t* idx, const float* w, int64_t nseg,
-               const Pieces& pc, int col_slice = 0, const int32_t* order = nullptr);
+               const Pieces& pc);
 
 int upload_weights(Device& d, const float* W, int d_in, int d_out);
 

@@ -473,16 +473,11 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
         return fail(HT_ESTATE, "project-first layer %d needs the one-device narrow backward", layer);
       const int64_t nseg = dx ? c.bx_rows : c.nn;
       float* views = dx ? d.mg[layer].as<float>() : d.se.as<float>();
-      static const int bwd_slice = [] {  // (experiment) column slices of the expanded CSR pass
-        const char* e = getenv("HT_COL_SLICE_BWD");
-        return e ? atoi(e) : 0;
-      }();
       HT_TRY(launch_seg(d.stream, d, (narrow || pfl) ? d.tT.as<float>() : views,
                         (narrow || pfl) ? GZ : GA, (narrow || pfl) ? ldz : kw,
                         (narrow || pfl) ? ldz : kw,
                         dx ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>(),
-                        c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), nseg, dx ? c.bx : c.bw,
-                        dx ? bwd_slice : 0, dx ? c.bx_order.as<int32_t>() : nullptr));
+                        c.csr_dst.as<int32_t>(), c.csr_w.as<float>(), nseg, dx ? c.bx : c.bw));
       timer_end(f, d, tr, 1, (double)c.ne * (8.0 + 4.0 * kw) + (double)c.nn * (4.0 * kw + 4.0),
                 d.stream);
       if (pfl && nseg > 0) {  // dW = h^T (A^T gz), rows in row order

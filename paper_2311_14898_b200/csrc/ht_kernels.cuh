@@ -575,77 +575,6 @@ __global__ void __launch_bounds__(256, MINB) k_seg_work_sub(float* __restrict__ 
   }
 }
 
-// Column-sliced work list for wide rows: the d columns are processed as
-// slices of 4G floats (slice-major units), G lanes per segment, segments in
-// `order` (null: ascending) - with a community-major order one slice of a
-// community's gathered rows (4G floats each) can stay L2-resident while the
-// community's segments are summed.  Each output element is still the sequential sum over its
-// segment's edges in edge order: bitwise the unsliced kernels' values.
-// Tickets: one per (slice, fixup).  out row stride ldo, X row stride ldx.
-template <int G, int U, int B, int MINB>
-__global__ void __launch_bounds__(256, MINB) k_seg_work_cols(float* __restrict__ out, int64_t ldo,
-                                                             const float* __restrict__ X,
-                                                             int64_t ldx, int d, int nfix,
-                                                             SegWork wk,
-                                                             const int32_t* __restrict__ order) {
-  constexpr int S = 32 / G, SW = 4 * G;
-  const int lane = lane_id(), sl = lane % G, sub = lane / G;
-  const int64_t npu = (wk.np + S - 1) / S;
-  const int64_t per_slice = npu + (wk.nseg + S * B - 1) / (S * B);
-  const int nsl = (d + SW - 1) / SW;
-  const int64_t nunits = per_slice * nsl;
-  for (;;) {
-    unsigned uu = 0;
-    if (lane == 0) uu = atomicAdd(wk.counter, 1u);
-    uu = __shfl_sync(0xffffffffu, uu, 0);
-    if ((int64_t)uu >= nunits) break;
-    const int slc = (int)((int64_t)uu / per_slice);
-    const int64_t u = (int64_t)uu - (int64_t)slc * per_slice;
-    const int c0 = slc * SW;
-    const int d4 = ((d - c0) < SW ? (d - c0) : SW) >> 2;  // float4 words of this slice
-    const float* Xs = X + c0;
-    if (u < npu) {  // S pieces, one per sub-group
-      const int64_t p = u * S + sub;
-      const bool mine = p < wk.np;
-      const int64_t e0 = mine ? wk.lo[p] : 0, e1 = mine ? wk.hi[p] : 0;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      seg_sum_sub<G, U>(acc, Xs, ldx, d4, wk.idx, wk.w, e0, e1, sl);
-      if (mine && sl < d4) reinterpret_cast<float4*>(wk.partial + p * (int64_t)d + c0)[sl] = acc;
-      __threadfence();  // this lane's partial stores, then the sub-group's ticket
-      __syncwarp();
-      const int f = mine ? wk.pf[p] : 0;
-      int last = 0;
-      if (mine && sl == 0)
-        last = atomicAdd(wk.tickets + (int64_t)slc * nfix + f, 1) == (int)wk.fcnt[f] - 1;
-      last = __shfl_sync(0xffffffffu, last, sub * G);
-      if (mine && last) {
-        __threadfence();
-        if (sl < d4)
-          reinterpret_cast<float4*>(out + wk.fseg[f] * ldo + c0)[sl] =
-              sum_partials(wk.partial + c0, wk.ffirst[f], wk.fcnt[f], d, sl);
-      }
-      continue;
-    }
-    const int64_t s0 = (u - npu) * (S * B);
-    for (int b = 0; b < B; ++b) {
-      const int64_t k = s0 + (int64_t)b * S + sub;
-      if (s0 + (int64_t)b * S >= wk.nseg) break;  // warp-uniform
-      int64_t e0 = 0, e1 = 0;
-      const bool inr = k < wk.nseg;
-      const int64_t sg = inr && order ? (int64_t)order[k] : k;
-      if (inr) {
-        e0 = wk.off[sg];
-        e1 = wk.off[sg + 1];
-      }
-      const bool skip = !inr || e1 - e0 > wk.split;  // long: its pieces
-      if (skip) e1 = e0;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      seg_sum_sub<G, U>(acc, Xs, ldx, d4, wk.idx, wk.w, e0, e1, sl);
-      if (!skip && sl < d4) reinterpret_cast<float4*>(out + sg * ldo + c0)[sl] = acc;
-    }
-  }
-}
-
 // out[seg[f]] = ((partial[first] + partial[first+1]) + ...) in piece order.
 static __global__ void __launch_bounds__(256) k_seg_fixup(float* __restrict__ out,
                                                    const float* __restrict__ partial, int d,

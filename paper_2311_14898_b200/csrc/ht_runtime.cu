@@ -253,7 +253,7 @@ int resident_grid(K kernel, int64_t warps_needed) {
 
 int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
                const int64_t* off, const int32_t* idx, const float* w, int64_t nseg,
-               const Pieces& pc, int col_slice, const int32_t* order) {
+               const Pieces& pc) {
   if (nseg <= 0) return HT_OK;
   const int64_t np = pc.np, nf = pc.nf;
   static const bool sub_ok = [] {  // HT_NO_SUBWARP=1: narrow rows on the warp kernels
@@ -269,24 +269,10 @@ int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t l
     ht::SegWork wk{off, idx, w, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(),
                    pc.pf.as<int32_t>(), np, pc.seg.as<int64_t>(), pc.first.as<int64_t>(),
                    pc.cnt.as<int64_t>(), dv.work.as<unsigned>(), dv.work.as<int>() + 1, partial};
-    const int nsl = (col_slice == 32 || col_slice == 64 || col_slice == 128) && d > col_slice
-                        ? (d + col_slice - 1) / col_slice : 1;
-    const int64_t wbytes = ((int64_t)nsl * nf + 2) * 4;
-    if (dv.work.bytes < wbytes) return fail(HT_ESTATE, "work-list buffer not sized");
-    CU(cudaMemsetAsync(dv.work.p, 0, wbytes, s));  // counter + fixup tickets
+    if (dv.work.bytes < (nf + 2) * 4) return fail(HT_ESTATE, "work-list buffer not sized");
+    CU(cudaMemsetAsync(dv.work.p, 0, (nf + 2) * 4, s));  // counter + fixup tickets
     count_launch();
-    if (nsl > 1) {  // column slices, segments in `order`
-      if (col_slice == 32) {
-        auto k = ht::k_seg_work_cols<8, 8, 4, 4>;
-        k<<<resident_grid(k, (nseg + 3) / 4), kThreads, 0, s>>>(out, d, X, ldx, d, (int)nf, wk, order);
-      } else if (col_slice == 64) {
-        auto k = ht::k_seg_work_cols<16, 8, 4, 4>;
-        k<<<resident_grid(k, (nseg + 1) / 2), kThreads, 0, s>>>(out, d, X, ldx, d, (int)nf, wk, order);
-      } else {
-        auto k = ht::k_seg_work_cols<32, 8, 16, 4>;
-        k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, d, X, ldx, d, (int)nf, wk, order);
-      }
-    } else if (d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
+    if (d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
       if (d <= 32) {
         auto k = ht::k_seg_work_sub<8, 8, 4, 4>;
         k<<<resident_grid(k, (nseg + 3) / 4), kThreads, 0, s>>>(out, X, ldx, d, wk);
@@ -876,7 +862,7 @@ int epoch_begin_impl(ht_fleet* f, int L, const int* dims, int64_t extra_grad, bo
     if (narrow_w)  // (the expanded CSR of one device / one batch has a row per host row)
       HT_TRY(d.tT.ensure(std::max<int64_t>(mn, f->m == 1 && f->n == 1 ? f->nrows : 0) * narrow_w * 4));
     HT_TRY(d.partial.ensure(np * dmax * 4));
-    HT_TRY(d.work.ensure((nf * ((dmax + 31) / 32) + 2) * 4));  // tickets per column slice
+    HT_TRY(d.work.ensure((nf + 2) * 4));
     HT_TRY(d.gemm_ws.ensure((int64_t)kSplitsMax * dmax * dmax * 4));
     HT_TRY(d.hL.ensure(std::max<int64_t>(1, d.hL_off[f->n]) * pad4(dims[L]) * 4));
     // HBM owner cache: decided per epoch (requested mode, plan, free HBM).
