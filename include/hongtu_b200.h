@@ -62,6 +62,14 @@ int ht_memset(void* dst, int value, int64_t bytes);
 int ht_build_graph(const int64_t* src, const int64_t* dst, int64_t E, int64_t V,
                    int64_t* csc_offsets, int64_t* csc_sources, int64_t* csr_offsets,
                    int64_t* csr_targets, int64_t* csr_edge_perm, double* weights);
+/* Lean build for 10^9-edge synthetic graphs (synth_graph_streaming): int32
+ * (src, dst) pairs, parallel edges removed (first of each (dst, src) pair,
+ * synth.py:154-157), then the same canonical CSC / CSR / weights as
+ * ht_build_graph.  Output edge arrays sized E; *e_out = edges kept. */
+int ht_build_graph_dedup32(const int32_t* src, const int32_t* dst, int64_t E, int64_t V,
+                           int64_t* csc_offsets, int64_t* csc_sources, int64_t* csr_offsets,
+                           int64_t* csr_targets, int64_t* csr_edge_perm, double* weights,
+                           int64_t* e_out);
 
 /* CSR -> canonical edge permutation rebuilt from CSC + CSR offsets in one
  * counting pass (replaces the np.lexsort of graph.py:262-264 on HTG1 load). */

@@ -45,6 +45,7 @@ _SIGS = {
     "ht_memcpy": (i32, [vp, vp, i64]),
     "ht_memset": (i32, [vp, i32, i64]),
     "ht_build_graph": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp, vp]),
+    "ht_build_graph_dedup32": (i32, [vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
     "ht_dedup_edges": (i32, [vp, vp, i64, i64, vp, P_I64]),
     "ht_csr_perm": (i32, [i64, i64, vp, vp, vp, vp]),
     "ht_ldg_partition": (i32, [i64, vp, vp, vp, vp, vp, i64, i64, vp]),

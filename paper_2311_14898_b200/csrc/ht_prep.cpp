@@ -455,3 +455,69 @@ extern "C" int ht_dedup_edges(const int64_t* src, const int64_t* dst, int64_t E,
   *n_keep = k;
   return HT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Lean graph build for 10^9-edge synthetic graphs (synth.synth_graph_streaming):
+// 32-bit (src, dst) pairs in, parallel edges removed, canonical CSC / CSR /
+// weights out - the same arrays as ht_dedup_edges + ht_build_graph
+// (graph.py:91-150, synth.py:154-157) without their 64-bit temporaries:
+// one counting sort by destination straight into csc_sources, a sort +
+// unique per destination, one counting sort by source for the CSR.  Peak
+// memory ~ the 8-byte inputs + the 32-byte/edge outputs.  Outputs are sized
+// for E edges; *e_out receives the edge count after deduplication.
+// ---------------------------------------------------------------------------
+extern "C" int ht_build_graph_dedup32(const int32_t* src, const int32_t* dst, int64_t E, int64_t V,
+                                      int64_t* csc_offsets, int64_t* csc_sources,
+                                      int64_t* csr_offsets, int64_t* csr_targets,
+                                      int64_t* csr_edge_perm, double* weights, int64_t* e_out) {
+  if (E < 0 || V < 0 || V >= ((int64_t)1 << 31)) return fail(HT_EINVAL, "bad graph size");
+  int bad = 0;
+#pragma omp parallel for reduction(| : bad)
+  for (int64_t e = 0; e < E; ++e)
+    bad |= (src[e] < 0 || dst[e] < 0 || src[e] >= V || dst[e] >= V);
+  if (bad) return fail(HT_EINVAL, "an edge lies outside [0, %lld)", (long long)V);
+  // counting sort by destination: csc_offsets = bucket starts
+  std::vector<int64_t> pos(V + 1, 0);
+  for (int64_t e = 0; e < E; ++e) pos[dst[e] + 1]++;
+  for (int64_t v = 0; v < V; ++v) pos[v + 1] += pos[v];
+  std::vector<int64_t> start(pos.begin(), pos.end());
+  for (int64_t e = 0; e < E; ++e) csc_sources[pos[dst[e]]++] = src[e];
+  // sort + unique each destination's sources, compact in place
+  std::vector<int64_t> cnt(V, 0);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < V; ++v) {
+    int64_t* b = csc_sources + start[v];
+    const int64_t n = start[v + 1] - start[v];
+    std::sort(b, b + n);
+    cnt[v] = std::unique(b, b + n) - b;
+  }
+  int64_t k = 0;
+  csc_offsets[0] = 0;
+  for (int64_t v = 0; v < V; ++v) {  // (sequential compaction: ranges move left only)
+    if (k != start[v]) std::memmove(csc_sources + k, csc_sources + start[v], cnt[v] * sizeof(int64_t));
+    k += cnt[v];
+    csc_offsets[v + 1] = k;
+  }
+  const int64_t Ed = k;
+  std::vector<double> inv(V);
+#pragma omp parallel for
+  for (int64_t v = 0; v < V; ++v)
+    inv[v] = 1.0 / std::sqrt(1.0 + (double)(csc_offsets[v + 1] - csc_offsets[v]));
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t v = 0; v < V; ++v)
+    for (int64_t p = csc_offsets[v]; p < csc_offsets[v + 1]; ++p)
+      weights[p] = inv[csc_sources[p]] * inv[v];
+  // CSR by (src, dst): canonical positions grouped by source, in position order
+  std::fill(pos.begin(), pos.end(), 0);
+  for (int64_t p = 0; p < Ed; ++p) pos[csc_sources[p] + 1]++;
+  for (int64_t v = 0; v < V; ++v) pos[v + 1] += pos[v];
+  std::memcpy(csr_offsets, pos.data(), (V + 1) * sizeof(int64_t));
+  for (int64_t v = 0; v < V; ++v)
+    for (int64_t p = csc_offsets[v]; p < csc_offsets[v + 1]; ++p) {
+      const int64_t q = pos[csc_sources[p]]++;
+      csr_targets[q] = v;
+      csr_edge_perm[q] = p;
+    }
+  *e_out = Ed;
+  return HT_OK;
+}
