@@ -22,6 +22,7 @@ from .planner import (MODES, BufferLayout, CostParams, DedupPlan, ReorgResult, V
 from .devices import DeviceArray, DeviceFleet, DeviceState, HostStore
 from .engine import (ActivationTracker, EpochResult, ModelConfig, comm_passes_per_epoch, init_model,
                      load_labels, load_matrix, save_labels, save_matrix, sync_and_update, train_epoch)
-from .synth import SynthDataset, SynthSpec, synth_dataset, synth_graph, synth_node_data
+from .synth import (SynthDataset, SynthSpec, synth_dataset, synth_graph, synth_graph_streaming,
+                    synth_node_data)
 
 __version__ = "0.1.0"

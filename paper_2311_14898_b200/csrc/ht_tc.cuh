@@ -302,8 +302,12 @@ __global__ void __launch_bounds__(256, 1)
           tc_fence_after();
           const uint32_t ah = smem_u32(sA(s)), al = smem_u32(sAlo(s));
           const uint32_t bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
+          // K-tail chunk: only the 8-wide k-steps that hold real columns
+          // (K = 100: 13 of 16 steps; the zero-filled rest is skipped)
+          const int nks = min(4, (K - kc * 32 + 7) >> 3);
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
+            if (ks >= nks) break;
             const uint64_t dah = sdesc(ah + ks * 32), dbh = sdesc(bh + ks * 32);
             mma_tf32(d, dah, dbh, idesc, (kc | ks) != 0);
             if (SPLIT) {
