@@ -91,7 +91,6 @@ extern "C" int ht_fleet_create(int m, int n, const int* ordinals, int mode, int 
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
       CU(cudaStreamCreateWithPriority(&d.tpre, cudaStreamNonBlocking, lo));
     }
-    CU(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
     d.chunks.resize(n);
     for (auto& c : d.chunks) c.csc_gid.release(), c.nbr_gid.release();
@@ -241,9 +240,6 @@ extern "C" int ht_fleet_destroy(ht_fleet* f) {
     if (d.tin) cudaStreamDestroy(d.tin);
     if (d.tout) cudaStreamDestroy(d.tout);
     if (d.tpre) cudaStreamDestroy(d.tpre);
-    if (d.side) cudaStreamDestroy(d.side);
-    for (cudaEvent_t e : {d.e_gz, d.e_wg})
-      if (e) cudaEventDestroy(e);
     for (auto& b : d.ck) b.release();
     for (cudaEvent_t e : d.e_ck)
       if (e) cudaEventDestroy(e);
@@ -759,11 +755,6 @@ extern "C" int ht_sgd2(ht_fleet* f, int L, const int* dims, float* const* W, flo
   // ascending device order and applies the identical update
   Device& d0 = f->dev[f->rank >= 0 ? f->rank : 0];
   if (A && !f->gat) return fail(HT_ESTATE, "attention update without ht_gat_epoch_begin");
-  for (auto& d : f->dev)  // weight gradients reduced on the side stream
-    if (d.local) {
-      HT_TRY(set_dev(d));
-      HT_TRY(ev_wait(d.stream, d.e_wg));
-    }
   if (f->rank >= 0 && f->m > 1) HT_TRY(xbarrier(f));  // every rank's dW complete
   HT_TRY(sync_all(f));
   HT_TRY(set_dev(d0));

@@ -220,11 +220,6 @@ struct Device {
   // checkpoint prefetch: agg rows of layer l come back from the host as
   // soon as they are stored (same bytes, moved while the link is idle)
   cudaStream_t tpre = nullptr;
-  // weight gradients (aggᵀ·gz) on a side stream: independent of the
-  // transposed aggregation that follows on the compute stream, so the
-  // streaming GEMM fills the gather's idle issue slots
-  cudaStream_t side = nullptr;
-  cudaEvent_t e_gz = nullptr, e_wg = nullptr;
   std::vector<DBuf> ck;
   std::vector<cudaEvent_t> e_ck;
   DBuf fa[2], fb[2], ba[2], bb[2];

@@ -313,9 +313,6 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       const int s = (int)(d.bwd_count & 1);
       const int64_t* rows = c.dest_rows.as<int64_t>();
       float *A = d.ba[s].as<float>(), *G = d.bb[s].as<float>();
-      // the previous batch's / layer's weight gradient (side stream) still
-      // reads GZ, gemm_ws and its agg rows (the recompute scratch, staging)
-      HT_TRY(ev_wait(d.stream, d.e_wg));
       if (d.cache) {  // checkpoint and gradient rows straight from the mirrors
         A = d.ma[layer].as<float>() + c.dest_m0 * d_in;
         G = d.mg[layer + 1].as<float>() + c.dest_m0 * d_out;
@@ -341,10 +338,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       } else {
       // K6 on tin: checkpoint rows (ready since the forward), then the
       // destination gradients (ready once the layer above has flushed)
-      if (d.bwd_count >= 2) {
-        HT_TRY(ev_wait(d.tin, d.e_bcomp[s]));
-        HT_TRY(ev_wait(d.tin, d.e_wg));  // (its wgrad read the staged agg rows)
-      }
+      if (d.bwd_count >= 2) HT_TRY(ev_wait(d.tin, d.e_bcomp[s]));
       if (f->prefetch) {
         A = d.ck[layer].as<float>() + d.hL_off[j] * d_in;  // reloaded during the forward
       } else if (c.dest.dma) {
@@ -418,21 +412,13 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
                                                 w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
                                                 nullptr, 0));
         if (M > 0 && !pfl) {  // (project-first layer: dW = h^T (A^T gz) after K8)
-          // on the side stream, overlapping the gagg GEMM and K8; the next
-          // writer of GZ / gemm_ws waits for e_wg
-          HT_TRY(ev_rec(d.e_gz, d.stream));
-          HT_TRY(ev_wait(d.side, d.e_gz));
-          TimerRec tw;
-          timer_begin(f, d, tw, d.side);
           int used = 1;
-          HT_TRY(ht::tc::wgrad(d.side, A, d_in, d_in, GZ, ldz, d_out, M, kSplitsMax,
+          HT_TRY(ht::tc::wgrad(d.stream, A, d_in, d_in, GZ, ldz, d_out, M, kSplitsMax,
                                d.gemm_ws.as<float>(), &used));
           count_launch(4);
-          ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.side>>>(
+          ht::k_reduce_splits<<<grid_for(nw / 32 + 1), 256, 0, d.stream>>>(
               d.gWall.as<float>() + d.gW_off[layer], d.gemm_ws.as<float>(), nw, used);
           CU(cudaGetLastError());
-          timer_end(f, d, tw, 2, 2.0 * c.nv * d_in * d_out, d.side);
-          HT_TRY(ev_rec(d.e_wg, d.side));
         }
       } else {
         int splits = (int)std::min<int64_t>(kSplitsMax, std::max<int64_t>(1, M / 2048));
@@ -454,8 +440,7 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
           HT_TRY((gemm<false, true, ht::EPI_STORE>(d.stream, GZ, ldz, w.W.as<float>(), d_out, GA,
                                                    d_in, nullptr, 0, M, d_in, d_out, 1, d_out)));
       }
-      timer_end(f, d, tg, 2, (pfl || precision != HT_PREC_TF32 ? 6.0 : 4.0) * c.nv * d_in * d_out,
-                d.stream);
+      timer_end(f, d, tg, 2, 6.0 * c.nv * d_in * d_out, d.stream);
       HT_TRY(ev_rec(d.e_bcomp[s], d.stream));
       if (no_in && !pfl) {
         d.bwd_count++;

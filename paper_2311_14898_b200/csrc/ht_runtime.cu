@@ -83,7 +83,6 @@ int sync_all(ht_fleet* f) {
     if (d.tin) CU(cudaStreamSynchronize(d.tin));
     if (d.tout) CU(cudaStreamSynchronize(d.tout));
     if (d.tpre) CU(cudaStreamSynchronize(d.tpre));
-    if (d.side) CU(cudaStreamSynchronize(d.side));
   }
   return HT_OK;
 }
