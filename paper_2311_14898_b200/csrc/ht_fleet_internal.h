@@ -352,6 +352,20 @@ namespace htf {
 
 inline int64_t chunk_bound(int64_t V, int g) { return V * g / kChunks; }
 
+// grid of a persistent (work-list) kernel: its resident CTAs on every SM
+template <class K>
+inline int resident_grid(K kernel, int64_t warps_needed) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0) != cudaSuccess ||
+      per_sm <= 0)
+    per_sm = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (warps_needed * 32 + kThreads - 1) / kThreads;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sms));
+}
+
 template <bool TA, bool TB, int EPI>
 int gemm(cudaStream_t s, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
          int64_t ldc, const float* G, int64_t ldg, int64_t M, int64_t N, int64_t K, int splits,

@@ -33,6 +33,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include "ht_kernels.cuh"  // sum_partials
+
 namespace ht {
 namespace gat {
 
@@ -476,7 +478,8 @@ static __global__ void __launch_bounds__(256) k_gat_src_fixup(
 // without re-aggregating): ONE row gather per edge instead of two.
 //   A  (per destination)  alpha_e, gs_v = g_v (s_v > 0), el_d[v]
 //   S1 (per source, CSR)  gathers gs_v rows: g_alpha_e = gs_v . q_u (q_u in
-//                         registers) and A_u = sum_e alpha_e gs_v in edge order
+//                         registers) and A_u = sum_e alpha_e gs_v in edge order;
+//                         one work-list launch (hub pieces first)
 //   B  (per destination)  sdot_v, g_t_e, seg sum of g_t (scalars only)
 //   S2 (per source)       gts_u = sum_e g_t_e; gq_u = A_u + gts_u a_src
 // alpha, g_alpha, g_t, sdot, gts are the fused kernels' values bitwise; gq
@@ -587,46 +590,61 @@ __device__ __forceinline__ void src_rows_a(float4 (&acc)[NV], const float4 (&qu)
   }
 }
 
-// S1: one warp per source segment (segments > split: k_gat_bwd_s1_pieces)
-template <int NV>
-__global__ void __launch_bounds__(256) k_gat_bwd_s1(
+// S1 as one work-list launch (like ht::k_seg_work_v4): units [0, np) are
+// the hub pieces, then batches of B short source segments, taken from a
+// device counter; the last piece of a hub (atomic ticket) sums the hub's
+// partial rows in piece order into GQ (k_seg_fixup's order).  counter and
+// tickets zeroed before the launch.
+template <int NV, int B>
+__global__ void __launch_bounds__(256) k_gat_bwd_s1_work(
     const int64_t* __restrict__ off, const int32_t* __restrict__ dst,
-    const int32_t* __restrict__ perm, int64_t nseg, int64_t split, const float* __restrict__ GS,
-    const float* __restrict__ Q, const int32_t* __restrict__ qrow, float* __restrict__ AL, int d,
-    float* __restrict__ GQ) {
-  const int lane = threadIdx.x & 31;
-  const int d4 = d >> 2;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nseg; u += nw) {
-    const int64_t e0 = off[u], e1 = off[u + 1];
-    if (e1 - e0 > split) continue;
-    float4 acc[NV], qu[NV];
-#pragma unroll
-    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e1 > e0) load4<NV>(qu, Q + (int64_t)(qrow ? qrow[u] : (int32_t)u) * d, d4, lane);
-    src_rows_a<NV>(acc, qu, e0, e1, dst, perm, GS, AL, d, d4, lane);
-    store4<NV>(GQ + u * (int64_t)d, acc, d4, lane);
-  }
-}
-
-// S1 pieces [lo, hi) of long source segments (seg[pf] gives the source)
-template <int NV>
-__global__ void __launch_bounds__(256) k_gat_bwd_s1_pieces(
+    const int32_t* __restrict__ perm, int64_t nseg, int64_t split,
     const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, const int32_t* __restrict__ pf,
-    const int64_t* __restrict__ fseg, int64_t np, const int32_t* __restrict__ dst,
-    const int32_t* __restrict__ perm, const float* __restrict__ GS, const float* __restrict__ Q,
-    const int32_t* __restrict__ qrow, float* __restrict__ AL, int d, float* __restrict__ part) {
+    const int64_t* __restrict__ fseg, const int64_t* __restrict__ ffirst,
+    const int64_t* __restrict__ fcnt, int64_t np, unsigned* __restrict__ counter,
+    int* __restrict__ tickets, const float* __restrict__ GS, const float* __restrict__ Q,
+    float* __restrict__ AL, int d, float* __restrict__ part, float* __restrict__ GQ) {
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < np; q += nw) {
-    const int64_t u = fseg[pf[q]];
+  const int64_t nunits = np + (nseg + B - 1) / B;
+  for (;;) {
+    unsigned uu = 0;
+    if (lane == 0) uu = atomicAdd(counter, 1u);
+    uu = __shfl_sync(0xffffffffu, uu, 0);
+    if ((int64_t)uu >= nunits) break;
     float4 acc[NV], qu[NV];
+    if ((int64_t)uu < np) {  // a hub piece
+      const int64_t q = uu;
+      const int f = pf[q];
+      const int64_t u = fseg[f];
 #pragma unroll
-    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    load4<NV>(qu, Q + (int64_t)(qrow ? qrow[u] : (int32_t)u) * d, d4, lane);
-    src_rows_a<NV>(acc, qu, lo[q], hi[q], dst, perm, GS, AL, d, d4, lane);
-    store4<NV>(part + q * (int64_t)d, acc, d4, lane);
+      for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      load4<NV>(qu, Q + u * (int64_t)d, d4, lane);
+      src_rows_a<NV>(acc, qu, lo[q], hi[q], dst, perm, GS, AL, d, d4, lane);
+      store4<NV>(part + q * (int64_t)d, acc, d4, lane);
+      __threadfence();
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) last = atomicAdd(tickets + f, 1) == (int)fcnt[f] - 1;
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {  // every piece written: their sum in piece order
+        __threadfence();
+        float4* o = reinterpret_cast<float4*>(GQ + u * (int64_t)d);
+        for (int c = lane; c < d4; c += kW) o[c] = ht::sum_partials(part, ffirst[f], fcnt[f], d, c);
+      }
+      continue;
+    }
+    const int64_t s0 = ((int64_t)uu - np) * B;
+    const int64_t s1 = s0 + B < nseg ? s0 + B : nseg;
+    for (int64_t u = s0; u < s1; ++u) {
+      const int64_t e0 = off[u], e1 = off[u + 1];
+      if (e1 - e0 > split) continue;  // a hub: its pieces
+#pragma unroll
+      for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e1 > e0) load4<NV>(qu, Q + u * (int64_t)d, d4, lane);
+      src_rows_a<NV>(acc, qu, e0, e1, dst, perm, GS, AL, d, d4, lane);
+      store4<NV>(GQ + u * (int64_t)d, acc, d4, lane);
+    }
   }
 }
 

@@ -89,22 +89,19 @@ int launch_gat_bwd_split(cudaStream_t s, Device& dv, const DevChunk& c, const fl
   const int32_t* perm = c.csr_perm.as<int32_t>();
   const int gv = grid_for(std::max<int64_t>(1, c.nv)), gs = grid_for(std::max<int64_t>(1, nseg));
   if (dv.work.bytes < (pc.nf + 2) * 4) return fail(HT_ESTATE, "work buffer not sized");
-  CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s));  // S2 tickets
-  count_launch(4 + (pc.np ? 2 : 0));
+  count_launch(4);
 #define GATB(NV)                                                                                   \
   if (c.nv > 0)                                                                                    \
     ht::gat::k_gat_bwd_a<NV><<<gv, kThreads, 0, s>>>(coff, cidx, c.nv, P, els, a_dst, d, slope, G,  \
                                                      HO, ho_rows, GS, AL, ELD);                    \
-  if (nseg > 0)                                                                                    \
-    ht::gat::k_gat_bwd_s1<NV><<<gs, kThreads, 0, s>>>(roff, dst, perm, nseg, kSplit, GS, Q,         \
-                                                      nullptr, AL, d, GQ);                          \
-  if (pc.np) {                                                                                     \
-    ht::gat::k_gat_bwd_s1_pieces<NV><<<grid_for(pc.np), kThreads, 0, s>>>(                         \
-        pc.lo.as<int64_t>(), pc.hi.as<int64_t>(), pc.pf.as<int32_t>(), pc.seg.as<int64_t>(),       \
-        pc.np, dst, perm, GS, Q, nullptr, AL, d, part);                                            \
-    ht::k_seg_fixup<<<grid_for(pc.nf), kThreads, 0, s>>>(GQ, part, d, pc.seg.as<int64_t>(),       \
-                                                          pc.first.as<int64_t>(),                  \
-                                                          pc.cnt.as<int64_t>(), pc.nf);            \
+  if (nseg > 0) {                                                                                  \
+    CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s)); /* S1 counter + tickets */               \
+    auto k1 = ht::gat::k_gat_bwd_s1_work<NV, 8>;                                                    \
+    k1<<<resident_grid(k1, nseg), kThreads, 0, s>>>(                                                \
+        roff, dst, perm, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(),                    \
+        pc.pf.as<int32_t>(), pc.seg.as<int64_t>(), pc.first.as<int64_t>(), pc.cnt.as<int64_t>(),     \
+        pc.np, dv.work.as<unsigned>(), dv.work.as<int>() + 1, GS, Q, AL, d, part, GQ);             \
+    CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s)); /* S2 tickets */                         \
   }                                                                                                \
   if (c.nv > 0)                                                                                    \
     ht::gat::k_gat_bwd_b<NV><<<gv, kThreads, 0, s>>>(coff, cidx, c.nv, els, ELD, slope, AL, SGT,    \

@@ -235,20 +235,6 @@ void timers_collect(ht_fleet* f) {
 // last piece of a long segment to finish sums its partials in piece order
 // (k_seg_work_*).  Other widths (the fp32 validation path's odd widths):
 // the per-segment kernel, the pieces kernel and the fixup in turn.
-namespace {
-template <class K>
-int resident_grid(K kernel, int64_t warps_needed) {
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0) != cudaSuccess ||
-      per_sm <= 0)
-    per_sm = 1;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t want = (warps_needed * 32 + kThreads - 1) / kThreads;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)per_sm * sms));
-}
-}  // namespace
 
 int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
                const int64_t* off, const int32_t* idx, const float* w, int64_t nseg,
