@@ -737,7 +737,7 @@ int plan_cache(ht_fleet* f, Device& d, int L, const int* dims, bool gat, int64_t
   for (int l = 0; l < L; ++l) base += R * dims[l] * 4;   // h mirrors
   for (int l = 0; l <= L; ++l) base += R * dims[l] * 4;  // grad mirrors
   const bool one = f->m == 1 && d.mcount == f->nrows && d.chunks[0].csc_gid.p &&
-                   (d.mrows.empty() || d.mrows.back() == d.mcount - 1);
+                   (d.mrows.empty() || d.mrows.back() == d.mcount - 1) && !f->sw.no_direct_read;
   if (gat) {  // GAT staging allocated after this decision (ht_gat_epoch_begin)
     int64_t me = 1;
     for (int j = 0; j < f->n; ++j) me = std::max(me, d.chunks[j].ne);
