@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(256) k_rowdot(float* __restrict__ out, const f
 #define HT_GAT_DU 4
 #endif
 constexpr int DU = HT_GAT_DU;
+constexpr int kDstBatch = 8;  // destinations per work unit
 template <int NV, bool BWD>
 __global__ void __launch_bounds__(256) k_gat_dst(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
@@ -137,192 +138,202 @@ __global__ void __launch_bounds__(256) k_gat_dst(
     const float* __restrict__ a_dst, int d, float slope, float* __restrict__ H,
     const float* __restrict__ G, float* __restrict__ GS, float* __restrict__ GP,
     float* __restrict__ AL, float* __restrict__ GT, float* __restrict__ SGT,
-    const float* __restrict__ HO, const int64_t* __restrict__ ho_rows) {
+    const float* __restrict__ HO, const int64_t* __restrict__ ho_rows,
+    unsigned* __restrict__ counter) {
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
   float4 ad[NV];
   load4<NV>(ad, a_dst, d4, lane);
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nseg; v += nw) {
-    const int64_t e0 = off[v], e1 = off[v + 1];
-    float4 pv[NV];
-    load4<NV>(pv, P + v * (int64_t)d, d4, lane);
-    const float el_d = warp_sum(dot4<NV>(pv, ad));
-    // the first 32 in-edges (most destinations have fewer) stay in
-    // registers across the passes: source id i0 and attention input t0
-    const int c0 = (e1 - e0) < (int64_t)kW ? (int)(e1 - e0) : kW;
-    const bool in0 = lane < c0;
-    const int i0 = in0 ? __ldg(idx + e0 + lane) : 0;
-    const float t0 = in0 ? el_d + __ldg(el_src + i0) : 0.f;
-    // segment max and softmax denominator, lane-parallel over edges
-    float mx = in0 ? leaky(t0, slope) : -CUDART_INF_F;
-    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
-      mx = fmaxf(mx, leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope));
-    mx = warp_max(mx);
-    const float x0 = in0 ? expf(leaky(t0, slope) - mx) : 0.f;
-    float den = x0;
-    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
-      den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
-    den = warp_sum(den);
-    const float a0 = in0 ? x0 / den : 0.f;  // alpha of the first chunk
-    // s_v = sum alpha_e q_u, sequential in edge order.  Backward with the
-    // layer output h = ReLU(s) in HBM (HO): (s > 0) == (h > 0) bitwise, so
-    // only alpha is recomputed, not s (one row gather per edge saved)
-    float4 acc[NV];
-#pragma unroll
-    for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (BWD && HO) {
-      load4<NV>(acc, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
-      if (in0) AL[2 * (e0 + lane)] = a0;
+  // destinations in batches of kDstBatch from a device counter (zeroed
+  // before the launch): whichever warp is free takes the next batch
+  for (;;) {
+    unsigned ub = 0;
+    if (lane == 0) ub = atomicAdd(counter, 1u);
+    ub = __shfl_sync(0xffffffffu, ub, 0);
+    const int64_t vb = (int64_t)ub * kDstBatch;
+    if (vb >= nseg) break;
+    const int64_t ve = vb + kDstBatch < nseg ? vb + kDstBatch : nseg;
+    for (int64_t v = vb; v < ve; ++v) {
+      const int64_t e0 = off[v], e1 = off[v + 1];
+      float4 pv[NV];
+      load4<NV>(pv, P + v * (int64_t)d, d4, lane);
+      const float el_d = warp_sum(dot4<NV>(pv, ad));
+      // the first 32 in-edges (most destinations have fewer) stay in
+      // registers across the passes: source id i0 and attention input t0
+      const int c0 = (e1 - e0) < (int64_t)kW ? (int)(e1 - e0) : kW;
+      const bool in0 = lane < c0;
+      const int i0 = in0 ? __ldg(idx + e0 + lane) : 0;
+      const float t0 = in0 ? el_d + __ldg(el_src + i0) : 0.f;
+      // segment max and softmax denominator, lane-parallel over edges
+      float mx = in0 ? leaky(t0, slope) : -CUDART_INF_F;
       for (int64_t e = e0 + kW + lane; e < e1; e += kW)
-        AL[2 * (e)] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
-    }
-    for (int64_t base = e0; base < ((BWD && HO) ? e0 : e1); base += kW) {
-      const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
-      int my_i = i0;
-      float my_a = a0;
-      if (base != e0 && lane < cnt) {
-        my_i = __ldg(idx + base + lane);
-        my_a = expf(leaky(el_d + __ldg(el_src + my_i), slope) - mx) / den;
+        mx = fmaxf(mx, leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope));
+      mx = warp_max(mx);
+      const float x0 = in0 ? expf(leaky(t0, slope) - mx) : 0.f;
+      float den = x0;
+      for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+        den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
+      den = warp_sum(den);
+      const float a0 = in0 ? x0 / den : 0.f;  // alpha of the first chunk
+      // s_v = sum alpha_e q_u, sequential in edge order.  Backward with the
+      // layer output h = ReLU(s) in HBM (HO): (s > 0) == (h > 0) bitwise, so
+      // only alpha is recomputed, not s (one row gather per edge saved)
+      float4 acc[NV];
+#pragma unroll
+      for (int t = 0; t < NV; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (BWD && HO) {
+        load4<NV>(acc, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
+        if (in0) AL[2 * (e0 + lane)] = a0;
+        for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+          AL[2 * (e)] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
       }
-      if (BWD && lane < cnt) AL[2 * (base + lane)] = my_a;
-      int k = 0;
-      if (!BWD && NV == 1 && d4 <= 16) {
-        // rows of <= 64 floats: each half-warp loads one row, so one
-        // instruction brings two; the adds stay in edge order (lanes 0-15
-        // hold the sums, lanes 16-31 hand over the odd rows)
-        const int hl = lane >> 4, sl = lane & 15;
-        for (; k + 8 <= cnt; k += 8) {
-          float4 x[4];
+      for (int64_t base = e0; base < ((BWD && HO) ? e0 : e1); base += kW) {
+        const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
+        int my_i = i0;
+        float my_a = a0;
+        if (base != e0 && lane < cnt) {
+          my_i = __ldg(idx + base + lane);
+          my_a = expf(leaky(el_d + __ldg(el_src + my_i), slope) - mx) / den;
+        }
+        if (BWD && lane < cnt) AL[2 * (base + lane)] = my_a;
+        int k = 0;
+        if (!BWD && NV == 1 && d4 <= 16) {
+          // rows of <= 64 floats: each half-warp loads one row, so one
+          // instruction brings two; the adds stay in edge order (lanes 0-15
+          // hold the sums, lanes 16-31 hand over the odd rows)
+          const int hl = lane >> 4, sl = lane & 15;
+          for (; k + 8 <= cnt; k += 8) {
+            float4 x[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int s = __shfl_sync(0xffffffffu, my_i, k + 2 * u + hl);
-            x[u] = sl < d4 ? __ldg(reinterpret_cast<const float4*>(Q + (int64_t)s * d) + sl)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
+            for (int u = 0; u < 4; ++u) {
+              const int s = __shfl_sync(0xffffffffu, my_i, k + 2 * u + hl);
+              x[u] = sl < d4 ? __ldg(reinterpret_cast<const float4*>(Q + (int64_t)s * d) + sl)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float4 y;
-            y.x = __shfl_down_sync(0xffffffffu, x[u].x, 16);
-            y.y = __shfl_down_sync(0xffffffffu, x[u].y, 16);
-            y.z = __shfl_down_sync(0xffffffffu, x[u].z, 16);
-            y.w = __shfl_down_sync(0xffffffffu, x[u].w, 16);
-            const float a0 = __shfl_sync(0xffffffffu, my_a, k + 2 * u);
-            const float a1 = __shfl_sync(0xffffffffu, my_a, k + 2 * u + 1);
-            axpy_rn(acc[0], a0, x[u]);
-            axpy_rn(acc[0], a1, y);
+            for (int u = 0; u < 4; ++u) {
+              float4 y;
+              y.x = __shfl_down_sync(0xffffffffu, x[u].x, 16);
+              y.y = __shfl_down_sync(0xffffffffu, x[u].y, 16);
+              y.z = __shfl_down_sync(0xffffffffu, x[u].z, 16);
+              y.w = __shfl_down_sync(0xffffffffu, x[u].w, 16);
+              const float a0 = __shfl_sync(0xffffffffu, my_a, k + 2 * u);
+              const float a1 = __shfl_sync(0xffffffffu, my_a, k + 2 * u + 1);
+              axpy_rn(acc[0], a0, x[u]);
+              axpy_rn(acc[0], a1, y);
+            }
           }
         }
-      }
-      for (; k + DU <= cnt; k += DU) {  // DU rows in flight
-        float4 x[DU][NV];
-        float a[DU];
+        for (; k + DU <= cnt; k += DU) {  // DU rows in flight
+          float4 x[DU][NV];
+          float a[DU];
 #pragma unroll
-        for (int u = 0; u < DU; ++u) {
-          const int s = __shfl_sync(0xffffffffu, my_i, k + u);
-          a[u] = __shfl_sync(0xffffffffu, my_a, k + u);
-          load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
+          for (int u = 0; u < DU; ++u) {
+            const int s = __shfl_sync(0xffffffffu, my_i, k + u);
+            a[u] = __shfl_sync(0xffffffffu, my_a, k + u);
+            load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
+          }
+#pragma unroll
+          for (int u = 0; u < DU; ++u)
+#pragma unroll
+            for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a[u], x[u][t]);
         }
+        for (; k < cnt; ++k) {
+          const int s = __shfl_sync(0xffffffffu, my_i, k);
+          const float a = __shfl_sync(0xffffffffu, my_a, k);
+          float4 x[NV];
+          load4<NV>(x, Q + (int64_t)s * d, d4, lane);
 #pragma unroll
-        for (int u = 0; u < DU; ++u)
-#pragma unroll
-          for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a[u], x[u][t]);
+          for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a, x[t]);
+        }
       }
-      for (; k < cnt; ++k) {
-        const int s = __shfl_sync(0xffffffffu, my_i, k);
-        const float a = __shfl_sync(0xffffffffu, my_a, k);
-        float4 x[NV];
-        load4<NV>(x, Q + (int64_t)s * d, d4, lane);
+      if (!BWD) {
 #pragma unroll
-        for (int t = 0; t < NV; ++t) axpy_rn(acc[t], a, x[t]);
+        for (int t = 0; t < NV; ++t) {
+          acc[t].x = fmaxf(acc[t].x, 0.f);
+          acc[t].y = fmaxf(acc[t].y, 0.f);
+          acc[t].z = fmaxf(acc[t].z, 0.f);
+          acc[t].w = fmaxf(acc[t].w, 0.f);
+        }
+        store4<NV>(H + v * (int64_t)d, acc, d4, lane);
+        continue;
       }
-    }
-    if (!BWD) {
+      // ---- backward: gs = g * (s > 0) ----
+      float4 gs[NV];
+      load4<NV>(gs, G + v * (int64_t)d, d4, lane);
 #pragma unroll
       for (int t = 0; t < NV; ++t) {
-        acc[t].x = fmaxf(acc[t].x, 0.f);
-        acc[t].y = fmaxf(acc[t].y, 0.f);
-        acc[t].z = fmaxf(acc[t].z, 0.f);
-        acc[t].w = fmaxf(acc[t].w, 0.f);
+        gs[t].x = acc[t].x > 0.f ? gs[t].x : 0.f;
+        gs[t].y = acc[t].y > 0.f ? gs[t].y : 0.f;
+        gs[t].z = acc[t].z > 0.f ? gs[t].z : 0.f;
+        gs[t].w = acc[t].w > 0.f ? gs[t].w : 0.f;
       }
-      store4<NV>(H + v * (int64_t)d, acc, d4, lane);
-      continue;
-    }
-    // ---- backward: gs = g * (s > 0) ----
-    float4 gs[NV];
-    load4<NV>(gs, G + v * (int64_t)d, d4, lane);
+      store4<NV>(GS + v * (int64_t)d, gs, d4, lane);
+      // g_alpha_e = gs . q_u, sum alpha_e g_alpha_e; the first chunk keeps
+      // its g_alpha in a register (g0), later chunks park it in GT
+      float sdot = 0.f, g0 = 0.f;
+      for (int64_t base = e0; base < e1; base += kW) {
+        const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
+        const int my_i = base == e0 ? i0 : (lane < cnt ? __ldg(idx + base + lane) : 0);
+        float my_g = 0.f;
+        int k = 0;
+        for (; k + DU <= cnt; k += DU) {  // DU rows in flight, DU interleaved reductions
+          float4 x[DU][NV];
 #pragma unroll
-    for (int t = 0; t < NV; ++t) {
-      gs[t].x = acc[t].x > 0.f ? gs[t].x : 0.f;
-      gs[t].y = acc[t].y > 0.f ? gs[t].y : 0.f;
-      gs[t].z = acc[t].z > 0.f ? gs[t].z : 0.f;
-      gs[t].w = acc[t].w > 0.f ? gs[t].w : 0.f;
-    }
-    store4<NV>(GS + v * (int64_t)d, gs, d4, lane);
-    // g_alpha_e = gs . q_u, sum alpha_e g_alpha_e; the first chunk keeps
-    // its g_alpha in a register (g0), later chunks park it in GT
-    float sdot = 0.f, g0 = 0.f;
-    for (int64_t base = e0; base < e1; base += kW) {
-      const int cnt = (int)((e1 - base) < (int64_t)kW ? (e1 - base) : (int64_t)kW);
-      const int my_i = base == e0 ? i0 : (lane < cnt ? __ldg(idx + base + lane) : 0);
-      float my_g = 0.f;
-      int k = 0;
-      for (; k + DU <= cnt; k += DU) {  // DU rows in flight, DU interleaved reductions
-        float4 x[DU][NV];
+          for (int u = 0; u < DU; ++u) {
+            const int s = __shfl_sync(0xffffffffu, my_i, k + u);
+            load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
+          }
+          float g[DU];
 #pragma unroll
-        for (int u = 0; u < DU; ++u) {
-          const int s = __shfl_sync(0xffffffffu, my_i, k + u);
-          load4<NV>(x[u], Q + (int64_t)s * d, d4, lane);
+          for (int u = 0; u < DU; ++u) g[u] = dot4<NV>(gs, x[u]);
+#pragma unroll
+          for (int o = 16; o; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < DU; ++u) g[u] += __shfl_xor_sync(0xffffffffu, g[u], o);
+#pragma unroll
+          for (int u = 0; u < DU; ++u)
+            if (lane == k + u) my_g = g[u];
         }
-        float g[DU];
-#pragma unroll
-        for (int u = 0; u < DU; ++u) g[u] = dot4<NV>(gs, x[u]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1)
-#pragma unroll
-          for (int u = 0; u < DU; ++u) g[u] += __shfl_xor_sync(0xffffffffu, g[u], o);
-#pragma unroll
-        for (int u = 0; u < DU; ++u)
-          if (lane == k + u) my_g = g[u];
-      }
-      for (; k < cnt; ++k) {
-        const int s = __shfl_sync(0xffffffffu, my_i, k);
-        float4 x[NV];
-        load4<NV>(x, Q + (int64_t)s * d, d4, lane);
-        const float g = warp_sum(dot4<NV>(gs, x));
-        if (lane == k) my_g = g;
-      }
-      if (lane < cnt) {
-        if (base == e0) {
-          g0 = my_g;
-          sdot += a0 * my_g;
-        } else {
-          GT[2 * (base + lane)] = my_g;
-          sdot += AL[2 * (base + lane)] * my_g;
+        for (; k < cnt; ++k) {
+          const int s = __shfl_sync(0xffffffffu, my_i, k);
+          float4 x[NV];
+          load4<NV>(x, Q + (int64_t)s * d, d4, lane);
+          const float g = warp_sum(dot4<NV>(gs, x));
+          if (lane == k) my_g = g;
+        }
+        if (lane < cnt) {
+          if (base == e0) {
+            g0 = my_g;
+            sdot += a0 * my_g;
+          } else {
+            GT[2 * (base + lane)] = my_g;
+            sdot += AL[2 * (base + lane)] * my_g;
+          }
         }
       }
-    }
-    sdot = warp_sum(sdot);
-    float sgt = 0.f;
-    if (in0) {
-      const float gt = a0 * (g0 - sdot) * (t0 > 0.f ? 1.f : slope);
-      GT[2 * (e0 + lane)] = gt;
-      sgt = gt;
-    }
-    for (int64_t e = e0 + kW + lane; e < e1; e += kW) {
-      const float t = el_d + __ldg(el_src + __ldg(idx + e));
-      const float gt = AL[2 * (e)] * (GT[2 * (e)] - sdot) * (t > 0.f ? 1.f : slope);
-      GT[2 * (e)] = gt;
-      sgt += gt;
-    }
-    sgt = warp_sum(sgt);
-    if (lane == 0) SGT[v] = sgt;
-    if (GP) {  // (null: the rank-1 gp = sgt a_dst is folded into gq by k_gat_src)
-      float4 gp[NV];
+      sdot = warp_sum(sdot);
+      float sgt = 0.f;
+      if (in0) {
+        const float gt = a0 * (g0 - sdot) * (t0 > 0.f ? 1.f : slope);
+        GT[2 * (e0 + lane)] = gt;
+        sgt = gt;
+      }
+      for (int64_t e = e0 + kW + lane; e < e1; e += kW) {
+        const float t = el_d + __ldg(el_src + __ldg(idx + e));
+        const float gt = AL[2 * (e)] * (GT[2 * (e)] - sdot) * (t > 0.f ? 1.f : slope);
+        GT[2 * (e)] = gt;
+        sgt += gt;
+      }
+      sgt = warp_sum(sgt);
+      if (lane == 0) SGT[v] = sgt;
+      if (GP) {  // (null: the rank-1 gp = sgt a_dst is folded into gq by k_gat_src)
+        float4 gp[NV];
 #pragma unroll
-      for (int t = 0; t < NV; ++t)
-        gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
-      store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+        for (int t = 0; t < NV; ++t)
+          gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
+        store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+      }
     }
   }
 }

@@ -46,20 +46,25 @@ int launch_rowdot(cudaStream_t s, float* out, const float* X, const float* a, in
 }
 
 template <bool BWD>
-int launch_gat_dst(cudaStream_t s, const DevChunk& c, const float* Q, const float* P,
+int launch_gat_dst(cudaStream_t s, Device& dv, const DevChunk& c, const float* Q, const float* P,
                    const float* els, const float* a_dst, int d, float slope, float* H,
                    const float* G, float* GS, float* GP, float* AL, float* GT, float* SGT,
                    const float* HO = nullptr, const int64_t* ho_rows = nullptr,
                    bool global_src = false) {
   if (c.nv <= 0) return HT_OK;
-  const int g = grid_for(c.nv);
   const int64_t* off = c.csc_off.as<int64_t>();
   // sources as chunk-local rows of Q, or (direct) as global rows of P
   const int32_t* idx = global_src ? c.csc_gid.as<int32_t>() : c.csc_loc.as<int32_t>();
+  if (dv.work.bytes < 4) return fail(HT_ESTATE, "work buffer not sized");
+  CU(cudaMemsetAsync(dv.work.p, 0, 4, s));  // the destination-batch counter
   count_launch();
 #define GATD(NV)                                                                              \
-  ht::gat::k_gat_dst<NV, BWD><<<g, kThreads, 0, s>>>(off, idx, c.nv, Q, P, els, a_dst, d, slope, \
-                                                     H, G, GS, GP, AL, GT, SGT, HO, ho_rows)
+  {                                                                                           \
+    auto k = ht::gat::k_gat_dst<NV, BWD>;                                                     \
+    k<<<resident_grid(k, c.nv), kThreads, 0, s>>>(off, idx, c.nv, Q, P, els, a_dst, d, slope, \
+                                                  H, G, GS, GP, AL, GT, SGT, HO, ho_rows,    \
+                                                  dv.work.as<unsigned>());                   \
+  }
   switch (nv_of(d)) {
     case 1: GATD(1); break;
     case 2: GATD(2); break;
@@ -472,7 +477,7 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
       HT_TRY(launch_rowdot(d.stream, els, Q, w.A.as<float>() + d_out, d_out, dir ? c.nv : c.nn));
       TimerRec tr;
       timer_begin(f, d, tr, d.stream);
-      HT_TRY(launch_gat_dst<false>(d.stream, c, Q, P, els, w.A.as<float>(), d_out, slope, H, nullptr,
+      HT_TRY(launch_gat_dst<false>(d.stream, d, c, Q, P, els, w.A.as<float>(), d_out, slope, H, nullptr,
                                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                                    dir));
       timer_end(f, d, tr, 0,
@@ -558,7 +563,7 @@ extern "C" int ht_gat_backward_layer(ht_fleet* f, int layer, int d_in, int d_out
                                     d.partial.as<float>(), d.g_pgts.as<float>(), dir,
                                     dir ? d.g_sgt.as<float>() : nullptr));
       } else {
-        HT_TRY(launch_gat_dst<true>(d.stream, c, Q, P, els, a_dst, d_out, slope,
+        HT_TRY(launch_gat_dst<true>(d.stream, d, c, Q, P, els, a_dst, d_out, slope,
                                     nullptr, Gin, GS, dir ? nullptr : GP, AL, GT, d.g_sgt.as<float>(),
                                     HO, hrows, dir));
         HT_TRY(launch_gat_src(d.stream, c, GS, AL, GT, a_src, d_out, GQ, d.g_gts.as<float>(),
