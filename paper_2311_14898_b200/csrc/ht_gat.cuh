@@ -505,43 +505,51 @@ __global__ void __launch_bounds__(256) k_gat_bwd_a(
     const float* __restrict__ P, const float* __restrict__ el_src, const float* __restrict__ a_dst,
     int d, float slope, const float* __restrict__ G, const float* __restrict__ HO,
     const int64_t* __restrict__ ho_rows, float* __restrict__ GS, float* __restrict__ AL,
-    float* __restrict__ ELD) {
+    float* __restrict__ ELD,
+    unsigned* __restrict__ counter) {
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
   float4 ad[NV];
   load4<NV>(ad, a_dst, d4, lane);
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nseg; v += nw) {
-    const int64_t e0 = off[v], e1 = off[v + 1];
-    float4 pv[NV], ho[NV], gv[NV];
-    load4<NV>(pv, P + v * (int64_t)d, d4, lane);
-    load4<NV>(ho, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
-    load4<NV>(gv, G + v * (int64_t)d, d4, lane);
-    const float el_d = warp_sum(dot4<NV>(pv, ad));
-    const int c0 = (e1 - e0) < (int64_t)kW ? (int)(e1 - e0) : kW;
-    const bool in0 = lane < c0;
-    const float t0 = in0 ? el_d + __ldg(el_src + __ldg(idx + e0 + lane)) : 0.f;
-    float mx = in0 ? leaky(t0, slope) : -CUDART_INF_F;
-    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
-      mx = fmaxf(mx, leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope));
-    mx = warp_max(mx);
-    const float x0 = in0 ? expf(leaky(t0, slope) - mx) : 0.f;
-    float den = x0;
-    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
-      den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
-    den = warp_sum(den);
-    if (in0) AL[2 * (e0 + lane)] = x0 / den;
-    for (int64_t e = e0 + kW + lane; e < e1; e += kW)
-      AL[2 * e] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
+  for (;;) {  // destinations in batches of kDstBatch from a device counter
+    unsigned ub = 0;
+    if (lane == 0) ub = atomicAdd(counter, 1u);
+    ub = __shfl_sync(0xffffffffu, ub, 0);
+    const int64_t vb = (int64_t)ub * kDstBatch;
+    if (vb >= nseg) break;
+    const int64_t ve = vb + kDstBatch < nseg ? vb + kDstBatch : nseg;
+    for (int64_t v = vb; v < ve; ++v) {
+      const int64_t e0 = off[v], e1 = off[v + 1];
+      float4 pv[NV], ho[NV], gv[NV];
+      load4<NV>(pv, P + v * (int64_t)d, d4, lane);
+      load4<NV>(ho, HO + (ho_rows ? ho_rows[v] : v) * (int64_t)d, d4, lane);
+      load4<NV>(gv, G + v * (int64_t)d, d4, lane);
+      const float el_d = warp_sum(dot4<NV>(pv, ad));
+      const int c0 = (e1 - e0) < (int64_t)kW ? (int)(e1 - e0) : kW;
+      const bool in0 = lane < c0;
+      const float t0 = in0 ? el_d + __ldg(el_src + __ldg(idx + e0 + lane)) : 0.f;
+      float mx = in0 ? leaky(t0, slope) : -CUDART_INF_F;
+      for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+        mx = fmaxf(mx, leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope));
+      mx = warp_max(mx);
+      const float x0 = in0 ? expf(leaky(t0, slope) - mx) : 0.f;
+      float den = x0;
+      for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+        den += expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx);
+      den = warp_sum(den);
+      if (in0) AL[2 * (e0 + lane)] = x0 / den;
+      for (int64_t e = e0 + kW + lane; e < e1; e += kW)
+        AL[2 * e] = expf(leaky(el_d + __ldg(el_src + __ldg(idx + e)), slope) - mx) / den;
 #pragma unroll
-    for (int t = 0; t < NV; ++t) {  // gs = g (s > 0), (s > 0) == (h > 0)
-      gv[t].x = ho[t].x > 0.f ? gv[t].x : 0.f;
-      gv[t].y = ho[t].y > 0.f ? gv[t].y : 0.f;
-      gv[t].z = ho[t].z > 0.f ? gv[t].z : 0.f;
-      gv[t].w = ho[t].w > 0.f ? gv[t].w : 0.f;
+      for (int t = 0; t < NV; ++t) {  // gs = g (s > 0), (s > 0) == (h > 0)
+        gv[t].x = ho[t].x > 0.f ? gv[t].x : 0.f;
+        gv[t].y = ho[t].y > 0.f ? gv[t].y : 0.f;
+        gv[t].z = ho[t].z > 0.f ? gv[t].z : 0.f;
+        gv[t].w = ho[t].w > 0.f ? gv[t].w : 0.f;
+      }
+      store4<NV>(GS + v * (int64_t)d, gv, d4, lane);
+      if (lane == 0) ELD[v] = el_d;
     }
-    store4<NV>(GS + v * (int64_t)d, gv, d4, lane);
-    if (lane == 0) ELD[v] = el_d;
   }
 }
 
@@ -667,36 +675,44 @@ __global__ void __launch_bounds__(256) k_gat_bwd_b(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
     const float* __restrict__ el_src, const float* __restrict__ ELD, float slope,
     float* __restrict__ AL, float* __restrict__ SGT, float* __restrict__ GP,
-    const float* __restrict__ a_dst, int d) {
+    const float* __restrict__ a_dst, int d,
+    unsigned* __restrict__ counter) {
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < nseg; v += nw) {
-    const int64_t e0 = off[v], e1 = off[v + 1];
-    const float el_d = ELD[v];
-    float sdot = 0.f;
-    for (int64_t e = e0 + lane; e < e1; e += kW) {
-      const float2 r = *reinterpret_cast<const float2*>(AL + 2 * e);
-      sdot += r.x * r.y;
-    }
-    sdot = warp_sum(sdot);
-    float sgt = 0.f;
-    for (int64_t e = e0 + lane; e < e1; e += kW) {
-      float2 r = *reinterpret_cast<float2*>(AL + 2 * e);
-      const float t = el_d + __ldg(el_src + __ldg(idx + e));
-      const float gt = r.x * (r.y - sdot) * (t > 0.f ? 1.f : slope);
-      AL[2 * e + 1] = gt;
-      sgt += gt;
-    }
-    sgt = warp_sum(sgt);
-    if (lane == 0) SGT[v] = sgt;
-    if (GP) {
-      float4 ad[NV], gp[NV];
-      load4<NV>(ad, a_dst, d4, lane);
+  for (;;) {  // destinations in batches of kDstBatch from a device counter
+    unsigned ub = 0;
+    if (lane == 0) ub = atomicAdd(counter, 1u);
+    ub = __shfl_sync(0xffffffffu, ub, 0);
+    const int64_t vb = (int64_t)ub * kDstBatch;
+    if (vb >= nseg) break;
+    const int64_t ve = vb + kDstBatch < nseg ? vb + kDstBatch : nseg;
+    for (int64_t v = vb; v < ve; ++v) {
+      const int64_t e0 = off[v], e1 = off[v + 1];
+      const float el_d = ELD[v];
+      float sdot = 0.f;
+      for (int64_t e = e0 + lane; e < e1; e += kW) {
+        const float2 r = *reinterpret_cast<const float2*>(AL + 2 * e);
+        sdot += r.x * r.y;
+      }
+      sdot = warp_sum(sdot);
+      float sgt = 0.f;
+      for (int64_t e = e0 + lane; e < e1; e += kW) {
+        float2 r = *reinterpret_cast<float2*>(AL + 2 * e);
+        const float t = el_d + __ldg(el_src + __ldg(idx + e));
+        const float gt = r.x * (r.y - sdot) * (t > 0.f ? 1.f : slope);
+        AL[2 * e + 1] = gt;
+        sgt += gt;
+      }
+      sgt = warp_sum(sgt);
+      if (lane == 0) SGT[v] = sgt;
+      if (GP) {
+        float4 ad[NV], gp[NV];
+        load4<NV>(ad, a_dst, d4, lane);
 #pragma unroll
-      for (int t = 0; t < NV; ++t)
-        gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
-      store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+        for (int t = 0; t < NV; ++t)
+          gp[t] = make_float4(sgt * ad[t].x, sgt * ad[t].y, sgt * ad[t].z, sgt * ad[t].w);
+        store4<NV>(GP + v * (int64_t)d, gp, d4, lane);
+      }
     }
   }
 }
@@ -743,14 +759,20 @@ __global__ void __launch_bounds__(256) k_gat_bwd_s2(
     int64_t split, const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
     const int32_t* __restrict__ pf, const int64_t* __restrict__ fseg,
     const int64_t* __restrict__ ffirst, const int64_t* __restrict__ fcnt, int64_t np,
-    int* __restrict__ tickets, float* __restrict__ pgts, const float* __restrict__ AL,
-    const float* __restrict__ a_src, const float* __restrict__ sgt_add,
-    const float* __restrict__ a_dst, int d, float* __restrict__ GQ, float* __restrict__ GTS) {
+    unsigned* __restrict__ counter, int* __restrict__ tickets, float* __restrict__ pgts,
+    const float* __restrict__ AL, const float* __restrict__ a_src,
+    const float* __restrict__ sgt_add, const float* __restrict__ a_dst, int d,
+    float* __restrict__ GQ, float* __restrict__ GTS) {
   const int lane = threadIdx.x & 31;
   const int d4 = d >> 2;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < np + nseg; w += nw) {
-    if (w < np) {  // a piece of a hub source
+  const int64_t nunits = np + (nseg + kDstBatch - 1) / kDstBatch;
+  for (;;) {  // hub pieces first, then batches of sources, from a device counter
+    unsigned uu = 0;
+    if (lane == 0) uu = atomicAdd(counter, 1u);
+    uu = __shfl_sync(0xffffffffu, uu, 0);
+    if ((int64_t)uu >= nunits) break;
+    if ((int64_t)uu < np) {  // a piece of a hub source
+      const int64_t w = uu;
       float gts = 0.f;
       for (int64_t e = lo[w] + lane; e < hi[w]; e += kW) gts += __ldg(AL + 2 * (int64_t)__ldg(perm + e) + 1);
       gts = warp_sum(gts);
@@ -769,13 +791,16 @@ __global__ void __launch_bounds__(256) k_gat_bwd_s2(
       }
       continue;
     }
-    const int64_t u = w - np;
-    const int64_t e0 = off[u], e1 = off[u + 1];
-    if (e1 - e0 > split) continue;
-    float gts = 0.f;
-    for (int64_t e = e0 + lane; e < e1; e += kW) gts += __ldg(AL + 2 * (int64_t)__ldg(perm + e) + 1);
-    gts = warp_sum(gts);
-    s2_finish<NV>(GQ, GTS, u, gts, a_src, sgt_add, a_dst, d, d4, lane);
+    const int64_t u0 = ((int64_t)uu - np) * kDstBatch;
+    const int64_t u1 = u0 + kDstBatch < nseg ? u0 + kDstBatch : nseg;
+    for (int64_t u = u0; u < u1; ++u) {
+      const int64_t e0 = off[u], e1 = off[u + 1];
+      if (e1 - e0 > split) continue;
+      float gts = 0.f;
+      for (int64_t e = e0 + lane; e < e1; e += kW) gts += __ldg(AL + 2 * (int64_t)__ldg(perm + e) + 1);
+      gts = warp_sum(gts);
+      s2_finish<NV>(GQ, GTS, u, gts, a_src, sgt_add, a_dst, d, d4, lane);
+    }
   }
 }
 

@@ -92,13 +92,16 @@ int launch_gat_bwd_split(cudaStream_t s, Device& dv, const DevChunk& c, const fl
   const int64_t* roff = expanded ? c.bx_off.as<int64_t>() : c.csr_off.as<int64_t>();
   const int32_t* dst = c.csr_dst.as<int32_t>();
   const int32_t* perm = c.csr_perm.as<int32_t>();
-  const int gv = grid_for(std::max<int64_t>(1, c.nv)), gs = grid_for(std::max<int64_t>(1, nseg));
   if (dv.work.bytes < (pc.nf + 2) * 4) return fail(HT_ESTATE, "work buffer not sized");
   count_launch(4);
 #define GATB(NV)                                                                                   \
-  if (c.nv > 0)                                                                                    \
-    ht::gat::k_gat_bwd_a<NV><<<gv, kThreads, 0, s>>>(coff, cidx, c.nv, P, els, a_dst, d, slope, G,  \
-                                                     HO, ho_rows, GS, AL, ELD);                    \
+  if (c.nv > 0) {                                                                                  \
+    CU(cudaMemsetAsync(dv.work.p, 0, 4, s));                                                       \
+    auto ka = ht::gat::k_gat_bwd_a<NV>;                                                            \
+    ka<<<resident_grid(ka, c.nv), kThreads, 0, s>>>(coff, cidx, c.nv, P, els, a_dst, d, slope, G,   \
+                                                    HO, ho_rows, GS, AL, ELD,                      \
+                                                    dv.work.as<unsigned>());                       \
+  }                                                                                                \
   if (nseg > 0) {                                                                                  \
     CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s)); /* S1 counter + tickets */               \
     auto k1 = ht::gat::k_gat_bwd_s1_work<NV, 8>;                                                    \
@@ -106,16 +109,22 @@ int launch_gat_bwd_split(cudaStream_t s, Device& dv, const DevChunk& c, const fl
         roff, dst, perm, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(),                    \
         pc.pf.as<int32_t>(), pc.seg.as<int64_t>(), pc.first.as<int64_t>(), pc.cnt.as<int64_t>(),     \
         pc.np, dv.work.as<unsigned>(), dv.work.as<int>() + 1, GS, Q, AL, d, part, GQ);             \
-    CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s)); /* S2 tickets */                         \
   }                                                                                                \
-  if (c.nv > 0)                                                                                    \
-    ht::gat::k_gat_bwd_b<NV><<<gv, kThreads, 0, s>>>(coff, cidx, c.nv, els, ELD, slope, AL, SGT,    \
-                                                     GP, a_dst, d);                                \
-  if (nseg > 0)                                                                                    \
-    ht::gat::k_gat_bwd_s2<NV><<<grid_for(nseg + pc.np), kThreads, 0, s>>>(                         \
+  if (c.nv > 0) {                                                                                  \
+    CU(cudaMemsetAsync(dv.work.p, 0, 4, s));                                                       \
+    auto kb = ht::gat::k_gat_bwd_b<NV>;                                                            \
+    kb<<<resident_grid(kb, c.nv), kThreads, 0, s>>>(coff, cidx, c.nv, els, ELD, slope, AL, SGT,     \
+                                                    GP, a_dst, d, dv.work.as<unsigned>());         \
+  }                                                                                                \
+  if (nseg > 0) {                                                                                  \
+    CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s)); /* S2 counter + tickets */               \
+    auto k2 = ht::gat::k_gat_bwd_s2<NV>;                                                           \
+    k2<<<resident_grid(k2, nseg + pc.np), kThreads, 0, s>>>(                                       \
         roff, perm, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(), pc.pf.as<int32_t>(),   \
         pc.seg.as<int64_t>(), pc.first.as<int64_t>(), pc.cnt.as<int64_t>(), pc.np,                 \
-        dv.work.as<int>() + 1, pgts, AL, a_src, sgt_add, a_dst, d, GQ, GTS)
+        dv.work.as<unsigned>(), dv.work.as<int>() + 1, pgts, AL, a_src, sgt_add, a_dst, d, GQ,     \
+        GTS);                                                                                      \
+  }
   switch (nv_of(d)) {
     case 1: GATB(1); break;
     case 2: GATB(2); break;
