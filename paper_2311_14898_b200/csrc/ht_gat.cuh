@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(256) k_rowdot(float* __restrict__ out, const f
 // chunk-local source ids (rows of Q / el_src), rows are d floats wide.
 // DU source rows in flight per warp in the row passes.
 #ifndef HT_GAT_DU
-#define HT_GAT_DU 4
+#define HT_GAT_DU 8
 #endif
 constexpr int DU = HT_GAT_DU;
 constexpr int kDstBatch = 8;  // destinations per work unit

@@ -236,6 +236,22 @@ void timers_collect(ht_fleet* f) {
 // (k_seg_work_*).  Other widths (the fp32 validation path's odd widths):
 // the per-segment kernel, the pieces kernel and the fixup in turn.
 
+// work-list kernel shape: segment rows in flight (NV = 1 / 2 float4 words
+// per lane), segments per unit, resident CTAs per SM - compile-time knobs
+// for same-box A/B variant builds (build.py --variant), defaults measured
+#ifndef HT_WL_US1
+#define HT_WL_US1 8
+#endif
+#ifndef HT_WL_US2
+#define HT_WL_US2 2
+#endif
+#ifndef HT_WL_B
+#define HT_WL_B 16
+#endif
+#ifndef HT_WL_MINB
+#define HT_WL_MINB 4
+#endif
+
 int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
                const int64_t* off, const int32_t* idx, const float* w, int64_t nseg,
                const Pieces& pc) {
@@ -267,8 +283,8 @@ int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t l
       }
     } else {
       switch ((d / 4 + 31) / 32) {
-        case 1: { auto k = ht::k_seg_work_v4<1, 8, 8, 16, 4>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
-        case 2: { auto k = ht::k_seg_work_v4<2, 2, 8, 16, 4>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+        case 1: { auto k = ht::k_seg_work_v4<1, HT_WL_US1, 8, HT_WL_B, HT_WL_MINB>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+        case 2: { auto k = ht::k_seg_work_v4<2, HT_WL_US2, 8, HT_WL_B, HT_WL_MINB>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
         case 3: { auto k = ht::k_seg_work_v4<3, 2, 4, 16, 2>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
         default: { auto k = ht::k_seg_work_v4<4, 2, 4, 16, 2>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
       }
