@@ -239,17 +239,18 @@ void timers_collect(ht_fleet* f) {
 // work-list kernel shape: segment rows in flight (NV = 1 / 2 float4 words
 // per lane), segments per unit, resident CTAs per SM - compile-time knobs
 // for same-box A/B variant builds (build.py --variant), defaults measured
+// (r2 sweep: US1 4, US2 4, B 8, MINB 3 - 42.6 vs 44.5 ms per cfg-2 epoch)
 #ifndef HT_WL_US1
-#define HT_WL_US1 8
+#define HT_WL_US1 4
 #endif
 #ifndef HT_WL_US2
-#define HT_WL_US2 2
+#define HT_WL_US2 4
 #endif
 #ifndef HT_WL_B
-#define HT_WL_B 16
+#define HT_WL_B 8
 #endif
 #ifndef HT_WL_MINB
-#define HT_WL_MINB 4
+#define HT_WL_MINB 3
 #endif
 
 int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
