@@ -252,6 +252,18 @@ void timers_collect(ht_fleet* f) {
 #ifndef HT_WL_MINB
 #define HT_WL_MINB 3
 #endif
+#ifndef HT_WL_UP
+#define HT_WL_UP 8  // piece rows in flight
+#endif
+#ifndef HT_WL_SUB_U
+#define HT_WL_SUB_U 8  // narrow rows: rows in flight per sub-group
+#endif
+#ifndef HT_WL_SUB_B
+#define HT_WL_SUB_B 4
+#endif
+#ifndef HT_WL_SUB_MINB
+#define HT_WL_SUB_MINB 4
+#endif
 
 int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t ldx, int d,
                const int64_t* off, const int32_t* idx, const float* w, int64_t nseg,
@@ -276,16 +288,16 @@ int launch_seg(cudaStream_t s, Device& dv, float* out, const float* X, int64_t l
     count_launch();
     if (d <= 64 && sub_ok) {  // narrow rows: 2 or 4 segments per warp
       if (d <= 32) {
-        auto k = ht::k_seg_work_sub<8, 8, 4, 4>;
+        auto k = ht::k_seg_work_sub<8, HT_WL_SUB_U, HT_WL_SUB_B, HT_WL_SUB_MINB>;
         k<<<resident_grid(k, (nseg + 3) / 4), kThreads, 0, s>>>(out, X, ldx, d, wk);
       } else {
-        auto k = ht::k_seg_work_sub<16, 8, 4, 4>;
+        auto k = ht::k_seg_work_sub<16, HT_WL_SUB_U, HT_WL_SUB_B, HT_WL_SUB_MINB>;
         k<<<resident_grid(k, (nseg + 1) / 2), kThreads, 0, s>>>(out, X, ldx, d, wk);
       }
     } else {
       switch ((d / 4 + 31) / 32) {
-        case 1: { auto k = ht::k_seg_work_v4<1, HT_WL_US1, 8, HT_WL_B, HT_WL_MINB>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
-        case 2: { auto k = ht::k_seg_work_v4<2, HT_WL_US2, 8, HT_WL_B, HT_WL_MINB>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+        case 1: { auto k = ht::k_seg_work_v4<1, HT_WL_US1, HT_WL_UP, HT_WL_B, HT_WL_MINB>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
+        case 2: { auto k = ht::k_seg_work_v4<2, HT_WL_US2, HT_WL_UP, HT_WL_B, HT_WL_MINB>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
         case 3: { auto k = ht::k_seg_work_v4<3, 2, 4, 16, 2>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
         default: { auto k = ht::k_seg_work_v4<4, 2, 4, 16, 2>; k<<<resident_grid(k, nseg), kThreads, 0, s>>>(out, X, ldx, d, wk); break; }
       }
