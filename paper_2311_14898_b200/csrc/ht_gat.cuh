@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(256) k_rowdot(float* __restrict__ out, const f
 #define HT_GAT_DU 8
 #endif
 constexpr int DU = HT_GAT_DU;
-constexpr int kDstBatch = 8;  // destinations per work unit
+#ifndef HT_GAT_DB
+#define HT_GAT_DB 8
+#endif
+constexpr int kDstBatch = HT_GAT_DB;  // destinations per work unit
 template <int NV, bool BWD>
 __global__ void __launch_bounds__(256) k_gat_dst(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,

@@ -22,6 +22,9 @@ using ht::fail;
 // ===========================================================================
 namespace {
 
+#ifndef HT_GAT_S1B
+#define HT_GAT_S1B 8  // sources per S1 work unit
+#endif
 constexpr int kColBlocks = 1184;  // 148 SMs x 8
 
 int gat_width_ok(int d) {
@@ -104,7 +107,7 @@ int launch_gat_bwd_split(cudaStream_t s, Device& dv, const DevChunk& c, const fl
   }                                                                                                \
   if (nseg > 0) {                                                                                  \
     CU(cudaMemsetAsync(dv.work.p, 0, (pc.nf + 2) * 4, s)); /* S1 counter + tickets */               \
-    auto k1 = ht::gat::k_gat_bwd_s1_work<NV, 8>;                                                    \
+    auto k1 = ht::gat::k_gat_bwd_s1_work<NV, HT_GAT_S1B>;                                                    \
     k1<<<resident_grid(k1, nseg), kThreads, 0, s>>>(                                                \
         roff, dst, perm, nseg, kSplit, pc.lo.as<int64_t>(), pc.hi.as<int64_t>(),                    \
         pc.pf.as<int32_t>(), pc.seg.as<int64_t>(), pc.first.as<int64_t>(), pc.cnt.as<int64_t>(),     \
