@@ -631,6 +631,16 @@ def gat_config_line(args, cfg, config, p, plan, ds, rk, slowest, hbm_peak, hbm_s
     cpu = None
     if not args.no_cpu_baseline:
         cpu = reference_cpu_baseline(ds.graph, ds.labels, ds.mask, cfg["dims"], model="gat")
+    pcie = pcie_peaks()
+    e2e_b = (r["e2e"]["h2d_bytes_per_step"] or 0) + (r["e2e"]["d2h_bytes_per_step"] or 0)
+    e2e_s = r["e2e"]["ms_per_step"] / 1e3
+    pcie_line = {"bound": "pcie", "what": "host<->GPU bytes of the e2e epoch (plan) / epoch time",
+                 "source": "plan", "achieved": e2e_b / e2e_s / 1e9 if e2e_b else None, "unit": "GB/s",
+                 "peak": pcie[2] if pcie else None,
+                 "peak_source": "measured (copy engines, both directions at once)",
+                 "frac": e2e_b / e2e_s / 1e9 / pcie[2] if pcie and e2e_b else None,
+                 "d2h_bound_frac": (r["e2e"]["d2h_bytes_per_step"] or 0) / e2e_s / 1e9 / pcie[1]
+                 if pcie else None}
     n_gpus = int(os.environ.get("WORLD_SIZE", "1"))
     out = {"metric": GAT_METRIC, "value": r["value"], "unit": "GTEPS",
            "n_gpus": n_gpus if n_gpus > 1 else args.gpus,
@@ -649,6 +659,7 @@ def gat_config_line(args, cfg, config, p, plan, ds, rk, slowest, hbm_peak, hbm_s
                         "share_of_step": ek["share_of_step"]},
            "gemm": r["gemm"], "gpu_launches": r["gpu_launches"],
            "gpu_launches_e2e": r["gpu_launches_e2e"], "cpu_baseline": cpu,
+           "roofline_pcie": pcie_line,
            "clocks": clk.summary(), "losses": r["losses"]}
     return out
 
