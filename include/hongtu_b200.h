@@ -331,7 +331,9 @@ int ht_pcie_probe(int device, int64_t bytes, double* out);
 
 /* GEMM unit entry for tests: runs the launchers the layer drivers use on
  * host arrays (device 0).  op 0: C = relu(A W); 1: C = [A W > 0] * G;
- * 2: C = A W^T (A: M x N, W: K x N); 3: C = A^T G (A: M x K, G: M x N).
+ * 2: C = A W^T (A: M x N, W: K x N); 3: C = A^T G (A: M x K, G: M x N);
+ * 4: C = (G * [A > 0]) W^T, 5: C = the TF32-rounded G * [A > 0] that op 4
+ * writes beside it (A: M x N; TF32 only - the backward's ReLU'-masked GEMM).
  * precision HT_PREC_FP32 (SIMT) or HT_PREC_TF32 (tcgen05). */
 int ht_gemm_test(int op, int precision, const float* A, const float* W, const float* G,
                  float* C, int64_t M, int K, int N);

@@ -361,6 +361,9 @@ extern "C" int ht_fleet_finalize(ht_fleet* f) {
       HT_TRY(upload(c.nbr_slot, nbr_slot, s));
       if (h.has_dest) {
         HT_TRY(upload(c.dest_rows, h.dest, s));
+        c.dest_ident = true;
+        for (int64_t r = 0; r < (int64_t)h.dest.size() && c.dest_ident; ++r)
+          c.dest_ident = h.dest[r] == r;
         std::vector<int64_t> pos(h.dest.size());
         std::iota(pos.begin(), pos.end(), 0);
         make_runs(c.dest, h.dest, pos, nullptr);

@@ -147,6 +147,7 @@ struct DevChunk {
   int64_t nv = 0, nn = 0, ne = 0, nlive = 0;
   DBuf nbr_slot;   // int64 [nn]
   DBuf dest_rows;  // int64 [nv]
+  bool dest_ident = false;  // dest_rows[r] == r for every r (one device, one batch)
   CopyList dest;   // runs of (host row = dest_rows[r], staging row r)
   std::vector<int64_t> dest_pos;  // [kChunks+1]: first staging row of each host-row chunk
   CopyList h2d;    // host row -> slot
@@ -282,6 +283,7 @@ using namespace htf;
 struct Switches {
   bool no_project_first = false, no_narrow_bwd = false, no_gat_direct = false;
   bool no_direct_bwd = false, no_direct_read = false, no_recompute = false, no_gat_split = false;
+  bool no_mask_fold = false;
   void read() {
     auto on = [](const char* k) { const char* e = getenv(k); return e && *e && atoi(e) != 0; };
     no_project_first = on("HT_NO_PROJECT_FIRST");
@@ -291,6 +293,7 @@ struct Switches {
     no_direct_read = on("HT_NO_DIRECT_READ");
     no_recompute = on("HT_NO_RECOMPUTE");
     no_gat_split = on("HT_NO_GAT_SPLIT");
+    no_mask_fold = on("HT_NO_MASK_FOLD");
   }
 };
 

@@ -398,7 +398,13 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       // A^T gz give dW = h^T (A^T gz); needs them in row order (expanded CSR)
       const bool pfl = layer < (int)f->agg_deferred.size() && f->agg_deferred[layer] &&
                        precision == HT_PREC_TF32;
-      if (HO && M > 0) {  // gz = g * (h > 0): z need not be recomputed
+      // gz = g * (h > 0) formed inside the gz . W^T GEMM (TMA loads of the g
+      // and h tiles, gz written back from the masked stage) when h's rows
+      // are the chunk rows; otherwise a separate masking pass
+      const bool fold = precision == HT_PREC_TF32 && HO && !hrows && !narrow && !no_in &&
+                        M > 0 && !f->sw.no_mask_fold && (d_out & 3) == 0 &&
+                        ((uintptr_t)G & 15) == 0 && ((uintptr_t)HO & 15) == 0;
+      if (HO && M > 0 && !fold) {  // gz = g * (h > 0): z need not be recomputed
         count_launch();
         ht::k_relu_mask<<<grid_for(M), kThreads, 0, d.stream>>>(GZ, ldz, G, HO, hrows, M, d_out);
         CU(cudaGetLastError());
@@ -407,7 +413,10 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
         if (!HO)
           HT_TRY(ht::tc::rows<ht::tc::TC_MASK>(d.stream, true, A, d_in, M, d_in, w.Wt_hi.as<float>(),
                                                w.Wt_lo.as<float>(), d_in, d_out, GZ, ldz, G, d_out));
-        if (!narrow && !no_in)
+        if (fold)
+          HT_TRY(ht::tc::rows_masked(d.stream, G, d_out, HO, d_out, GZ, ldz, M, d_out,
+                                     w.Wp_hi.as<float>(), ldz, d_in, GA, d_in));
+        else if (!narrow && !no_in)
           HT_TRY(ht::tc::rows<ht::tc::TC_STORE>(d.stream, false, GZ, ldz, M, d_out,
                                                 w.Wp_hi.as<float>(), nullptr, ldz, d_in, GA, d_in,
                                                 nullptr, 0));

@@ -70,7 +70,9 @@ extern "C" int ht_pcie_probe(int device, int64_t bytes, double* out /* [5] GB/s 
 // ---------------------------------------------------------------------------
 // GEMM unit entry (tests): the exact launchers the layer drivers use, on
 // host arrays.  op 0: C = relu(A W); 1: C = [A W > 0] * G; 2: C = A W^T
-// (A is M x N, W is K x N); 3: C = A^T G (A is M x K, G is M x N).
+// (A is M x N, W is K x N); 3: C = A^T G (A is M x K, G is M x N);
+// 4: C = (G * [A > 0]) W^T and 5: C = that gz (M x N, TF32-rounded) - the
+// masked-A GEMM of the backward (A is h, M x N; TF32 only).
 // precision: HT_PREC_FP32 (SIMT) or HT_PREC_TF32 (tcgen05; 3xTF32 for ops
 // 0/1, 1xTF32 for ops 2/3).
 // ---------------------------------------------------------------------------
@@ -81,19 +83,20 @@ extern "C" int ht_gemm_test(int op, int precision, const float* A, const float* 
   CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   // row operands are staged with row strides padded to 4 floats (the TMA
   // alignment rule the layer drivers follow for their own staging)
-  const int ka = op == 2 ? N : K, lda = pad4(ka), ldn = pad4(N);
-  const int64_t c_rows = op == 3 ? K : M, c_cols = op == 2 ? K : N;
+  const int ka = (op == 2 || op >= 4) ? N : K, lda = pad4(ka), ldn = pad4(N);
+  const int64_t c_rows = op == 3 ? K : M, c_cols = (op == 2 || op == 4) ? K : N;
   Device d;
   d.stream = s;
-  DBuf dA, dG, dC, ws;
+  DBuf dA, dG, dC, ws, dZ;
   HT_TRY(dA.ensure(std::max<int64_t>(1, M * lda) * 4));
+  if (op >= 4) HT_TRY(dZ.ensure(std::max<int64_t>(1, M * ldn) * 4));
   HT_TRY(dG.ensure(std::max<int64_t>(1, M * ldn) * 4));
-  HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * c_cols) * 4));
+  HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * std::max<int64_t>(c_cols, op == 5 ? K : 0)) * 4));
   HT_TRY(ws.ensure((int64_t)148 * K * N * 4 + 4));
   CU(cudaMemcpy2D(dA.p, lda * 4, A, ka * 4, ka * 4, M, cudaMemcpyHostToDevice));
   if (G) CU(cudaMemcpy2D(dG.p, ldn * 4, G, N * 4, N * 4, M, cudaMemcpyHostToDevice));
   if (W) HT_TRY(upload_weights(d, W, K, N));
-  CU(cudaMemset(dC.p, 0, c_rows * c_cols * 4));
+  CU(cudaMemset(dC.p, 0, dC.bytes));
   const bool tc = precision == HT_PREC_TF32;
   int rc = HT_OK;
   if (op == 0) {
@@ -128,14 +131,22 @@ extern "C" int ht_gemm_test(int op, int precision, const float* A, const float* 
       ht::k_reduce_splits<<<64, 256, 0, s>>>(dC.as<float>(), ws.as<float>(), (int64_t)K * N, used);
       CU(cudaGetLastError());
     }
+  } else if (op == 4 || op == 5) {
+    if (!tc) rc = fail(HT_EINVAL, "masked-A GEMM is TF32 only");
+    else
+      rc = ht::tc::rows_masked(s, dG.as<float>(), ldn, dA.as<float>(), lda, dZ.as<float>(), ldn, M,
+                               N, d.Wp_hi.as<float>(), pad4(N), K, dC.as<float>(), K);
   } else {
     rc = fail(HT_EINVAL, "unknown gemm op %d", op);
   }
   if (rc == HT_OK) {
     CU(cudaStreamSynchronize(s));
-    CU(cudaMemcpy(C, dC.p, c_rows * c_cols * 4, cudaMemcpyDeviceToHost));
+    if (op == 5)
+      CU(cudaMemcpy2D(C, N * 4, dZ.p, ldn * 4, N * 4, M, cudaMemcpyDeviceToHost));
+    else
+      CU(cudaMemcpy(C, dC.p, c_rows * c_cols * 4, cudaMemcpyDeviceToHost));
   }
-  for (DBuf* b : {&dA, &dG, &dC, &ws, &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo})
+  for (DBuf* b : {&dA, &dG, &dC, &ws, &dZ, &d.W, &d.Wt, &d.Wp, &d.Wt_hi, &d.Wt_lo, &d.Wp_hi, &d.Wp_lo})
     b->release();
   cudaStreamDestroy(s);
   return rc;
@@ -166,14 +177,15 @@ extern "C" int ht_gemm_rate(int op, int precision, int64_t M, int K, int N, int 
   if (iters <= 0) return fail(HT_EINVAL, "gemm rate: iters %d", iters);
   cudaStream_t s = nullptr;
   CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  const int ka = op == 2 ? N : K, lda = pad4(ka), ldn = pad4(N);
-  const int64_t c_rows = op == 3 ? K : M, c_cols = op == 2 ? K : N;
+  const int ka = (op == 2 || op >= 4) ? N : K, lda = pad4(ka), ldn = pad4(N);
+  const int64_t c_rows = op == 3 ? K : M, c_cols = (op == 2 || op == 4) ? K : N;
   Device d;
   d.stream = s;
-  DBuf dA, dG, dC, ws;
+  DBuf dA, dG, dC, ws, dZ;
   HT_TRY(dA.ensure(std::max<int64_t>(1, M * lda) * 4));
+  if (op >= 4) HT_TRY(dZ.ensure(std::max<int64_t>(1, M * ldn) * 4));
   HT_TRY(dG.ensure(std::max<int64_t>(1, M * ldn) * 4));
-  HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * c_cols) * 4));
+  HT_TRY(dC.ensure(std::max<int64_t>(1, c_rows * std::max<int64_t>(c_cols, op == 5 ? K : 0)) * 4));
   HT_TRY(ws.ensure((int64_t)148 * K * N * 4 + 4));
   // operands: a fixed bit pattern in [-1, 1) (values do not affect timing)
   count_launch(2);

@@ -605,7 +605,7 @@ const float* hbm_outputs(ht_fleet* f, Device& d, int j, int layer, int d_out,
   if (layer + 1 == f->L) return d.hL.as<float>() + d.hL_off[j] * d_out;
   if (d.cache) return d.mh[layer + 1].as<float>() + c.dest_m0 * d_out;
   if ((int)f->hdev.size() > layer + 1 && f->hdev[layer + 1]) {
-    *rows = c.dest_rows.as<int64_t>();
+    *rows = c.dest_ident ? nullptr : c.dest_rows.as<int64_t>();  // (identity: row r is r)
     return static_cast<const float*>(f->hptr[layer + 1]);
   }
   return nullptr;

@@ -58,10 +58,11 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
   return d;
 }
 
-// instruction descriptor: A,B = TF32 (K-major), D = F32, M = 128, N = n
-__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+// instruction descriptor: A,B = TF32 (K-major), D = F32, M = m (128, or
+// 256 for a CTA pair), N = n
+__host__ __device__ constexpr uint32_t idesc_tf32(int n, int m = 128) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
+         ((uint32_t)(m >> 4) << 24);
 }
 
 __host__ __device__ constexpr uint32_t tmem_cols(int n) {
@@ -75,6 +76,71 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// CTA pair (cta_group::2, issued by the leader CTA): A rows split across the
+// pair (each CTA's smem holds its 128 rows), B columns split (each holds
+// N/2), D rows in each CTA's own TMEM lanes
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// the pair's MMAs done -> arrive on the barrier at this offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+// shared::cluster address of the same barrier in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t peer_bar(uint64_t* bar, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(bar)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// wait with cluster-scope acquire (arrivals come from the peer CTA too)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -215,33 +281,43 @@ enum { TC_STORE = 0, TC_RELU = 1, TC_MASK = 2 };
 // K-major N x K matrix (tensor maps tmBh / tmBl); A through tmA (row-major,
 // lda*4 bytes per row).  BN >= N, multiple of 32.
 // ---------------------------------------------------------------------------
-template <int BN, bool SPLIT>
+// AM (masked-A, 1xTF32 only): the A operand is g * (h > 0) - TMA brings
+// the g and h tiles (h in the A-lo slot), the converters mask and round in
+// place, and one converter thread stores the masked tile to Z by TMA (the
+// ReLU'-mask of the GCN backward folded into the gz . W^T GEMM: gz is
+// written once here instead of by a separate read-g-read-h-write-gz pass).
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes 256-row tiles with
+// M = 256 MMAs; each CTA stages its 128 A rows and half of B's BN rows.
+template <int BN, bool SPLIT, bool AM = false, bool PAIR = false>
 struct GemmCfg {
   static constexpr int A_BYTES = 128 * 128;
-  static constexpr int B_BYTES = BN * 128;
-  static constexpr int STAGE = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * 128;
+  static constexpr int STAGE = ((SPLIT || AM) ? 2 : 1) * A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;
   static constexpr int STAGES = (200 * 1024 / STAGE) < 4 ? (200 * 1024 / STAGE) : 4;
-  static constexpr int TX = A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;  // TMA bytes per stage
+  static constexpr int TX = (AM ? 2 : 1) * A_BYTES + (SPLIT ? 2 : 1) * B_BYTES;  // TMA bytes per stage
   // epilogue staging: per warp two 32 x 32 swizzled tiles for the TMA
   // stores (or one padded 32 x 33 transpose tile on the scalar-store path)
   static constexpr int EPI_BYTES = 4 * 2 * 32 * 32 * 4;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + EPI_BYTES + 256;
 };
 
-template <int BN, bool SPLIT, int EPI>
+template <int BN, bool SPLIT, int EPI, bool AM = false, bool PAIR = false>
 __global__ void __launch_bounds__(256, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmBh,
               const __grid_constant__ CUtensorMap tmBl, const __grid_constant__ CUtensorMap tmC,
+              const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmZ,
               int tma_store, int64_t M, int K, int N, float* __restrict__ C, int64_t ldc,
               const float* __restrict__ G, int64_t ldg) {
-  using Cfg = GemmCfg<BN, SPLIT>;
+  static_assert(!(AM && SPLIT), "masked A is a 1xTF32 operand");
+  static_assert(!(AM && PAIR), "masked A runs on single CTAs");
+  using Cfg = GemmCfg<BN, SPLIT, AM, PAIR>;
   constexpr int ST = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  // stage s: [A hi (raw)][A lo][B hi][B lo]
+  // stage s: [A hi (raw)][A lo | h tile (AM)][B hi][B lo]
   auto sA = [&](int s) { return smem + (size_t)s * Cfg::STAGE; };
   auto sAlo = [&](int s) { return sA(s) + Cfg::A_BYTES; };
-  auto sBh = [&](int s) { return sA(s) + (SPLIT ? 2 : 1) * Cfg::A_BYTES; };
+  auto sBh = [&](int s) { return sA(s) + ((SPLIT || AM) ? 2 : 1) * Cfg::A_BYTES; };
   auto sBl = [&](int s) { return sBh(s) + Cfg::B_BYTES; };
   uint8_t* epi = smem + (size_t)ST * Cfg::STAGE;  // 1024-aligned
   uint64_t* bar = reinterpret_cast<uint64_t*>(epi + Cfg::EPI_BYTES);
@@ -254,51 +330,66 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t NCOL = tmem_cols(2 * BN);
-  if (warp == 1) tmem_alloc(slot, NCOL);
+  // PAIR: rank 0 (the leader) issues the MMAs; its conv / tempty barriers
+  // also count the peer's converters / epilogue warps (remote arrivals)
+  const uint32_t rank = PAIR ? cluster_rank() : 0;
+  constexpr int TM = PAIR ? 256 : 128;  // rows per tile
+  const int64_t first = PAIR ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+  const int64_t step = PAIR ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair(slot, NCOL);
+    else tmem_alloc(slot, NCOL);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 64);
-      mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], PAIR ? 128 : 64);
+      mbar_init(&empty[s], AM ? 2 : 1);  // (AM: + the Z store has read the stage)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], PAIR ? 8 : 4);  // one arrival per epilogue warp
     }
     fence_barrier_init();
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
   const int KC = (K + 31) >> 5;
-  const int64_t ntiles = (M + 127) >> 7;
+  const int64_t ntiles = (M + TM - 1) / TM;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
       int it = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+      const int brow = PAIR ? (int)rank * (BN / 2) : 0;  // this CTA's half of B
+      for (int64_t t = first; t < ntiles; t += step)
         for (int kc = 0; kc < KC; ++kc, ++it) {
           const int s = it % ST;
+          const int arow = (int)(t * TM) + (int)rank * 128;
           mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
           mbar_expect_tx(&full[s], Cfg::TX);
-          tma_load_2d(sA(s), &tmA, &full[s], kc * 32, (int)(t * 128));
-          tma_load_2d(sBh(s), &tmBh, &full[s], kc * 32, 0);
-          if (SPLIT) tma_load_2d(sBl(s), &tmBl, &full[s], kc * 32, 0);
+          tma_load_2d(sA(s), &tmA, &full[s], kc * 32, arow);
+          if (AM) tma_load_2d(sAlo(s), &tmH, &full[s], kc * 32, arow);
+          tma_load_2d(sBh(s), &tmBh, &full[s], kc * 32, brow);
+          if (SPLIT) tma_load_2d(sBl(s), &tmBl, &full[s], kc * 32, brow);
         }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer ----------------
-      const uint32_t idesc = idesc_tf32(BN);
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer ----------------
+      const uint32_t idesc = idesc_tf32(BN, TM);
       int it = 0, acc = 0;
-      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
+      for (int64_t t = first; t < ntiles; t += step, ++acc) {
         const int a = acc & 1;
-        mbar_wait(&tempty[a], ((acc >> 1) & 1) ^ 1);
+        if (PAIR) mbar_wait_cluster(&tempty[a], ((acc >> 1) & 1) ^ 1);
+        else mbar_wait(&tempty[a], ((acc >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(a * BN);
         for (int kc = 0; kc < KC; ++kc, ++it) {
           const int s = it % ST;
-          mbar_wait(&conv[s], (it / ST) & 1);
+          if (PAIR) mbar_wait_cluster(&conv[s], (it / ST) & 1);
+          else mbar_wait(&conv[s], (it / ST) & 1);
           tc_fence_after();
           const uint32_t ah = smem_u32(sA(s)), al = smem_u32(sAlo(s));
           const uint32_t bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
@@ -309,21 +400,32 @@ __global__ void __launch_bounds__(256, 1)
           for (int ks = 0; ks < 4; ++ks) {
             if (ks >= nks) break;
             const uint64_t dah = sdesc(ah + ks * 32), dbh = sdesc(bh + ks * 32);
-            mma_tf32(d, dah, dbh, idesc, (kc | ks) != 0);
-            if (SPLIT) {
-              mma_tf32(d, dah, sdesc(bl + ks * 32), idesc, 1);
-              mma_tf32(d, sdesc(al + ks * 32), dbh, idesc, 1);
+            if (PAIR) {
+              mma_tf32_pair(d, dah, dbh, idesc, (kc | ks) != 0);
+              if (SPLIT) {
+                mma_tf32_pair(d, dah, sdesc(bl + ks * 32), idesc, 1);
+                mma_tf32_pair(d, sdesc(al + ks * 32), dbh, idesc, 1);
+              }
+            } else {
+              mma_tf32(d, dah, dbh, idesc, (kc | ks) != 0);
+              if (SPLIT) {
+                mma_tf32(d, dah, sdesc(bl + ks * 32), idesc, 1);
+                mma_tf32(d, sdesc(al + ks * 32), dbh, idesc, 1);
+              }
             }
           }
-          mma_commit(&empty[s]);
+          if (PAIR) mma_commit_pair(&empty[s]);
+          else mma_commit(&empty[s]);
         }
-        mma_commit(&tfull[a]);
+        if (PAIR) mma_commit_pair(&tfull[a]);
+        else mma_commit(&tfull[a]);
       }
     }
   } else if (warp < 4) {  // ---------------- converters (64 threads) ----------------
     const int ct = threadIdx.x - 64;
+    const uint32_t conv0 = PAIR ? peer_bar(conv, 0) : 0;  // the leader's conv[0]
     int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+    for (int64_t t = first; t < ntiles; t += step)
       for (int kc = 0; kc < KC; ++kc, ++it) {
         const int s = it % ST;
         mbar_wait(&full[s], (it / ST) & 1);
@@ -331,14 +433,41 @@ __global__ void __launch_bounds__(256, 1)
         float4* lo = reinterpret_cast<float4*>(sAlo(s));
 #pragma unroll 4
         for (int q = ct; q < Cfg::A_BYTES / 16; q += 64) {
-          const float4 v = hi[q];
+          float4 v = hi[q];
+          if (AM) {  // gz = g * (h > 0) (same swizzled position in both tiles)
+            const float4 m = lo[q];
+            v = make_float4(m.x > 0.f ? v.x : 0.f, m.y > 0.f ? v.y : 0.f, m.z > 0.f ? v.z : 0.f,
+                            m.w > 0.f ? v.w : 0.f);
+          }
           const float4 h = make_float4(tf32_rna(v.x), tf32_rna(v.y), tf32_rna(v.z), tf32_rna(v.w));
           hi[q] = h;
           if (SPLIT) lo[q] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
         }
         fence_proxy_async();
-        mbar_arrive(&conv[s]);
+        if (PAIR) mbar_arrive_cluster(conv0 + (uint32_t)s * 8u);
+        else mbar_arrive(&conv[s]);
+        if (AM && ct == 0) {
+          // every converter's writes are in (conv phase complete): the
+          // rounded gz tile leaves by TMA (RNA rounding is idempotent, so
+          // k_tc_wgrad's own rounding of it is unchanged); the stage is
+          // released to the producer once the store has read it (lagging
+          // one stage so the wait rarely blocks)
+          mbar_wait(&conv[s], (it / ST) & 1);
+          tma_store_2d(&tmZ, sA(s), kc * 32, (int)(t * 128));
+          bulk_commit();
+          if (it > 0) {
+            bulk_wait_read<1>();
+            mbar_arrive(&empty[(it - 1) % ST]);
+          }
+        }
       }
+    if (AM && ct == 0) {
+      if (it > 0) {
+        bulk_wait_read<0>();
+        mbar_arrive(&empty[(it - 1) % ST]);
+      }
+      bulk_wait_all();
+    }
   } else if (tma_store) {  // ---------------- epilogue (warps 4-7), TMA stores ----------------
     // TMEM gives a thread one row; each 32-column block goes to a 32 x 32
     // SWIZZLE_128B smem tile (16-byte chunk j of row r at j ^ (r & 7):
@@ -348,12 +477,13 @@ __global__ void __launch_bounds__(256, 1)
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
     float* tiles = reinterpret_cast<float*>(epi) + q4 * 2 * 32 * 32;
     const bool g4 = (ldg & 3) == 0 && ((uintptr_t)G & 15) == 0;
+    const uint32_t tempty0 = PAIR ? peer_bar(tempty, 0) : 0;
     int acc = 0, buf = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
+    for (int64_t t = first; t < ntiles; t += step, ++acc) {
       const int a = acc & 1;
       mbar_wait(&tfull[a], (acc >> 1) & 1);
       tc_fence_after();
-      const int64_t r0 = t * 128 + q4 * 32;
+      const int64_t r0 = t * TM + rank * 128 + q4 * 32;
       const uint32_t base = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(a * BN);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -401,7 +531,11 @@ __global__ void __launch_bounds__(256, 1)
         buf ^= 1;
       }
       tc_fence_before();
-      mbar_arrive(&tempty[a]);
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(tempty0 + (uint32_t)a * 8u);
+        else mbar_arrive(&tempty[a]);
+      }
     }
     if (lane == 0) bulk_wait_all();
   } else {  // ---------------- epilogue (warps 4-7), scalar stores ----------------
@@ -410,12 +544,13 @@ __global__ void __launch_bounds__(256, 1)
     // stores (and G loads) per warp instruction
     const int q4 = warp & 3;  // TMEM lane quarter this warp may access
     float* tile = reinterpret_cast<float*>(epi) + q4 * 32 * 33;
+    const uint32_t tempty0 = PAIR ? peer_bar(tempty, 0) : 0;
     int acc = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++acc) {
+    for (int64_t t = first; t < ntiles; t += step, ++acc) {
       const int a = acc & 1;
       mbar_wait(&tfull[a], (acc >> 1) & 1);
       tc_fence_after();
-      const int64_t r0 = t * 128 + q4 * 32;
+      const int64_t r0 = t * TM + rank * 128 + q4 * 32;
       const uint32_t base = tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(a * BN);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -450,14 +585,20 @@ __global__ void __launch_bounds__(256, 1)
         __syncwarp();
       }
       tc_fence_before();
-      mbar_arrive(&tempty[a]);
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(tempty0 + (uint32_t)a * 8u);
+        else mbar_arrive(&tempty[a]);
+      }
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();  // (the leader's MMAs read the peer's smem / TMEM)
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, NCOL);
+    if (PAIR) tmem_dealloc_pair(tmem, NCOL);
+    else tmem_dealloc(tmem, NCOL);
   }
 }
 
@@ -692,15 +833,24 @@ inline int sm_count() {
   return n;
 }
 
-template <int BN, bool SPLIT, int EPI>
+template <int BN, bool SPLIT, int EPI, bool AM = false, bool PAIR = false>
 inline int launch_gemm_t(cudaStream_t s, const float* A, int64_t lda, int64_t M, int K, const float* Bh,
                   const float* Bl, int64_t ldb, int N, float* C, int64_t ldc, const float* G,
-                  int64_t ldg) {
-  using Cfg = GemmCfg<BN, SPLIT>;
-  CUtensorMap ta, tbh, tbl, tc_;
+                  int64_t ldg, const float* Hm = nullptr, int64_t ldh = 0, float* Z = nullptr,
+                  int64_t ldz = 0) {
+  using Cfg = GemmCfg<BN, SPLIT, AM, PAIR>;
+  constexpr int BR = PAIR ? BN / 2 : BN;  // B rows staged per CTA
+  CUtensorMap ta, tbh, tbl, tc_, th, tz;
   HT_TRY(tmap(&ta, A, M, K, lda, 32, 128, true));
-  HT_TRY(tmap(&tbh, Bh, N, K, ldb, 32, BN, true));
-  HT_TRY(tmap(&tbl, SPLIT ? Bl : Bh, N, K, ldb, 32, BN, true));
+  if (AM) {  // h tiles like A's; Z is written ldz columns wide (zero pad columns)
+    HT_TRY(tmap(&th, Hm, M, K, ldh, 32, 128, true));
+    HT_TRY(tmap(&tz, Z, M, ldz, ldz, 32, 128, true));
+  } else {
+    th = ta;  // (unused)
+    tz = ta;
+  }
+  HT_TRY(tmap(&tbh, Bh, N, K, ldb, 32, BR, true));
+  HT_TRY(tmap(&tbl, SPLIT ? Bl : Bh, N, K, ldb, 32, BR, true));
   // TMA stores of the output when its rows are 16-byte aligned
   static const bool no_tma_store = [] {
     const char* e = getenv("HT_NO_TMA_STORE");
@@ -709,13 +859,32 @@ inline int launch_gemm_t(cudaStream_t s, const float* A, int64_t lda, int64_t M,
   const int use_tma = !no_tma_store && ((uintptr_t)C & 15) == 0 && (ldc & 3) == 0;
   if (use_tma) HT_TRY(tmap(&tc_, C, M, N, ldc, 32, 32, true));
   else tc_ = ta;  // (unused)
-  auto kern = k_tc_gemm<BN, SPLIT, EPI>;
+  auto kern = k_tc_gemm<BN, SPLIT, EPI, AM, PAIR>;
   cudaError_t e =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
   if (e != cudaSuccess) return fail(HT_ECUDA, "tc smem attribute: %s", cudaGetErrorString(e));
+  if (PAIR) {  // persistent CTA pairs (clusters of 2: the two SMs of a TPC)
+    const int64_t ntiles = (M + 255) / 256;
+    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count() / 2));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, ta, tbh, tbl, tc_, th, tz, use_tma, M, K, N, C, ldc, G, ldg);
+    if (e != cudaSuccess) return fail(HT_ECUDA, "k_tc_gemm pair launch: %s", cudaGetErrorString(e));
+    return HT_OK;
+  }
   const int64_t ntiles = (M + 127) / 128;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, sm_count()));
-  kern<<<grid, 256, Cfg::SMEM, s>>>(ta, tbh, tbl, tc_, use_tma, M, K, N, C, ldc, G, ldg);
+  kern<<<grid, 256, Cfg::SMEM, s>>>(ta, tbh, tbl, tc_, th, tz, use_tma, M, K, N, C, ldc, G, ldg);
   e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HT_ECUDA, "k_tc_gemm launch: %s", cudaGetErrorString(e));
   return HT_OK;
@@ -730,6 +899,18 @@ inline int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t
   if (M <= 0 || N <= 0) return HT_OK;
   if (K < 1 || N > 256) return fail(HT_EINVAL, "tcgen05 GEMM supports N <= 256 (got %d)", N);
   if (split) {
+    // 3xTF32 with N > 128: CTA pairs (M = 256 MMAs, half of B per SM) -
+    // the 128 x 256 single-CTA tile is bound by shared-memory bandwidth
+    // (three MMAs per k step each reading A and all of B).  Narrower
+    // tiles are HBM-bound and the pair handshake per stage costs more than
+    // it saves there (N = 64: 1.38 vs 0.81 ms at cfg 2).  HT_NO_PAIR=1:
+    // single CTAs throughout.
+    static const bool no_pair = [] {
+      const char* e = getenv("HT_NO_PAIR");
+      return e && atoi(e);
+    }();
+    if (!no_pair && N > 128)
+      return launch_gemm_t<256, true, EPI, false, true>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
     if (N <= 32) return launch_gemm_t<32, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
     if (N <= 64) return launch_gemm_t<64, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
     if (N <= 128) return launch_gemm_t<128, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
@@ -739,6 +920,20 @@ inline int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t
   if (N <= 64) return launch_gemm_t<64, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
   if (N <= 128) return launch_gemm_t<128, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
   return launch_gemm_t<256, false, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
+}
+
+// C = (gz . B^T) with gz = G * (H > 0) formed in the GEMM and written to Z
+// (ldz >= K columns, pad columns zero; TF32-rounded, RNA) - 1xTF32; G and H
+// are M x K with row strides ldg / ldh.
+inline int rows_masked(cudaStream_t s, const float* G, int64_t ldg, const float* Hm, int64_t ldh,
+                       float* Z, int64_t ldz, int64_t M, int K, const float* Bh, int64_t ldb,
+                       int N, float* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return HT_OK;
+  if (K < 1 || N > 256 || ldz < K) return fail(HT_EINVAL, "masked tcgen05 GEMM: N <= 256, ldz >= K");
+  if (N <= 32) return launch_gemm_t<32, false, TC_STORE, true>(s, G, ldg, M, K, Bh, nullptr, ldb, N, C, ldc, nullptr, 0, Hm, ldh, Z, ldz);
+  if (N <= 64) return launch_gemm_t<64, false, TC_STORE, true>(s, G, ldg, M, K, Bh, nullptr, ldb, N, C, ldc, nullptr, 0, Hm, ldh, Z, ldz);
+  if (N <= 128) return launch_gemm_t<128, false, TC_STORE, true>(s, G, ldg, M, K, Bh, nullptr, ldb, N, C, ldc, nullptr, 0, Hm, ldh, Z, ldz);
+  return launch_gemm_t<256, false, TC_STORE, true>(s, G, ldg, M, K, Bh, nullptr, ldb, N, C, ldc, nullptr, 0, Hm, ldh, Z, ldz);
 }
 
 template <int KT, int BN>

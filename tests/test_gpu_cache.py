@@ -404,3 +404,34 @@ def test_budget_too_small_for_the_mirrors():
             with pytest.raises(H.ChunktrainError, match="recompute"):
                 H.train_epoch(p, fleet, model, host, ds.labels, ds.mask)
         fleet.close()
+
+
+@pytest.mark.parametrize("placement,cache", [("host", "on"), ("device", "off")])
+def test_mask_fold_bitwise(placement, cache, monkeypatch):
+    """The ReLU'-mask folded into the backward's gz . W^T GEMM (g and h tiles
+    by TMA, gz written from the masked stage; ht_gcn.cu) against the separate
+    masking pass (HT_NO_MASK_FOLD=1): the same TF32-rounded gz feeds both
+    GEMMs, so two epochs are bitwise equal - loss, weights, h, grad_h.  Both
+    layouts of h^{l+1} in HBM: the owner-cache mirror and an HBM store."""
+    ds = H.synth_dataset(H.SynthSpec(num_vertices=3000, avg_degree=9.0, seed=9), 16, 8)
+    p = H.split_chunks(ds.graph, H.partition_vertices(ds.graph, 1, seed=9), 1)
+    plan = H.plan_for_partition(p)
+    dims = [16, 32, 32, 8]  # layers 0 / 1 run gz . W^T; layer 2 is narrow
+    out = {}
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("HT_NO_MASK_FOLD", flag)
+        else:
+            monkeypatch.delenv("HT_NO_MASK_FOLD", raising=False)
+        model = H.init_model("gcn", dims, seed=5, lr=0.1, dtype=np.float32)
+        host = H.HostStore(ds.graph.num_vertices, dims, dtype=np.float32, placement=placement)
+        host.set_features(ds.features)
+        fleet = H.DeviceFleet(plan, mode="full", dtype=np.float32, cache=cache)
+        losses = [H.train_epoch(p, fleet, model, host, ds.labels, ds.mask).loss for _ in range(2)]
+        out[flag] = (losses, [w.copy() for w in model.weights],
+                     [np.array(x) for x in host.h[1:]], [np.array(g) for g in host.grad_h])
+        fleet.close()
+    a, b = out["1"], out[None]
+    assert a[0] == b[0]
+    for x, y in zip(a[1] + a[2] + a[3], b[1] + b[2] + b[3]):
+        np.testing.assert_array_equal(x, y)
