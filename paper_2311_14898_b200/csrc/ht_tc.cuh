@@ -899,17 +899,20 @@ inline int rows(cudaStream_t s, bool split, const float* A, int64_t lda, int64_t
   if (M <= 0 || N <= 0) return HT_OK;
   if (K < 1 || N > 256) return fail(HT_EINVAL, "tcgen05 GEMM supports N <= 256 (got %d)", N);
   if (split) {
-    // 3xTF32 with N > 128: CTA pairs (M = 256 MMAs, half of B per SM) -
-    // the 128 x 256 single-CTA tile is bound by shared-memory bandwidth
-    // (three MMAs per k step each reading A and all of B).  Narrower
-    // tiles are HBM-bound and the pair handshake per stage costs more than
-    // it saves there (N = 64: 1.38 vs 0.81 ms at cfg 2).  HT_NO_PAIR=1:
-    // single CTAs throughout.
-    static const bool no_pair = [] {
-      const char* e = getenv("HT_NO_PAIR");
+    // HT_PAIR=1: 3xTF32 with N > 128 on CTA pairs (M = 256 MMAs, half of B
+    // per SM) - the 128 x 256 single-CTA tile is bound by shared-memory
+    // bandwidth (three MMAs per k step each reading A and all of B).  The
+    // pair kernel is faster alone (cfg 2, N = 256: 2.65 vs 2.89 ms for the
+    // two launches, ncu) but the value epoch measured 0.3 ms slower with it
+    // (42.5 vs 42.2 ms, three interleaved runs, sw_power_cap active), so
+    // single CTAs are the default.  Narrower tiles are HBM-bound and the
+    // pair handshake per stage costs more than it saves (N = 64: 1.38 vs
+    // 0.81 ms), so pairs never apply to N <= 128.
+    static const bool pair = [] {
+      const char* e = getenv("HT_PAIR");
       return e && atoi(e);
     }();
-    if (!no_pair && N > 128)
+    if (pair && N > 128)
       return launch_gemm_t<256, true, EPI, false, true>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
     if (N <= 32) return launch_gemm_t<32, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);
     if (N <= 64) return launch_gemm_t<64, true, EPI>(s, A, lda, M, K, Bh, Bl, ldb, N, C, ldc, G, ldg);

@@ -35,11 +35,12 @@ def dataset(V=3000):
     return g, X, y, mask
 
 
-def run(g, X, y, mask, kind, m, n, placement, cache, budget=None, rank=None):
+def run(g, X, y, mask, kind, m, n, placement, cache, budget=None, rank=None, dims=None):
     a = H.partition_vertices(g, m, seed=3)
     p = H.split_chunks(g, a, n)
     plan = H.plan_for_partition(p)
-    dims = [16, 24, 8] if kind == "gcn" else [16, 12, 8]
+    if dims is None:
+        dims = [16, 24, 8] if kind == "gcn" else [16, 12, 8]
     model = H.init_model(kind, dims, seed=3, dtype=np.float32)
     host = H.HostStore(g.num_vertices, dims, dtype=np.float32, placement=placement)
     host.set_features(X)
@@ -49,7 +50,7 @@ def run(g, X, y, mask, kind, m, n, placement, cache, budget=None, rank=None):
     if kind == "gcn" and rank is None:
         _ = [np.asarray(host.agg[l]) for l in range(len(dims) - 1)]  # checkpoint reads
     fleet.close()
-    print(f"{kind} m={m} n={n} {placement} cache={cache} budget={budget} rank={rank}: "
+    print(f"{kind} {dims} m={m} n={n} {placement} cache={cache} budget={budget} rank={rank}: "
           f"loss {loss:.6f}", flush=True)
 
 
@@ -73,6 +74,10 @@ if __name__ == "__main__":
         run(g, X, y, mask, kind, 1, 1, "host", "auto")
         run(g, X, y, mask, kind, 2, 2, "host", "off")
         run(g, X, y, mask, kind, 2, 2, "host", "on")
+    # a 144-wide layer: the 3xTF32 forward GEMM on CTA pairs (N > 128) and the
+    # masked-A backward GEMM (gz formed from the g and h tiles) of session 3
+    run(g, X, y, mask, "gcn", 1, 1, "device", "auto", dims=[16, 144, 144, 8])
+    run(g, X, y, mask, "gcn", 1, 1, "host", "auto", dims=[16, 144, 144, 8])
     V = g.num_vertices
     # h + grad mirrors, project-first buffers, one 24-wide scratch: both agg^l recomputed
     run(g, X, y, mask, "gcn", 1, 1, "host", "on",

@@ -98,9 +98,9 @@ def test_masked_gemm_equals_mask_then_gemm(M, K, Nn):
 
 
 def test_pair_gemm_matches_single_cta():
-    """3xTF32 row GEMMs with N > 128 run on CTA pairs (cta_group::2, M = 256
-    MMAs, each SM staging half of the weights); HT_NO_PAIR=1 runs one CTA
-    per 128-row tile.
+    """HT_PAIR=1: 3xTF32 row GEMMs with N > 128 run on CTA pairs
+    (cta_group::2, M = 256 MMAs, each SM staging half of the weights); the
+    default runs one CTA per 128-row tile.
     Same operands, same k order, same three products per k step: the
     outputs agree to FP32 accumulation-order noise (checked bitwise-or-1ulp),
     including tiles whose second half lies past the last row."""
@@ -125,7 +125,7 @@ def test_pair_gemm_matches_single_cta():
     with tempfile.TemporaryDirectory() as td:
         for flag in ("0", "1"):
             f = os.path.join(td, "o%s.npz" % flag)
-            env = dict(os.environ, HT_NO_PAIR=flag)
+            env = dict(os.environ, HT_PAIR=flag)
             subprocess.run([sys.executable, "-c", code, f], check=True, env=env, timeout=600)
             z = np.load(f)
             res[flag] = [z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))]
