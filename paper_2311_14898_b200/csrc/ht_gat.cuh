@@ -134,16 +134,23 @@ constexpr int DU = HT_GAT_DU;
 #define HT_GAT_DB 8
 #endif
 constexpr int kDstBatch = HT_GAT_DB;  // destinations per work unit
-// minimum resident 256-thread CTAs per SM asked of ptxas (occupancy knob
-// for same-box A/B builds; the grids follow the occupancy they get)
+// Minimum resident 256-thread CTAs per SM asked of ptxas for the one-
+// float4-per-lane (d <= 128) row passes; the grids follow the occupancy
+// they get.  Both passes wait on random row fetches (long-scoreboard
+// stalls 12-17 per issue at 40 / 64 registers): forward at 8 CTAs (32
+// registers, 32 B of spill), S1 at 5 (48 registers) measured 59.2 -> 51.3
+// ms per cfg-2 GAT value epoch on one box (forward edge pass 13.6 -> 8.4
+// ms, backward 36.8 -> 30.9; profiles/r3_gat_occupancy_ab.txt).  Wider
+// rows (NV > 1) and the fused backward keep the compiler's choice (they
+// would spill hundreds of bytes).
 #ifndef HT_GAT_DST_MINB
-#define HT_GAT_DST_MINB 1
+#define HT_GAT_DST_MINB 8
 #endif
 #ifndef HT_GAT_S1_MINB
-#define HT_GAT_S1_MINB 1
+#define HT_GAT_S1_MINB 5
 #endif
 template <int NV, bool BWD>
-__global__ void __launch_bounds__(256, HT_GAT_DST_MINB) k_gat_dst(
+__global__ void __launch_bounds__(256, (NV == 1 && !BWD) ? HT_GAT_DST_MINB : 1) k_gat_dst(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
     const float* __restrict__ Q, const float* __restrict__ P, const float* __restrict__ el_src,
     const float* __restrict__ a_dst, int d, float slope, float* __restrict__ H,
@@ -626,7 +633,7 @@ __device__ __forceinline__ void src_rows_a(float4 (&acc)[NV], const float4 (&qu)
 // partial rows in piece order into GQ (k_seg_fixup's order).  counter and
 // tickets zeroed before the launch.
 template <int NV, int B>
-__global__ void __launch_bounds__(256, HT_GAT_S1_MINB) k_gat_bwd_s1_work(
+__global__ void __launch_bounds__(256, NV == 1 ? HT_GAT_S1_MINB : 1) k_gat_bwd_s1_work(
     const int64_t* __restrict__ off, const int32_t* __restrict__ dst,
     const int32_t* __restrict__ perm, int64_t nseg, int64_t split,
     const int64_t* __restrict__ lo, const int64_t* __restrict__ hi, const int32_t* __restrict__ pf,
