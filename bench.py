@@ -908,7 +908,7 @@ def main():
     lt, mst, tb = e2e["stats"][3]
     traffic, traffic_src = None, None
     try:  # DRAM bytes per bracket from the committed ncu launch list of this workload
-        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r3_traffic.json")) as fh:
             tj = json.load(fh)
         if tj.get("config_id") == args.config and tj.get("m") == m:
             traffic, traffic_src = tj["dram_bytes_per_launch"], tj["source"]
