@@ -196,6 +196,7 @@ struct TimerRec {
 
 struct Device {
   int ordinal = 0;
+  int gz_loss_ld = 0;  // > 0: the loss wrote the top layer's gz rows into sc (row stride)
   cudaStream_t stream = nullptr;
   cudaEvent_t ev = nullptr;
   int64_t cap = 0;
@@ -305,6 +306,9 @@ struct ht_fleet {
   bool finalized = false;
   int dim = 0, elem = 4;
   int hL_dim = 0;
+  // last forward layer was a GCN layer in this precision (-1: GAT / none):
+  // the loss then also writes the top layer's gz = g * (h^L > 0) rows
+  int top_gcn_prec = -1;
   bool timing = false;
   std::vector<TimerRec> timers;
   int64_t t_launch[4] = {0, 0, 0, 0};

@@ -460,7 +460,10 @@ extern "C" int ht_gat_forward_layer(ht_fleet* f, int layer, int d_in, int d_out,
     HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
     HT_TRY(upload_attn(d, layer, A, d_out));
   }
-  if (last) f->hL_dim = d_out;
+  if (last) {
+    f->hL_dim = d_out;
+    f->top_gcn_prec = -1;  // (the loss writes no GCN gz rows)
+  }
   for (int j = 0; j < f->n; ++j) {
     HT_TRY(gat_stage(f, layer, j, hin, d_in, nullptr, d_out, j == 0, false));
     for (int i = 0; i < f->m; ++i) {

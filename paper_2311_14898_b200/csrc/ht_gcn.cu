@@ -26,7 +26,10 @@ extern "C" int ht_forward_layer(ht_fleet* f, int layer, int d_in, int d_out, con
     HT_TRY(set_dev(d));
     HT_TRY(upload_layer_weights(d, layer, W, d_in, d_out));
   }
-  if (last) f->hL_dim = d_out;
+  if (last) {
+    f->hL_dim = d_out;
+    f->top_gcn_prec = precision;
+  }
   for (int j = 0; j < f->n; ++j) {
     // ---- step 1: host loads into slots (tin) ----
     for (int i = 0; i < f->m; ++i) {
@@ -245,6 +248,14 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
     CU(cudaMemcpyAsync(d.labels.p, d.lpin, V * 8, cudaMemcpyHostToDevice, d.stream));
     CU(cudaMemcpyAsync(d.mask.p, d.lpin + V * 8, V, cudaMemcpyHostToDevice, d.stream));
     CU(cudaMemsetAsync(d.loss_part.p, 0, (int64_t)blocks * f->n * 8, d.stream));
+    // one batch, GCN top layer: the loss also writes gz = g * (h^L > 0)
+    // (the top layer's ReLU' mask, with zero pad columns) into the GZ
+    // scratch the top backward reads - its separate masking pass is skipped
+    const int gz_ld = f->top_gcn_prec == HT_PREC_TF32 ? pad4(d_last) : d_last;
+    d.gz_loss_ld = 0;
+    const bool gz_fold = count > 0 && f->n == 1 && f->top_gcn_prec >= 0 &&
+                         !f->sw.no_mask_fold && d.chunks[0].nv > 0 &&
+                         d.sc.bytes >= d.chunks[0].nv * (int64_t)gz_ld * 4;
     if (count > 0)
       for (int j = 0; j < f->n; ++j) {
         DevChunk& c = d.chunks[j];
@@ -253,9 +264,11 @@ extern "C" int ht_loss(ht_fleet* f, int d_last, const int64_t* labels, const uin
             d.hL.as<float>() + d.hL_off[j] * d_last, c.nv, d_last, d.labels.as<int64_t>(),
             d.mask.as<uint8_t>(), c.dest_rows.as<int64_t>(),
             d.cache ? d.mg[f->L].as<float>() : (float*)gout, d.cache ? c.dest_m0 : -1,
-            (float)count, d.loss_part.as<double>() + (int64_t)j * blocks);
+            (float)count, d.loss_part.as<double>() + (int64_t)j * blocks,
+            gz_fold ? d.sc.as<float>() : nullptr, gz_ld);
         CU(cudaGetLastError());
       }
+    if (gz_fold) d.gz_loss_ld = gz_ld;
     if (d.cache) {  // grad_h[L] rows live in the mirror; write them through
       if (count <= 0) CU(cudaMemsetAsync(d.mg[f->L].p, 0, d.mcount * (int64_t)d_last * 4, d.stream));
       if (!f->lean) HT_TRY(cache_writeback(f, d, gout, d.mg[f->L].as<float>(), (int64_t)d_last * 4));
@@ -404,7 +417,10 @@ extern "C" int ht_backward_layer(ht_fleet* f, int layer, int d_in, int d_out, co
       const bool fold = precision == HT_PREC_TF32 && HO && !hrows && !narrow && !no_in &&
                         M > 0 && !f->sw.no_mask_fold && (d_out & 3) == 0 &&
                         ((uintptr_t)G & 15) == 0 && ((uintptr_t)HO & 15) == 0;
-      if (HO && M > 0 && !fold) {  // gz = g * (h > 0): z need not be recomputed
+      // (top layer: the loss kernel may already have written gz)
+      const bool gz_loss = layer == f->L - 1 && d.gz_loss_ld == ldz && f->n == 1;
+      d.gz_loss_ld = 0;
+      if (HO && M > 0 && !fold && !gz_loss) {  // gz = g * (h > 0): z need not be recomputed
         count_launch();
         ht::k_relu_mask<<<grid_for(M), kThreads, 0, d.stream>>>(GZ, ldz, G, HO, hrows, M, d_out);
         CU(cudaGetLastError());

@@ -742,7 +742,8 @@ static __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H
                                               const uint8_t* __restrict__ mask,
                                               const int64_t* __restrict__ out_rows,
                                               float* __restrict__ out, int64_t out_base,
-                                              float count, double* __restrict__ block_loss) {
+                                              float count, double* __restrict__ block_loss,
+                                              float* __restrict__ gz = nullptr, int ldz = 0) {
   __shared__ double wsum[8];
   const int lane = lane_id(), wib = threadIdx.x >> 5;
   double my = 0.0;
@@ -772,6 +773,9 @@ static __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H
         } else {
           loss_row(H + r * d, g, d, y, count, lane, my);
         }
+        if (gz)  // gz = g * (h > 0), pad columns zero (each lane rereads its own g)
+          for (int c = lane; c < ldz; c += kWarp)
+            gz[r * ldz + c] = (m && c < d && H[r * d + c] > 0.f) ? g[c] : 0.f;
         continue;
       }
       const float c0 = z0, c1 = z1;
@@ -782,6 +786,10 @@ static __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H
       if (!m) {
         if (lane < d) g[lane] = 0.f;
         if (lane + kWarp < d) g[lane + kWarp] = 0.f;
+        if (gz) {
+          if (lane < ldz) gz[r * ldz + lane] = 0.f;
+          if (lane + kWarp < ldz) gz[r * ldz + lane + kWarp] = 0.f;
+        }
         continue;
       }
       float mx = fmaxf(c0, c1);
@@ -792,15 +800,22 @@ static __global__ void __launch_bounds__(256) k_loss(const float* __restrict__ H
       float sum = e0 + e1;
 #pragma unroll
       for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      float g0 = 0.f, g1 = 0.f;
       if (lane < d) {
         const float p = __fdiv_rn(e0, sum);
         if (lane == y) my += -(double)logf(p);
-        g[lane] = __fdiv_rn(lane == y ? __fsub_rn(p, 1.f) : p, count);
+        g0 = __fdiv_rn(lane == y ? __fsub_rn(p, 1.f) : p, count);
+        g[lane] = g0;
       }
       if (lane + kWarp < d) {
         const float p = __fdiv_rn(e1, sum);
         if (lane + kWarp == y) my += -(double)logf(p);
-        g[lane + kWarp] = __fdiv_rn(lane + kWarp == y ? __fsub_rn(p, 1.f) : p, count);
+        g1 = __fdiv_rn(lane + kWarp == y ? __fsub_rn(p, 1.f) : p, count);
+        g[lane + kWarp] = g1;
+      }
+      if (gz) {  // gz = g * (h > 0) (c0 / c1 = -inf past d), pad columns zero
+        if (lane < ldz) gz[r * ldz + lane] = c0 > 0.f ? g0 : 0.f;
+        if (lane + kWarp < ldz) gz[r * ldz + lane + kWarp] = c1 > 0.f ? g1 : 0.f;
       }
     }
   }
