@@ -149,6 +149,9 @@ constexpr int kDstBatch = HT_GAT_DB;  // destinations per work unit
 #ifndef HT_GAT_S1_MINB
 #define HT_GAT_S1_MINB 5
 #endif
+#ifndef HT_GAT_AB_MINB  // split-backward destination passes A and B (A/B knob)
+#define HT_GAT_AB_MINB 1
+#endif
 template <int NV, bool BWD>
 __global__ void __launch_bounds__(256, (NV == 1 && !BWD) ? HT_GAT_DST_MINB : 1) k_gat_dst(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
@@ -518,7 +521,7 @@ static __global__ void __launch_bounds__(256) k_gat_src_fixup(
 // Per-edge records {alpha, g_alpha -> g_t} in CSC order.
 // ---------------------------------------------------------------------------
 template <int NV>
-__global__ void __launch_bounds__(256) k_gat_bwd_a(
+__global__ void __launch_bounds__(256, NV == 1 ? HT_GAT_AB_MINB : 1) k_gat_bwd_a(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
     const float* __restrict__ P, const float* __restrict__ el_src, const float* __restrict__ a_dst,
     int d, float slope, const float* __restrict__ G, const float* __restrict__ HO,
@@ -689,7 +692,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? HT_GAT_S1_MINB : 1) k_gat_bwd_s
 // partial sums, then the warp sum: the fused kernel's association), g_t_e
 // into record .y, sgt_v = seg sum of g_t, optionally gp_v = sgt_v a_dst
 template <int NV>
-__global__ void __launch_bounds__(256) k_gat_bwd_b(
+__global__ void __launch_bounds__(256, NV == 1 ? HT_GAT_AB_MINB : 1) k_gat_bwd_b(
     const int64_t* __restrict__ off, const int32_t* __restrict__ idx, int64_t nseg,
     const float* __restrict__ el_src, const float* __restrict__ ELD, float slope,
     float* __restrict__ AL, float* __restrict__ SGT, float* __restrict__ GP,
