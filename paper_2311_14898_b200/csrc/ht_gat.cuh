@@ -149,8 +149,9 @@ constexpr int kDstBatch = HT_GAT_DB;  // destinations per work unit
 #ifndef HT_GAT_S1_MINB
 #define HT_GAT_S1_MINB 5
 #endif
-#ifndef HT_GAT_AB_MINB  // split-backward destination passes A and B (A/B knob)
-#define HT_GAT_AB_MINB 1
+#ifndef HT_GAT_AB_MINB  // split-backward destination passes A and B: 8 CTAs/SM (32 registers)
+// took the GAT edge backward 32.1 -> 31.0 ms (profiles/r3_gat_ab8_ab.txt)
+#define HT_GAT_AB_MINB 8
 #endif
 template <int NV, bool BWD>
 __global__ void __launch_bounds__(256, (NV == 1 && !BWD) ? HT_GAT_DST_MINB : 1) k_gat_dst(
